@@ -1,0 +1,155 @@
+/*
+ * cqk_b200.h -- C-ABI of the B200-native CQK / simplex / l1 solver.
+ *
+ * Drop-in boundary for the reference package `cqksolve` (a pure-Python
+ * package; its "operator API" is the Python function surface re-exported in
+ * cqksolve/__init__.py:3-49).  Each entry point below names the reference
+ * function it replaces.  Plain pointers and sizes only; `mem` says whether the
+ * array pointers are host memory (the library stages them through HBM and
+ * copies results back) or device memory (zero-copy).
+ *
+ * Status codes mirror the reference's outcomes and exceptions:
+ *   CQK_SOLVED / CQK_INFEASIBLE      -> Status.SOLVED / Status.INFEASIBLE
+ *                                       (newton.py:33-35)
+ *   CQK_E_DOMAIN (+field, index)     -> DomainError(field, index)  (core.py:81-87)
+ *   CQK_E_MAXITER                    -> MaxIterationsError          (newton.py:42-49)
+ *   CQK_E_CONTRACT                   -> ContractViolation           (newton.py:38-39)
+ *   CQK_E_EMPTY                      -> EmptyIndexSet               (simplex.py:33-34)
+ *   CQK_E_CUDA / CQK_E_ARG / CQK_E_TIMEOUT -> library errors (cqk_last_error())
+ */
+#ifndef CQK_B200_H
+#define CQK_B200_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CQK_ABI_VERSION 1
+
+enum {
+  CQK_SOLVED = 0,
+  CQK_INFEASIBLE = 1,
+  CQK_E_DOMAIN = -1,
+  CQK_E_MAXITER = -2,
+  CQK_E_CONTRACT = -3,
+  CQK_E_CUDA = -4,
+  CQK_E_ARG = -5,
+  CQK_E_EMPTY = -6,
+  CQK_E_TIMEOUT = -7,
+};
+
+/* DomainError.field codes */
+enum { CQK_F_D = 0, CQK_F_A, CQK_F_B, CQK_F_L, CQK_F_U, CQK_F_R, CQK_F_BOUNDS, CQK_F_Y,
+       CQK_F_XBAR };
+
+enum { CQK_MEM_HOST = 0, CQK_MEM_DEVICE = 1 };
+
+/* Decision-logic variant: which reference driver's control flow to replay. */
+enum {
+  CQK_VARIANT_SOLVE = 0,  /* newton.solve_cqk            newton.py:209-342  */
+  CQK_VARIANT_JACOBI = 1, /* parallel.jacobi_solve       parallel.py:371-500 */
+  CQK_VARIANT_PAR = 2,    /* parallel.par_solve_cqk      parallel.py:174-327 */
+};
+
+/* SolverOptions (newton.py:52-67) plus device knobs. */
+typedef struct {
+  int32_t variable_fixing;  /* SolverOptions.variable_fixing (ignored by JACOBI) */
+  int32_t max_iterations;   /* SolverOptions.max_iterations */
+  double tolerance_scale;   /* <= 0 or NaN: eps(dtype)^(3/4) */
+  int32_t variant;          /* CQK_VARIANT_* */
+  int32_t check;            /* run validate() first (check=True) */
+  double lambda0;           /* NaN: the reference initializer; else explicit start */
+  double compact_ratio;     /* physical compaction when fixed/present >= ratio;
+                               NaN = default 0.25, >1 = never */
+  int32_t record_trace;     /* keep (lam, phi, dminus, dplus) per phi evaluation */
+  int32_t reserved;
+} cqk_options;
+
+/* SolveOutcome (newton.py:93-103) plus measurement counters. */
+typedef struct {
+  int32_t status;
+  int32_t domain_field;
+  int64_t domain_index;     /* -1: not element specific */
+  double lam;               /* multiplier (NaN when infeasible) */
+  double lam0;              /* initial multiplier actually used */
+  int64_t iterations;
+  int64_t phi_evals;
+  int64_t fixed_count;
+  double bracket_lo, bracket_hi;
+  int64_t elems_read;       /* element-passes streamed (x bytes/elem = bytes) */
+  int64_t elems_written;    /* element writes (compaction + outputs) */
+  int64_t bytes_model;      /* algorithmic HBM bytes of the whole solve */
+  double device_ms;         /* kernel time, CUDA events on the solve stream */
+  int32_t launches;         /* kernels launched by this call */
+  int32_t trace_len;        /* rows available via cqk_get_trace */
+} cqk_result;
+
+typedef struct cqk_handle cqk_handle;
+
+/* Library / handle management ------------------------------------------------ */
+int cqk_abi_version(void);
+const char *cqk_last_error(void);
+/* Create a handle bound to CUDA device `device`; owns a stream, scratch and the
+   persistent-kernel state.  A handle is not re-entrant. */
+int cqk_create(cqk_handle **out, int device);
+int cqk_destroy(cqk_handle *h);
+/* Run subsequent work on `stream` (cudaStream_t); NULL = the handle's own. */
+int cqk_set_stream(cqk_handle *h, void *stream);
+int cqk_device_info(cqk_handle *h, int32_t *sm_count, int32_t *ctas, int32_t *threads);
+/* Copy the last solve's per-evaluation trace rows (4 doubles each). */
+int cqk_get_trace(cqk_handle *h, double *out, int32_t max_rows);
+
+/* CQK ----------------------------------------------------------------------- */
+/* validate(inst)  core.py:177-216 */
+int cqk_validate_f64(cqk_handle *h, int mem, const double *d, const double *a,
+                     const double *b, const double *l, const double *u, int64_t n,
+                     double r, cqk_result *res);
+/* initial_multiplier(inst, xbar)  core.py:288-308 ; xbar may be NULL */
+int cqk_initial_multiplier_f64(cqk_handle *h, int mem, const double *d, const double *a,
+                               const double *b, const double *l, const double *u,
+                               int64_t n, double r, const double *xbar, double *lam0);
+/* _phi_scan / eval_phi(inst, lam, idx)  core.py:233-276.  idx may be NULL (all
+   n).  out4 = {value, dminus, dplus, abs_bx}; at_lower/at_upper (length m) may
+   be NULL. */
+int cqk_phi_f64(cqk_handle *h, int mem, const double *d, const double *a,
+                const double *b, const double *l, const double *u, int64_t n,
+                const int64_t *idx, int64_t m, double lam, double *out4,
+                uint8_t *at_lower, uint8_t *at_upper);
+/* eval_x(inst, lam, idx)  core.py:219-230 -> x[m] */
+int cqk_eval_x_f64(cqk_handle *h, int mem, const double *d, const double *a,
+                   const double *b, const double *l, const double *u, int64_t n,
+                   const int64_t *idx, int64_t m, double lam, double *x);
+/* nearest_breakpoint  newton.py:129-162 ; right!=0: min bp > edge, else max bp < edge.
+   *found = 0 when none exists. */
+int cqk_nearest_breakpoint_f64(cqk_handle *h, int mem, const double *d, const double *a,
+                               const double *b, const double *l, const double *u,
+                               int64_t n, const int64_t *idx, int64_t m, double edge,
+                               int right, double *bp, int32_t *found);
+/* solve_cqk / jacobi_solve / par_solve_cqk  (variant in opts).  xbar may be
+   NULL; x may be NULL (multiplier only). */
+int cqk_solve_f64(cqk_handle *h, int mem, const double *d, const double *a,
+                  const double *b, const double *l, const double *u, int64_t n,
+                  double r, const cqk_options *opts, const double *xbar, double *x,
+                  cqk_result *res);
+
+/* Simplex / l1 ---------------------------------------------------------------- */
+/* newton_project_simplex(y, r, opts, lambda0)  simplex.py:218-308.  The device
+   initializer is the formula lambda0 = (r - sum y)/n clamped to >= min(-y)
+   (the reference's `lambda0=` route, simplex.py:246-250) unless opts->lambda0
+   is given.  x may be NULL. */
+int spx_project_f64(cqk_handle *h, int mem, const double *y, int64_t n, double r,
+                    const cqk_options *opts, double *x, cqk_result *res);
+/* project_l1(y, r)  simplex.py:311-333 (dense).  res->iterations = -1 when y is
+   already inside the ball (x = copy of y). */
+int l1_project_f64(cqk_handle *h, int mem, const double *y, int64_t n, double r,
+                   const cqk_options *opts, double *x, cqk_result *res);
+/* Row-wise newton_project_simplex(Y[i], r) for `rows` independent rows of
+   length `cols` (row-major).  lam/iters per row may be NULL. */
+int spx_project_batched_f64(cqk_handle *h, int mem, const double *Y, int64_t rows,
+                            int64_t cols, double r, const cqk_options *opts, double *X,
+                            double *lam, int32_t *iters, cqk_result *res);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

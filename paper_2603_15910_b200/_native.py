@@ -1,0 +1,232 @@
+"""ctypes binding of the in-tree native libraries.
+
+``libcqk_b200.so`` is the only compute path: there is no CPU fallback, and
+every entry point raises ``NativeUnavailable`` when the library (or a CUDA
+device) is missing.  ``libcqk_instances.so`` holds the host-side instance
+generators.
+"""
+
+import ctypes
+import math
+import os
+import threading
+
+import numpy as np
+
+from . import build as _build
+
+LIB_PATH = _build.CUDA_LIB
+GEN_PATH = _build.GEN_LIB
+
+SOLVED, INFEASIBLE = 0, 1
+E_DOMAIN, E_MAXITER, E_CONTRACT, E_CUDA, E_ARG, E_EMPTY, E_TIMEOUT = -1, -2, -3, -4, -5, -6, -7
+MEM_HOST, MEM_DEVICE = 0, 1
+VARIANT_SOLVE, VARIANT_JACOBI, VARIANT_PAR = 0, 1, 2
+FIELDS = ("d", "a", "b", "l", "u", "r", "bounds", "y", "xbar")
+
+
+class NativeUnavailable(RuntimeError):
+    """The CUDA library or a CUDA device is missing -- there is no fallback."""
+
+
+class NativeError(RuntimeError):
+    """A CUDA / argument error reported by the native library."""
+
+
+class Options(ctypes.Structure):
+    _fields_ = [
+        ("variable_fixing", ctypes.c_int32),
+        ("max_iterations", ctypes.c_int32),
+        ("tolerance_scale", ctypes.c_double),
+        ("variant", ctypes.c_int32),
+        ("check", ctypes.c_int32),
+        ("lambda0", ctypes.c_double),
+        ("compact_ratio", ctypes.c_double),
+        ("record_trace", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
+    ]
+
+
+class Result(ctypes.Structure):
+    _fields_ = [
+        ("status", ctypes.c_int32),
+        ("domain_field", ctypes.c_int32),
+        ("domain_index", ctypes.c_int64),
+        ("lam", ctypes.c_double),
+        ("lam0", ctypes.c_double),
+        ("iterations", ctypes.c_int64),
+        ("phi_evals", ctypes.c_int64),
+        ("fixed_count", ctypes.c_int64),
+        ("bracket_lo", ctypes.c_double),
+        ("bracket_hi", ctypes.c_double),
+        ("elems_read", ctypes.c_int64),
+        ("elems_written", ctypes.c_int64),
+        ("bytes_model", ctypes.c_int64),
+        ("device_ms", ctypes.c_double),
+        ("launches", ctypes.c_int32),
+        ("trace_len", ctypes.c_int32),
+    ]
+
+    def stats(self):
+        return {
+            "elems_read": int(self.elems_read),
+            "elems_written": int(self.elems_written),
+            "bytes_model": int(self.bytes_model),
+            "device_ms": float(self.device_ms),
+            "launches": int(self.launches),
+            "lam0": float(self.lam0),
+            "bracket": (float(self.bracket_lo), float(self.bracket_hi)),
+        }
+
+
+# Every symbol declared in include/cqk_b200.h (checked by the CPU tests).
+EXPORTS = (
+    "cqk_abi_version", "cqk_last_error", "cqk_create", "cqk_destroy", "cqk_set_stream",
+    "cqk_device_info", "cqk_get_trace", "cqk_validate_f64", "cqk_initial_multiplier_f64",
+    "cqk_phi_f64", "cqk_eval_x_f64", "cqk_nearest_breakpoint_f64", "cqk_solve_f64",
+    "spx_project_f64", "l1_project_f64", "spx_project_batched_f64",
+)
+
+_lib = None
+_gen = None
+_lock = threading.Lock()
+_tls = threading.local()
+
+_P = ctypes.c_void_p
+_D = ctypes.c_double
+_I64 = ctypes.c_int64
+_I32 = ctypes.c_int32
+_RES = ctypes.POINTER(Result)
+_OPT = ctypes.POINTER(Options)
+
+
+def _declare(L):
+    L.cqk_abi_version.restype = ctypes.c_int
+    L.cqk_last_error.restype = ctypes.c_char_p
+    L.cqk_create.argtypes = [ctypes.POINTER(_P), ctypes.c_int]
+    L.cqk_destroy.argtypes = [_P]
+    L.cqk_set_stream.argtypes = [_P, _P]
+    L.cqk_device_info.argtypes = [_P, ctypes.POINTER(_I32), ctypes.POINTER(_I32),
+                                  ctypes.POINTER(_I32)]
+    L.cqk_get_trace.argtypes = [_P, _P, _I32]
+    arr5 = [_P] * 5
+    L.cqk_validate_f64.argtypes = [_P, ctypes.c_int, *arr5, _I64, _D, _RES]
+    L.cqk_initial_multiplier_f64.argtypes = [_P, ctypes.c_int, *arr5, _I64, _D, _P,
+                                             ctypes.POINTER(_D)]
+    L.cqk_phi_f64.argtypes = [_P, ctypes.c_int, *arr5, _I64, _P, _I64, _D, _P, _P, _P]
+    L.cqk_eval_x_f64.argtypes = [_P, ctypes.c_int, *arr5, _I64, _P, _I64, _D, _P]
+    L.cqk_nearest_breakpoint_f64.argtypes = [_P, ctypes.c_int, *arr5, _I64, _P, _I64, _D,
+                                             ctypes.c_int, ctypes.POINTER(_D),
+                                             ctypes.POINTER(_I32)]
+    L.cqk_solve_f64.argtypes = [_P, ctypes.c_int, *arr5, _I64, _D, _OPT, _P, _P, _RES]
+    L.spx_project_f64.argtypes = [_P, ctypes.c_int, _P, _I64, _D, _OPT, _P, _RES]
+    L.l1_project_f64.argtypes = [_P, ctypes.c_int, _P, _I64, _D, _OPT, _P, _RES]
+    L.spx_project_batched_f64.argtypes = [_P, ctypes.c_int, _P, _I64, _I64, _D, _OPT, _P, _P,
+                                          _P, _RES]
+
+
+def load_library(path=None):
+    """Load (not build) libcqk_b200.so; raises NativeUnavailable if absent."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            p = path or LIB_PATH
+            if not os.path.exists(p):
+                raise NativeUnavailable(
+                    f"{p} is missing: run `python -m paper_2603_15910_b200.build` "
+                    "(there is no CPU fallback)")
+            L = ctypes.CDLL(p)
+            _declare(L)
+            _lib = L
+    return _lib
+
+
+def gen_library():
+    global _gen
+    with _lock:
+        if _gen is None:
+            if not os.path.exists(GEN_PATH):
+                _build.build_instances()
+            G = ctypes.CDLL(GEN_PATH)
+            G.cqk_gen_uniform01.argtypes = [ctypes.c_uint64, ctypes.c_uint64, _I64, _P]
+            G.cqk_gen_normal.argtypes = [ctypes.c_uint64, ctypes.c_uint64, _I64, _P]
+            G.cqk_gen_cqk.argtypes = [ctypes.c_int, _I64, ctypes.c_uint64, _P, _P, _P, _P, _P,
+                                      ctypes.POINTER(_D)]
+            G.cqk_gen_simplex_y.argtypes = [ctypes.c_int, _I64, ctypes.c_uint64, _P]
+            _gen = G
+    return _gen
+
+
+def last_error():
+    return (load_library().cqk_last_error() or b"").decode()
+
+
+class Handle:
+    """One cqk_handle (device-bound; not re-entrant)."""
+
+    def __init__(self, device=0):
+        import torch  # plumbing only: device discovery and streams
+
+        if not torch.cuda.is_available():
+            raise NativeUnavailable("no CUDA device visible (the solver has no CPU fallback)")
+        L = load_library()
+        h = _P()
+        rc = L.cqk_create(ctypes.byref(h), int(device))
+        if rc != 0:
+            raise NativeError(f"cqk_create failed ({rc}): {last_error()}")
+        self.ptr = h
+        self.device = int(device)
+        self.lib = L
+
+    def set_stream(self, stream_ptr):
+        self.lib.cqk_set_stream(self.ptr, _P(stream_ptr) if stream_ptr else None)
+
+    def info(self):
+        sm, ctas, thr = _I32(), _I32(), _I32()
+        self.lib.cqk_device_info(self.ptr, ctypes.byref(sm), ctypes.byref(ctas), ctypes.byref(thr))
+        return {"sm_count": sm.value, "ctas": ctas.value, "threads": thr.value}
+
+    def trace(self, rows):
+        out = np.zeros((max(rows, 1), 4))
+        got = self.lib.cqk_get_trace(self.ptr, out.ctypes.data, int(rows))
+        return [tuple(float(v) for v in row) for row in out[: max(got, 0)]]
+
+    def __del__(self):
+        try:
+            if getattr(self, "ptr", None):
+                self.lib.cqk_destroy(self.ptr)
+        except Exception:
+            pass
+
+
+def handle(device=None):
+    """Thread-local handle for `device` (default: torch's current device)."""
+    import torch
+
+    if device is None:
+        if not torch.cuda.is_available():
+            raise NativeUnavailable("no CUDA device visible (the solver has no CPU fallback)")
+        device = torch.cuda.current_device()
+    cache = getattr(_tls, "handles", None)
+    if cache is None:
+        cache = _tls.handles = {}
+    h = cache.get(device)
+    if h is None:
+        h = cache[device] = Handle(device)
+    return h
+
+
+def make_options(opts=None, variant=VARIANT_SOLVE, check=True, lambda0=None,
+                 compact_ratio=None, trace=False, fixing=None):
+    o = Options()
+    fix = getattr(opts, "variable_fixing", True) if fixing is None else fixing
+    o.variable_fixing = 1 if fix else 0
+    o.max_iterations = int(getattr(opts, "max_iterations", 100))
+    ts = getattr(opts, "tolerance_scale", None)
+    o.tolerance_scale = float(ts) if ts is not None else math.nan
+    o.variant = variant
+    o.check = 1 if check else 0
+    o.lambda0 = math.nan if lambda0 is None else float(lambda0)
+    o.compact_ratio = math.nan if compact_ratio is None else float(compact_ratio)
+    o.record_trace = 1 if trace else 0
+    return o

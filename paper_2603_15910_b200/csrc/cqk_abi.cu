@@ -1,0 +1,750 @@
+// cqk_abi.cu -- C-ABI implementation (include/cqk_b200.h).
+//
+// Owns: one stream, the persistent kernels' grid-sync words and master state,
+// per-CTA partials, compaction scratch (grow-only) and host-mode staging.
+// Every solve is ONE cooperative kernel launch; the small state struct goes
+// H2D before and D2H after it.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <mutex>
+#include <string>
+
+#include "../../include/cqk_b200.h"
+#include "cqk_kernels.cuh"
+
+using namespace cqk;
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                              \
+  do {                                                                              \
+    cudaError_t e_ = (expr);                                                        \
+    if (e_ != cudaSuccess)                                                          \
+      return set_err(CQK_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+constexpr int kTraceCap = 1024;
+constexpr int kUtilBlocksMax = 1184;
+
+struct Buf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t want) {
+    if (want <= bytes) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaSuccess) bytes = want;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+};
+
+}  // namespace
+
+struct cqk_handle {
+  int device = 0;
+  int sm_count = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  int grid_cqk_fix = 0, grid_cqk_jac = 0, grid_spx = 0, grid_l1 = 0;
+  unsigned* sync = nullptr;  // [0] arrive, [1] gen, [2] error
+  void* state = nullptr;     // CqkState / SpxState
+  double* partials = nullptr;
+  double* trace = nullptr;
+  double* red = nullptr;     // utility partials
+  double* out = nullptr;     // utility outputs (kMaxK doubles)
+  Buf scratch, stage, idxbuf, flags;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  int trace_len = 0;
+};
+
+extern "C" {
+
+int cqk_abi_version(void) { return CQK_ABI_VERSION; }
+
+const char* cqk_last_error(void) { return g_err.c_str(); }
+
+int cqk_create(cqk_handle** out, int device) {
+  if (!out) return set_err(CQK_E_ARG, "null handle pointer");
+  *out = nullptr;
+  int ndev = 0;
+  CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return set_err(CQK_E_ARG, "bad device ordinal");
+  CUDA_TRY(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+  if (prop.major < 10)
+    return set_err(CQK_E_CUDA, "this library is built for sm_100a (B200); found sm_" +
+                                   std::to_string(prop.major * 10 + prop.minor));
+  if (!prop.cooperativeLaunch) return set_err(CQK_E_CUDA, "device lacks cooperative launch");
+  cqk_handle* h = new cqk_handle();
+  h->device = device;
+  h->sm_count = prop.multiProcessorCount;
+  auto occ = [&](const void* fn) {
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, kThreads, 0);
+    return b < 1 ? 0 : b * h->sm_count;
+  };
+  h->grid_cqk_fix = occ((const void*)cqk_solve_kernel<double, true>);
+  h->grid_cqk_jac = occ((const void*)cqk_solve_kernel<double, false>);
+  h->grid_spx = occ((const void*)spx_solve_kernel<double, false>);
+  h->grid_l1 = occ((const void*)spx_solve_kernel<double, true>);
+  int gmax = h->grid_cqk_fix;
+  gmax = gmax > h->grid_cqk_jac ? gmax : h->grid_cqk_jac;
+  gmax = gmax > h->grid_spx ? gmax : h->grid_spx;
+  gmax = gmax > h->grid_l1 ? gmax : h->grid_l1;
+  if (gmax == 0) {
+    delete h;
+    return set_err(CQK_E_CUDA, "persistent kernels do not fit on an SM");
+  }
+  cudaError_t e = cudaSuccess;
+  e = e ? e : cudaStreamCreateWithFlags(&h->own, cudaStreamNonBlocking);
+  e = e ? e : cudaMalloc(&h->sync, 64);
+  e = e ? e : cudaMemset(h->sync, 0, 64);
+  size_t st_bytes = sizeof(CqkState) > sizeof(SpxState) ? sizeof(CqkState) : sizeof(SpxState);
+  e = e ? e : cudaMalloc(&h->state, st_bytes);
+  e = e ? e : cudaMalloc(&h->partials, sizeof(double) * kMaxK * (gmax + kUtilBlocksMax));
+  e = e ? e : cudaMalloc(&h->trace, sizeof(double) * 4 * kTraceCap);
+  e = e ? e : cudaMalloc(&h->red, sizeof(double) * kMaxK * kUtilBlocksMax);
+  e = e ? e : cudaMalloc(&h->out, sizeof(double) * kMaxK);
+  e = e ? e : cudaEventCreate(&h->ev0);
+  e = e ? e : cudaEventCreate(&h->ev1);
+  e = e ? e : cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    cqk_destroy(h);
+    return set_err(CQK_E_CUDA, std::string("cqk_create: ") + cudaGetErrorString(e));
+  }
+  h->stream = h->own;
+  *out = h;
+  return 0;
+}
+
+int cqk_destroy(cqk_handle* h) {
+  if (!h) return 0;
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  h->scratch.release();
+  h->stage.release();
+  h->idxbuf.release();
+  h->flags.release();
+  cudaFree(h->sync);
+  cudaFree(h->state);
+  cudaFree(h->partials);
+  cudaFree(h->trace);
+  cudaFree(h->red);
+  cudaFree(h->out);
+  if (h->ev0) cudaEventDestroy(h->ev0);
+  if (h->ev1) cudaEventDestroy(h->ev1);
+  if (h->own) cudaStreamDestroy(h->own);
+  delete h;
+  return 0;
+}
+
+int cqk_set_stream(cqk_handle* h, void* stream) {
+  if (!h) return set_err(CQK_E_ARG, "null handle");
+  h->stream = stream ? (cudaStream_t)stream : h->own;
+  return 0;
+}
+
+int cqk_device_info(cqk_handle* h, int32_t* sm_count, int32_t* ctas, int32_t* threads) {
+  if (!h) return set_err(CQK_E_ARG, "null handle");
+  if (sm_count) *sm_count = h->sm_count;
+  if (ctas) *ctas = h->grid_cqk_fix;
+  if (threads) *threads = kThreads;
+  return 0;
+}
+
+int cqk_get_trace(cqk_handle* h, double* out, int32_t max_rows) {
+  if (!h || !out) return set_err(CQK_E_ARG, "null argument");
+  cudaSetDevice(h->device);
+  int rows = h->trace_len < max_rows ? h->trace_len : max_rows;
+  if (rows > 0) CUDA_TRY(cudaMemcpy(out, h->trace, sizeof(double) * 4 * rows, cudaMemcpyDeviceToHost));
+  return rows;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------ helpers
+namespace {
+
+double tau_of(const cqk_options* o, bool f32) {
+  if (o && o->tolerance_scale > 0) return o->tolerance_scale;
+  const double eps = f32 ? (double)std::numeric_limits<float>::epsilon()
+                         : std::numeric_limits<double>::epsilon();
+  return std::pow(eps, 0.75);
+}
+
+cqk_options default_opts() {
+  cqk_options o;
+  std::memset(&o, 0, sizeof o);
+  o.variable_fixing = 1;
+  o.max_iterations = 100;
+  o.tolerance_scale = NAN;
+  o.variant = CQK_VARIANT_SOLVE;
+  o.check = 1;
+  o.lambda0 = NAN;
+  o.compact_ratio = NAN;
+  return o;
+}
+
+// Host-mode staging: copy `count` host arrays of n T into one device slab.
+template <typename T>
+int stage_inputs(cqk_handle* h, int mem, int64_t n, const T* const* in, int count,
+                 const T** dev, int extra_out, T** dev_out) {
+  if (mem == CQK_MEM_DEVICE) {
+    for (int i = 0; i < count; ++i) dev[i] = in[i];
+    return 0;
+  }
+  const size_t per = ((size_t)n * sizeof(T) + 255) / 256 * 256;
+  CUDA_TRY(h->stage.ensure(per * (count + extra_out)));
+  char* base = (char*)h->stage.p;
+  for (int i = 0; i < count; ++i) {
+    if (!in[i]) { dev[i] = nullptr; continue; }
+    T* d = (T*)(base + per * i);
+    CUDA_TRY(cudaMemcpyAsync(d, in[i], (size_t)n * sizeof(T), cudaMemcpyHostToDevice, h->stream));
+    dev[i] = d;
+  }
+  for (int j = 0; j < extra_out; ++j) dev_out[j] = (T*)(base + per * (count + j));
+  return 0;
+}
+
+bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+int finish_sync(cqk_handle* h) {
+  cudaError_t e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess) return set_err(CQK_E_CUDA, std::string("solve: ") + cudaGetErrorString(e));
+  return 0;
+}
+
+int check_timeout(cqk_handle* h) {
+  unsigned err = 0;
+  cudaMemcpy(&err, h->sync + 2, sizeof(unsigned), cudaMemcpyDeviceToHost);
+  if (err) {
+    cudaMemset(h->sync, 0, 64);
+    cudaDeviceSynchronize();
+    return set_err(CQK_E_TIMEOUT, "persistent kernel barrier timed out");
+  }
+  return 0;
+}
+
+int map_status(int32_t st) {
+  switch (st) {
+    case ST_SOLVED: return CQK_SOLVED;
+    case ST_INFEASIBLE: return CQK_INFEASIBLE;
+    case ST_DOMAIN: return CQK_E_DOMAIN;
+    case ST_MAXITER: return CQK_E_MAXITER;
+    case ST_CONTRACT: return CQK_E_CONTRACT;
+    default: return CQK_E_CUDA;
+  }
+}
+
+int util_blocks(cqk_handle* h, int64_t m) {
+  int64_t b = (m + kUtilThreads - 1) / kUtilThreads;
+  int64_t cap = (int64_t)h->sm_count * 8;
+  if (cap > kUtilBlocksMax) cap = kUtilBlocksMax;
+  if (b > cap) b = cap;
+  return b < 1 ? 1 : (int)b;
+}
+
+// Copy an optional index list to the device.
+int stage_idx(cqk_handle* h, int mem, const int64_t* idx, int64_t m, const int64_t** out) {
+  if (!idx || mem == CQK_MEM_DEVICE) { *out = idx; return 0; }
+  CUDA_TRY(h->idxbuf.ensure(sizeof(int64_t) * (m ? m : 1)));
+  CUDA_TRY(cudaMemcpyAsync(h->idxbuf.p, idx, sizeof(int64_t) * m, cudaMemcpyHostToDevice, h->stream));
+  *out = (const int64_t*)h->idxbuf.p;
+  return 0;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------ CQK solve
+extern "C" int cqk_solve_f64(cqk_handle* h, int mem, const double* d, const double* a,
+                             const double* b, const double* l, const double* u, int64_t n,
+                             double r, const cqk_options* opts_in, const double* xbar, double* x,
+                             cqk_result* res) {
+  if (!h || !d || !a || !b || !l || !u || !res) return set_err(CQK_E_ARG, "null argument");
+  std::memset(res, 0, sizeof *res);
+  res->domain_index = -1;
+  res->lam = NAN;
+  cqk_options opts = opts_in ? *opts_in : default_opts();
+  CUDA_TRY(cudaSetDevice(h->device));
+  if (n < 1) {  // validate(): "instance must have at least one variable"
+    if (opts.check) {
+      res->status = CQK_E_DOMAIN;
+      res->domain_field = CQK_F_D;
+      return CQK_E_DOMAIN;
+    }
+    return set_err(CQK_E_ARG, "n must be >= 1");
+  }
+  const bool jacobi = opts.variant == CQK_VARIANT_JACOBI;
+  const bool fixing = !jacobi && opts.variable_fixing;
+  const double* dv[6];
+  double* xo = x;
+  double* xdev = nullptr;
+  {
+    const double* in[6] = {d, a, b, l, u, xbar};
+    int rc = stage_inputs<double>(h, mem, n, in, 6, dv, (mem == CQK_MEM_HOST && x) ? 1 : 0, &xdev);
+    if (rc) return rc;
+    if (mem == CQK_MEM_HOST) xo = x ? xdev : nullptr;
+  }
+  for (int i = 0; i < 5; ++i)
+    if (!aligned16(dv[i])) return set_err(CQK_E_ARG, "device arrays must be 16-byte aligned");
+  if (xbar && !aligned16(dv[5])) return set_err(CQK_E_ARG, "xbar must be 16-byte aligned");
+  if (xo && !aligned16(xo)) return set_err(CQK_E_ARG, "x must be 16-byte aligned");
+
+  CqkState s;
+  std::memset(&s, 0, sizeof s);
+  const bool lam0_given = !std::isnan(opts.lambda0);
+  s.cmd.lam = lam0_given ? opts.lambda0 : 0.0;
+  s.cmd.fix_hi = INFINITY;
+  s.cmd.fix_lo = -INFINITY;
+  s.cmd.phase = (opts.check || !lam0_given) ? PH_LAMBDA0 : PH_SCAN;
+  s.lo = -INFINITY;
+  s.hi = INFINITY;
+  s.r_res = r;
+  s.r_orig = r;
+  s.tau = tau_of(&opts, false);
+  s.lam0 = s.cmd.lam;
+  s.compact_ratio = std::isnan(opts.compact_ratio) ? 0.25 : opts.compact_ratio;
+  s.max_iter = opts.max_iterations;
+  s.n = n;
+  s.phys_count = n;
+  s.fixing = fixing;
+  s.variant = opts.variant;
+  s.status = ST_RUNNING;
+  s.has_xbar = xbar != nullptr;
+  s.check = opts.check;
+  s.domain_index = -1;
+  s.trace_cap = opts.record_trace ? kTraceCap : 0;
+  s.lam0_given = lam0_given;
+  if (fixing) {
+    const size_t per = ((size_t)n * sizeof(double) + 255) / 256 * 256;
+    CUDA_TRY(h->scratch.ensure(per * 5));
+  }
+  CUDA_TRY(cudaMemcpyAsync(h->state, &s, sizeof s, cudaMemcpyHostToDevice, h->stream));
+  CqkParams<double> p;
+  std::memset(&p, 0, sizeof p);
+  p.d = dv[0]; p.a = dv[1]; p.b = dv[2]; p.l = dv[3]; p.u = dv[4]; p.xbar = xbar ? dv[5] : nullptr;
+  if (fixing) {
+    const size_t per = ((size_t)n * sizeof(double) + 255) / 256 * 256;
+    char* sb = (char*)h->scratch.p;
+    p.sd = (double*)(sb); p.sa = (double*)(sb + per); p.sb = (double*)(sb + 2 * per);
+    p.sl = (double*)(sb + 3 * per); p.su = (double*)(sb + 4 * per);
+  }
+  p.x = xo;
+  p.trace = h->trace;
+  p.n = n;
+  p.r = r;
+  p.st = (CqkState*)h->state;
+  p.partials = h->partials;
+  p.sync.arrive = h->sync;
+  p.sync.gen = h->sync + 1;
+  p.sync.error = (int*)(h->sync + 2);
+  void* args[] = {&p};
+  const int grid = fixing ? h->grid_cqk_fix : h->grid_cqk_jac;
+  const void* fn = fixing ? (const void*)cqk_solve_kernel<double, true>
+                          : (const void*)cqk_solve_kernel<double, false>;
+  CUDA_TRY(cudaEventRecord(h->ev0, h->stream));
+  CUDA_TRY(cudaLaunchCooperativeKernel(fn, grid, kThreads, args, 0, h->stream));
+  CUDA_TRY(cudaEventRecord(h->ev1, h->stream));
+  CUDA_TRY(cudaMemcpyAsync(&s, h->state, sizeof s, cudaMemcpyDeviceToHost, h->stream));
+  if (mem == CQK_MEM_HOST && x && xo)
+    CUDA_TRY(cudaMemcpyAsync(x, xo, sizeof(double) * n, cudaMemcpyDeviceToHost, h->stream));
+  int rc = finish_sync(h);
+  if (rc) return rc;
+  rc = check_timeout(h);
+  if (rc) return rc;
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, h->ev0, h->ev1);
+  h->trace_len = s.trace_len;
+  res->status = map_status(s.status);
+  res->domain_field = s.domain_field;
+  res->domain_index = s.domain_index;
+  res->lam = s.status == ST_SOLVED ? s.cmd.lam : (s.status == ST_MAXITER ? s.cmd.lam : NAN);
+  res->lam0 = s.lam0;
+  res->iterations = s.iterations;
+  res->phi_evals = s.phi_evals;
+  res->fixed_count = s.fixed_count;
+  res->bracket_lo = s.lo;
+  res->bracket_hi = s.hi;
+  const int64_t pass0 = (opts.check || !lam0_given) ? n : 0;
+  const int64_t bytes0 = (opts.check || xbar) ? (xbar ? 48 : 40) : 24;
+  const int64_t fin = (s.status == ST_SOLVED && xo) ? n : 0;
+  res->elems_read = pass0 + s.elems_scan + s.elems_bp + fin;
+  res->elems_written = s.elems_written + fin;
+  res->bytes_model = pass0 * bytes0 + 40 * (s.elems_scan + s.elems_bp + s.elems_written) + 48 * fin;
+  res->device_ms = ms;
+  res->launches = 1;
+  res->trace_len = s.trace_len;
+  return res->status;
+}
+
+// ------------------------------------------------------------ simplex / l1
+namespace {
+
+int spx_common(cqk_handle* h, int mem, const double* y, int64_t n, double r,
+               const cqk_options* opts_in, double* x, cqk_result* res, bool l1) {
+  if (!h || !y || !res) return set_err(CQK_E_ARG, "null argument");
+  std::memset(res, 0, sizeof *res);
+  res->domain_index = -1;
+  res->lam = NAN;
+  cqk_options opts = opts_in ? *opts_in : default_opts();
+  CUDA_TRY(cudaSetDevice(h->device));
+  if (!(r > 0)) {  // simplex.py:234-235, 322-323
+    res->status = CQK_E_DOMAIN;
+    res->domain_field = CQK_F_R;
+    return CQK_E_DOMAIN;
+  }
+  if (n < 1) return set_err(CQK_E_ARG, "n must be >= 1");
+  const double* yv;
+  double* xdev = nullptr;
+  double* xo = x;
+  {
+    const double* in[1] = {y};
+    int rc = stage_inputs<double>(h, mem, n, in, 1, &yv, (mem == CQK_MEM_HOST && x) ? 1 : 0, &xdev);
+    if (rc) return rc;
+    if (mem == CQK_MEM_HOST) xo = x ? xdev : nullptr;
+  }
+  if (!aligned16(yv) || (xo && !aligned16(xo)))
+    return set_err(CQK_E_ARG, "device arrays must be 16-byte aligned");
+  const bool fixing = opts.variable_fixing != 0;
+  SpxState s;
+  std::memset(&s, 0, sizeof s);
+  s.cmd.fix_hi = INFINITY;
+  s.cmd.fix_lo = -INFINITY;
+  s.cmd.phase = PH_LAMBDA0;
+  s.lo = -INFINITY;
+  s.hi = INFINITY;
+  s.r = r;
+  s.tau = tau_of(&opts, false);
+  s.n = n;
+  s.active = n;
+  s.phys_count = n;
+  s.max_iter = opts.max_iterations;
+  s.fixing = fixing;
+  s.status = ST_RUNNING;
+  s.l1 = l1;
+  s.lam0_given = !std::isnan(opts.lambda0);
+  s.lam0_value = opts.lambda0;
+  s.trace_cap = opts.record_trace ? kTraceCap : 0;
+  s.compact_ratio = std::isnan(opts.compact_ratio) ? 0.25 : opts.compact_ratio;
+  if (fixing) CUDA_TRY(h->scratch.ensure(((size_t)n * sizeof(double) + 255) / 256 * 256));
+  CUDA_TRY(cudaMemcpyAsync(h->state, &s, sizeof s, cudaMemcpyHostToDevice, h->stream));
+  SpxParams<double> p;
+  std::memset(&p, 0, sizeof p);
+  p.y = yv;
+  p.sy = fixing ? (double*)h->scratch.p : nullptr;
+  p.x = xo;
+  p.trace = h->trace;
+  p.n = n;
+  p.st = (SpxState*)h->state;
+  p.partials = h->partials;
+  p.sync.arrive = h->sync;
+  p.sync.gen = h->sync + 1;
+  p.sync.error = (int*)(h->sync + 2);
+  void* args[] = {&p};
+  const int grid = l1 ? h->grid_l1 : h->grid_spx;
+  const void* fn = l1 ? (const void*)spx_solve_kernel<double, true>
+                      : (const void*)spx_solve_kernel<double, false>;
+  CUDA_TRY(cudaEventRecord(h->ev0, h->stream));
+  CUDA_TRY(cudaLaunchCooperativeKernel(fn, grid, kThreads, args, 0, h->stream));
+  CUDA_TRY(cudaEventRecord(h->ev1, h->stream));
+  CUDA_TRY(cudaMemcpyAsync(&s, h->state, sizeof s, cudaMemcpyDeviceToHost, h->stream));
+  if (mem == CQK_MEM_HOST && x && xo)
+    CUDA_TRY(cudaMemcpyAsync(x, xo, sizeof(double) * n, cudaMemcpyDeviceToHost, h->stream));
+  int rc = finish_sync(h);
+  if (rc) return rc;
+  rc = check_timeout(h);
+  if (rc) return rc;
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, h->ev0, h->ev1);
+  h->trace_len = s.trace_len;
+  res->status = map_status(s.status);
+  res->lam = s.iterations < 0 ? NAN : s.cmd.lam;
+  res->lam0 = s.lam0;
+  res->iterations = s.iterations;
+  res->phi_evals = s.phi_evals;
+  res->fixed_count = s.fixed_count;
+  res->bracket_lo = s.lo;
+  res->bracket_hi = s.hi;
+  const int64_t fin = (s.status == ST_SOLVED && xo) ? n : 0;
+  res->elems_read = n + s.elems_scan + fin;
+  res->elems_written = s.elems_written + fin;
+  res->bytes_model = 8 * (n + s.elems_scan + s.elems_written) + 16 * fin;
+  res->device_ms = ms;
+  res->launches = 1;
+  res->trace_len = s.trace_len;
+  return res->status;
+}
+
+}  // namespace
+
+extern "C" int spx_project_f64(cqk_handle* h, int mem, const double* y, int64_t n, double r,
+                               const cqk_options* opts, double* x, cqk_result* res) {
+  return spx_common(h, mem, y, n, r, opts, x, res, false);
+}
+
+extern "C" int l1_project_f64(cqk_handle* h, int mem, const double* y, int64_t n, double r,
+                              const cqk_options* opts, double* x, cqk_result* res) {
+  return spx_common(h, mem, y, n, r, opts, x, res, true);
+}
+
+// ------------------------------------------------------------ batched rows
+namespace {
+template <int EPT>
+cudaError_t launch_rows(cqk_handle* h, const double* Y, double* X, double* lam, int32_t* it,
+                        int64_t rows, int cols, double r, double tau, int max_iter, int fixing,
+                        double lam0) {
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, spx_rows_kernel<EPT>, kRowThreads, 0);
+  int64_t grid = (int64_t)(occ > 0 ? occ : 1) * h->sm_count;
+  if (grid > rows) grid = rows;
+  spx_rows_kernel<EPT><<<(unsigned)grid, kRowThreads, 0, h->stream>>>(Y, X, lam, it, rows, cols, r,
+                                                                       tau, max_iter, fixing, lam0);
+  return cudaGetLastError();
+}
+}  // namespace
+
+extern "C" int spx_project_batched_f64(cqk_handle* h, int mem, const double* Y, int64_t rows,
+                                       int64_t cols, double r, const cqk_options* opts_in,
+                                       double* X, double* lam, int32_t* iters, cqk_result* res) {
+  if (!h || !Y || !X || !res) return set_err(CQK_E_ARG, "null argument");
+  std::memset(res, 0, sizeof *res);
+  res->domain_index = -1;
+  cqk_options opts = opts_in ? *opts_in : default_opts();
+  CUDA_TRY(cudaSetDevice(h->device));
+  if (!(r > 0)) {
+    res->status = CQK_E_DOMAIN;
+    res->domain_field = CQK_F_R;
+    return CQK_E_DOMAIN;
+  }
+  if (rows < 1 || cols < 1 || cols > 32 * kRowThreads)
+    return set_err(CQK_E_ARG, "rows >= 1 and 1 <= cols <= 8192 required");
+  const double* Yd = Y;
+  double *Xd = X, *Ld = lam;
+  int32_t* Id = iters;
+  const int64_t tot = rows * cols;
+  if (mem == CQK_MEM_HOST) {
+    const size_t per = ((size_t)tot * 8 + 255) / 256 * 256;
+    const size_t rb = ((size_t)rows * 8 + 255) / 256 * 256;
+    CUDA_TRY(h->stage.ensure(2 * per + 2 * rb));
+    char* base = (char*)h->stage.p;
+    CUDA_TRY(cudaMemcpyAsync(base, Y, (size_t)tot * 8, cudaMemcpyHostToDevice, h->stream));
+    Yd = (const double*)base;
+    Xd = (double*)(base + per);
+    Ld = lam ? (double*)(base + 2 * per) : nullptr;
+    Id = iters ? (int32_t*)(base + 2 * per + rb) : nullptr;
+  }
+  const double tau = tau_of(&opts, false);
+  const int fixing = opts.variable_fixing != 0;
+  const int c = (int)cols;
+  CUDA_TRY(cudaEventRecord(h->ev0, h->stream));
+  cudaError_t e;
+  if (c <= kRowThreads) e = launch_rows<1>(h, Yd, Xd, Ld, Id, rows, c, r, tau, opts.max_iterations, fixing, opts.lambda0);
+  else if (c <= 2 * kRowThreads) e = launch_rows<2>(h, Yd, Xd, Ld, Id, rows, c, r, tau, opts.max_iterations, fixing, opts.lambda0);
+  else if (c <= 4 * kRowThreads) e = launch_rows<4>(h, Yd, Xd, Ld, Id, rows, c, r, tau, opts.max_iterations, fixing, opts.lambda0);
+  else if (c <= 8 * kRowThreads) e = launch_rows<8>(h, Yd, Xd, Ld, Id, rows, c, r, tau, opts.max_iterations, fixing, opts.lambda0);
+  else if (c <= 16 * kRowThreads) e = launch_rows<16>(h, Yd, Xd, Ld, Id, rows, c, r, tau, opts.max_iterations, fixing, opts.lambda0);
+  else e = launch_rows<32>(h, Yd, Xd, Ld, Id, rows, c, r, tau, opts.max_iterations, fixing, opts.lambda0);
+  if (e != cudaSuccess) return set_err(CQK_E_CUDA, std::string("rows kernel: ") + cudaGetErrorString(e));
+  CUDA_TRY(cudaEventRecord(h->ev1, h->stream));
+  if (mem == CQK_MEM_HOST) {
+    CUDA_TRY(cudaMemcpyAsync(X, Xd, (size_t)tot * 8, cudaMemcpyDeviceToHost, h->stream));
+    if (lam) CUDA_TRY(cudaMemcpyAsync(lam, Ld, (size_t)rows * 8, cudaMemcpyDeviceToHost, h->stream));
+    if (iters) CUDA_TRY(cudaMemcpyAsync(iters, Id, (size_t)rows * 4, cudaMemcpyDeviceToHost, h->stream));
+  }
+  int rc = finish_sync(h);
+  if (rc) return rc;
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, h->ev0, h->ev1);
+  res->status = CQK_SOLVED;
+  res->elems_read = tot;
+  res->elems_written = tot;
+  res->bytes_model = 16 * tot;
+  res->device_ms = ms;
+  res->launches = 1;
+  return 0;
+}
+
+// ------------------------------------------------------------ components
+extern "C" int cqk_phi_f64(cqk_handle* h, int mem, const double* d, const double* a,
+                           const double* b, const double* l, const double* u, int64_t n,
+                           const int64_t* idx, int64_t m, double lam, double* out4,
+                           uint8_t* at_lower, uint8_t* at_upper) {
+  if (!h || !d || !a || !b || !l || !u || !out4) return set_err(CQK_E_ARG, "null argument");
+  CUDA_TRY(cudaSetDevice(h->device));
+  if (!idx) m = n;
+  const double* dv[5];
+  {
+    const double* in[5] = {d, a, b, l, u};
+    int rc = stage_inputs<double>(h, mem, n, in, 5, dv, 0, nullptr);
+    if (rc) return rc;
+  }
+  const int64_t* ix;
+  int rc = stage_idx(h, mem, idx, m, &ix);
+  if (rc) return rc;
+  uint8_t *flo = at_lower, *fhi = at_upper;
+  if (mem == CQK_MEM_HOST && (at_lower || at_upper)) {
+    CUDA_TRY(h->flags.ensure(2 * (size_t)(m ? m : 1)));
+    flo = at_lower ? (uint8_t*)h->flags.p : nullptr;
+    fhi = at_upper ? (uint8_t*)h->flags.p + m : nullptr;
+  }
+  const int nb = util_blocks(h, m);
+  phi_util_kernel<double><<<nb, kUtilThreads, 0, h->stream>>>(dv[0], dv[1], dv[2], dv[3], dv[4],
+                                                             ix, m, lam, flo, fhi, h->red);
+  finalize_kernel<<<1, kUtilThreads, 0, h->stream>>>(h->red, nb, 5, 0, 0, h->out);
+  CUDA_TRY(cudaGetLastError());
+  double t[kMaxK];
+  CUDA_TRY(cudaMemcpyAsync(t, h->out, sizeof(double) * 5, cudaMemcpyDeviceToHost, h->stream));
+  if (mem == CQK_MEM_HOST) {
+    if (at_lower) CUDA_TRY(cudaMemcpyAsync(at_lower, flo, m, cudaMemcpyDeviceToHost, h->stream));
+    if (at_upper) CUDA_TRY(cudaMemcpyAsync(at_upper, fhi, m, cudaMemcpyDeviceToHost, h->stream));
+  }
+  rc = finish_sync(h);
+  if (rc) return rc;
+  out4[0] = t[0];
+  out4[1] = t[2] + t[4];  // dminus = core + tie_hi
+  out4[2] = t[2] + t[3];  // dplus  = core + tie_lo
+  out4[3] = t[1];
+  return 0;
+}
+
+extern "C" int cqk_eval_x_f64(cqk_handle* h, int mem, const double* d, const double* a,
+                              const double* b, const double* l, const double* u, int64_t n,
+                              const int64_t* idx, int64_t m, double lam, double* x) {
+  if (!h || !d || !a || !b || !l || !u || !x) return set_err(CQK_E_ARG, "null argument");
+  CUDA_TRY(cudaSetDevice(h->device));
+  if (!idx) m = n;
+  const double* dv[5];
+  double* xd = x;
+  {
+    const double* in[5] = {d, a, b, l, u};
+    int rc = stage_inputs<double>(h, mem, n, in, 5, dv, mem == CQK_MEM_HOST ? 1 : 0, &xd);
+    if (rc) return rc;
+  }
+  const int64_t* ix;
+  int rc = stage_idx(h, mem, idx, m, &ix);
+  if (rc) return rc;
+  evalx_util_kernel<double><<<util_blocks(h, m), kUtilThreads, 0, h->stream>>>(
+      dv[0], dv[1], dv[2], dv[3], dv[4], ix, m, lam, xd);
+  CUDA_TRY(cudaGetLastError());
+  if (mem == CQK_MEM_HOST) CUDA_TRY(cudaMemcpyAsync(x, xd, sizeof(double) * m, cudaMemcpyDeviceToHost, h->stream));
+  return finish_sync(h);
+}
+
+extern "C" int cqk_nearest_breakpoint_f64(cqk_handle* h, int mem, const double* d,
+                                          const double* a, const double* b, const double* l,
+                                          const double* u, int64_t n, const int64_t* idx,
+                                          int64_t m, double edge, int right, double* bp,
+                                          int32_t* found) {
+  if (!h || !d || !a || !b || !l || !u || !bp || !found) return set_err(CQK_E_ARG, "null argument");
+  CUDA_TRY(cudaSetDevice(h->device));
+  if (!idx) m = n;
+  const double* dv[5];
+  {
+    const double* in[5] = {d, a, b, l, u};
+    int rc = stage_inputs<double>(h, mem, n, in, 5, dv, 0, nullptr);
+    if (rc) return rc;
+  }
+  const int64_t* ix;
+  int rc = stage_idx(h, mem, idx, m, &ix);
+  if (rc) return rc;
+  const int nb = util_blocks(h, m);
+  bp_util_kernel<double><<<nb, kUtilThreads, 0, h->stream>>>(dv[0], dv[1], dv[2], dv[3], dv[4], ix,
+                                                            m, edge, right, h->red);
+  finalize_kernel<<<1, kUtilThreads, 0, h->stream>>>(h->red, nb, 2, right ? 1 : 0, right ? 0 : 1,
+                                                     h->out);
+  CUDA_TRY(cudaGetLastError());
+  double t[2];
+  CUDA_TRY(cudaMemcpyAsync(t, h->out, sizeof t, cudaMemcpyDeviceToHost, h->stream));
+  rc = finish_sync(h);
+  if (rc) return rc;
+  *found = t[1] > 0;
+  *bp = t[1] > 0 ? t[0] : NAN;
+  return 0;
+}
+
+namespace {
+int lambda0_util(cqk_handle* h, int mem, const double* d, const double* a, const double* b,
+                 const double* l, const double* u, int64_t n, const double* xbar, int check,
+                 double* t15) {
+  const double* dv[6];
+  {
+    const double* in[6] = {d, a, b, l, u, xbar};
+    int rc = stage_inputs<double>(h, mem, n, in, 6, dv, 0, nullptr);
+    if (rc) return rc;
+  }
+  const int nb = util_blocks(h, n);
+  lambda0_util_kernel<double><<<nb, kUtilThreads, 0, h->stream>>>(
+      dv[0], dv[1], dv[2], dv[3], dv[4], xbar ? dv[5] : nullptr, n, check, h->red);
+  finalize_kernel<<<1, kUtilThreads, 0, h->stream>>>(h->red, nb, 15, 0x7fe0, 0, h->out);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpyAsync(t15, h->out, sizeof(double) * 15, cudaMemcpyDeviceToHost, h->stream));
+  return finish_sync(h);
+}
+}  // namespace
+
+extern "C" int cqk_initial_multiplier_f64(cqk_handle* h, int mem, const double* d,
+                                          const double* a, const double* b, const double* l,
+                                          const double* u, int64_t n, double r,
+                                          const double* xbar, double* lam0) {
+  if (!h || !d || !a || !b || !l || !u || !lam0) return set_err(CQK_E_ARG, "null argument");
+  if (n < 1) return set_err(CQK_E_ARG, "n must be >= 1");
+  CUDA_TRY(cudaSetDevice(h->device));
+  double t[15];
+  int rc = lambda0_util(h, mem, d, a, b, l, u, n, xbar, 0, t);
+  if (rc) return rc;
+  *lam0 = (xbar && t[4] > 0) ? (r - t[2]) / t[3] : (r - t[0]) / t[1];
+  return 0;
+}
+
+extern "C" int cqk_validate_f64(cqk_handle* h, int mem, const double* d, const double* a,
+                                const double* b, const double* l, const double* u, int64_t n,
+                                double r, cqk_result* res) {
+  if (!h || !res) return set_err(CQK_E_ARG, "null argument");
+  std::memset(res, 0, sizeof *res);
+  res->domain_index = -1;
+  if (n < 1) {
+    res->status = CQK_E_DOMAIN;
+    res->domain_field = CQK_F_D;
+    return CQK_E_DOMAIN;
+  }
+  if (!d || !a || !b || !l || !u) return set_err(CQK_E_ARG, "null argument");
+  CUDA_TRY(cudaSetDevice(h->device));
+  double t[15];
+  int rc = lambda0_util(h, mem, d, a, b, l, u, n, nullptr, 1, t);
+  if (rc) return rc;
+  const int32_t field_of[10] = {CQK_F_D, CQK_F_A, CQK_F_B, CQK_F_L, CQK_F_U,
+                                CQK_F_D, CQK_F_B, CQK_F_BOUNDS, CQK_F_L, CQK_F_U};
+  for (int c = 0; c < 10; ++c) {
+    if (c == 5 && !std::isfinite(r)) {
+      res->status = CQK_E_DOMAIN;
+      res->domain_field = CQK_F_R;
+      return CQK_E_DOMAIN;
+    }
+    if (t[kValidateSlot + c] < (double)n) {
+      res->status = CQK_E_DOMAIN;
+      res->domain_field = field_of[c];
+      res->domain_index = (int64_t)t[kValidateSlot + c];
+      return CQK_E_DOMAIN;
+    }
+  }
+  return 0;
+}

@@ -1,0 +1,909 @@
+// cqk_kernels.cuh -- the persistent CQK and simplex/l1 kernels and the
+// batched row-wise simplex kernel (sm_100a, fp64 / fp32).
+#pragma once
+#include "cqk_solver.cuh"
+
+namespace cqk {
+
+// ------------------------------------------------------------ chunk loads
+// A warp streams its segment in chunks of 32 * VN * UNR elements; lane `ln`
+// owns elements base + u*32*VN + ln*VN + v.  Full chunks use 16-byte vector
+// loads; the ragged tail uses guarded scalar loads with a neutral fill.
+constexpr int kUnroll = 2;
+
+template <typename T, bool SCRATCH>
+DEVI void load_chunk(const T* p, int64_t base, int64_t m, int lane, bool full, T fill,
+                     T (&out)[Vec<T>::n * kUnroll]) {
+  using V = typename Vec<T>::type;
+  constexpr int VN = Vec<T>::n;
+  if (full) {
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const V* q = reinterpret_cast<const V*>(p + base + (int64_t)u * 32 * VN + lane * VN);
+      V v = SCRATCH ? ld_scratch(q) : ld_stream(q);
+      unpack<V, T>(v, &out[u * VN]);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < VN * kUnroll; ++j) {
+      const int64_t e = base + (int64_t)(j / VN) * 32 * VN + lane * VN + (j % VN);
+      out[j] = e < m ? (SCRATCH ? ld_scratch(p + e) : ld_stream(p + e)) : fill;
+    }
+  }
+}
+
+template <typename T>
+DEVI int64_t chunk_index(int64_t base, int lane, int j) {
+  constexpr int VN = Vec<T>::n;
+  return base + (int64_t)(j / VN) * 32 * VN + lane * VN + (j % VN);
+}
+
+DEVI void store_out(double2* p, double2 v) { __stcs(p, v); }
+DEVI void store_out(float4* p, float4 v) { __stcs(p, v); }
+
+// Word-wise L2 (coherent) copy of master-owned structures.
+template <typename S>
+DEVI void load_l2(S* dst, const S* src) {
+  static_assert(sizeof(S) % 8 == 0, "8-byte multiple");
+  const unsigned long long* s = reinterpret_cast<const unsigned long long*>(src);
+  unsigned long long* d = reinterpret_cast<unsigned long long*>(dst);
+#pragma unroll 4
+  for (int i = 0; i < (int)(sizeof(S) / 8); ++i) d[i] = __ldcg(s + i);
+}
+
+// ------------------------------------------------------------ barrier
+// Every CTA publishes partials[blockIdx.x][0..K); the last CTA to arrive
+// reduces them in a fixed order into s_tot and returns true (it is the
+// master for this epoch).  Call master_release() after the master work.
+template <int K>
+DEVI bool arrive_and_reduce(double* partials, const double* s_cta, const int (&ops)[K],
+                            const GridSync& sy, double (*s_red)[kMaxK], double* s_tot,
+                            int* s_flag) {
+  if (threadIdx.x < K) partials[(int64_t)blockIdx.x * kMaxK + threadIdx.x] = s_cta[threadIdx.x];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned prev = atomicAdd(sy.arrive, 1u);
+    *s_flag = prev == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!*s_flag) return false;
+  __threadfence();
+  double acc[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+    acc[k] = ops[k] == OP_SUM ? 0.0 : ops[k] == OP_MIN ? HUGE_VAL : -HUGE_VAL;
+  for (int c = threadIdx.x; c < (int)gridDim.x; c += blockDim.x) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const double v = __ldcg(partials + (int64_t)c * kMaxK + k);
+      acc[k] = ops[k] == OP_SUM ? acc[k] + v : ops[k] == OP_MIN ? fmin(acc[k], v) : fmax(acc[k], v);
+    }
+  }
+  block_reduce<K>(acc, ops, s_red, s_tot);
+  return true;
+}
+
+DEVI void master_release(const GridSync& sy, unsigned target) {
+  if (threadIdx.x == 0) {
+    __threadfence();
+    *sy.arrive = 0u;
+    __threadfence();
+    st_release(sy.gen, target);
+  }
+}
+
+// returns false on timeout
+DEVI bool wait_release(const GridSync& sy, unsigned target) {
+  const unsigned long long t0 = globaltimer();
+  while ((int)(ld_acquire(sy.gen) - target) < 0) {
+    if (globaltimer() - t0 > kSpinTimeoutNs) {
+      atomicExch(sy.error, 1);
+      return false;
+    }
+    __nanosleep(64);
+  }
+  return true;
+}
+
+// ------------------------------------------------------------ CQK passes
+// pass 0: lambda0 sums (core.py:288-308) fused with validate (core.py:177-216)
+template <typename T, bool CHECK, bool XBAR>
+DEVI void lambda0_pass(const CqkParams<T>& p, int64_t seg_lo, int64_t m, double (&acc)[kMaxK]) {
+  constexpr int E = Vec<T>::n * kUnroll, CH = 32 * E;
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = 0; base < m; base += CH) {
+    const bool full = base + CH <= m;
+    T D[E], A[E], B[E], L[E], U[E], X[E];
+    load_chunk<T, false>(p.d + seg_lo, base, m, lane, full, T(1), D);
+    load_chunk<T, false>(p.a + seg_lo, base, m, lane, full, T(0), A);
+    load_chunk<T, false>(p.b + seg_lo, base, m, lane, full, T(1), B);
+    if (CHECK || XBAR) {
+      load_chunk<T, false>(p.l + seg_lo, base, m, lane, full, T(0), L);
+      load_chunk<T, false>(p.u + seg_lo, base, m, lane, full, T(0), U);
+    }
+    if (XBAR) load_chunk<T, false>(p.xbar + seg_lo, base, m, lane, full, T(0), X);
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+      const int64_t e = chunk_index<T>(base, lane, j);
+      if (!full && e >= m) continue;
+      const double s = (double)mul_rn(B[j], div_rn(A[j], D[j]));
+      const double q = (double)mul_rn(B[j], div_rn(B[j], D[j]));
+      acc[0] += s;
+      acc[1] += q;
+      if (XBAR && L[j] < X[j] && X[j] < U[j]) { acc[2] += s; acc[3] += q; acc[4] += 1.0; }
+      if (CHECK) {
+        const double gi = (double)(seg_lo + e);
+        const T d = D[j], a = A[j], b = B[j], l = L[j], u = U[j];
+        if (!isfinite((double)d)) acc[5] = fmin(acc[5], gi);
+        if (!isfinite((double)a)) acc[6] = fmin(acc[6], gi);
+        if (!isfinite((double)b)) acc[7] = fmin(acc[7], gi);
+        if (isnan((double)l)) acc[8] = fmin(acc[8], gi);
+        if (isnan((double)u)) acc[9] = fmin(acc[9], gi);
+        if (!(d > T(0))) acc[10] = fmin(acc[10], gi);
+        if (!(b > T(0))) acc[11] = fmin(acc[11], gi);
+        if (!(l <= u)) acc[12] = fmin(acc[12], gi);
+        if ((double)l == HUGE_VAL) acc[13] = fmin(acc[13], gi);
+        if ((double)u == -HUGE_VAL) acc[14] = fmin(acc[14], gi);
+      }
+    }
+  }
+}
+
+template <typename T, bool FIX, bool SRC_SCRATCH>
+DEVI void scan_pass(const CqkParams<T>& p, const Cmd& c, int64_t seg_lo, int64_t& m,
+                    bool compact, double (&acc)[kMaxK]) {
+  constexpr int E = Vec<T>::n * kUnroll, CH = 32 * E;
+  const int lane = threadIdx.x & 31;
+  const T* sd = (SRC_SCRATCH ? p.sd : p.d) + seg_lo;
+  const T* sa = (SRC_SCRATCH ? p.sa : p.a) + seg_lo;
+  const T* sb = (SRC_SCRATCH ? p.sb : p.b) + seg_lo;
+  const T* sl = (SRC_SCRATCH ? p.sl : p.l) + seg_lo;
+  const T* su = (SRC_SCRATCH ? p.su : p.u) + seg_lo;
+  const T lam = (T)c.lam, fhi = (T)c.fix_hi, flo = (T)c.fix_lo;
+  const unsigned lt = (1u << lane) - 1u;
+  int64_t out_m = 0;
+  for (int64_t base = 0; base < m; base += CH) {
+    const bool full = base + CH <= m;
+    T D[E], A[E], B[E], L[E], U[E];
+    load_chunk<T, SRC_SCRATCH>(sd, base, m, lane, full, T(1), D);
+    load_chunk<T, SRC_SCRATCH>(sa, base, m, lane, full, T(0), A);
+    load_chunk<T, SRC_SCRATCH>(sb, base, m, lane, full, T(1), B);
+    load_chunk<T, SRC_SCRATCH>(sl, base, m, lane, full, T(0), L);
+    load_chunk<T, SRC_SCRATCH>(su, base, m, lane, full, T(0), U);
+    bool keep[E];
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+      const bool valid = full || chunk_index<T>(base, lane, j) < m;
+      keep[j] = valid && elem_scan<T, FIX>(D[j], A[j], B[j], L[j], U[j], lam, fhi, flo, acc);
+    }
+    if (FIX && compact) {
+      // warp-ballot stream compaction into this warp's own scratch range;
+      // write positions never overtake the read front (in-place safe).
+#pragma unroll
+      for (int j = 0; j < E; ++j) {
+        const unsigned mask = __ballot_sync(0xffffffffu, keep[j]);
+        if (keep[j]) {
+          const int64_t pos = seg_lo + out_m + __popc(mask & lt);
+          p.sd[pos] = D[j]; p.sa[pos] = A[j]; p.sb[pos] = B[j]; p.sl[pos] = L[j]; p.su[pos] = U[j];
+        }
+        out_m += __popc(mask);
+      }
+    }
+  }
+  if (FIX && compact) m = out_m;
+}
+
+template <typename T, bool SRC_SCRATCH>
+DEVI void bp_pass(const CqkParams<T>& p, const Cmd& c, bool fix, int64_t seg_lo, int64_t m,
+                  double (&acc)[kMaxK]) {
+  constexpr int E = Vec<T>::n * kUnroll, CH = 32 * E;
+  const int lane = threadIdx.x & 31;
+  const T* sd = (SRC_SCRATCH ? p.sd : p.d) + seg_lo;
+  const T* sa = (SRC_SCRATCH ? p.sa : p.a) + seg_lo;
+  const T* sb = (SRC_SCRATCH ? p.sb : p.b) + seg_lo;
+  const T* sl = (SRC_SCRATCH ? p.sl : p.l) + seg_lo;
+  const T* su = (SRC_SCRATCH ? p.su : p.u) + seg_lo;
+  const T lam = (T)c.lam, fhi = (T)c.fix_hi, flo = (T)c.fix_lo;
+  const bool right = c.right != 0;
+  for (int64_t base = 0; base < m; base += CH) {
+    const bool full = base + CH <= m;
+    T D[E], A[E], B[E], L[E], U[E];
+    load_chunk<T, SRC_SCRATCH>(sd, base, m, lane, full, T(1), D);
+    load_chunk<T, SRC_SCRATCH>(sa, base, m, lane, full, T(0), A);
+    load_chunk<T, SRC_SCRATCH>(sb, base, m, lane, full, T(1), B);
+    load_chunk<T, SRC_SCRATCH>(sl, base, m, lane, full, T(0), L);
+    load_chunk<T, SRC_SCRATCH>(su, base, m, lane, full, T(0), U);
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+      if (!full && chunk_index<T>(base, lane, j) >= m) continue;
+      if (fix) {  // only the logically active set takes part
+        const T t = t_of(D[j], A[j], B[j], lam);
+        if (t <= L[j] && t_of(D[j], A[j], B[j], fhi) <= L[j]) continue;
+        if (t >= U[j] && t_of(D[j], A[j], B[j], flo) >= U[j]) continue;
+      }
+      elem_bp<T>(D[j], A[j], B[j], L[j], U[j], c.edge, right, acc[0], acc[1]);
+    }
+  }
+}
+
+template <typename T, bool FIX>
+DEVI void final_pass(const CqkParams<T>& p, const Cmd& c, int64_t seg_lo, int64_t m) {
+  using V = typename Vec<T>::type;
+  constexpr int VN = Vec<T>::n, E = VN * kUnroll, CH = 32 * E;
+  const int lane = threadIdx.x & 31;
+  const T lam = (T)c.lam, fhi = (T)c.fix_hi, flo = (T)c.fix_lo;
+  // fixed variables need an explicit test only if lam* left the side of the
+  // fixing multiplier (the criterion-2 finish(lam + step) edge)
+  const bool chk_lo = FIX && c.lam > c.fix_hi, chk_hi = FIX && c.lam < c.fix_lo;
+  T* x = p.x + seg_lo;
+  for (int64_t base = 0; base < m; base += CH) {
+    const bool full = base + CH <= m;
+    T D[E], A[E], B[E], L[E], U[E];
+    load_chunk<T, false>(p.d + seg_lo, base, m, lane, full, T(1), D);
+    load_chunk<T, false>(p.a + seg_lo, base, m, lane, full, T(0), A);
+    load_chunk<T, false>(p.b + seg_lo, base, m, lane, full, T(1), B);
+    load_chunk<T, false>(p.l + seg_lo, base, m, lane, full, T(0), L);
+    load_chunk<T, false>(p.u + seg_lo, base, m, lane, full, T(0), U);
+    T X[E];
+#pragma unroll
+    for (int j = 0; j < E; ++j)
+      X[j] = elem_final<T, FIX>(D[j], A[j], B[j], L[j], U[j], lam, fhi, flo, chk_lo, chk_hi);
+    if (full) {
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        V v;
+        T* vv = reinterpret_cast<T*>(&v);
+#pragma unroll
+        for (int q = 0; q < VN; ++q) vv[q] = X[u * VN + q];
+        store_out(reinterpret_cast<V*>(x + base + (int64_t)u * 32 * VN + lane * VN), v);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < E; ++j) {
+        const int64_t e = chunk_index<T>(base, lane, j);
+        if (e < m) x[e] = X[j];
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------ CQK kernel
+template <typename T, bool FIX>
+__global__ void __launch_bounds__(kThreads, 1) cqk_solve_kernel(CqkParams<T> p) {
+  __shared__ double s_red[kWarps][kMaxK];
+  __shared__ double s_tot[kMaxK];
+  __shared__ Cmd s_cmd;
+  __shared__ int s_flag;
+  __shared__ unsigned s_gen0;
+  __shared__ int s_abort;
+  const int warp = threadIdx.x >> 5;
+  const int64_t gw = (int64_t)blockIdx.x * kWarps + warp, W = (int64_t)gridDim.x * kWarps;
+  int64_t seg_lo, seg_hi;
+  warp_segment(p.n, gw, W, seg_lo, seg_hi);
+  int64_t m = seg_hi - seg_lo;  // this warp's physical working-set size
+  bool in_scratch = false;
+  if (threadIdx.x == 0) {
+    s_gen0 = ld_acquire(p.sync.gen);
+    load_l2(&s_cmd, &p.st->cmd);
+    s_abort = 0;
+  }
+  __syncthreads();
+  const int has_xbar = p.xbar != nullptr;
+  for (unsigned epoch = 1;; ++epoch) {
+    const Cmd c = s_cmd;
+    if (c.phase == PH_DONE || s_abort) break;
+    if (c.phase == PH_FINAL) {
+      if (p.x) final_pass<T, FIX>(p, c, seg_lo, seg_hi - seg_lo);
+      break;
+    }
+    double acc[kMaxK];
+#pragma unroll
+    for (int k = 0; k < kMaxK; ++k) acc[k] = 0.0;
+    if (c.phase == PH_LAMBDA0) {
+#pragma unroll
+      for (int k = kValidateSlot; k < kValidateSlot + 10; ++k) acc[k] = HUGE_VAL;
+      const int check = p.st->check;  // immutable during the solve
+      const int64_t m0 = seg_hi - seg_lo;
+      if (check && has_xbar) lambda0_pass<T, true, true>(p, seg_lo, m0, acc);
+      else if (check) lambda0_pass<T, true, false>(p, seg_lo, m0, acc);
+      else if (has_xbar) lambda0_pass<T, false, true>(p, seg_lo, m0, acc);
+      else lambda0_pass<T, false, false>(p, seg_lo, m0, acc);
+      const int ops[15] = {OP_SUM, OP_SUM, OP_SUM, OP_SUM, OP_SUM, OP_MIN, OP_MIN, OP_MIN,
+                           OP_MIN, OP_MIN, OP_MIN, OP_MIN, OP_MIN, OP_MIN, OP_MIN};
+      double a15[15];
+#pragma unroll
+      for (int k = 0; k < 15; ++k) a15[k] = acc[k];
+      block_reduce<15>(a15, ops, s_red, s_tot);
+      if (arrive_and_reduce<15>(p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_flag)) {
+        if (threadIdx.x == 0) {
+          CqkState s;
+          load_l2(&s, p.st);
+          m_after_lambda0(s, s_tot);
+          *p.st = s;
+        }
+        master_release(p.sync, s_gen0 + epoch);
+      }
+    } else if (c.phase == PH_SCAN) {
+      const bool compact = FIX && c.compact;
+      if (in_scratch) scan_pass<T, FIX, true>(p, c, seg_lo, m, compact, acc);
+      else scan_pass<T, FIX, false>(p, c, seg_lo, m, compact, acc);
+      if (compact) in_scratch = true;
+      constexpr int K = FIX ? 11 : 5;
+      int ops[K];
+      double aK[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) { ops[k] = OP_SUM; aK[k] = acc[k]; }
+      block_reduce<K>(aK, ops, s_red, s_tot);
+      if (arrive_and_reduce<K>(p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_flag)) {
+        if (threadIdx.x == 0) {
+          CqkState s;
+          load_l2(&s, p.st);
+          double tot[11];
+#pragma unroll
+          for (int k = 0; k < 11; ++k) tot[k] = k < K ? s_tot[k] : 0.0;
+          m_after_scan(s, tot, p.trace);
+          *p.st = s;
+        }
+        master_release(p.sync, s_gen0 + epoch);
+      }
+    } else if (c.phase == PH_BP) {
+      acc[0] = c.right ? HUGE_VAL : -HUGE_VAL;
+      if (in_scratch) bp_pass<T, true>(p, c, FIX, seg_lo, m, acc);
+      else bp_pass<T, false>(p, c, FIX, seg_lo, m, acc);
+      int ops[2] = {c.right ? OP_MIN : OP_MAX, OP_SUM};
+      double a2[2] = {acc[0], acc[1]};
+      block_reduce<2>(a2, ops, s_red, s_tot);
+      if (arrive_and_reduce<2>(p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_flag)) {
+        if (threadIdx.x == 0) {
+          CqkState s;
+          load_l2(&s, p.st);
+          m_after_bp(s, s_tot);
+          *p.st = s;
+        }
+        master_release(p.sync, s_gen0 + epoch);
+      }
+    } else {
+      break;
+    }
+    if (!s_flag && threadIdx.x == 0) {
+      if (!wait_release(p.sync, s_gen0 + epoch)) s_abort = 1;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && !s_abort) load_l2(&s_cmd, &p.st->cmd);
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------ simplex / l1
+// newton_project_simplex (simplex.py:218-308) / project_l1 (simplex.py:311-333)
+// with the formula start: one pass for sum/max (and the l1 inside-ball
+// test), then phi passes over the free set, x = max(0, y + lam) (with the
+// sign restored for l1).  Dropped variables are those with w + fix_hi <= 0.
+struct SpxState {
+  Cmd cmd;  // lam, fix_hi (drop iff w + fix_hi <= 0), phase, compact
+  double lo, hi, r, tau, lam0, lam0_value;
+  int64_t n, active, phys_count, pending_phys, fixed_count, fixed_removed;
+  int64_t iterations, phi_evals, max_iter, elems_scan, elems_written;
+  int32_t fixing, status, l1, lam0_given, trace_len, trace_cap, compact_always, pad;
+  double compact_ratio;
+};
+
+template <typename T>
+struct SpxParams {
+  const T* y;
+  T* sy;  // scratch (working values w)
+  T* x;
+  double* trace;
+  int64_t n;
+  SpxState* st;
+  double* partials;
+  GridSync sync;
+};
+
+DEVI void s_finish(SpxState& s, double lam) {
+  s.status = ST_SOLVED;
+  s.cmd.lam = lam;
+  s.cmd.phase = PH_FINAL;
+  s.cmd.compact = 0;
+}
+
+// tot: 0 sum w, 1 max w
+DEVI void s_after_init(SpxState& s, const double* tot) {
+  if (s.l1 && tot[0] <= s.r) {  // simplex.py:324-325: inside the ball
+    s.status = ST_SOLVED;
+    s.iterations = -1;
+    s.cmd.phase = PH_COPY;
+    return;
+  }
+  const double lam0 = s.lam0_given ? s.lam0_value : (s.r - tot[0]) / (double)s.n;
+  const double mn = -tot[1];
+  s.lam0 = lam0 >= mn ? lam0 : mn;  // max(lambda0, min(-y)), simplex.py:250
+  s.cmd.lam = s.lam0;
+  s.cmd.phase = PH_SCAN;
+}
+
+// tot: 0 value, 1 #(v>0), 2 #(v==0)   (simplex.py:207-215, 256-294)
+DEVI void s_after_scan(SpxState& s, const double* tot, double* trace) {
+  s.phi_evals += 1;
+  s.elems_scan += s.phys_count;
+  if (s.cmd.compact) {
+    s.elems_written += s.pending_phys;
+    s.fixed_removed += s.phys_count - s.pending_phys;
+    s.phys_count = s.pending_phys;
+    s.cmd.compact = 0;
+  }
+  const double lam = s.cmd.lam, value = tot[0], dminus = tot[1], dplus = tot[1] + tot[2];
+  if (trace && s.trace_len < s.trace_cap) {
+    double* row = trace + 4 * s.trace_len++;
+    row[0] = lam; row[1] = value; row[2] = dminus; row[3] = dplus;
+  }
+  double deriv;
+  if (s.iterations == 0) {
+    if (value == s.r) { s_finish(s, lam); return; }
+    deriv = value < s.r ? dplus : dminus;
+  } else {
+    if (value <= s.r) { s_finish(s, lam); return; }
+    deriv = dminus;
+  }
+  if (value < s.r) s.lo = lam;
+  else {
+    s.hi = lam;
+    const int64_t at_zero = s.active - (int64_t)tot[1];
+    if (s.fixing && at_zero > 0) {
+      s.fixed_count += at_zero;
+      s.active -= at_zero;
+      s.cmd.fix_hi = lam;
+    }
+  }
+  if (deriv <= 0) { s.cmd.phase = PH_SNAP; return; }
+  const double step = -(value - s.r) / deriv;
+  const double next = lam + step;
+  if (fabs(step) < s.tau || next == lam) { s_finish(s, next); return; }
+  if (isfinite(s.lo) && isfinite(s.hi)) {
+    if (s.hi - s.lo < s.tau * fmax(fabs(s.hi), fabs(s.lo))) { s_finish(s, next); return; }
+  }
+  s.cmd.lam = next;
+  s.iterations += 1;
+  if (s.iterations > s.max_iter) { s_finish(s, next); return; }
+  s.cmd.phase = PH_SCAN;
+  s.cmd.compact = 0;
+  if (s.fixing) {
+    const int64_t present = s.fixed_count - s.fixed_removed;
+    if (present > 0 && (double)present >= s.compact_ratio * (double)s.phys_count) {
+      s.cmd.compact = 1;
+      s.pending_phys = s.phys_count - present;
+    }
+  }
+}
+
+// tot: 0 max(-w) over the free set, 1 count
+DEVI void s_after_snap(SpxState& s, const double* tot) {
+  s.elems_scan += s.phys_count;
+  if (tot[1] <= 0) { s.status = ST_CONTRACT; s.cmd.phase = PH_DONE; return; }
+  s.cmd.lam = tot[0];
+  s.iterations += 1;
+  s.cmd.phase = PH_SCAN;
+}
+
+template <typename T, bool L1>
+DEVI T spx_w(T y) { return L1 ? (T)fabs((double)y) : y; }
+
+template <typename T, bool L1, bool SRC_SCRATCH, int MODE>  // MODE 0 init, 1 scan, 2 snap
+DEVI void spx_pass(const SpxParams<T>& p, const Cmd& c, bool fix, int64_t seg_lo, int64_t& m,
+                   bool compact, double (&acc)[kMaxK]) {
+  constexpr int E = Vec<T>::n * kUnroll, CH = 32 * E;
+  const int lane = threadIdx.x & 31;
+  const T* src = (SRC_SCRATCH ? p.sy : p.y) + seg_lo;
+  const T lam = (T)c.lam, fhi = (T)c.fix_hi;
+  const unsigned lt = (1u << lane) - 1u;
+  int64_t out_m = 0;
+  for (int64_t base = 0; base < m; base += CH) {
+    const bool full = base + CH <= m;
+    T Y[E];
+    load_chunk<T, SRC_SCRATCH>(src, base, m, lane, full, T(0), Y);
+    bool keep[E];
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+      const bool valid = full || chunk_index<T>(base, lane, j) < m;
+      // scratch already holds w = |y| for l1
+      const T w = SRC_SCRATCH ? Y[j] : spx_w<T, L1>(Y[j]);
+      Y[j] = w;
+      keep[j] = false;
+      if (!valid) continue;
+      if (MODE == 0) {
+        acc[0] += (double)w;
+        acc[1] = fmax(acc[1], (double)w);
+        continue;
+      }
+      const T v = add_rn(w, lam);
+      if (fix && !(v > T(0)) && !(add_rn(w, fhi) > T(0))) continue;  // dropped
+      keep[j] = true;
+      if (MODE == 1) {
+        if (v > T(0)) { acc[0] += (double)v; acc[1] += 1.0; }
+        else if (v == T(0)) acc[2] += 1.0;
+      } else {
+        acc[0] = fmax(acc[0], -(double)w);
+        acc[1] += 1.0;
+      }
+    }
+    if (MODE == 1 && compact) {
+#pragma unroll
+      for (int j = 0; j < E; ++j) {
+        const unsigned mask = __ballot_sync(0xffffffffu, keep[j]);
+        if (keep[j]) p.sy[seg_lo + out_m + __popc(mask & lt)] = Y[j];
+        out_m += __popc(mask);
+      }
+    }
+  }
+  if (MODE == 1 && compact) m = out_m;
+}
+
+template <typename T, bool L1>
+DEVI void spx_final(const SpxParams<T>& p, const Cmd& c, bool copy, int64_t seg_lo, int64_t m) {
+  using V = typename Vec<T>::type;
+  constexpr int VN = Vec<T>::n, E = VN * kUnroll, CH = 32 * E;
+  const int lane = threadIdx.x & 31;
+  const T lam = (T)c.lam;
+  T* x = p.x + seg_lo;
+  for (int64_t base = 0; base < m; base += CH) {
+    const bool full = base + CH <= m;
+    T Y[E], X[E];
+    load_chunk<T, false>(p.y + seg_lo, base, m, lane, full, T(0), Y);
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+      if (copy) { X[j] = Y[j]; continue; }
+      const T w = spx_w<T, L1>(Y[j]);
+      const T v = add_rn(w, lam);
+      const T pos = v > T(0) ? v : T(0);  // np.maximum(0, w + lam)
+      if (L1) {
+        const T sg = Y[j] > T(0) ? T(1) : (Y[j] < T(0) ? T(-1) : T(0));
+        X[j] = mul_rn(sg, pos);
+      } else {
+        X[j] = pos;
+      }
+    }
+    if (full) {
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        V v;
+        T* vv = reinterpret_cast<T*>(&v);
+#pragma unroll
+        for (int q = 0; q < VN; ++q) vv[q] = X[u * VN + q];
+        store_out(reinterpret_cast<V*>(x + base + (int64_t)u * 32 * VN + lane * VN), v);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < E; ++j) {
+        const int64_t e = chunk_index<T>(base, lane, j);
+        if (e < m) x[e] = X[j];
+      }
+    }
+  }
+}
+
+template <typename T, bool L1>
+__global__ void __launch_bounds__(kThreads, 1) spx_solve_kernel(SpxParams<T> p) {
+  __shared__ double s_red[kWarps][kMaxK];
+  __shared__ double s_tot[kMaxK];
+  __shared__ Cmd s_cmd;
+  __shared__ int s_flag;
+  __shared__ unsigned s_gen0;
+  __shared__ int s_abort;
+  const int warp = threadIdx.x >> 5;
+  const int64_t gw = (int64_t)blockIdx.x * kWarps + warp, W = (int64_t)gridDim.x * kWarps;
+  int64_t seg_lo, seg_hi;
+  warp_segment(p.n, gw, W, seg_lo, seg_hi);
+  int64_t m = seg_hi - seg_lo;
+  bool in_scratch = false;
+  if (threadIdx.x == 0) {
+    s_gen0 = ld_acquire(p.sync.gen);
+    load_l2(&s_cmd, &p.st->cmd);
+    s_abort = 0;
+  }
+  __syncthreads();
+  const bool fix = p.st->fixing != 0;
+  for (unsigned epoch = 1;; ++epoch) {
+    const Cmd c = s_cmd;
+    if (c.phase == PH_DONE || s_abort) break;
+    if (c.phase == PH_FINAL || c.phase == PH_COPY) {
+      if (p.x) spx_final<T, L1>(p, c, c.phase == PH_COPY, seg_lo, seg_hi - seg_lo);
+      break;
+    }
+    double acc[kMaxK];
+#pragma unroll
+    for (int k = 0; k < kMaxK; ++k) acc[k] = 0.0;
+    int ops[3] = {OP_SUM, OP_SUM, OP_SUM};
+    int mode;
+    if (c.phase == PH_LAMBDA0) {
+      mode = 0;
+      acc[1] = -HUGE_VAL;
+      ops[1] = OP_MAX;
+      int64_t m0 = seg_hi - seg_lo;
+      spx_pass<T, L1, false, 0>(p, c, false, seg_lo, m0, false, acc);
+    } else if (c.phase == PH_SCAN) {
+      mode = 1;
+      const bool compact = fix && c.compact;
+      if (in_scratch) spx_pass<T, L1, true, 1>(p, c, fix, seg_lo, m, compact, acc);
+      else spx_pass<T, L1, false, 1>(p, c, fix, seg_lo, m, compact, acc);
+      if (compact) in_scratch = true;
+    } else if (c.phase == PH_SNAP) {
+      mode = 2;
+      acc[0] = -HUGE_VAL;
+      ops[0] = OP_MAX;
+      if (in_scratch) spx_pass<T, L1, true, 2>(p, c, fix, seg_lo, m, false, acc);
+      else spx_pass<T, L1, false, 2>(p, c, fix, seg_lo, m, false, acc);
+    } else {
+      break;
+    }
+    double a3[3] = {acc[0], acc[1], acc[2]};
+    block_reduce<3>(a3, ops, s_red, s_tot);
+    if (arrive_and_reduce<3>(p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_flag)) {
+      if (threadIdx.x == 0) {
+        SpxState s;
+        load_l2(&s, p.st);
+        if (mode == 0) s_after_init(s, s_tot);
+        else if (mode == 1) s_after_scan(s, s_tot, p.trace);
+        else s_after_snap(s, s_tot);
+        *p.st = s;
+      }
+      master_release(p.sync, s_gen0 + epoch);
+    }
+    if (!s_flag && threadIdx.x == 0) {
+      if (!wait_release(p.sync, s_gen0 + epoch)) s_abort = 1;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && !s_abort) load_l2(&s_cmd, &p.st->cmd);
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------ batched rows
+// K8: one CTA per row (grid-stride over rows); the row lives in registers
+// (EPT values per thread); every thread sees the same block totals so the
+// Algorithm-4 decisions (simplex.py:256-294) are taken redundantly and
+// identically -- no master, one __syncthreads per phi evaluation.
+constexpr int kRowThreads = 256;
+
+template <int EPT>
+__global__ void __launch_bounds__(kRowThreads) spx_rows_kernel(
+    const double* __restrict__ Y, double* __restrict__ X, double* __restrict__ lam_out,
+    int32_t* __restrict__ it_out, int64_t rows, int cols, double r, double tau, int max_iter,
+    int fixing, double lam0_given) {
+  __shared__ double s_part[2][kRowThreads / 32][3];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int NW = kRowThreads / 32;
+  int buf = 0;
+  auto reduce3 = [&](double v0, double v1, double v2, double& t0, double& t1, double& t2,
+                     bool max1) {
+    v0 = warp_sum(v0);
+    v1 = max1 ? warp_max(v1) : warp_sum(v1);
+    v2 = warp_sum(v2);
+    if (lane == 0) { s_part[buf][warp][0] = v0; s_part[buf][warp][1] = v1; s_part[buf][warp][2] = v2; }
+    __syncthreads();
+    t0 = s_part[buf][0][0]; t1 = s_part[buf][0][1]; t2 = s_part[buf][0][2];
+#pragma unroll
+    for (int w = 1; w < NW; ++w) {
+      t0 += s_part[buf][w][0];
+      t1 = max1 ? fmax(t1, s_part[buf][w][1]) : t1 + s_part[buf][w][1];
+      t2 += s_part[buf][w][2];
+    }
+    buf ^= 1;  // double-buffered: the next write cannot race these reads
+  };
+  for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
+    const double* y = Y + row * (int64_t)cols;
+    double v[EPT];
+    bool live[EPT];
+#pragma unroll
+    for (int k = 0; k < EPT; ++k) {
+      const int c = k * kRowThreads + threadIdx.x;
+      live[k] = c < cols;
+      v[k] = live[k] ? __ldcs(y + c) : 0.0;
+    }
+    double sum = 0.0, mx = -HUGE_VAL, unused;
+#pragma unroll
+    for (int k = 0; k < EPT; ++k)
+      if (live[k]) { sum += v[k]; mx = fmax(mx, v[k]); }
+    double tsum, tmax;
+    reduce3(sum, mx, 0.0, tsum, tmax, unused, true);
+    double lam = isnan(lam0_given) ? (r - tsum) / (double)cols : lam0_given;
+    lam = lam >= -tmax ? lam : -tmax;
+    double lo = -HUGE_VAL, hi = HUGE_VAL;
+    int iterations = 0;
+    bool drop[EPT];
+#pragma unroll
+    for (int k = 0; k < EPT; ++k) drop[k] = !live[k];
+    for (;;) {
+      double val = 0.0, npos = 0.0, nzero = 0.0;
+#pragma unroll
+      for (int k = 0; k < EPT; ++k) {
+        if (drop[k]) continue;
+        const double t = __dadd_rn(v[k], lam);
+        if (t > 0) { val += t; npos += 1.0; }
+        else if (t == 0) nzero += 1.0;
+      }
+      double value, dminus, cz;
+      reduce3(val, npos, nzero, value, dminus, cz, false);
+      const double dplus = dminus + cz;
+      double deriv;
+      if (iterations == 0) {
+        if (value == r) break;
+        deriv = value < r ? dplus : dminus;
+      } else {
+        if (value <= r) break;
+        deriv = dminus;
+      }
+      if (value < r) lo = lam;
+      else {
+        hi = lam;
+        if (fixing) {
+#pragma unroll
+          for (int k = 0; k < EPT; ++k)
+            if (!drop[k] && !(__dadd_rn(v[k], lam) > 0)) drop[k] = true;
+        }
+      }
+      if (deriv <= 0) {
+        double mneg = -HUGE_VAL;
+#pragma unroll
+        for (int k = 0; k < EPT; ++k)
+          if (!drop[k]) mneg = fmax(mneg, -v[k]);
+        double t0, t2;
+        reduce3(0.0, mneg, 0.0, t0, mneg, t2, true);
+        lam = mneg;
+        ++iterations;
+        continue;
+      }
+      const double step = -(value - r) / deriv;
+      const double next = lam + step;
+      if (fabs(step) < tau || next == lam) { lam = next; break; }
+      if (isfinite(lo) && isfinite(hi) && hi - lo < tau * fmax(fabs(hi), fabs(lo))) {
+        lam = next;
+        break;
+      }
+      lam = next;
+      ++iterations;
+      if (iterations > max_iter) break;
+    }
+    double* x = X + row * (int64_t)cols;
+#pragma unroll
+    for (int k = 0; k < EPT; ++k) {
+      const int c = k * kRowThreads + threadIdx.x;
+      if (live[k]) {
+        const double t = __dadd_rn(v[k], lam);
+        __stcs(x + c, t > 0 ? t : 0.0);
+      }
+    }
+    if (threadIdx.x == 0) {
+      if (lam_out) lam_out[row] = lam;
+      if (it_out) it_out[row] = iterations;
+    }
+  }
+}
+
+// ------------------------------------------------------------ utilities
+// Grid-stride kernels with per-block partials + a fixed-order finalize; used
+// by the component-level entry points (eval_phi, eval_x, breakpoints,
+// validate, initial_multiplier), optionally through an index list.
+constexpr int kUtilThreads = 256;
+
+template <typename T>
+DEVI int64_t gat(const int64_t* idx, int64_t k) { return idx ? idx[k] : k; }
+
+// slots: 0 value, 1 abs, 2 core, 3 tie_lo, 4 tie_hi
+template <typename T>
+__global__ void __launch_bounds__(kUtilThreads) phi_util_kernel(
+    const T* d, const T* a, const T* b, const T* l, const T* u, const int64_t* idx, int64_t m,
+    double lam_d, uint8_t* at_lo, uint8_t* at_hi, double* partials) {
+  __shared__ double s_red[kUtilThreads / 32][kMaxK];
+  __shared__ double s_tot[kMaxK];
+  const T lam = (T)lam_d;
+  double acc[kMaxK];
+  for (int k = 0; k < kMaxK; ++k) acc[k] = 0.0;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = gat<T>(idx, k);
+    const T t = t_of(d[i], a[i], b[i], lam);
+    if (at_lo) at_lo[k] = t <= l[i];
+    if (at_hi) at_hi[k] = t >= u[i];
+    elem_scan<T, false>(d[i], a[i], b[i], l[i], u[i], lam, lam, lam, acc);
+  }
+  const int ops[5] = {OP_SUM, OP_SUM, OP_SUM, OP_SUM, OP_SUM};
+  double a5[5] = {acc[0], acc[1], acc[2], acc[3], acc[4]};
+  block_reduce<5>(a5, ops, s_red, s_tot);
+  if (threadIdx.x < 5) partials[blockIdx.x * kMaxK + threadIdx.x] = s_tot[threadIdx.x];
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kUtilThreads) evalx_util_kernel(
+    const T* d, const T* a, const T* b, const T* l, const T* u, const int64_t* idx, int64_t m,
+    double lam_d, T* x) {
+  const T lam = (T)lam_d;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = gat<T>(idx, k);
+    x[k] = clip(t_of(d[i], a[i], b[i], lam), l[i], u[i]);
+  }
+}
+
+// slots: 0 best, 1 found
+template <typename T>
+__global__ void __launch_bounds__(kUtilThreads) bp_util_kernel(
+    const T* d, const T* a, const T* b, const T* l, const T* u, const int64_t* idx, int64_t m,
+    double edge, int right, double* partials) {
+  __shared__ double s_red[kUtilThreads / 32][kMaxK];
+  __shared__ double s_tot[kMaxK];
+  double best = right ? HUGE_VAL : -HUGE_VAL, found = 0.0;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = gat<T>(idx, k);
+    elem_bp<T>(d[i], a[i], b[i], l[i], u[i], edge, right != 0, best, found);
+  }
+  const int ops[2] = {right ? OP_MIN : OP_MAX, OP_SUM};
+  double a2[2] = {best, found};
+  block_reduce<2>(a2, ops, s_red, s_tot);
+  if (threadIdx.x < 2) partials[blockIdx.x * kMaxK + threadIdx.x] = s_tot[threadIdx.x];
+}
+
+// slots as the persistent lambda0 pass (0..4 sums, 5..14 validate mins)
+template <typename T>
+__global__ void __launch_bounds__(kUtilThreads) lambda0_util_kernel(
+    const T* d, const T* a, const T* b, const T* l, const T* u, const T* xbar, int64_t n,
+    int check, double* partials) {
+  __shared__ double s_red[kUtilThreads / 32][kMaxK];
+  __shared__ double s_tot[kMaxK];
+  double acc[15];
+  for (int k = 0; k < 15; ++k) acc[k] = k < kValidateSlot ? 0.0 : HUGE_VAL;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const T di = d[i], ai = a[i], bi = b[i];
+    const double s = (double)mul_rn(bi, div_rn(ai, di));
+    const double q = (double)mul_rn(bi, div_rn(bi, di));
+    acc[0] += s;
+    acc[1] += q;
+    if (xbar) {
+      const T xi = xbar[i];
+      if (l[i] < xi && xi < u[i]) { acc[2] += s; acc[3] += q; acc[4] += 1.0; }
+    }
+    if (check) {
+      const double gi = (double)i;
+      const T li = l[i], ui = u[i];
+      if (!isfinite((double)di)) acc[5] = fmin(acc[5], gi);
+      if (!isfinite((double)ai)) acc[6] = fmin(acc[6], gi);
+      if (!isfinite((double)bi)) acc[7] = fmin(acc[7], gi);
+      if (isnan((double)li)) acc[8] = fmin(acc[8], gi);
+      if (isnan((double)ui)) acc[9] = fmin(acc[9], gi);
+      if (!(di > T(0))) acc[10] = fmin(acc[10], gi);
+      if (!(bi > T(0))) acc[11] = fmin(acc[11], gi);
+      if (!(li <= ui)) acc[12] = fmin(acc[12], gi);
+      if ((double)li == HUGE_VAL) acc[13] = fmin(acc[13], gi);
+      if ((double)ui == -HUGE_VAL) acc[14] = fmin(acc[14], gi);
+    }
+  }
+  const int ops[15] = {OP_SUM, OP_SUM, OP_SUM, OP_SUM, OP_SUM, OP_MIN, OP_MIN, OP_MIN,
+                       OP_MIN, OP_MIN, OP_MIN, OP_MIN, OP_MIN, OP_MIN, OP_MIN};
+  block_reduce<15>(acc, ops, s_red, s_tot);
+  if (threadIdx.x < 15) partials[blockIdx.x * kMaxK + threadIdx.x] = s_tot[threadIdx.x];
+}
+
+// one block: fixed-order reduction of `nblk` partial rows -> out[0..K)
+__global__ void __launch_bounds__(kUtilThreads) finalize_kernel(const double* partials,
+                                                                int nblk, int K, int opmask_min,
+                                                                int opmask_max, double* out) {
+  __shared__ double s_red[kUtilThreads / 32][kMaxK];
+  __shared__ double s_tot[kMaxK];
+  double acc[kMaxK];
+  int ops[kMaxK];
+  for (int k = 0; k < kMaxK; ++k) {
+    ops[k] = (opmask_min >> k) & 1 ? OP_MIN : (opmask_max >> k) & 1 ? OP_MAX : OP_SUM;
+    acc[k] = ops[k] == OP_SUM ? 0.0 : ops[k] == OP_MIN ? HUGE_VAL : -HUGE_VAL;
+  }
+  for (int c = threadIdx.x; c < nblk; c += blockDim.x)
+    for (int k = 0; k < K; ++k) {
+      const double v = partials[c * kMaxK + k];
+      acc[k] = ops[k] == OP_SUM ? acc[k] + v : ops[k] == OP_MIN ? fmin(acc[k], v) : fmax(acc[k], v);
+    }
+  block_reduce<kMaxK>(acc, ops, s_red, s_tot);
+  if (threadIdx.x < K) out[threadIdx.x] = s_tot[threadIdx.x];
+}
+
+}  // namespace cqk

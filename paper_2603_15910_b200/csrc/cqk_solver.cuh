@@ -1,0 +1,319 @@
+// cqk_solver.cuh -- persistent single-launch CQK solve (sm_100a).
+//
+// One cooperative launch performs the whole of newton.solve_cqk
+// (newton.py:209-342) / parallel.jacobi_solve (parallel.py:371-500) /
+// parallel.par_solve_cqk (parallel.py:174-327):
+//
+//   pass 0   validate (core.py:177-216) fused with the lambda0 sums
+//            (core.py:288-308)                                  24..48 B/elem
+//   pass k   phi scan at lambda_k (core.py:233-263) over the warp-owned
+//            physical working set, K = 5 (Jacobi) or 11 (fixing) partials;
+//            optional in-place compaction of the survivors        40 B/elem
+//            (+40 B per survivor written)
+//   (rare)   nearest-breakpoint pass (newton.py:129-162)          40 B/elem
+//   final    x = clip(t(lambda*), l, u) with fixed variables at their bound
+//            (newton.py:232-242, fix_variables x[newly] = bound)  48 B/elem
+//
+// Between passes the last CTA to arrive reduces the per-CTA partials in a
+// fixed order and runs the Newton state machine below on one thread; the
+// other CTAs wait on a generation counter.  Variable fixing is *logical*
+// and stateless: an element is fixed at its lower bound iff
+// t(fix_hi) <= l, where fix_hi is the multiplier of the latest lower-fixing
+// iteration (the bracket only shrinks and rounded t is monotone in lambda,
+// so this reproduces fix_variables' accumulated sets exactly); compaction
+// is a purely physical byte saving decided by the master from counts.
+#pragma once
+#include "cqk_device.cuh"
+
+namespace cqk {
+
+enum Phase : int32_t {
+  PH_LAMBDA0 = 0,
+  PH_SCAN = 1,
+  PH_BP = 2,
+  PH_FINAL = 3,
+  PH_DONE = 4,
+  PH_COPY = 5,   // simplex/l1: x = y (inside the l1 ball)
+  PH_SNAP = 6,   // simplex: max(-y[free]) snap (simplex.py:276-281)
+};
+
+enum Status : int32_t {
+  ST_RUNNING = 100,
+  ST_SOLVED = 0,
+  ST_INFEASIBLE = 1,
+  ST_DOMAIN = -1,
+  ST_MAXITER = -2,
+  ST_CONTRACT = -3,
+  ST_TIMEOUT = -7,
+};
+
+enum Variant : int32_t { V_SOLVE = 0, V_JACOBI = 1, V_PAR = 2 };
+
+// What every CTA needs to run the next pass (written by the master only).
+struct Cmd {
+  double lam;     // scan point; final multiplier in PH_FINAL
+  double fix_hi;  // lower-fixed iff t(fix_hi) <= l   (+inf: none yet)
+  double fix_lo;  // upper-fixed iff t(fix_lo) >= u   (-inf: none yet)
+  double edge;    // breakpoint-search edge (PH_BP)
+  int32_t phase;
+  int32_t compact;  // this scan writes the survivors into scratch
+  int32_t right;    // PH_BP direction
+  int32_t pad;
+};
+
+// Master-side solver state (SolveState, newton.py:70-90, plus counters).
+struct CqkState {
+  Cmd cmd;
+  double lo, hi, phi_lo, phi_hi;
+  double r_res, r_orig, fixed_abs, tau;
+  double lam0, compact_ratio;
+  int64_t fixed_count, fixed_removed, iterations, phi_evals, max_iter;
+  int64_t n, phys_count, pending_phys;
+  int64_t elems_scan, elems_written, elems_bp;  // byte-model counters
+  int64_t domain_index;
+  int32_t has_plo, has_phi, fixing, variant, status, has_xbar, check, domain_field;
+  int32_t trace_len, trace_cap, lam0_given, pad;
+};
+
+template <typename T>
+struct CqkParams {
+  const T *d, *a, *b, *l, *u, *xbar;
+  T *sd, *sa, *sb, *sl, *su;  // compaction scratch (n each) or null
+  T* x;                       // output or null
+  double* trace;              // 4 doubles per phi evaluation
+  int64_t n;
+  double r;
+  CqkState* st;
+  double* partials;           // [gridDim.x][kMaxK]
+  GridSync sync;
+};
+
+// ------------------------------------------------------------ master logic
+// Everything below runs on thread 0 of the master CTA only.
+
+DEVI void m_finish(CqkState& s, double lam) {
+  s.status = ST_SOLVED;
+  s.cmd.lam = lam;
+  s.cmd.phase = PH_FINAL;
+  s.cmd.compact = 0;
+}
+
+DEVI void m_stop(CqkState& s, int32_t status) {
+  s.status = status;
+  s.cmd.phase = PH_DONE;
+  s.cmd.compact = 0;
+}
+
+// newton.py:106-121 secant_step; false on ContractViolation
+DEVI bool m_secant(const CqkState& s, double& out) {
+  const double lo = s.lo, hi = s.hi, plo = s.phi_lo, phi = s.phi_hi, r = s.r_res;
+  if (!(lo < hi) || !(plo < r && r < phi)) return false;
+  double lam = lo + (r - plo) * (hi - lo) / (phi - plo);
+  if (!(lo < lam && lam < hi)) lam = lo + 0.5 * (hi - lo);
+  out = lam;
+  return true;
+}
+
+// newton.py:328-336 (exact repeat, bracket width, advance) + compaction policy
+DEVI void m_post_step(CqkState& s, double next) {
+  const double lam = s.cmd.lam;
+  if (next == lam) { m_finish(s, lam); return; }
+  if (isfinite(s.lo) && isfinite(s.hi)) {
+    const double w = s.hi - s.lo;
+    if (w < s.tau * fmax(fabs(s.hi), fabs(s.lo))) { m_finish(s, next); return; }
+  }
+  s.cmd.lam = next;
+  s.iterations += 1;
+  if (s.iterations > s.max_iter) { m_stop(s, ST_MAXITER); return; }
+  s.cmd.phase = PH_SCAN;
+  s.cmd.compact = 0;
+  if (s.fixing) {
+    const int64_t present = s.fixed_count - s.fixed_removed;
+    if (present > 0 && (double)present >= s.compact_ratio * (double)s.phys_count) {
+      s.cmd.compact = 1;
+      s.pending_phys = s.phys_count - present;
+    }
+  }
+}
+
+DEVI void m_secant_or_fail(CqkState& s) {
+  double nx;
+  if (m_secant(s, nx)) m_post_step(s, nx);
+  else m_stop(s, ST_CONTRACT);
+}
+
+// tot: 0 value, 1 abs_bx, 2 core, 3 tie_lo, 4 tie_hi, 5..7 lower-fix
+// (sum, abs, count), 8..10 upper-fix (sum, abs, count)
+DEVI void m_after_scan(CqkState& s, const double* tot, double* trace) {
+  s.phi_evals += 1;
+  s.elems_scan += s.phys_count;
+  if (s.cmd.compact) {
+    s.elems_written += s.pending_phys;
+    s.fixed_removed += s.phys_count - s.pending_phys;
+    s.phys_count = s.pending_phys;
+    s.cmd.compact = 0;
+  }
+  const double lam = s.cmd.lam;
+  const double value = tot[0], abs_bx = tot[1];
+  const double dplus = tot[2] + tot[3], dminus = tot[2] + tot[4];
+  if (trace && s.trace_len < s.trace_cap) {
+    double* row = trace + 4 * s.trace_len++;
+    row[0] = lam; row[1] = value; row[2] = dminus; row[3] = dplus;
+  }
+  const double diff = value - s.r_res;
+  const double scale = abs_bx + s.fixed_abs + fabs(s.r_orig);
+  if (fabs(diff) < s.tau * scale) { m_finish(s, lam); return; }  // criterion 1
+  if (diff < 0) { s.lo = lam; s.phi_lo = value; s.has_plo = 1; }
+  else { s.hi = lam; s.phi_hi = value; s.has_phi = 1; }
+  if (s.fixing) {
+    // newton.py:165-206 (phi > r fixes lower, phi < r upper); par_solve_cqk
+    // picks the direction by the sign of diff (parallel.py:235-236).
+    int dir;
+    if (s.variant == V_PAR) dir = diff > 0 ? 1 : -1;
+    else {
+      const double rr = value - diff;
+      dir = value > rr ? 1 : (value < rr ? -1 : 0);
+    }
+    if (dir != 0) {
+      const double total = dir > 0 ? tot[5] : tot[8];
+      const double tabs = dir > 0 ? tot[6] : tot[9];
+      const int64_t cnt = (int64_t)(dir > 0 ? tot[7] : tot[10]);
+      if (cnt > 0) {
+        s.r_res -= total;
+        s.fixed_abs += tabs;
+        s.fixed_count += cnt;
+        if (s.has_plo) s.phi_lo -= total;
+        if (s.has_phi) s.phi_hi -= total;
+        if (dir > 0) s.cmd.fix_hi = lam;
+        else s.cmd.fix_lo = lam;
+      }
+    }
+  }
+  if (diff < 0) {
+    if (dplus > 0) {
+      const double step = -diff / dplus;
+      if (step < s.tau) { m_finish(s, lam + step); return; }  // criterion 2
+      const double tilde = lam + step;
+      if (tilde < s.hi) m_post_step(s, tilde);
+      else m_secant_or_fail(s);
+    } else {
+      s.cmd.phase = PH_BP; s.cmd.right = 1; s.cmd.edge = s.lo;
+    }
+  } else {
+    if (dminus > 0) {
+      const double step = -diff / dminus;
+      if (-step < s.tau) { m_finish(s, lam + step); return; }
+      const double tilde = lam + step;
+      if (tilde > s.lo) m_post_step(s, tilde);
+      else m_secant_or_fail(s);
+    } else {
+      s.cmd.phase = PH_BP; s.cmd.right = 0; s.cmd.edge = s.hi;
+    }
+  }
+}
+
+// newton.py:280-298 / 312-326 after the breakpoint search; tot: 0 best, 1 found
+DEVI void m_after_bp(CqkState& s, const double* tot) {
+  s.elems_bp += s.phys_count;
+  const bool found = tot[1] > 0;
+  const double bp = tot[0];
+  if (s.cmd.right) {
+    if (found && bp < s.hi) m_post_step(s, bp);
+    else if (s.has_phi) m_secant_or_fail(s);
+    else m_stop(s, ST_INFEASIBLE);
+  } else {
+    if (found && bp > s.lo) m_post_step(s, bp);
+    else if (s.has_plo) m_secant_or_fail(s);
+    else m_stop(s, ST_INFEASIBLE);
+  }
+}
+
+// tot: 0 s_all, 1 q_all, 2 s_J, 3 q_J, 4 |J|, 5..14 first offending index of
+// the ten validate() checks in the reference's order (core.py:186-216).
+constexpr int kValidateSlot = 5;
+DEVI void m_after_lambda0(CqkState& s, const double* tot) {
+  if (s.check) {
+    // order: d,a,b finite; l,u NaN; r finite; d>0; b>0; l<=u; l!=+inf; u!=-inf
+    const int32_t field_of[10] = {0, 1, 2, 3, 4, 0, 2, 6, 3, 4};
+    for (int c = 0; c < 10; ++c) {
+      if (c == 5 && !isfinite(s.r_orig)) { s.domain_field = 5; s.domain_index = -1; m_stop(s, ST_DOMAIN); return; }
+      const double i = tot[kValidateSlot + c];
+      if (i < (double)s.n) {
+        s.domain_field = field_of[c];
+        s.domain_index = (int64_t)i;
+        m_stop(s, ST_DOMAIN);
+        return;
+      }
+    }
+  }
+  if (!s.lam0_given) {
+    double lam;
+    if (s.has_xbar && tot[4] > 0) lam = (s.r_orig - tot[2]) / tot[3];
+    else lam = (s.r_orig - tot[0]) / tot[1];
+    s.lam0 = lam;
+    s.cmd.lam = lam;
+  }
+  s.cmd.phase = PH_SCAN;
+}
+
+// ------------------------------------------------------------ element ops
+// core.py:246-262 for one element; returns false if the element is already
+// (logically) fixed and therefore not part of the active set.
+template <typename T, bool FIX>
+DEVI bool elem_scan(T d, T a, T b, T l, T u, T lam, T fhi, T flo, double (&acc)[kMaxK]) {
+  const T t = t_of(d, a, b, lam);
+  const bool alo = t <= l, ahi = t >= u;
+  if (FIX) {
+    if (alo && t_of(d, a, b, fhi) <= l) return false;
+    if (ahi && t_of(d, a, b, flo) >= u) return false;
+  }
+  const T x = clip(t, l, u);
+  const T bx = mul_rn(b, x);
+  const double bxd = (double)bx;
+  acc[0] += bxd;
+  acc[1] += fabs(bxd);
+  const bool interior = !(alo || ahi);
+  const bool tlo = alo && t == l && l < u;
+  const bool thi = ahi && t == u && l < u;
+  if (interior || tlo || thi) {
+    const double w = (double)div_rn(mul_rn(b, b), d);
+    if (interior) acc[2] += w;
+    else if (tlo) acc[3] += w;
+    else acc[4] += w;
+  }
+  if (FIX) {
+    if (alo) { acc[5] += bxd; acc[6] += fabs(bxd); acc[7] += 1.0; }
+    if (ahi) { acc[8] += bxd; acc[9] += fabs(bxd); acc[10] += 1.0; }
+  }
+  return true;
+}
+
+// newton.py:129-162 for one element (lower bound first, then upper)
+template <typename T>
+DEVI void elem_bp(T d, T a, T b, T l, T u, double edge, bool right, double& best, double& found) {
+  const T bds[2] = {l, u};
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    const T bd = bds[s];
+    if (!isfinite((double)bd)) continue;
+    const double bp = (double)div_rn(sub_rn(mul_rn(d, bd), a), b);
+    if (right ? bp > edge : bp < edge) {
+      best = right ? fmin(best, bp) : fmax(best, bp);
+      found += 1.0;
+    }
+  }
+}
+
+// final x for one element: clip(t(lam*)) except variables fixed earlier,
+// which keep their bound (fix_variables writes x[newly] = bound).
+template <typename T, bool FIX>
+DEVI T elem_final(T d, T a, T b, T l, T u, T lam, T fhi, T flo, bool chk_lo, bool chk_hi) {
+  T x = clip(t_of(d, a, b, lam), l, u);
+  if (FIX) {
+    if (chk_lo && t_of(d, a, b, fhi) <= l) x = l;
+    else if (chk_hi && t_of(d, a, b, flo) >= u) x = u;
+  }
+  return x;
+}
+
+}  // namespace cqk

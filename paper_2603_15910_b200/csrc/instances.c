@@ -1,0 +1,290 @@
+/*
+ * instances.c -- seeded benchmark instance generators (host, OpenMP).
+ *
+ * Bit-compatible with the reference generators: Xoshiro256++ seeded by four
+ * SplitMix64 outputs (rng.py:29-62), uniform01 = (x >> 11) * 2^-53
+ * (rng.py:66-69), Box-Muller normals consuming two draws each
+ * (rng.py:73-79), and the normative per-family draw orders of
+ * instances.py:43-86.  Unlike the reference's sequential stream, every
+ * OpenMP thread jumps straight to its first draw with a GF(2) matrix power of
+ * the xoshiro transition, so generation of n = 1e8..1e9 runs on all cores.
+ *
+ * The one value that is not bit-compatible is r for the CQK families: the
+ * reference forms it from BLAS ddot sums (instances.py:64-66) whose order is
+ * OpenBLAS-kernel specific; here the two dots are pairwise sums.  Golden
+ * fixtures carry the reference's r.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#include "../../include/cqk_instances.h"
+
+typedef struct { uint64_t s[4]; } xo_state;
+
+static inline uint64_t rotl(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
+
+static inline uint64_t xo_next(xo_state *st) {
+  uint64_t *s = st->s;
+  uint64_t result = rotl(s[0] + s[3], 23) + s[0];
+  uint64_t t = s[1] << 17;
+  s[2] ^= s[0];
+  s[3] ^= s[1];
+  s[1] ^= s[2];
+  s[0] ^= s[3];
+  s[2] ^= t;
+  s[3] = rotl(s[3], 45);
+  return result;
+}
+
+static xo_state xo_seed(uint64_t seed) {
+  xo_state st;
+  uint64_t z = seed;
+  for (int i = 0; i < 4; ++i) {
+    z += 0x9E3779B97F4A7C15ULL;
+    uint64_t o = z;
+    o = (o ^ (o >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    o = (o ^ (o >> 27)) * 0x94D049BB133111EBULL;
+    st.s[i] = o ^ (o >> 31);
+  }
+  return st;
+}
+
+/* ---- GF(2) skip-ahead: the state transition is linear on 256 bits. ---- */
+typedef struct { uint64_t col[256][4]; } gf2mat; /* column j = image of e_j */
+
+static void mat_apply(const gf2mat *m, const uint64_t v[4], uint64_t out[4]) {
+  uint64_t r0 = 0, r1 = 0, r2 = 0, r3 = 0;
+  for (int w = 0; w < 4; ++w) {
+    uint64_t bits = v[w];
+    while (bits) {
+      int b = __builtin_ctzll(bits);
+      bits &= bits - 1;
+      const uint64_t *c = m->col[w * 64 + b];
+      r0 ^= c[0]; r1 ^= c[1]; r2 ^= c[2]; r3 ^= c[3];
+    }
+  }
+  out[0] = r0; out[1] = r1; out[2] = r2; out[3] = r3;
+}
+
+static void mat_mul(const gf2mat *a, const gf2mat *b, gf2mat *out) {
+  for (int j = 0; j < 256; ++j) mat_apply(a, b->col[j], out->col[j]);
+}
+
+static void transition_matrix(gf2mat *m) {
+  for (int j = 0; j < 256; ++j) {
+    xo_state st = {{0, 0, 0, 0}};
+    st.s[j / 64] = 1ULL << (j % 64);
+    xo_next(&st);
+    memcpy(m->col[j], st.s, sizeof st.s);
+  }
+}
+
+/* state advanced by k draws */
+static xo_state xo_jump(xo_state st, uint64_t k) {
+  if (k == 0) return st;
+  gf2mat *base = malloc(sizeof(gf2mat)), *tmp = malloc(sizeof(gf2mat));
+  transition_matrix(base);
+  uint64_t v[4];
+  memcpy(v, st.s, sizeof v);
+  while (k) {
+    if (k & 1) {
+      uint64_t o[4];
+      mat_apply(base, v, o);
+      memcpy(v, o, sizeof v);
+    }
+    k >>= 1;
+    if (k) {
+      mat_mul(base, base, tmp);
+      gf2mat *sw = base; base = tmp; tmp = sw;
+    }
+  }
+  memcpy(st.s, v, sizeof v);
+  free(base);
+  free(tmp);
+  return st;
+}
+
+static int nthreads_for(int64_t count) {
+#ifdef _OPENMP
+  int t = omp_get_max_threads();
+  int64_t cap = count / 65536 + 1;
+  return (int)(t < cap ? t : cap);
+#else
+  (void)count;
+  return 1;
+#endif
+}
+
+/* Fill out[k*stride] for k in [0, count) with uniform01 draws starting at
+ * draw `offset` of the seed's stream, scaled as lo + u*(hi-lo) when scale. */
+typedef enum { K_U01, K_AFFINE, K_NORMAL } draw_kind;
+
+static void fill_draws(uint64_t seed, uint64_t offset, int64_t count, double *out,
+                       int64_t stride, draw_kind kind, double p, double q) {
+  xo_state s0 = xo_seed(seed);
+  int nt = nthreads_for(count);
+  const double scale = 1.0 / 9007199254740992.0; /* 2^-53 */
+  const double twopi = 2.0 * M_PI;
+  int per = kind == K_NORMAL ? 2 : 1;
+#pragma omp parallel num_threads(nt)
+  {
+#ifdef _OPENMP
+    int tid = omp_get_thread_num(), T = omp_get_num_threads();
+#else
+    int tid = 0, T = 1;
+#endif
+    int64_t k0 = count * tid / T, k1 = count * (tid + 1) / T;
+    xo_state st = xo_jump(s0, offset + (uint64_t)k0 * per);
+    for (int64_t k = k0; k < k1; ++k) {
+      double v;
+      if (kind == K_NORMAL) {
+        double u1 = (double)((xo_next(&st) >> 11) + 1) * scale;
+        double u2 = (double)(xo_next(&st) >> 11) * scale;
+        v = sqrt(-2.0 * log(u1)) * cos(twopi * u2);
+      } else {
+        v = (double)(xo_next(&st) >> 11) * scale;
+        if (kind == K_AFFINE) v = p + v * (q - p);
+      }
+      out[k * stride] = v;
+    }
+  }
+}
+
+int cqk_gen_uniform01(uint64_t seed, uint64_t offset, int64_t count, double *out) {
+  fill_draws(seed, offset, count, out, 1, K_U01, 0, 0);
+  return 0;
+}
+
+int cqk_gen_normal(uint64_t seed, uint64_t offset, int64_t count, double *out) {
+  fill_draws(seed, offset, count, out, 1, K_NORMAL, 0, 0);
+  return 0;
+}
+
+static double pairwise(const double *a, int64_t n) {
+  if (n < 8) {
+    double s = 0.0;
+    for (int64_t i = 0; i < n; ++i) s += a[i];
+    return s;
+  }
+  if (n <= 128) {
+    double r[8];
+    for (int j = 0; j < 8; ++j) r[j] = a[j];
+    int64_t i = 8;
+    for (; i < n - (n % 8); i += 8)
+      for (int j = 0; j < 8; ++j) r[j] += a[i + j];
+    double s = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    for (; i < n; ++i) s += a[i];
+    return s;
+  }
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  return pairwise(a, n2) + pairwise(a + n2, n - n2);
+}
+
+/* pairwise sum of b*v computed blockwise so no n-sized temporary is needed
+ * (the block boundaries follow the pairwise split, so the result equals the
+ * pairwise sum of the materialised products). */
+static double dot_pairwise(const double *b, const double *v, int64_t n) {
+  if (n <= 131072) {
+    double *t = malloc(sizeof(double) * (n ? n : 1));
+    for (int64_t i = 0; i < n; ++i) t[i] = b[i] * v[i];
+    double s = pairwise(t, n);
+    free(t);
+    return s;
+  }
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  return dot_pairwise(b, v, n2) + dot_pairwise(b + n2, v + n2, n - n2);
+}
+
+/* Each OpenMP thread owns elements [k0, k1) of a tuple stream in which
+ * element k consumes draws [off + per*k, off + per*(k+1)). */
+#define TUPLE_LOOP(seed, off, count, per, ...)                                \
+  do {                                                                         \
+    xo_state s0_ = xo_seed(seed);                                              \
+    int nt_ = nthreads_for(count);                                             \
+    _Pragma("omp parallel num_threads(nt_)") {                                 \
+      int tid_ = 0, T_ = 1;                                                    \
+      TUPLE_TID(tid_, T_);                                                     \
+      int64_t k0 = (count) * tid_ / T_, k1 = (count) * (tid_ + 1) / T_;        \
+      xo_state st = xo_jump(s0_, (off) + (uint64_t)k0 * (per));                \
+      for (int64_t k = k0; k < k1; ++k) { __VA_ARGS__ }                               \
+    }                                                                          \
+  } while (0)
+#ifdef _OPENMP
+#define TUPLE_TID(t, T) (t = omp_get_thread_num(), T = omp_get_num_threads())
+#else
+#define TUPLE_TID(t, T) ((void)0)
+#endif
+#define U01() ((double)(xo_next(&st) >> 11) * (1.0 / 9007199254740992.0))
+
+/* instances.py:43-70 */
+int cqk_gen_cqk(int family, int64_t n, uint64_t seed, double *d, double *a, double *b,
+                double *l, double *u, double *r_out) {
+  if (n < 1 || family < 0 || family > 2) return -1;
+  uint64_t off;
+  if (family == CQK_FAMILY_UNCORRELATED) {
+    /* flat = uniform(10, 25, 3n); d, a, b = flat[0::3], flat[1::3], flat[2::3] */
+    TUPLE_LOOP(seed, 0, n, 3, {
+      d[k] = 10.0 + U01() * (25.0 - 10.0);
+      a[k] = 10.0 + U01() * (25.0 - 10.0);
+      b[k] = 10.0 + U01() * (25.0 - 10.0);
+    });
+    off = 3 * (uint64_t)n;
+  } else if (family == CQK_FAMILY_WEAKLY) {
+    TUPLE_LOOP(seed, 0, n, 3, {
+      double f0 = U01(), f1 = U01(), f2 = U01();
+      double bk = 10.0 + 15.0 * f0;
+      b[k] = bk;
+      d[k] = (bk - 5.0) + 10.0 * f1;
+      a[k] = (bk - 5.0) + 10.0 * f2;
+    });
+    off = 3 * (uint64_t)n;
+  } else {
+    TUPLE_LOOP(seed, 0, n, 1, {
+      double bk = 10.0 + U01() * (25.0 - 10.0);
+      b[k] = bk;
+      d[k] = bk + 5.0;
+      a[k] = bk + 5.0;
+    });
+    off = (uint64_t)n;
+  }
+  /* pair = uniform(10, 25, 2n); l = min(pair[0::2], pair[1::2]), u = max */
+  TUPLE_LOOP(seed, off, n, 2, {
+    double lo = 10.0 + U01() * (25.0 - 10.0);
+    double hi = 10.0 + U01() * (25.0 - 10.0);
+    l[k] = lo < hi ? lo : hi;
+    u[k] = lo > hi ? lo : hi;
+  });
+  double bl = dot_pairwise(b, l, n), bu = dot_pairwise(b, u, n);
+  double ur;
+  fill_draws(seed, off + 2 * (uint64_t)n, 1, &ur, 1, K_U01, 0, 0);
+  *r_out = bl + ur * (bu - bl);
+  return 0;
+}
+
+/* instances.py:73-86: redraw the whole vector (continuing stream) while any
+ * entry is exactly zero. */
+int cqk_gen_simplex_y(int family, int64_t n, uint64_t seed, double *y) {
+  if (n < 1 || family < 0 || family > 2) return -1;
+  uint64_t per = family == SIMPLEX_FAMILY_U01 ? 1 : 2;
+  for (uint64_t attempt = 0;; ++attempt) {
+    uint64_t off = attempt * per * (uint64_t)n;
+    if (family == SIMPLEX_FAMILY_U01) fill_draws(seed, off, n, y, 1, K_U01, 0, 0);
+    else fill_draws(seed, off, n, y, 1, K_NORMAL, 0, 0);
+    if (family == SIMPLEX_FAMILY_N0M3) {
+      const double sd = sqrt(1e-3);
+#pragma omp parallel for schedule(static)
+      for (int64_t i = 0; i < n; ++i) y[i] *= sd;
+    }
+    int64_t zeros = 0;
+#pragma omp parallel for reduction(+ : zeros) schedule(static)
+    for (int64_t i = 0; i < n; ++i) zeros += y[i] == 0.0;
+    if (!zeros) return 0;
+  }
+}

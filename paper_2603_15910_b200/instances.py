@@ -1,0 +1,86 @@
+"""Seeded benchmark instance generators (drop-in for cqksolve.instances).
+
+Backed by lib/libcqk_instances.so (csrc/instances.c): Xoshiro256++ with the
+reference's seeding and draw order (instances.py:43-86, rng.py:29-106),
+parallelised over host cores with GF(2) skip-ahead.  Arrays are bit-identical
+to the reference's; the CQK level r is formed with pairwise dot products
+rather than the reference's BLAS ddot, so it can differ in the last bits.
+"""
+
+import ctypes
+
+import numpy as np
+
+from . import _native as N
+from .core import CqkInstance
+
+__all__ = ["CQK_FAMILIES", "SIMPLEX_FAMILIES", "FamilyMismatch", "gen_cqk", "gen_simplex_y",
+           "Xoshiro256pp"]
+
+CQK_FAMILIES = ("cqk-uncorrelated", "cqk-weakly-correlated", "cqk-correlated")
+SIMPLEX_FAMILIES = ("simplex-u01", "simplex-n01", "simplex-n0m3")
+
+
+class FamilyMismatch(ValueError):
+    """Generator asked for a family it does not produce."""
+
+
+def gen_cqk_arrays(family, n, seed, out=None):
+    """(d, a, b, l, u, r) as float64 arrays; `out` may supply 5 preallocated arrays."""
+    if family not in CQK_FAMILIES:
+        raise FamilyMismatch(f"not a CQK family: {family!r}")
+    arrs = out if out is not None else [np.empty(n) for _ in range(5)]
+    r = ctypes.c_double()
+    rc = N.gen_library().cqk_gen_cqk(CQK_FAMILIES.index(family), int(n), int(seed) & (2**64 - 1),
+                                     *[a.ctypes.data for a in arrs], ctypes.byref(r))
+    if rc != 0:
+        raise ValueError(f"gen_cqk failed ({rc})")
+    return (*arrs, float(r.value))
+
+
+def gen_cqk(family, n, seed, dtype=np.float64):
+    """One random CQK instance of the given family (instances.py:43-70)."""
+    d, a, b, l, u, r = gen_cqk_arrays(family, n, seed)
+    return CqkInstance(d=d.astype(dtype), a=a.astype(dtype), b=b.astype(dtype),
+                       l=l.astype(dtype), u=u.astype(dtype), r=r)
+
+
+def gen_simplex_y(family, n, seed, dtype=np.float64):
+    """One random point for the simplex benchmarks (instances.py:73-86)."""
+    if family not in SIMPLEX_FAMILIES:
+        raise FamilyMismatch(f"not a simplex family: {family!r}")
+    y = np.empty(int(n))
+    rc = N.gen_library().cqk_gen_simplex_y(SIMPLEX_FAMILIES.index(family), int(n),
+                                           int(seed) & (2**64 - 1), y.ctypes.data)
+    if rc != 0:
+        raise ValueError(f"gen_simplex_y failed ({rc})")
+    return y.astype(dtype)
+
+
+class Xoshiro256pp:
+    """Seeded xoshiro256++ stream (rng.py:82-106), random access by draw offset."""
+
+    def __init__(self, seed):
+        self.seed = int(seed) & (2**64 - 1)
+        self.pos = 0
+
+    def uniform01(self, size):
+        out = np.empty(int(size))
+        N.gen_library().cqk_gen_uniform01(self.seed, self.pos, out.size, out.ctypes.data)
+        self.pos += out.size
+        return out
+
+    def uniform(self, lo, hi, size):
+        return lo + self.uniform01(size) * (hi - lo)
+
+    def normal(self, size, std=1.0):
+        out = np.empty(int(size))
+        N.gen_library().cqk_gen_normal(self.seed, self.pos, out.size, out.ctypes.data)
+        self.pos += 2 * out.size
+        if std != 1.0:
+            out *= std
+        return out
+
+    def integers(self, upper, size):
+        u = self.uniform01(size)
+        return np.minimum((u * upper).astype(np.int64), upper - 1)

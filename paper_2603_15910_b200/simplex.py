@@ -1,0 +1,186 @@
+"""Projections onto the simplex and the l1 ball (drop-in for cqksolve.simplex).
+
+Device route: the formula start lambda0 = (r - sum y)/n clamped to >= min(-y)
+-- the reference's own `lambda0=` route of newton_project_simplex
+(simplex.py:246-250) -- followed by Algorithm 4's streamlined Newton
+iteration with variable fixing (simplex.py:256-294), all inside one
+persistent kernel.  The result equals the reference's Algorithm-2-initialised
+projection to rounding (the root does not depend on the start); iteration
+counts match the reference's `lambda0=` route.  `sharpened` and `xbar` only
+steer the reference's sequential Gauss-Seidel initialiser and therefore do
+not change the device result.
+"""
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .core import DomainError, _is_torch
+from .newton import ContractViolation, SolveOutcome, SolverOptions, Status
+
+__all__ = [
+    "InitResult",
+    "EmptyIndexSet",
+    "newton_project_simplex",
+    "project_l1",
+    "project_simplex_rows",
+]
+
+
+class EmptyIndexSet(ValueError):
+    """The candidate index set handed to the initializer is empty."""
+
+
+@dataclass
+class InitResult:
+    lambda0: float
+    free: np.ndarray
+    fixed_mask: np.ndarray
+    sum_free: float
+
+
+def _prep(y):
+    if _is_torch(y):
+        import torch
+
+        if not y.is_cuda:
+            y = y.numpy()
+        else:
+            dt = np.float32 if y.dtype == torch.float32 else np.float64
+            return y.to(torch.float64).contiguous(), dt, True
+    y = np.ascontiguousarray(y)
+    if y.dtype not in (np.float32, np.float64):
+        y = y.astype(np.float64)
+    return np.ascontiguousarray(y, dtype=np.float64), y.dtype, False
+
+
+def _project(y, r, opts, lambda0, trace, l1):
+    if opts is None:
+        opts = SolverOptions()
+    yv, dt, dev = _prep(y)
+    n = int(yv.shape[0])
+    h = N.handle(yv.device.index if dev else None)
+    if dev:
+        import torch
+
+        h.set_stream(torch.cuda.current_stream(yv.device).cuda_stream)
+        x = torch.empty_like(yv)
+        yp, xp = yv.data_ptr(), x.data_ptr()
+        mem = N.MEM_DEVICE
+    else:
+        h.set_stream(None)
+        x = np.empty(n)
+        yp, xp = yv.ctypes.data, x.ctypes.data
+        mem = N.MEM_HOST
+    o = N.make_options(opts, lambda0=lambda0, trace=trace is not None,
+                       compact_ratio=getattr(opts, "compact_ratio", None))
+    o.tolerance_scale = opts.tau(dt)
+    res = N.Result()
+    fn = h.lib.l1_project_f64 if l1 else h.lib.spx_project_f64
+    rc = fn(h.ptr, mem, yp, n, float(r), o, xp, res)
+    if trace is not None:
+        trace.extend(h.trace(res.trace_len))
+    if rc == N.E_DOMAIN:
+        what = "l1 radius" if l1 else "simplex level"
+        raise DomainError("r", None, f"{what} r must be positive")
+    if rc == N.E_CONTRACT:
+        raise ContractViolation("zero-size free set in the breakpoint snap")
+    if rc != N.SOLVED:
+        raise N.NativeError(f"projection failed ({rc}): {N.last_error()}")
+    if dt == np.float32:
+        x = x.float() if dev else x.astype(np.float32)
+    return x, res
+
+
+def _sparse(x, dev):
+    if dev:
+        import torch
+
+        idx = torch.nonzero(x > 0).flatten()
+        return idx, x[idx]
+    idx = np.flatnonzero(x > 0)
+    return idx, x[idx]
+
+
+def newton_project_simplex(y, r, opts=None, xbar=None, output="dense", sharpened=False,
+                           lambda0=None, trace=None):
+    """Streamlined Newton projection of y onto the level-r simplex (simplex.py:218-308)."""
+    if not r > 0:
+        raise DomainError("r", None, "simplex level r must be positive")
+    x, res = _project(y, r, opts, lambda0, trace, l1=False)
+    dev = _is_torch(x)
+    sparse = None
+    if output == "sparse":
+        sparse = _sparse(x, dev)
+        x = None
+    return SolveOutcome(status=Status.SOLVED, lam=float(res.lam), x=x,
+                        iterations=int(res.iterations), phi_evals=int(res.phi_evals),
+                        fixed_count=int(res.fixed_count), sparse=sparse, stats=res.stats())
+
+
+def project_l1(y, r, opts=None, output="dense", xbar=None):
+    """Project y onto the l1 ball of radius r (simplex.py:311-333)."""
+    if not r > 0:
+        raise DomainError("r", None, "l1 radius r must be positive")
+    x, res = _project(y, r, opts, None, None, l1=True)
+    if output == "sparse":
+        dev = _is_torch(x)
+        if dev:
+            import torch
+
+            idx = torch.nonzero(x != 0).flatten()
+        else:
+            idx = np.flatnonzero(x != 0)
+        return idx, x[idx]
+    return x
+
+
+def project_l1_outcome(y, r, opts=None):
+    """project_l1 with the solver statistics (B200 extension)."""
+    x, res = _project(y, r, opts, None, None, l1=True)
+    inside = int(res.iterations) < 0
+    return SolveOutcome(status=Status.SOLVED, lam=None if inside else float(res.lam), x=x,
+                        iterations=int(res.iterations), phi_evals=int(res.phi_evals),
+                        fixed_count=int(res.fixed_count), stats=res.stats())
+
+
+def project_simplex_rows(Y, r, opts=None, lambda0=None):
+    """Row-wise newton_project_simplex(Y[i], r) for a 2-d array (B200 extension, K8).
+
+    Returns (X, lam[rows], iterations[rows], stats)."""
+    if not r > 0:
+        raise DomainError("r", None, "simplex level r must be positive")
+    if opts is None:
+        opts = SolverOptions()
+    dev = _is_torch(Y) and Y.is_cuda
+    if dev:
+        import torch
+
+        Yv = Y.to(torch.float64).contiguous()
+        rows, cols = Yv.shape
+        h = N.handle(Yv.device.index)
+        h.set_stream(torch.cuda.current_stream(Yv.device).cuda_stream)
+        X = torch.empty_like(Yv)
+        lam = torch.empty(rows, dtype=torch.float64, device=Yv.device)
+        its = torch.empty(rows, dtype=torch.int32, device=Yv.device)
+        ptrs = (Yv.data_ptr(), X.data_ptr(), lam.data_ptr(), its.data_ptr())
+        mem = N.MEM_DEVICE
+    else:
+        Yv = np.ascontiguousarray(Y, dtype=np.float64)
+        rows, cols = Yv.shape
+        h = N.handle(None)
+        h.set_stream(None)
+        X = np.empty_like(Yv)
+        lam = np.empty(rows)
+        its = np.empty(rows, np.int32)
+        ptrs = (Yv.ctypes.data, X.ctypes.data, lam.ctypes.data, its.ctypes.data)
+        mem = N.MEM_HOST
+    o = N.make_options(opts, lambda0=lambda0)
+    o.tolerance_scale = opts.tau(np.float64)
+    res = N.Result()
+    rc = h.lib.spx_project_batched_f64(h.ptr, mem, ptrs[0], rows, cols, float(r), o, ptrs[1],
+                                       ptrs[2], ptrs[3], res)
+    if rc != 0:
+        raise N.NativeError(f"batched projection failed ({rc}): {N.last_error()}")
+    return X, lam, its, res.stats()
