@@ -93,9 +93,15 @@ const char *cqk_last_error(void);
    persistent-kernel state.  A handle is not re-entrant. */
 int cqk_create(cqk_handle **out, int device);
 int cqk_destroy(cqk_handle *h);
-/* Run subsequent work on `stream` (cudaStream_t); NULL = the handle's own. */
+/* Run subsequent work on `stream` (cudaStream_t; cudaStreamLegacy = 0x1 is
+   accepted); NULL = the handle's own non-blocking stream. */
 int cqk_set_stream(cqk_handle *h, void *stream);
 int cqk_device_info(cqk_handle *h, int32_t *sm_count, int32_t *ctas, int32_t *threads);
+/* Per-pass device timeline of the last persistent solve: rows of 4 int64
+   {phase, elements streamed, compacted, globaltimer ns}; row 0 = kernel start,
+   row e = end of grid epoch e (phase -1 start, 0 lambda0/init, 1 scan, 2
+   breakpoint, 6 snap).  Returns rows copied. */
+int cqk_get_timeline(cqk_handle *h, long long *out, int32_t max_rows);
 /* Copy the last solve's per-evaluation trace rows (4 doubles each). */
 int cqk_get_trace(cqk_handle *h, double *out, int32_t max_rows);
 
@@ -148,6 +154,13 @@ int l1_project_f64(cqk_handle *h, int mem, const double *y, int64_t n, double r,
 int spx_project_batched_f64(cqk_handle *h, int mem, const double *Y, int64_t rows,
                             int64_t cols, double r, const cqk_options *opts, double *X,
                             double *lam, int32_t *iters, cqk_result *res);
+
+/* Diagnostics ------------------------------------------------------------------ */
+/* Bitwise check of the solver's shared-reciprocal division against the IEEE
+   library division on `count` random operand pairs (mode 0: exponents in
+   [-500, 500]; 1: solver-like ranges; 2: quotients at rounding boundaries). */
+int cqk_selftest_division(cqk_handle *h, uint64_t seed, int64_t count, int mode,
+                          uint64_t *mismatches, double *example2);
 
 #ifdef __cplusplus
 }

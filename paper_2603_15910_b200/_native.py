@@ -82,9 +82,9 @@ class Result(ctypes.Structure):
 # Every symbol declared in include/cqk_b200.h (checked by the CPU tests).
 EXPORTS = (
     "cqk_abi_version", "cqk_last_error", "cqk_create", "cqk_destroy", "cqk_set_stream",
-    "cqk_device_info", "cqk_get_trace", "cqk_validate_f64", "cqk_initial_multiplier_f64",
+    "cqk_device_info", "cqk_get_trace", "cqk_get_timeline", "cqk_validate_f64", "cqk_initial_multiplier_f64",
     "cqk_phi_f64", "cqk_eval_x_f64", "cqk_nearest_breakpoint_f64", "cqk_solve_f64",
-    "spx_project_f64", "l1_project_f64", "spx_project_batched_f64",
+    "spx_project_f64", "l1_project_f64", "spx_project_batched_f64", "cqk_selftest_division",
 )
 
 _lib = None
@@ -109,6 +109,7 @@ def _declare(L):
     L.cqk_device_info.argtypes = [_P, ctypes.POINTER(_I32), ctypes.POINTER(_I32),
                                   ctypes.POINTER(_I32)]
     L.cqk_get_trace.argtypes = [_P, _P, _I32]
+    L.cqk_get_timeline.argtypes = [_P, _P, _I32]
     arr5 = [_P] * 5
     L.cqk_validate_f64.argtypes = [_P, ctypes.c_int, *arr5, _I64, _D, _RES]
     L.cqk_initial_multiplier_f64.argtypes = [_P, ctypes.c_int, *arr5, _I64, _D, _P,
@@ -121,6 +122,8 @@ def _declare(L):
     L.cqk_solve_f64.argtypes = [_P, ctypes.c_int, *arr5, _I64, _D, _OPT, _P, _P, _RES]
     L.spx_project_f64.argtypes = [_P, ctypes.c_int, _P, _I64, _D, _OPT, _P, _RES]
     L.l1_project_f64.argtypes = [_P, ctypes.c_int, _P, _I64, _D, _OPT, _P, _RES]
+    L.cqk_selftest_division.argtypes = [_P, ctypes.c_uint64, _I64, ctypes.c_int,
+                                        ctypes.POINTER(ctypes.c_uint64), _P]
     L.spx_project_batched_f64.argtypes = [_P, ctypes.c_int, _P, _I64, _I64, _D, _OPT, _P, _P,
                                           _P, _RES]
 
@@ -179,7 +182,9 @@ class Handle:
         self.lib = L
 
     def set_stream(self, stream_ptr):
-        self.lib.cqk_set_stream(self.ptr, _P(stream_ptr) if stream_ptr else None)
+        """Bind to a cudaStream_t; 0 (torch's default stream) maps to
+        cudaStreamLegacy so work stays ordered with the caller's stream."""
+        self.lib.cqk_set_stream(self.ptr, _P(stream_ptr if stream_ptr else 1))
 
     def info(self):
         sm, ctas, thr = _I32(), _I32(), _I32()
@@ -190,6 +195,12 @@ class Handle:
         out = np.zeros((max(rows, 1), 4))
         got = self.lib.cqk_get_trace(self.ptr, out.ctypes.data, int(rows))
         return [tuple(float(v) for v in row) for row in out[: max(got, 0)]]
+
+    def timeline(self, rows=64):
+        """Per-pass device timeline of the last persistent solve (see cqk_b200.h)."""
+        out = np.zeros((rows, 4), dtype=np.int64)
+        got = self.lib.cqk_get_timeline(self.ptr, out.ctypes.data, int(rows))
+        return out[: max(got, 0)]
 
     def __del__(self):
         try:

@@ -193,13 +193,12 @@ class Marshal:
             self.mem = N.MEM_HOST
 
     def handle(self):
-        h = N.handle(self.device)
-        if self.torch:
-            import torch
+        """Handle bound to torch's current stream on the target device, so
+        callers can order and time solves with ordinary torch events."""
+        import torch
 
-            h.set_stream(torch.cuda.current_stream(self.device).cuda_stream)
-        else:
-            h.set_stream(None)
+        h = N.handle(self.device)
+        h.set_stream(torch.cuda.current_stream(h.device).cuda_stream)
         return h
 
     def empty(self, n):

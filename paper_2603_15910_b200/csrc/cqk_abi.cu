@@ -8,6 +8,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <mutex>
@@ -68,6 +69,7 @@ struct cqk_handle {
   void* state = nullptr;     // CqkState / SpxState
   double* partials = nullptr;
   double* trace = nullptr;
+  long long* timeline = nullptr;
   double* red = nullptr;     // utility partials
   double* out = nullptr;     // utility outputs (kMaxK doubles)
   Buf scratch, stage, idxbuf, flags;
@@ -122,6 +124,7 @@ int cqk_create(cqk_handle** out, int device) {
   e = e ? e : cudaMalloc(&h->state, st_bytes);
   e = e ? e : cudaMalloc(&h->partials, sizeof(double) * kMaxK * (gmax + kUtilBlocksMax));
   e = e ? e : cudaMalloc(&h->trace, sizeof(double) * 4 * kTraceCap);
+  e = e ? e : cudaMalloc(&h->timeline, sizeof(long long) * 4 * kTimelineCap);
   e = e ? e : cudaMalloc(&h->red, sizeof(double) * kMaxK * kUtilBlocksMax);
   e = e ? e : cudaMalloc(&h->out, sizeof(double) * kMaxK);
   e = e ? e : cudaEventCreate(&h->ev0);
@@ -148,6 +151,7 @@ int cqk_destroy(cqk_handle* h) {
   cudaFree(h->state);
   cudaFree(h->partials);
   cudaFree(h->trace);
+  cudaFree(h->timeline);
   cudaFree(h->red);
   cudaFree(h->out);
   if (h->ev0) cudaEventDestroy(h->ev0);
@@ -169,6 +173,14 @@ int cqk_device_info(cqk_handle* h, int32_t* sm_count, int32_t* ctas, int32_t* th
   if (ctas) *ctas = h->grid_cqk_fix;
   if (threads) *threads = kThreads;
   return 0;
+}
+
+int cqk_get_timeline(cqk_handle* h, long long* out, int32_t max_rows) {
+  if (!h || !out) return set_err(CQK_E_ARG, "null argument");
+  cudaSetDevice(h->device);
+  int rows = max_rows < kTimelineCap ? max_rows : kTimelineCap;
+  CUDA_TRY(cudaMemcpy(out, h->timeline, sizeof(long long) * 4 * rows, cudaMemcpyDeviceToHost));
+  return rows;
 }
 
 int cqk_get_trace(cqk_handle* h, double* out, int32_t max_rows) {
@@ -226,6 +238,14 @@ int stage_inputs(cqk_handle* h, int mem, int64_t n, const T* const* in, int coun
 }
 
 bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+// L2 bulk-prefetch distance (chunks) for the persistent kernels; tunable via
+// CQK_PREFETCH="cqk,y" for measurement sweeps.
+cudaError_t set_prefetch(cudaStream_t s) {
+  int pf[2] = {0, 2};
+  if (const char* e = getenv("CQK_PREFETCH")) sscanf(e, "%d,%d", &pf[0], &pf[1]);
+  return cudaMemcpyToSymbolAsync(c_prefetch, pf, sizeof pf, 0, cudaMemcpyHostToDevice, s);
+}
 
 int finish_sync(cqk_handle* h) {
   cudaError_t e = cudaStreamSynchronize(h->stream);
@@ -339,6 +359,7 @@ extern "C" int cqk_solve_f64(cqk_handle* h, int mem, const double* d, const doub
     CUDA_TRY(h->scratch.ensure(per * 5));
   }
   CUDA_TRY(cudaMemcpyAsync(h->state, &s, sizeof s, cudaMemcpyHostToDevice, h->stream));
+  CUDA_TRY(set_prefetch(h->stream));
   CqkParams<double> p;
   std::memset(&p, 0, sizeof p);
   p.d = dv[0]; p.a = dv[1]; p.b = dv[2]; p.l = dv[3]; p.u = dv[4]; p.xbar = xbar ? dv[5] : nullptr;
@@ -357,6 +378,7 @@ extern "C" int cqk_solve_f64(cqk_handle* h, int mem, const double* d, const doub
   p.sync.arrive = h->sync;
   p.sync.gen = h->sync + 1;
   p.sync.error = (int*)(h->sync + 2);
+  p.sync.timeline = h->timeline;
   void* args[] = {&p};
   const int grid = fixing ? h->grid_cqk_fix : h->grid_cqk_jac;
   const void* fn = fixing ? (const void*)cqk_solve_kernel<double, true>
@@ -447,6 +469,7 @@ int spx_common(cqk_handle* h, int mem, const double* y, int64_t n, double r,
   s.compact_ratio = std::isnan(opts.compact_ratio) ? 0.25 : opts.compact_ratio;
   if (fixing) CUDA_TRY(h->scratch.ensure(((size_t)n * sizeof(double) + 255) / 256 * 256));
   CUDA_TRY(cudaMemcpyAsync(h->state, &s, sizeof s, cudaMemcpyHostToDevice, h->stream));
+  CUDA_TRY(set_prefetch(h->stream));
   SpxParams<double> p;
   std::memset(&p, 0, sizeof p);
   p.y = yv;
@@ -459,6 +482,7 @@ int spx_common(cqk_handle* h, int mem, const double* y, int64_t n, double r,
   p.sync.arrive = h->sync;
   p.sync.gen = h->sync + 1;
   p.sync.error = (int*)(h->sync + 2);
+  p.sync.timeline = h->timeline;
   void* args[] = {&p};
   const int grid = l1 ? h->grid_l1 : h->grid_spx;
   const void* fn = l1 ? (const void*)spx_solve_kernel<double, true>
@@ -746,5 +770,28 @@ extern "C" int cqk_validate_f64(cqk_handle* h, int mem, const double* d, const d
       return CQK_E_DOMAIN;
     }
   }
+  return 0;
+}
+
+// ------------------------------------------------------------ self-test
+extern "C" int cqk_selftest_division(cqk_handle* h, uint64_t seed, int64_t count, int mode,
+                                     uint64_t* mismatches, double* example2) {
+  if (!h || !mismatches) return set_err(CQK_E_ARG, "null argument");
+  CUDA_TRY(cudaSetDevice(h->device));
+  unsigned long long* dm = nullptr;
+  double* dex = nullptr;
+  CUDA_TRY(cudaMalloc(&dm, sizeof(unsigned long long) + 2 * sizeof(double)));
+  dex = (double*)(dm + 1);
+  cudaMemsetAsync(dm, 0, sizeof(unsigned long long) + 2 * sizeof(double), h->stream);
+  div_selftest_kernel<<<h->sm_count * 8, 256, 0, h->stream>>>(seed, count, mode, dm, dex);
+  unsigned long long m = 0;
+  double ex[2] = {0, 0};
+  cudaMemcpyAsync(&m, dm, sizeof m, cudaMemcpyDeviceToHost, h->stream);
+  cudaMemcpyAsync(ex, dex, sizeof ex, cudaMemcpyDeviceToHost, h->stream);
+  cudaError_t e = cudaStreamSynchronize(h->stream);
+  cudaFree(dm);
+  if (e != cudaSuccess) return set_err(CQK_E_CUDA, cudaGetErrorString(e));
+  *mismatches = m;
+  if (example2) { example2[0] = ex[0]; example2[1] = ex[1]; }
   return 0;
 }

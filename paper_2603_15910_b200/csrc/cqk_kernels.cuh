@@ -11,28 +11,58 @@ namespace cqk {
 // loads; the ragged tail uses guarded scalar loads with a neutral fill.
 constexpr int kUnroll = 2;
 
-template <typename T, bool SCRATCH>
+constexpr int kUnrollY = 8;  // single-array passes: 8 x 16 B in flight per lane
+
+template <typename T, bool SCRATCH, int UNR = kUnroll>
 DEVI void load_chunk(const T* p, int64_t base, int64_t m, int lane, bool full, T fill,
-                     T (&out)[Vec<T>::n * kUnroll]) {
+                     T (&out)[Vec<T>::n * UNR]) {
   using V = typename Vec<T>::type;
   constexpr int VN = Vec<T>::n;
   if (full) {
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
+    for (int u = 0; u < UNR; ++u) {
       const V* q = reinterpret_cast<const V*>(p + base + (int64_t)u * 32 * VN + lane * VN);
       V v = SCRATCH ? ld_scratch(q) : ld_stream(q);
       unpack<V, T>(v, &out[u * VN]);
     }
   } else {
 #pragma unroll
-    for (int j = 0; j < VN * kUnroll; ++j) {
+    for (int j = 0; j < VN * UNR; ++j) {
       const int64_t e = base + (int64_t)(j / VN) * 32 * VN + lane * VN + (j % VN);
       out[j] = e < m ? (SCRATCH ? ld_scratch(p + e) : ld_stream(p + e)) : fill;
     }
   }
 }
 
-template <typename T>
+// Memory-level parallelism without registers: each warp keeps c_prefetch[0]
+// chunks of every streamed array in flight into L2 with bulk prefetches
+// (cp.async.bulk.prefetch.L2, one instruction per array-chunk, issued by
+// distinct lanes), so the vector loads of a chunk mostly hit L2.
+// [0]: chunks ahead for the 3..5-array CQK passes, [1]: for the single-array
+// simplex / l1 passes (set per launch by the ABI; CQK_PREFETCH env override).
+__constant__ int c_prefetch[2];
+
+DEVI void bulk_prefetch_l2(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// Prefetch chunks [c0, c0 + nchunk) of NARR arrays (chunk = CH elements of T)
+// of a segment of m elements; lane k handles (array k % NARR, chunk k / NARR).
+template <typename T, int NARR, int UNR = kUnroll>
+DEVI void prefetch_chunks(const T* const (&arr)[NARR], int64_t c0, int nchunk, int64_t m,
+                          int lane) {
+  constexpr int CH = 32 * Vec<T>::n * UNR;
+  if (nchunk > 0 && lane < NARR * nchunk) {
+    const int64_t e = (c0 + lane / NARR) * CH;
+    if (e < m) {
+      const int64_t cnt = m - e < CH ? m - e : CH;
+      const unsigned bytes = (unsigned)(cnt * sizeof(T)) & ~15u;
+      if (bytes) bulk_prefetch_l2(arr[lane % NARR] + e, bytes);
+    }
+  }
+}
+
+template <typename T, int UNR = kUnroll>
 DEVI int64_t chunk_index(int64_t base, int lane, int j) {
   constexpr int VN = Vec<T>::n;
   return base + (int64_t)(j / VN) * 32 * VN + lane * VN + (j % VN);
@@ -52,23 +82,35 @@ DEVI void load_l2(S* dst, const S* src) {
 }
 
 // ------------------------------------------------------------ barrier
-// Every CTA publishes partials[blockIdx.x][0..K); the last CTA to arrive
-// reduces them in a fixed order into s_tot and returns true (it is the
-// master for this epoch).  Call master_release() after the master work.
+// Fixed-master grid step: CTA 0 owns the solver state in shared memory for
+// the whole kernel.  Every CTA publishes partials[blockIdx.x][0..K) and
+// arrives; CTA 0 waits for all arrivals, reduces the rows in a fixed order
+// into s_tot (deterministic, no float atomics) and returns true; the caller
+// then runs the state machine and master_release()s the others, which wait
+// in wait_release() and pick up the new command with one L2 round trip.
 template <int K>
-DEVI bool arrive_and_reduce(double* partials, const double* s_cta, const int (&ops)[K],
-                            const GridSync& sy, double (*s_red)[kMaxK], double* s_tot,
-                            int* s_flag) {
+DEVI bool grid_step(double* partials, const double* s_cta, const int (&ops)[K],
+                    const GridSync& sy, double (*s_red)[kMaxK], double* s_tot, int* s_abort) {
   if (threadIdx.x < K) partials[(int64_t)blockIdx.x * kMaxK + threadIdx.x] = s_cta[threadIdx.x];
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    const unsigned prev = atomicAdd(sy.arrive, 1u);
-    *s_flag = prev == gridDim.x - 1;
+    atomicAdd(sy.arrive, 1u);
+  }
+  if (blockIdx.x != 0) return false;
+  if (threadIdx.x == 0) {
+    const unsigned long long t0 = globaltimer();
+    while (ld_acquire(sy.arrive) < gridDim.x) {
+      if (globaltimer() - t0 > kSpinTimeoutNs) {
+        atomicExch(sy.error, 1);
+        *s_abort = 1;
+        break;
+      }
+    }
+    if (!*s_abort) *sy.arrive = 0u;  // nobody arrives again before the release
   }
   __syncthreads();
-  if (!*s_flag) return false;
-  __threadfence();
+  if (*s_abort) return false;
   double acc[K];
 #pragma unroll
   for (int k = 0; k < K; ++k)
@@ -84,25 +126,32 @@ DEVI bool arrive_and_reduce(double* partials, const double* s_cta, const int (&o
   return true;
 }
 
-DEVI void master_release(const GridSync& sy, unsigned target) {
-  if (threadIdx.x == 0) {
-    __threadfence();
-    *sy.arrive = 0u;
-    __threadfence();
-    st_release(sy.gen, target);
-  }
+// Master (CTA 0, thread 0): publish the next command and release the grid.
+DEVI void master_release(const GridSync& sy, unsigned target, const Cmd& cmd, Cmd* gcmd) {
+  const unsigned long long* s = reinterpret_cast<const unsigned long long*>(&cmd);
+  unsigned long long* d = reinterpret_cast<unsigned long long*>(gcmd);
+#pragma unroll
+  for (int i = 0; i < (int)(sizeof(Cmd) / 8); ++i) __stcg(d + i, s[i]);
+  __threadfence();
+  st_release(sy.gen, target);
 }
 
-// returns false on timeout
-DEVI bool wait_release(const GridSync& sy, unsigned target) {
+// Non-master CTAs (thread 0): wait for the release, then fetch the command.
+DEVI bool wait_release(const GridSync& sy, unsigned target, const Cmd* gcmd, Cmd* out) {
   const unsigned long long t0 = globaltimer();
   while ((int)(ld_acquire(sy.gen) - target) < 0) {
     if (globaltimer() - t0 > kSpinTimeoutNs) {
       atomicExch(sy.error, 1);
       return false;
     }
-    __nanosleep(64);
   }
+  const unsigned long long* s = reinterpret_cast<const unsigned long long*>(gcmd);
+  unsigned long long w[sizeof(Cmd) / 8];
+#pragma unroll
+  for (int i = 0; i < (int)(sizeof(Cmd) / 8); ++i) w[i] = __ldcg(s + i);
+  unsigned long long* d = reinterpret_cast<unsigned long long*>(out);
+#pragma unroll
+  for (int i = 0; i < (int)(sizeof(Cmd) / 8); ++i) d[i] = w[i];
   return true;
 }
 
@@ -112,7 +161,13 @@ template <typename T, bool CHECK, bool XBAR>
 DEVI void lambda0_pass(const CqkParams<T>& p, int64_t seg_lo, int64_t m, double (&acc)[kMaxK]) {
   constexpr int E = Vec<T>::n * kUnroll, CH = 32 * E;
   const int lane = threadIdx.x & 31;
+  const T* const pf[5] = {p.d + seg_lo, p.a + seg_lo, p.b + seg_lo, p.l + seg_lo, p.u + seg_lo};
+  const T* const pf3[3] = {pf[0], pf[1], pf[2]};
+  if (CHECK || XBAR) prefetch_chunks<T, 5>(pf, 0, c_prefetch[0], m, lane);
+  else prefetch_chunks<T, 3>(pf3, 0, c_prefetch[0], m, lane);
   for (int64_t base = 0; base < m; base += CH) {
+    if (CHECK || XBAR) prefetch_chunks<T, 5>(pf, base / CH + c_prefetch[0], c_prefetch[0] > 0 ? 1 : 0, m, lane);
+    else prefetch_chunks<T, 3>(pf3, base / CH + c_prefetch[0], c_prefetch[0] > 0 ? 1 : 0, m, lane);
     const bool full = base + CH <= m;
     T D[E], A[E], B[E], L[E], U[E], X[E];
     load_chunk<T, false>(p.d + seg_lo, base, m, lane, full, T(1), D);
@@ -127,8 +182,9 @@ DEVI void lambda0_pass(const CqkParams<T>& p, int64_t seg_lo, int64_t m, double 
     for (int j = 0; j < E; ++j) {
       const int64_t e = chunk_index<T>(base, lane, j);
       if (!full && e >= m) continue;
-      const double s = (double)mul_rn(B[j], div_rn(A[j], D[j]));
-      const double q = (double)mul_rn(B[j], div_rn(B[j], D[j]));
+      const T y = rcp_nr(D[j]);
+      const double s = (double)mul_rn(B[j], A[j] * y);
+      const double q = (double)mul_rn(B[j], B[j] * y);
       acc[0] += s;
       acc[1] += q;
       if (XBAR && L[j] < X[j] && X[j] < U[j]) { acc[2] += s; acc[3] += q; acc[4] += 1.0; }
@@ -161,9 +217,13 @@ DEVI void scan_pass(const CqkParams<T>& p, const Cmd& c, int64_t seg_lo, int64_t
   const T* sl = (SRC_SCRATCH ? p.sl : p.l) + seg_lo;
   const T* su = (SRC_SCRATCH ? p.su : p.u) + seg_lo;
   const T lam = (T)c.lam, fhi = (T)c.fix_hi, flo = (T)c.fix_lo;
+  const bool chk_lo = FIX && isfinite(c.fix_hi), chk_hi = FIX && isfinite(c.fix_lo);
   const unsigned lt = (1u << lane) - 1u;
+  const T* const pf[5] = {sd, sa, sb, sl, su};
+  prefetch_chunks<T, 5>(pf, 0, c_prefetch[0], m, lane);
   int64_t out_m = 0;
   for (int64_t base = 0; base < m; base += CH) {
+    prefetch_chunks<T, 5>(pf, base / CH + c_prefetch[0], c_prefetch[0] > 0 ? 1 : 0, m, lane);
     const bool full = base + CH <= m;
     T D[E], A[E], B[E], L[E], U[E];
     load_chunk<T, SRC_SCRATCH>(sd, base, m, lane, full, T(1), D);
@@ -175,7 +235,8 @@ DEVI void scan_pass(const CqkParams<T>& p, const Cmd& c, int64_t seg_lo, int64_t
 #pragma unroll
     for (int j = 0; j < E; ++j) {
       const bool valid = full || chunk_index<T>(base, lane, j) < m;
-      keep[j] = valid && elem_scan<T, FIX>(D[j], A[j], B[j], L[j], U[j], lam, fhi, flo, acc);
+      keep[j] = valid && elem_scan<T, FIX>(D[j], A[j], B[j], L[j], U[j], lam, fhi, flo, chk_lo,
+                                           chk_hi, acc);
     }
     if (FIX && compact) {
       // warp-ballot stream compaction into this warp's own scratch range;
@@ -206,7 +267,10 @@ DEVI void bp_pass(const CqkParams<T>& p, const Cmd& c, bool fix, int64_t seg_lo,
   const T* su = (SRC_SCRATCH ? p.su : p.u) + seg_lo;
   const T lam = (T)c.lam, fhi = (T)c.fix_hi, flo = (T)c.fix_lo;
   const bool right = c.right != 0;
+  const T* const pf[5] = {sd, sa, sb, sl, su};
+  prefetch_chunks<T, 5>(pf, 0, c_prefetch[0], m, lane);
   for (int64_t base = 0; base < m; base += CH) {
+    prefetch_chunks<T, 5>(pf, base / CH + c_prefetch[0], c_prefetch[0] > 0 ? 1 : 0, m, lane);
     const bool full = base + CH <= m;
     T D[E], A[E], B[E], L[E], U[E];
     load_chunk<T, SRC_SCRATCH>(sd, base, m, lane, full, T(1), D);
@@ -218,9 +282,10 @@ DEVI void bp_pass(const CqkParams<T>& p, const Cmd& c, bool fix, int64_t seg_lo,
     for (int j = 0; j < E; ++j) {
       if (!full && chunk_index<T>(base, lane, j) >= m) continue;
       if (fix) {  // only the logically active set takes part
-        const T t = t_of(D[j], A[j], B[j], lam);
-        if (t <= L[j] && t_of(D[j], A[j], B[j], fhi) <= L[j]) continue;
-        if (t >= U[j] && t_of(D[j], A[j], B[j], flo) >= U[j]) continue;
+        const T yd = rcp_div(D[j]);
+        const T t = t_of_y(D[j], A[j], B[j], lam, yd);
+        if (isfinite(c.fix_hi) && t <= L[j] && t_of_y(D[j], A[j], B[j], fhi, yd) <= L[j]) continue;
+        if (isfinite(c.fix_lo) && t >= U[j] && t_of_y(D[j], A[j], B[j], flo, yd) >= U[j]) continue;
       }
       elem_bp<T>(D[j], A[j], B[j], L[j], U[j], c.edge, right, acc[0], acc[1]);
     }
@@ -237,7 +302,10 @@ DEVI void final_pass(const CqkParams<T>& p, const Cmd& c, int64_t seg_lo, int64_
   // fixing multiplier (the criterion-2 finish(lam + step) edge)
   const bool chk_lo = FIX && c.lam > c.fix_hi, chk_hi = FIX && c.lam < c.fix_lo;
   T* x = p.x + seg_lo;
+  const T* const pf[5] = {p.d + seg_lo, p.a + seg_lo, p.b + seg_lo, p.l + seg_lo, p.u + seg_lo};
+  prefetch_chunks<T, 5>(pf, 0, c_prefetch[0], m, lane);
   for (int64_t base = 0; base < m; base += CH) {
+    prefetch_chunks<T, 5>(pf, base / CH + c_prefetch[0], c_prefetch[0] > 0 ? 1 : 0, m, lane);
     const bool full = base + CH <= m;
     T D[E], A[E], B[E], L[E], U[E];
     load_chunk<T, false>(p.d + seg_lo, base, m, lane, full, T(1), D);
@@ -274,10 +342,11 @@ __global__ void __launch_bounds__(kThreads, 1) cqk_solve_kernel(CqkParams<T> p) 
   __shared__ double s_red[kWarps][kMaxK];
   __shared__ double s_tot[kMaxK];
   __shared__ Cmd s_cmd;
-  __shared__ int s_flag;
+  __shared__ CqkState s_st;  // master (CTA 0) only
   __shared__ unsigned s_gen0;
   __shared__ int s_abort;
   const int warp = threadIdx.x >> 5;
+  const bool master = blockIdx.x == 0;
   const int64_t gw = (int64_t)blockIdx.x * kWarps + warp, W = (int64_t)gridDim.x * kWarps;
   int64_t seg_lo, seg_hi;
   warp_segment(p.n, gw, W, seg_lo, seg_hi);
@@ -285,11 +354,18 @@ __global__ void __launch_bounds__(kThreads, 1) cqk_solve_kernel(CqkParams<T> p) 
   bool in_scratch = false;
   if (threadIdx.x == 0) {
     s_gen0 = ld_acquire(p.sync.gen);
-    load_l2(&s_cmd, &p.st->cmd);
     s_abort = 0;
+    if (master) {
+      s_st = *p.st;  // host-initialised before the launch
+      s_cmd = s_st.cmd;
+      tl_record(p.sync, 0, -1, p.n, 0);
+    } else {
+      load_l2(&s_cmd, &p.st->cmd);
+    }
   }
   __syncthreads();
   const int has_xbar = p.xbar != nullptr;
+  const int check = p.st->check;  // immutable during the solve
   for (unsigned epoch = 1;; ++epoch) {
     const Cmd c = s_cmd;
     if (c.phase == PH_DONE || s_abort) break;
@@ -300,10 +376,10 @@ __global__ void __launch_bounds__(kThreads, 1) cqk_solve_kernel(CqkParams<T> p) 
     double acc[kMaxK];
 #pragma unroll
     for (int k = 0; k < kMaxK; ++k) acc[k] = 0.0;
+    bool is_master = false;
     if (c.phase == PH_LAMBDA0) {
 #pragma unroll
       for (int k = kValidateSlot; k < kValidateSlot + 10; ++k) acc[k] = HUGE_VAL;
-      const int check = p.st->check;  // immutable during the solve
       const int64_t m0 = seg_hi - seg_lo;
       if (check && has_xbar) lambda0_pass<T, true, true>(p, seg_lo, m0, acc);
       else if (check) lambda0_pass<T, true, false>(p, seg_lo, m0, acc);
@@ -315,14 +391,10 @@ __global__ void __launch_bounds__(kThreads, 1) cqk_solve_kernel(CqkParams<T> p) 
 #pragma unroll
       for (int k = 0; k < 15; ++k) a15[k] = acc[k];
       block_reduce<15>(a15, ops, s_red, s_tot);
-      if (arrive_and_reduce<15>(p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_flag)) {
-        if (threadIdx.x == 0) {
-          CqkState s;
-          load_l2(&s, p.st);
-          m_after_lambda0(s, s_tot);
-          *p.st = s;
-        }
-        master_release(p.sync, s_gen0 + epoch);
+      is_master = grid_step<15>(p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort);
+      if (is_master && threadIdx.x == 0) {
+        tl_record(p.sync, epoch, PH_LAMBDA0, s_st.n, 0);
+        m_after_lambda0(s_st, s_tot);
       }
     } else if (c.phase == PH_SCAN) {
       const bool compact = FIX && c.compact;
@@ -335,17 +407,13 @@ __global__ void __launch_bounds__(kThreads, 1) cqk_solve_kernel(CqkParams<T> p) 
 #pragma unroll
       for (int k = 0; k < K; ++k) { ops[k] = OP_SUM; aK[k] = acc[k]; }
       block_reduce<K>(aK, ops, s_red, s_tot);
-      if (arrive_and_reduce<K>(p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_flag)) {
-        if (threadIdx.x == 0) {
-          CqkState s;
-          load_l2(&s, p.st);
-          double tot[11];
+      is_master = grid_step<K>(p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort);
+      if (is_master && threadIdx.x == 0) {
+        double tot[11];
 #pragma unroll
-          for (int k = 0; k < 11; ++k) tot[k] = k < K ? s_tot[k] : 0.0;
-          m_after_scan(s, tot, p.trace);
-          *p.st = s;
-        }
-        master_release(p.sync, s_gen0 + epoch);
+        for (int k = 0; k < 11; ++k) tot[k] = k < K ? s_tot[k] : 0.0;
+        tl_record(p.sync, epoch, PH_SCAN, s_st.phys_count, s_st.cmd.compact);
+        m_after_scan(s_st, tot, p.trace);
       }
     } else if (c.phase == PH_BP) {
       acc[0] = c.right ? HUGE_VAL : -HUGE_VAL;
@@ -354,23 +422,24 @@ __global__ void __launch_bounds__(kThreads, 1) cqk_solve_kernel(CqkParams<T> p) 
       int ops[2] = {c.right ? OP_MIN : OP_MAX, OP_SUM};
       double a2[2] = {acc[0], acc[1]};
       block_reduce<2>(a2, ops, s_red, s_tot);
-      if (arrive_and_reduce<2>(p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_flag)) {
-        if (threadIdx.x == 0) {
-          CqkState s;
-          load_l2(&s, p.st);
-          m_after_bp(s, s_tot);
-          *p.st = s;
-        }
-        master_release(p.sync, s_gen0 + epoch);
+      is_master = grid_step<2>(p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort);
+      if (is_master && threadIdx.x == 0) {
+        tl_record(p.sync, epoch, PH_BP, s_st.phys_count, 0);
+        m_after_bp(s_st, s_tot);
       }
     } else {
       break;
     }
-    if (!s_flag && threadIdx.x == 0) {
-      if (!wait_release(p.sync, s_gen0 + epoch)) s_abort = 1;
+    if (threadIdx.x == 0) {
+      if (is_master) {
+        const int ph = s_st.cmd.phase;
+        if (ph == PH_FINAL || ph == PH_DONE) *p.st = s_st;  // results for the host
+        s_cmd = s_st.cmd;
+        master_release(p.sync, s_gen0 + epoch, s_st.cmd, &p.st->cmd);
+      } else if (!s_abort) {
+        if (!wait_release(p.sync, s_gen0 + epoch, &p.st->cmd, &s_cmd)) s_abort = 1;
+      }
     }
-    __syncthreads();
-    if (threadIdx.x == 0 && !s_abort) load_l2(&s_cmd, &p.st->cmd);
     __syncthreads();
   }
 }
@@ -492,20 +561,23 @@ DEVI T spx_w(T y) { return L1 ? (T)fabs((double)y) : y; }
 template <typename T, bool L1, bool SRC_SCRATCH, int MODE>  // MODE 0 init, 1 scan, 2 snap
 DEVI void spx_pass(const SpxParams<T>& p, const Cmd& c, bool fix, int64_t seg_lo, int64_t& m,
                    bool compact, double (&acc)[kMaxK]) {
-  constexpr int E = Vec<T>::n * kUnroll, CH = 32 * E;
+  constexpr int E = Vec<T>::n * kUnrollY, CH = 32 * E;
   const int lane = threadIdx.x & 31;
   const T* src = (SRC_SCRATCH ? p.sy : p.y) + seg_lo;
   const T lam = (T)c.lam, fhi = (T)c.fix_hi;
   const unsigned lt = (1u << lane) - 1u;
+  const T* const pf[1] = {src};
+  prefetch_chunks<T, 1, kUnrollY>(pf, 0, c_prefetch[1], m, lane);
   int64_t out_m = 0;
   for (int64_t base = 0; base < m; base += CH) {
+    prefetch_chunks<T, 1, kUnrollY>(pf, base / CH + c_prefetch[1], c_prefetch[1] > 0 ? 1 : 0, m, lane);
     const bool full = base + CH <= m;
     T Y[E];
-    load_chunk<T, SRC_SCRATCH>(src, base, m, lane, full, T(0), Y);
+    load_chunk<T, SRC_SCRATCH, kUnrollY>(src, base, m, lane, full, T(0), Y);
     bool keep[E];
 #pragma unroll
     for (int j = 0; j < E; ++j) {
-      const bool valid = full || chunk_index<T>(base, lane, j) < m;
+      const bool valid = full || chunk_index<T, kUnrollY>(base, lane, j) < m;
       // scratch already holds w = |y| for l1
       const T w = SRC_SCRATCH ? Y[j] : spx_w<T, L1>(Y[j]);
       Y[j] = w;
@@ -542,14 +614,17 @@ DEVI void spx_pass(const SpxParams<T>& p, const Cmd& c, bool fix, int64_t seg_lo
 template <typename T, bool L1>
 DEVI void spx_final(const SpxParams<T>& p, const Cmd& c, bool copy, int64_t seg_lo, int64_t m) {
   using V = typename Vec<T>::type;
-  constexpr int VN = Vec<T>::n, E = VN * kUnroll, CH = 32 * E;
+  constexpr int VN = Vec<T>::n, E = VN * kUnrollY, CH = 32 * E;
   const int lane = threadIdx.x & 31;
   const T lam = (T)c.lam;
   T* x = p.x + seg_lo;
+  const T* const pf[1] = {p.y + seg_lo};
+  prefetch_chunks<T, 1, kUnrollY>(pf, 0, c_prefetch[1], m, lane);
   for (int64_t base = 0; base < m; base += CH) {
+    prefetch_chunks<T, 1, kUnrollY>(pf, base / CH + c_prefetch[1], c_prefetch[1] > 0 ? 1 : 0, m, lane);
     const bool full = base + CH <= m;
     T Y[E], X[E];
-    load_chunk<T, false>(p.y + seg_lo, base, m, lane, full, T(0), Y);
+    load_chunk<T, false, kUnrollY>(p.y + seg_lo, base, m, lane, full, T(0), Y);
 #pragma unroll
     for (int j = 0; j < E; ++j) {
       if (copy) { X[j] = Y[j]; continue; }
@@ -565,7 +640,7 @@ DEVI void spx_final(const SpxParams<T>& p, const Cmd& c, bool copy, int64_t seg_
     }
     if (full) {
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
+      for (int u = 0; u < kUnrollY; ++u) {
         V v;
         T* vv = reinterpret_cast<T*>(&v);
 #pragma unroll
@@ -575,7 +650,7 @@ DEVI void spx_final(const SpxParams<T>& p, const Cmd& c, bool copy, int64_t seg_
     } else {
 #pragma unroll
       for (int j = 0; j < E; ++j) {
-        const int64_t e = chunk_index<T>(base, lane, j);
+        const int64_t e = chunk_index<T, kUnrollY>(base, lane, j);
         if (e < m) x[e] = X[j];
       }
     }
@@ -587,10 +662,11 @@ __global__ void __launch_bounds__(kThreads, 1) spx_solve_kernel(SpxParams<T> p) 
   __shared__ double s_red[kWarps][kMaxK];
   __shared__ double s_tot[kMaxK];
   __shared__ Cmd s_cmd;
-  __shared__ int s_flag;
+  __shared__ SpxState s_st;  // master (CTA 0) only
   __shared__ unsigned s_gen0;
   __shared__ int s_abort;
   const int warp = threadIdx.x >> 5;
+  const bool master = blockIdx.x == 0;
   const int64_t gw = (int64_t)blockIdx.x * kWarps + warp, W = (int64_t)gridDim.x * kWarps;
   int64_t seg_lo, seg_hi;
   warp_segment(p.n, gw, W, seg_lo, seg_hi);
@@ -598,8 +674,14 @@ __global__ void __launch_bounds__(kThreads, 1) spx_solve_kernel(SpxParams<T> p) 
   bool in_scratch = false;
   if (threadIdx.x == 0) {
     s_gen0 = ld_acquire(p.sync.gen);
-    load_l2(&s_cmd, &p.st->cmd);
     s_abort = 0;
+    if (master) {
+      s_st = *p.st;
+      s_cmd = s_st.cmd;
+      tl_record(p.sync, 0, -1, p.n, 0);
+    } else {
+      load_l2(&s_cmd, &p.st->cmd);
+    }
   }
   __syncthreads();
   const bool fix = p.st->fixing != 0;
@@ -638,22 +720,21 @@ __global__ void __launch_bounds__(kThreads, 1) spx_solve_kernel(SpxParams<T> p) 
     }
     double a3[3] = {acc[0], acc[1], acc[2]};
     block_reduce<3>(a3, ops, s_red, s_tot);
-    if (arrive_and_reduce<3>(p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_flag)) {
-      if (threadIdx.x == 0) {
-        SpxState s;
-        load_l2(&s, p.st);
-        if (mode == 0) s_after_init(s, s_tot);
-        else if (mode == 1) s_after_scan(s, s_tot, p.trace);
-        else s_after_snap(s, s_tot);
-        *p.st = s;
+    const bool is_master = grid_step<3>(p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort);
+    if (threadIdx.x == 0) {
+      if (is_master) {
+        tl_record(p.sync, epoch, c.phase, mode == 0 ? s_st.n : s_st.phys_count, s_st.cmd.compact);
+        if (mode == 0) s_after_init(s_st, s_tot);
+        else if (mode == 1) s_after_scan(s_st, s_tot, p.trace);
+        else s_after_snap(s_st, s_tot);
+        const int ph = s_st.cmd.phase;
+        if (ph == PH_FINAL || ph == PH_DONE || ph == PH_COPY) *p.st = s_st;
+        s_cmd = s_st.cmd;
+        master_release(p.sync, s_gen0 + epoch, s_st.cmd, &p.st->cmd);
+      } else if (!s_abort) {
+        if (!wait_release(p.sync, s_gen0 + epoch, &p.st->cmd, &s_cmd)) s_abort = 1;
       }
-      master_release(p.sync, s_gen0 + epoch);
     }
-    if (!s_flag && threadIdx.x == 0) {
-      if (!wait_release(p.sync, s_gen0 + epoch)) s_abort = 1;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0 && !s_abort) load_l2(&s_cmd, &p.st->cmd);
     __syncthreads();
   }
 }
@@ -805,7 +886,7 @@ __global__ void __launch_bounds__(kUtilThreads) phi_util_kernel(
     const T t = t_of(d[i], a[i], b[i], lam);
     if (at_lo) at_lo[k] = t <= l[i];
     if (at_hi) at_hi[k] = t >= u[i];
-    elem_scan<T, false>(d[i], a[i], b[i], l[i], u[i], lam, lam, lam, acc);
+    elem_scan<T, false>(d[i], a[i], b[i], l[i], u[i], lam, lam, lam, false, false, acc);
   }
   const int ops[5] = {OP_SUM, OP_SUM, OP_SUM, OP_SUM, OP_SUM};
   double a5[5] = {acc[0], acc[1], acc[2], acc[3], acc[4]};
@@ -856,8 +937,9 @@ __global__ void __launch_bounds__(kUtilThreads) lambda0_util_kernel(
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const T di = d[i], ai = a[i], bi = b[i];
-    const double s = (double)mul_rn(bi, div_rn(ai, di));
-    const double q = (double)mul_rn(bi, div_rn(bi, di));
+    const T y = rcp_nr(di);
+    const double s = (double)mul_rn(bi, ai * y);
+    const double q = (double)mul_rn(bi, bi * y);
     acc[0] += s;
     acc[1] += q;
     if (xbar) {
@@ -904,6 +986,45 @@ __global__ void __launch_bounds__(kUtilThreads) finalize_kernel(const double* pa
     }
   block_reduce<kMaxK>(acc, ops, s_red, s_tot);
   if (threadIdx.x < K) out[threadIdx.x] = s_tot[threadIdx.x];
+}
+
+// Division self-test: bitwise comparison of div_y (shared reciprocal) with
+// __ddiv_rn over random operands (counter-based hash RNG); counts mismatches.
+DEVI unsigned long long mix64(unsigned long long z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__global__ void div_selftest_kernel(unsigned long long seed, long long count, int mode,
+                                    unsigned long long* mismatches, double* example) {
+  unsigned long long bad = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+       i += (long long)gridDim.x * blockDim.x) {
+    const unsigned long long h1 = mix64(seed ^ (2 * i)), h2 = mix64(seed ^ (2 * i + 1));
+    double a, b;
+    if (mode == 0) {  // random mantissas, exponents over [-500, 500]
+      const long long ea = (long long)(h1 % 1001) - 500, eb = (long long)(h2 % 1001) - 500;
+      a = __longlong_as_double((long long)((ea + 1023) << 52) | (long long)(mix64(h1) & 0xFFFFFFFFFFFFFull));
+      b = __longlong_as_double((long long)((eb + 1023) << 52) | (long long)(mix64(h2) & 0xFFFFFFFFFFFFFull));
+      if (h1 & (1ull << 63)) a = -a;
+    } else if (mode == 1) {  // the solver's numerators/denominators: |a| < 1e4, d in [1, 64)
+      a = ((double)(h1 >> 11) * 0x1p-53 - 0.5) * 2e4;
+      b = 1.0 + (double)(h2 >> 11) * 0x1p-53 * 63.0;
+    } else {  // quotients near representable midpoints: a = q*b +- tiny
+      b = 1.0 + (double)(h2 >> 11) * 0x1p-53 * 63.0;
+      const double q = 1.0 + (double)(h1 >> 11) * 0x1p-53;
+      a = __dmul_rn(q, b);
+      a = __longlong_as_double(__double_as_longlong(a) + (long long)(mix64(h1) % 5) - 2);
+    }
+    const double ref = __ddiv_rn(a, b);
+    const double got = div_y(a, b, rcp_div(b));
+    if (__double_as_longlong(ref) != __double_as_longlong(got)) {
+      ++bad;
+      if (example) { example[0] = a; example[1] = b; }
+    }
+  }
+  if (bad) atomicAdd(mismatches, bad);
 }
 
 }  // namespace cqk

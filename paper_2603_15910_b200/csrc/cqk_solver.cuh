@@ -259,13 +259,17 @@ DEVI void m_after_lambda0(CqkState& s, const double* tot) {
 // ------------------------------------------------------------ element ops
 // core.py:246-262 for one element; returns false if the element is already
 // (logically) fixed and therefore not part of the active set.
+// chk_lo / chk_hi: a lower / upper fixing multiplier exists (finite), so
+// the stateless fixed test is needed at all (never divide by infinities).
 template <typename T, bool FIX>
-DEVI bool elem_scan(T d, T a, T b, T l, T u, T lam, T fhi, T flo, double (&acc)[kMaxK]) {
-  const T t = t_of(d, a, b, lam);
+DEVI bool elem_scan(T d, T a, T b, T l, T u, T lam, T fhi, T flo, bool chk_lo, bool chk_hi,
+                    double (&acc)[kMaxK]) {
+  const T yd = rcp_div(d);  // one reciprocal serves t, t(fix) and w
+  const T t = t_of_y(d, a, b, lam, yd);
   const bool alo = t <= l, ahi = t >= u;
   if (FIX) {
-    if (alo && t_of(d, a, b, fhi) <= l) return false;
-    if (ahi && t_of(d, a, b, flo) >= u) return false;
+    if (chk_lo && alo && t_of_y(d, a, b, fhi, yd) <= l) return false;
+    if (chk_hi && ahi && t_of_y(d, a, b, flo, yd) >= u) return false;
   }
   const T x = clip(t, l, u);
   const T bx = mul_rn(b, x);
@@ -276,7 +280,7 @@ DEVI bool elem_scan(T d, T a, T b, T l, T u, T lam, T fhi, T flo, double (&acc)[
   const bool tlo = alo && t == l && l < u;
   const bool thi = ahi && t == u && l < u;
   if (interior || tlo || thi) {
-    const double w = (double)div_rn(mul_rn(b, b), d);
+    const double w = (double)(mul_rn(b, b) * yd);
     if (interior) acc[2] += w;
     else if (tlo) acc[3] += w;
     else acc[4] += w;
@@ -308,10 +312,11 @@ DEVI void elem_bp(T d, T a, T b, T l, T u, double edge, bool right, double& best
 // which keep their bound (fix_variables writes x[newly] = bound).
 template <typename T, bool FIX>
 DEVI T elem_final(T d, T a, T b, T l, T u, T lam, T fhi, T flo, bool chk_lo, bool chk_hi) {
-  T x = clip(t_of(d, a, b, lam), l, u);
+  const T yd = rcp_div(d);
+  T x = clip(t_of_y(d, a, b, lam, yd), l, u);
   if (FIX) {
-    if (chk_lo && t_of(d, a, b, fhi) <= l) x = l;
-    else if (chk_hi && t_of(d, a, b, flo) >= u) x = u;
+    if (chk_lo && t_of_y(d, a, b, fhi, yd) <= l) x = l;
+    else if (chk_hi && t_of_y(d, a, b, flo, yd) >= u) x = u;
   }
   return x;
 }

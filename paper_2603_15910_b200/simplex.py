@@ -69,7 +69,9 @@ def _project(y, r, opts, lambda0, trace, l1):
         yp, xp = yv.data_ptr(), x.data_ptr()
         mem = N.MEM_DEVICE
     else:
-        h.set_stream(None)
+        import torch
+
+        h.set_stream(torch.cuda.current_stream(h.device).cuda_stream)
         x = np.empty(n)
         yp, xp = yv.ctypes.data, x.ctypes.data
         mem = N.MEM_HOST
@@ -170,7 +172,9 @@ def project_simplex_rows(Y, r, opts=None, lambda0=None):
         Yv = np.ascontiguousarray(Y, dtype=np.float64)
         rows, cols = Yv.shape
         h = N.handle(None)
-        h.set_stream(None)
+        import torch
+
+        h.set_stream(torch.cuda.current_stream(h.device).cuda_stream)
         X = np.empty_like(Yv)
         lam = np.empty(rows)
         its = np.empty(rows, np.int32)

@@ -1,0 +1,54 @@
+"""Per-pass device timeline of one persistent solve (perf-iteration aid)."""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch
+
+import paper_2603_15910_b200 as P
+from paper_2603_15910_b200 import _native as N
+
+kind = sys.argv[1] if len(sys.argv) > 1 else "weak"
+n = int(float(sys.argv[2])) if len(sys.argv) > 2 else 10**8
+if kind in ("weak", "corr", "unc", "jac"):
+    fam = {"weak": "cqk-weakly-correlated", "corr": "cqk-correlated", "unc": "cqk-uncorrelated",
+           "jac": "cqk-weakly-correlated"}[kind]
+    d, a, b, l, u, r = P.instances.gen_cqk_arrays(fam, n, 1)
+    inst = P.CqkInstance(*[torch.from_numpy(v).cuda() for v in (d, a, b, l, u)], r=r)
+    f = (lambda: P.jacobi_solve(inst)) if kind == "jac" else (lambda: P.solve_cqk(inst))
+    B = {0: 40, 1: 40, 2: 40}
+    fin = 48
+else:
+    y = torch.from_numpy(P.gen_simplex_y("simplex-n01", n, 1)).cuda()
+    f = (lambda: P.newton_project_simplex(y, 1.0)) if kind == "spx" else (lambda: P.simplex.project_l1_outcome(y, 1.0))
+    B = {0: 8, 1: 8, 6: 8}
+    fin = 16
+for _ in range(3):
+    out = f()
+torch.cuda.synchronize()
+h = N.handle()
+tl = h.timeline(64)
+t0 = tl[0, 3]
+prev = t0
+rows = []
+last = 0
+for k in range(1, len(tl)):
+    ph, el, comp, t = (int(v) for v in tl[k])
+    if t == 0 or t < prev:
+        break
+    dt = (t - prev) / 1e3
+    by = el * B.get(ph, 40)
+    rows.append({"epoch": k, "phase": ph, "elems": el, "compact": comp, "us": round(dt, 1),
+                 "GBps": round(by / dt / 1e3, 0) if dt > 0 else None})
+    prev = t
+    last = t
+tot_ms = out.stats["device_ms"]
+final_us = tot_ms * 1e3 - (last - t0) / 1e3
+rows.append({"phase": "final(+launch)", "elems": n, "us": round(final_us, 1),
+             "GBps": round(n * fin / final_us / 1e3, 0)})
+print(json.dumps({"kind": kind, "n": n, "kernel_ms": tot_ms, "evals": out.phi_evals,
+                  "bytes_model": out.stats["bytes_model"]}))
+for r_ in rows:
+    print(json.dumps(r_))
