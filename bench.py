@@ -132,13 +132,25 @@ def max_over_ranks(v, world):
 
 
 def gen_shard(n_total, world, rank):
-    """This rank's contiguous shard of the full instance (and the global r)."""
+    """This rank's contiguous shard of the instance (generated directly with
+    GF(2) skip-ahead) and the global r from the shards' b.l / b.u sums."""
     import paper_2603_15910_b200 as P
 
-    d, a, b, l, u, r = P.instances.gen_cqk_arrays(FAMILY, n_total, SEED)
-    lo = n_total * rank // world
-    hi = n_total * (rank + 1) // world
-    return [v[lo:hi].copy() if world > 1 else v for v in (d, a, b, l, u)], r, lo, hi
+    if world == 1:
+        d, a, b, l, u, r = P.instances.gen_cqk_arrays(FAMILY, n_total, SEED)
+        return [d, a, b, l, u], r, 0, n_total
+    from paper_2603_15910_b200.distributed import allgather_bytes, shard_bounds
+
+    lo, hi = shard_bounds(n_total, world, rank)
+    d, a, b, l, u, bl, bu = P.instances.gen_cqk_shard(FAMILY, n_total, SEED, lo, hi)
+    parts = [np.frombuffer(x, dtype=np.float64) for x in
+             allgather_bytes(np.array([bl, bu]).tobytes())]
+    sbl = sbu = 0.0
+    for pbl, pbu in parts:  # rank order: identical on every rank
+        sbl += pbl
+        sbu += pbu
+    r = P.instances.cqk_r(FAMILY, n_total, SEED, sbl, sbu)
+    return [d, a, b, l, u], r, lo, hi
 
 
 def cpu_baseline_sample(arrs, r, cores):
@@ -230,7 +242,7 @@ def main():
         from paper_2603_15910_b200 import distributed as D
 
         solver = D.ShardedCQK(dev, r, n_total=args.n, offset=lo)
-        solve = lambda: solver.solve(fixing=args.variant == "solve")  # noqa: E731
+        solve = lambda: solver.solve(variant=args.variant)  # noqa: E731
     else:
         inst = P.CqkInstance(*dev, r=r)
         if args.variant == "solve":

@@ -155,6 +155,45 @@ int spx_project_batched_f64(cqk_handle *h, int mem, const double *Y, int64_t row
                             int64_t cols, double r, const cqk_options *opts, double *X,
                             double *lam, int32_t *iters, cqk_result *res);
 
+/* Multi-GPU (one process / handle per GPU, n sharded contiguously) -------------
+   Replaces the reference's chunked fork-join (parallel.py:174-327, chunks =
+   _chunk_ranges parallel.py:82-85, fixed-order _tree_sum parallel.py:62-72)
+   with one rank per GPU: every Newton epoch the persistent kernel of each rank
+   stores its partial-sum vector into every peer's mailbox over NVLink and
+   reduces the W vectors in rank order (identical decisions on all ranks). */
+/* Size of the opaque IPC handle written by cqk_comm_create (bytes). */
+int cqk_comm_ipc_handle_size(void);
+/* Allocate this rank's mailbox; writes its CUDA IPC handle to ipc_handle_out
+   (cqk_comm_ipc_handle_size() bytes) for exchange between the processes. */
+int cqk_comm_create(cqk_handle *h, int rank, int world, void *ipc_handle_out);
+/* Map all ranks' mailboxes from the concatenated handles (world x size bytes). */
+int cqk_comm_connect(cqk_handle *h, const void *handles);
+/* Same-process ranks (e.g. several handles on one device): direct pointers. */
+int cqk_comm_connect_local(cqk_handle *h, cqk_handle *const *ranks, int world);
+/* Pre-allocate compaction scratch for solves of up to n elements, so that a
+   later solve performs no allocation (which could synchronise the device
+   while another rank's persistent kernel is running). */
+int cqk_reserve(cqk_handle *h, int64_t n);
+/* Cap the persistent grid (CTAs); 0 = the full device.  Lets several ranks
+   share one GPU (virtual ranks) or leave SMs for other work. */
+int cqk_set_grid_limit(cqk_handle *h, int max_ctas);
+/* Sharded solve_cqk / jacobi_solve / par_solve_cqk: this rank's shard
+   [offset, offset + n_local) of an n_total-element instance.  All ranks call
+   it collectively with identical r and options; x (length n_local) receives
+   this rank's part of the solution; res is identical on every rank except the
+   byte counters, which are per rank. */
+int cqk_solve_sharded_f64(cqk_handle *h, int mem, const double *d, const double *a,
+                          const double *b, const double *l, const double *u, int64_t n_local,
+                          int64_t offset, int64_t n_total, double r, const cqk_options *opts,
+                          const double *xbar, double *x, cqk_result *res);
+/* Sharded newton_project_simplex / project_l1 (formula start over n_total). */
+int spx_project_sharded_f64(cqk_handle *h, int mem, const double *y, int64_t n_local,
+                            int64_t n_total, double r, const cqk_options *opts, double *x,
+                            cqk_result *res);
+int l1_project_sharded_f64(cqk_handle *h, int mem, const double *y, int64_t n_local,
+                           int64_t n_total, double r, const cqk_options *opts, double *x,
+                           cqk_result *res);
+
 /* Diagnostics ------------------------------------------------------------------ */
 /* Bitwise check of the solver's shared-reciprocal division against the IEEE
    library division on `count` random operand pairs (mode 0: exponents in

@@ -23,6 +23,12 @@ int cqk_gen_normal(uint64_t seed, uint64_t offset, int64_t count, double *out);
 /* gen_cqk(family, n, seed): fills d, a, b, l, u (length n) and *r */
 int cqk_gen_cqk(int family, int64_t n, uint64_t seed, double *d, double *a, double *b,
                 double *l, double *u, double *r);
+/* elements [lo, hi) of gen_cqk(family, n, seed) (arrays of length hi - lo),
+   with the shard's b.l and b.u sums (for r on a sharded instance) */
+int cqk_gen_cqk_range(int family, int64_t n, uint64_t seed, int64_t lo, int64_t hi, double *d,
+                      double *a, double *b, double *l, double *u, double *bl, double *bu);
+/* r from the full b.l and b.u sums and the stream's final draw */
+double cqk_gen_cqk_r(int family, int64_t n, uint64_t seed, double bl, double bu);
 /* gen_simplex_y(family, n, seed) */
 int cqk_gen_simplex_y(int family, int64_t n, uint64_t seed, double *y);
 

@@ -85,6 +85,9 @@ EXPORTS = (
     "cqk_device_info", "cqk_get_trace", "cqk_get_timeline", "cqk_validate_f64", "cqk_initial_multiplier_f64",
     "cqk_phi_f64", "cqk_eval_x_f64", "cqk_nearest_breakpoint_f64", "cqk_solve_f64",
     "spx_project_f64", "l1_project_f64", "spx_project_batched_f64", "cqk_selftest_division",
+    "cqk_comm_ipc_handle_size", "cqk_comm_create", "cqk_comm_connect", "cqk_comm_connect_local",
+    "cqk_set_grid_limit", "cqk_reserve", "cqk_solve_sharded_f64", "spx_project_sharded_f64",
+    "l1_project_sharded_f64",
 )
 
 _lib = None
@@ -124,6 +127,16 @@ def _declare(L):
     L.l1_project_f64.argtypes = [_P, ctypes.c_int, _P, _I64, _D, _OPT, _P, _RES]
     L.cqk_selftest_division.argtypes = [_P, ctypes.c_uint64, _I64, ctypes.c_int,
                                         ctypes.POINTER(ctypes.c_uint64), _P]
+    L.cqk_comm_ipc_handle_size.restype = ctypes.c_int
+    L.cqk_comm_create.argtypes = [_P, ctypes.c_int, ctypes.c_int, _P]
+    L.cqk_comm_connect.argtypes = [_P, _P]
+    L.cqk_comm_connect_local.argtypes = [_P, _P, ctypes.c_int]
+    L.cqk_set_grid_limit.argtypes = [_P, ctypes.c_int]
+    L.cqk_reserve.argtypes = [_P, _I64]
+    L.cqk_solve_sharded_f64.argtypes = [_P, ctypes.c_int, *arr5, _I64, _I64, _I64, _D, _OPT, _P,
+                                        _P, _RES]
+    L.spx_project_sharded_f64.argtypes = [_P, ctypes.c_int, _P, _I64, _I64, _D, _OPT, _P, _RES]
+    L.l1_project_sharded_f64.argtypes = [_P, ctypes.c_int, _P, _I64, _I64, _D, _OPT, _P, _RES]
     L.spx_project_batched_f64.argtypes = [_P, ctypes.c_int, _P, _I64, _I64, _D, _OPT, _P, _P,
                                           _P, _RES]
 
@@ -156,6 +169,11 @@ def gen_library():
             G.cqk_gen_cqk.argtypes = [ctypes.c_int, _I64, ctypes.c_uint64, _P, _P, _P, _P, _P,
                                       ctypes.POINTER(_D)]
             G.cqk_gen_simplex_y.argtypes = [ctypes.c_int, _I64, ctypes.c_uint64, _P]
+            G.cqk_gen_cqk_range.argtypes = [ctypes.c_int, _I64, ctypes.c_uint64, _I64, _I64,
+                                            _P, _P, _P, _P, _P, ctypes.POINTER(_D),
+                                            ctypes.POINTER(_D)]
+            G.cqk_gen_cqk_r.argtypes = [ctypes.c_int, _I64, ctypes.c_uint64, _D, _D]
+            G.cqk_gen_cqk_r.restype = _D
             _gen = G
     return _gen
 

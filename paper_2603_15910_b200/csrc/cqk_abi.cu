@@ -57,6 +57,15 @@ struct Buf {
   }
 };
 
+// L2 bulk-prefetch distance (chunks) for the persistent kernels, set once per
+// process at handle creation (a per-solve constant-bank update would
+// serialise against kernels of other handles); CQK_PREFETCH="cqk,y" tunes it.
+cudaError_t set_prefetch() {
+  int pf[2] = {0, 2};
+  if (const char* e = getenv("CQK_PREFETCH")) sscanf(e, "%d,%d", &pf[0], &pf[1]);
+  return cudaMemcpyToSymbol(c_prefetch, pf, sizeof pf);
+}
+
 }  // namespace
 
 struct cqk_handle {
@@ -75,6 +84,15 @@ struct cqk_handle {
   Buf scratch, stage, idxbuf, flags;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int trace_len = 0;
+  int grid_limit = 0;                 // 0: full device (virtual ranks share a GPU)
+  unsigned* err_host = nullptr;       // pinned: barrier-timeout flag readback
+  void* host_state = nullptr;         // pinned: solver state in / out (no pageable copies)
+  // multi-GPU communicator (one rank per GPU; mailboxes in device memory)
+  int rank = 0, world = 1;
+  double* mbox = nullptr;             // this rank's mailbox
+  double* peers[kMaxRanks] = {};      // every rank's mailbox (IPC-mapped or local)
+  bool ipc_opened[kMaxRanks] = {};
+  unsigned long long seq = 0;         // sharded-solve sequence number
 };
 
 extern "C" {
@@ -127,6 +145,9 @@ int cqk_create(cqk_handle** out, int device) {
   e = e ? e : cudaMalloc(&h->timeline, sizeof(long long) * 4 * kTimelineCap);
   e = e ? e : cudaMalloc(&h->red, sizeof(double) * kMaxK * kUtilBlocksMax);
   e = e ? e : cudaMalloc(&h->out, sizeof(double) * kMaxK);
+  e = e ? e : cudaMallocHost(&h->err_host, 64);
+  e = e ? e : cudaMallocHost(&h->host_state, st_bytes);
+  e = e ? e : set_prefetch();
   e = e ? e : cudaEventCreate(&h->ev0);
   e = e ? e : cudaEventCreate(&h->ev1);
   e = e ? e : cudaDeviceSynchronize();
@@ -147,6 +168,9 @@ int cqk_destroy(cqk_handle* h) {
   h->stage.release();
   h->idxbuf.release();
   h->flags.release();
+  for (int q = 0; q < kMaxRanks; ++q)
+    if (h->ipc_opened[q] && h->peers[q]) cudaIpcCloseMemHandle(h->peers[q]);
+  if (h->mbox) cudaFree(h->mbox);
   cudaFree(h->sync);
   cudaFree(h->state);
   cudaFree(h->partials);
@@ -154,6 +178,8 @@ int cqk_destroy(cqk_handle* h) {
   cudaFree(h->timeline);
   cudaFree(h->red);
   cudaFree(h->out);
+  if (h->err_host) cudaFreeHost(h->err_host);
+  if (h->host_state) cudaFreeHost(h->host_state);
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
   if (h->own) cudaStreamDestroy(h->own);
@@ -239,13 +265,7 @@ int stage_inputs(cqk_handle* h, int mem, int64_t n, const T* const* in, int coun
 
 bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 
-// L2 bulk-prefetch distance (chunks) for the persistent kernels; tunable via
-// CQK_PREFETCH="cqk,y" for measurement sweeps.
-cudaError_t set_prefetch(cudaStream_t s) {
-  int pf[2] = {0, 2};
-  if (const char* e = getenv("CQK_PREFETCH")) sscanf(e, "%d,%d", &pf[0], &pf[1]);
-  return cudaMemcpyToSymbolAsync(c_prefetch, pf, sizeof pf, 0, cudaMemcpyHostToDevice, s);
-}
+
 
 int finish_sync(cqk_handle* h) {
   cudaError_t e = cudaStreamSynchronize(h->stream);
@@ -253,12 +273,14 @@ int finish_sync(cqk_handle* h) {
   return 0;
 }
 
+// The barrier-timeout flag travels back with the state (async, on the solve
+// stream: no legacy-stream or device-wide synchronisation, so several handles
+// can run concurrent persistent kernels, e.g. virtual ranks on one GPU).
 int check_timeout(cqk_handle* h) {
-  unsigned err = 0;
-  cudaMemcpy(&err, h->sync + 2, sizeof(unsigned), cudaMemcpyDeviceToHost);
-  if (err) {
-    cudaMemset(h->sync, 0, 64);
-    cudaDeviceSynchronize();
+  if (*h->err_host) {
+    *h->err_host = 0;
+    cudaMemsetAsync(h->sync, 0, 64, h->stream);
+    cudaStreamSynchronize(h->stream);
     return set_err(CQK_E_TIMEOUT, "persistent kernel barrier timed out");
   }
   return 0;
@@ -294,18 +316,119 @@ int stage_idx(cqk_handle* h, int mem, const int64_t* idx, int64_t m, const int64
 
 }  // namespace
 
+// ------------------------------------------------------------ communicator
+namespace {
+int limit_grid(const cqk_handle* h, int grid) {
+  return h->grid_limit > 0 && h->grid_limit < grid ? h->grid_limit : grid;
+}
+Exchange make_exchange(cqk_handle* h, bool sharded) {
+  Exchange ex;
+  std::memset(&ex, 0, sizeof ex);
+  ex.world = sharded ? h->world : 1;
+  ex.rank = sharded ? h->rank : 0;
+  ex.mbox = h->mbox;
+  for (int q = 0; q < kMaxRanks; ++q) ex.peer[q] = h->peers[q];
+  if (sharded) ex.seq = ++h->seq;
+  return ex;
+}
+}  // namespace
+
+extern "C" int cqk_reserve(cqk_handle* h, int64_t n) {
+  if (!h || n < 0) return set_err(CQK_E_ARG, "bad reserve");
+  CUDA_TRY(cudaSetDevice(h->device));
+  const size_t per = ((size_t)n * sizeof(double) + 255) / 256 * 256;
+  CUDA_TRY(h->scratch.ensure(per * 5));
+  CUDA_TRY(cudaDeviceSynchronize());
+  return 0;
+}
+
+extern "C" int cqk_set_grid_limit(cqk_handle* h, int max_ctas) {
+  if (!h) return set_err(CQK_E_ARG, "null handle");
+  h->grid_limit = max_ctas;
+  return 0;
+}
+
+extern "C" int cqk_comm_create(cqk_handle* h, int rank, int world, void* ipc_handle_out) {
+  if (!h || world < 1 || world > kMaxRanks || rank < 0 || rank >= world)
+    return set_err(CQK_E_ARG, "need 0 <= rank < world <= 8");
+  CUDA_TRY(cudaSetDevice(h->device));
+  if (!h->mbox) {
+    CUDA_TRY(cudaMalloc(&h->mbox, sizeof(double) * kMboxDoubles));
+    CUDA_TRY(cudaMemset(h->mbox, 0, sizeof(double) * kMboxDoubles));
+  }
+  h->rank = rank;
+  h->world = world;
+  h->seq = 0;
+  h->peers[rank] = h->mbox;
+  if (ipc_handle_out) {
+    cudaIpcMemHandle_t ih;
+    CUDA_TRY(cudaIpcGetMemHandle(&ih, h->mbox));
+    std::memcpy(ipc_handle_out, &ih, sizeof ih);
+  }
+  CUDA_TRY(cudaDeviceSynchronize());
+  return 0;
+}
+
+extern "C" int cqk_comm_ipc_handle_size(void) { return (int)sizeof(cudaIpcMemHandle_t); }
+
+extern "C" int cqk_comm_connect(cqk_handle* h, const void* handles) {
+  if (!h || !handles || !h->mbox) return set_err(CQK_E_ARG, "cqk_comm_create first");
+  CUDA_TRY(cudaSetDevice(h->device));
+  const char* hb = (const char*)handles;
+  for (int q = 0; q < h->world; ++q) {
+    if (q == h->rank) continue;
+    cudaIpcMemHandle_t ih;
+    std::memcpy(&ih, hb + q * sizeof(cudaIpcMemHandle_t), sizeof ih);
+    void* ptr = nullptr;
+    CUDA_TRY(cudaIpcOpenMemHandle(&ptr, ih, cudaIpcMemLazyEnablePeerAccess));
+    h->peers[q] = (double*)ptr;
+    h->ipc_opened[q] = true;
+  }
+  return 0;
+}
+
+extern "C" int cqk_comm_connect_local(cqk_handle* h, cqk_handle* const* ranks, int world) {
+  if (!h || !ranks || world != h->world) return set_err(CQK_E_ARG, "bad local rank table");
+  for (int q = 0; q < world; ++q) {
+    if (!ranks[q] || !ranks[q]->mbox) return set_err(CQK_E_ARG, "peer without mailbox");
+    h->peers[q] = ranks[q]->mbox;
+  }
+  return 0;
+}
+
 // ------------------------------------------------------------ CQK solve
+static int solve_impl(cqk_handle* h, int mem, const double* d, const double* a, const double* b,
+                      const double* l, const double* u, int64_t n, int64_t offset,
+                      int64_t n_total, double r, const cqk_options* opts_in, const double* xbar,
+                      double* x, cqk_result* res, bool sharded);
+
 extern "C" int cqk_solve_f64(cqk_handle* h, int mem, const double* d, const double* a,
                              const double* b, const double* l, const double* u, int64_t n,
                              double r, const cqk_options* opts_in, const double* xbar, double* x,
                              cqk_result* res) {
+  return solve_impl(h, mem, d, a, b, l, u, n, 0, n, r, opts_in, xbar, x, res, false);
+}
+
+extern "C" int cqk_solve_sharded_f64(cqk_handle* h, int mem, const double* d, const double* a,
+                                     const double* b, const double* l, const double* u,
+                                     int64_t n_local, int64_t offset, int64_t n_total, double r,
+                                     const cqk_options* opts, const double* xbar, double* x,
+                                     cqk_result* res) {
+  if (!h || h->world < 1 || !h->mbox) return set_err(CQK_E_ARG, "communicator not set up");
+  return solve_impl(h, mem, d, a, b, l, u, n_local, offset, n_total, r, opts, xbar, x, res, true);
+}
+
+static int solve_impl(cqk_handle* h, int mem, const double* d, const double* a, const double* b,
+                      const double* l, const double* u, int64_t n, int64_t offset,
+                      int64_t n_total, double r, const cqk_options* opts_in, const double* xbar,
+                      double* x, cqk_result* res, bool sharded) {
   if (!h || !d || !a || !b || !l || !u || !res) return set_err(CQK_E_ARG, "null argument");
   std::memset(res, 0, sizeof *res);
   res->domain_index = -1;
   res->lam = NAN;
   cqk_options opts = opts_in ? *opts_in : default_opts();
   CUDA_TRY(cudaSetDevice(h->device));
-  if (n < 1) {  // validate(): "instance must have at least one variable"
+  if (n_total < 1 || (!sharded && n < 1)) {  // validate(): at least one variable
     if (opts.check) {
       res->status = CQK_E_DOMAIN;
       res->domain_field = CQK_F_D;
@@ -344,7 +467,7 @@ extern "C" int cqk_solve_f64(cqk_handle* h, int mem, const double* d, const doub
   s.lam0 = s.cmd.lam;
   s.compact_ratio = std::isnan(opts.compact_ratio) ? 0.25 : opts.compact_ratio;
   s.max_iter = opts.max_iterations;
-  s.n = n;
+  s.n = n_total;
   s.phys_count = n;
   s.fixing = fixing;
   s.variant = opts.variant;
@@ -358,8 +481,8 @@ extern "C" int cqk_solve_f64(cqk_handle* h, int mem, const double* d, const doub
     const size_t per = ((size_t)n * sizeof(double) + 255) / 256 * 256;
     CUDA_TRY(h->scratch.ensure(per * 5));
   }
-  CUDA_TRY(cudaMemcpyAsync(h->state, &s, sizeof s, cudaMemcpyHostToDevice, h->stream));
-  CUDA_TRY(set_prefetch(h->stream));
+  std::memcpy(h->host_state, &s, sizeof s);  // pinned staging: fully asynchronous
+  CUDA_TRY(cudaMemcpyAsync(h->state, h->host_state, sizeof s, cudaMemcpyHostToDevice, h->stream));
   CqkParams<double> p;
   std::memset(&p, 0, sizeof p);
   p.d = dv[0]; p.a = dv[1]; p.b = dv[2]; p.l = dv[3]; p.u = dv[4]; p.xbar = xbar ? dv[5] : nullptr;
@@ -372,25 +495,30 @@ extern "C" int cqk_solve_f64(cqk_handle* h, int mem, const double* d, const doub
   p.x = xo;
   p.trace = h->trace;
   p.n = n;
+  p.offset = offset;
   p.r = r;
   p.st = (CqkState*)h->state;
+  p.ex = make_exchange(h, sharded);
   p.partials = h->partials;
   p.sync.arrive = h->sync;
   p.sync.gen = h->sync + 1;
   p.sync.error = (int*)(h->sync + 2);
   p.sync.timeline = h->timeline;
   void* args[] = {&p};
-  const int grid = fixing ? h->grid_cqk_fix : h->grid_cqk_jac;
+  const int grid = limit_grid(h, fixing ? h->grid_cqk_fix : h->grid_cqk_jac);
   const void* fn = fixing ? (const void*)cqk_solve_kernel<double, true>
                           : (const void*)cqk_solve_kernel<double, false>;
   CUDA_TRY(cudaEventRecord(h->ev0, h->stream));
   CUDA_TRY(cudaLaunchCooperativeKernel(fn, grid, kThreads, args, 0, h->stream));
   CUDA_TRY(cudaEventRecord(h->ev1, h->stream));
-  CUDA_TRY(cudaMemcpyAsync(&s, h->state, sizeof s, cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(cudaMemcpyAsync(h->host_state, h->state, sizeof s, cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(cudaMemcpyAsync(h->err_host, h->sync + 2, sizeof(unsigned), cudaMemcpyDeviceToHost,
+                           h->stream));
   if (mem == CQK_MEM_HOST && x && xo)
     CUDA_TRY(cudaMemcpyAsync(x, xo, sizeof(double) * n, cudaMemcpyDeviceToHost, h->stream));
   int rc = finish_sync(h);
   if (rc) return rc;
+  std::memcpy(&s, h->host_state, sizeof s);
   rc = check_timeout(h);
   if (rc) return rc;
   float ms = 0.f;
@@ -421,8 +549,8 @@ extern "C" int cqk_solve_f64(cqk_handle* h, int mem, const double* d, const doub
 // ------------------------------------------------------------ simplex / l1
 namespace {
 
-int spx_common(cqk_handle* h, int mem, const double* y, int64_t n, double r,
-               const cqk_options* opts_in, double* x, cqk_result* res, bool l1) {
+int spx_common(cqk_handle* h, int mem, const double* y, int64_t n, int64_t n_total, double r,
+               const cqk_options* opts_in, double* x, cqk_result* res, bool l1, bool sharded) {
   if (!h || !y || !res) return set_err(CQK_E_ARG, "null argument");
   std::memset(res, 0, sizeof *res);
   res->domain_index = -1;
@@ -434,7 +562,7 @@ int spx_common(cqk_handle* h, int mem, const double* y, int64_t n, double r,
     res->domain_field = CQK_F_R;
     return CQK_E_DOMAIN;
   }
-  if (n < 1) return set_err(CQK_E_ARG, "n must be >= 1");
+  if (n_total < 1 || (!sharded && n < 1)) return set_err(CQK_E_ARG, "n must be >= 1");
   const double* yv;
   double* xdev = nullptr;
   double* xo = x;
@@ -456,8 +584,9 @@ int spx_common(cqk_handle* h, int mem, const double* y, int64_t n, double r,
   s.hi = INFINITY;
   s.r = r;
   s.tau = tau_of(&opts, false);
-  s.n = n;
-  s.active = n;
+  s.n = n_total;
+  s.active = n_total;
+  s.local_active = n;
   s.phys_count = n;
   s.max_iter = opts.max_iterations;
   s.fixing = fixing;
@@ -468,8 +597,8 @@ int spx_common(cqk_handle* h, int mem, const double* y, int64_t n, double r,
   s.trace_cap = opts.record_trace ? kTraceCap : 0;
   s.compact_ratio = std::isnan(opts.compact_ratio) ? 0.25 : opts.compact_ratio;
   if (fixing) CUDA_TRY(h->scratch.ensure(((size_t)n * sizeof(double) + 255) / 256 * 256));
-  CUDA_TRY(cudaMemcpyAsync(h->state, &s, sizeof s, cudaMemcpyHostToDevice, h->stream));
-  CUDA_TRY(set_prefetch(h->stream));
+  std::memcpy(h->host_state, &s, sizeof s);  // pinned staging: fully asynchronous
+  CUDA_TRY(cudaMemcpyAsync(h->state, h->host_state, sizeof s, cudaMemcpyHostToDevice, h->stream));
   SpxParams<double> p;
   std::memset(&p, 0, sizeof p);
   p.y = yv;
@@ -478,23 +607,27 @@ int spx_common(cqk_handle* h, int mem, const double* y, int64_t n, double r,
   p.trace = h->trace;
   p.n = n;
   p.st = (SpxState*)h->state;
+  p.ex = make_exchange(h, sharded);
   p.partials = h->partials;
   p.sync.arrive = h->sync;
   p.sync.gen = h->sync + 1;
   p.sync.error = (int*)(h->sync + 2);
   p.sync.timeline = h->timeline;
   void* args[] = {&p};
-  const int grid = l1 ? h->grid_l1 : h->grid_spx;
+  const int grid = limit_grid(h, l1 ? h->grid_l1 : h->grid_spx);
   const void* fn = l1 ? (const void*)spx_solve_kernel<double, true>
                       : (const void*)spx_solve_kernel<double, false>;
   CUDA_TRY(cudaEventRecord(h->ev0, h->stream));
   CUDA_TRY(cudaLaunchCooperativeKernel(fn, grid, kThreads, args, 0, h->stream));
   CUDA_TRY(cudaEventRecord(h->ev1, h->stream));
-  CUDA_TRY(cudaMemcpyAsync(&s, h->state, sizeof s, cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(cudaMemcpyAsync(h->host_state, h->state, sizeof s, cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(cudaMemcpyAsync(h->err_host, h->sync + 2, sizeof(unsigned), cudaMemcpyDeviceToHost,
+                           h->stream));
   if (mem == CQK_MEM_HOST && x && xo)
     CUDA_TRY(cudaMemcpyAsync(x, xo, sizeof(double) * n, cudaMemcpyDeviceToHost, h->stream));
   int rc = finish_sync(h);
   if (rc) return rc;
+  std::memcpy(&s, h->host_state, sizeof s);
   rc = check_timeout(h);
   if (rc) return rc;
   float ms = 0.f;
@@ -522,12 +655,26 @@ int spx_common(cqk_handle* h, int mem, const double* y, int64_t n, double r,
 
 extern "C" int spx_project_f64(cqk_handle* h, int mem, const double* y, int64_t n, double r,
                                const cqk_options* opts, double* x, cqk_result* res) {
-  return spx_common(h, mem, y, n, r, opts, x, res, false);
+  return spx_common(h, mem, y, n, n, r, opts, x, res, false, false);
+}
+
+extern "C" int spx_project_sharded_f64(cqk_handle* h, int mem, const double* y, int64_t n_local,
+                                       int64_t n_total, double r, const cqk_options* opts,
+                                       double* x, cqk_result* res) {
+  if (!h || !h->mbox) return set_err(CQK_E_ARG, "communicator not set up");
+  return spx_common(h, mem, y, n_local, n_total, r, opts, x, res, false, true);
+}
+
+extern "C" int l1_project_sharded_f64(cqk_handle* h, int mem, const double* y, int64_t n_local,
+                                      int64_t n_total, double r, const cqk_options* opts,
+                                      double* x, cqk_result* res) {
+  if (!h || !h->mbox) return set_err(CQK_E_ARG, "communicator not set up");
+  return spx_common(h, mem, y, n_local, n_total, r, opts, x, res, true, true);
 }
 
 extern "C" int l1_project_f64(cqk_handle* h, int mem, const double* y, int64_t n, double r,
                               const cqk_options* opts, double* x, cqk_result* res) {
-  return spx_common(h, mem, y, n, r, opts, x, res, true);
+  return spx_common(h, mem, y, n, n, r, opts, x, res, true, false);
 }
 
 // ------------------------------------------------------------ batched rows

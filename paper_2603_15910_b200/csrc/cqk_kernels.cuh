@@ -189,7 +189,7 @@ DEVI void lambda0_pass(const CqkParams<T>& p, int64_t seg_lo, int64_t m, double 
       acc[1] += q;
       if (XBAR && L[j] < X[j] && X[j] < U[j]) { acc[2] += s; acc[3] += q; acc[4] += 1.0; }
       if (CHECK) {
-        const double gi = (double)(seg_lo + e);
+        const double gi = (double)(p.offset + seg_lo + e);
         const T d = D[j], a = A[j], b = B[j], l = L[j], u = U[j];
         if (!isfinite((double)d)) acc[5] = fmin(acc[5], gi);
         if (!isfinite((double)a)) acc[6] = fmin(acc[6], gi);
@@ -393,8 +393,10 @@ __global__ void __launch_bounds__(kThreads, 1) cqk_solve_kernel(CqkParams<T> p) 
       block_reduce<15>(a15, ops, s_red, s_tot);
       is_master = grid_step<15>(p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort);
       if (is_master && threadIdx.x == 0) {
-        tl_record(p.sync, epoch, PH_LAMBDA0, s_st.n, 0);
-        m_after_lambda0(s_st, s_tot);
+        tl_record(p.sync, epoch, PH_LAMBDA0, p.n, 0);
+        double glob[15];
+        if (exchange_totals(p.ex, epoch, 15, ops, s_tot, glob)) m_after_lambda0(s_st, glob);
+        else m_stop(s_st, ST_TIMEOUT);
       }
     } else if (c.phase == PH_SCAN) {
       const bool compact = FIX && c.compact;
@@ -409,11 +411,12 @@ __global__ void __launch_bounds__(kThreads, 1) cqk_solve_kernel(CqkParams<T> p) 
       block_reduce<K>(aK, ops, s_red, s_tot);
       is_master = grid_step<K>(p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort);
       if (is_master && threadIdx.x == 0) {
-        double tot[11];
+        double loc[11], glob[11];
 #pragma unroll
-        for (int k = 0; k < 11; ++k) tot[k] = k < K ? s_tot[k] : 0.0;
+        for (int k = 0; k < 11; ++k) loc[k] = glob[k] = k < K ? s_tot[k] : 0.0;
         tl_record(p.sync, epoch, PH_SCAN, s_st.phys_count, s_st.cmd.compact);
-        m_after_scan(s_st, tot, p.trace);
+        if (exchange_totals(p.ex, epoch, K, ops, loc, glob)) m_after_scan(s_st, glob, loc, p.trace);
+        else m_stop(s_st, ST_TIMEOUT);
       }
     } else if (c.phase == PH_BP) {
       acc[0] = c.right ? HUGE_VAL : -HUGE_VAL;
@@ -425,7 +428,9 @@ __global__ void __launch_bounds__(kThreads, 1) cqk_solve_kernel(CqkParams<T> p) 
       is_master = grid_step<2>(p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort);
       if (is_master && threadIdx.x == 0) {
         tl_record(p.sync, epoch, PH_BP, s_st.phys_count, 0);
-        m_after_bp(s_st, s_tot);
+        double glob[2];
+        if (exchange_totals(p.ex, epoch, 2, ops, s_tot, glob)) m_after_bp(s_st, glob);
+        else m_stop(s_st, ST_TIMEOUT);
       }
     } else {
       break;
@@ -453,6 +458,7 @@ struct SpxState {
   Cmd cmd;  // lam, fix_hi (drop iff w + fix_hi <= 0), phase, compact
   double lo, hi, r, tau, lam0, lam0_value;
   int64_t n, active, phys_count, pending_phys, fixed_count, fixed_removed;
+  int64_t local_active, fixed_local;  // this rank's share (multi-GPU)
   int64_t iterations, phi_evals, max_iter, elems_scan, elems_written;
   int32_t fixing, status, l1, lam0_given, trace_len, trace_cap, compact_always, pad;
   double compact_ratio;
@@ -464,10 +470,11 @@ struct SpxParams {
   T* sy;  // scratch (working values w)
   T* x;
   double* trace;
-  int64_t n;
+  int64_t n;  // elements of this rank's shard
   SpxState* st;
   double* partials;
   GridSync sync;
+  Exchange ex;
 };
 
 DEVI void s_finish(SpxState& s, double lam) {
@@ -493,7 +500,7 @@ DEVI void s_after_init(SpxState& s, const double* tot) {
 }
 
 // tot: 0 value, 1 #(v>0), 2 #(v==0)   (simplex.py:207-215, 256-294)
-DEVI void s_after_scan(SpxState& s, const double* tot, double* trace) {
+DEVI void s_after_scan(SpxState& s, const double* tot, const double* loc, double* trace) {
   s.phi_evals += 1;
   s.elems_scan += s.phys_count;
   if (s.cmd.compact) {
@@ -520,8 +527,11 @@ DEVI void s_after_scan(SpxState& s, const double* tot, double* trace) {
     s.hi = lam;
     const int64_t at_zero = s.active - (int64_t)tot[1];
     if (s.fixing && at_zero > 0) {
+      const int64_t at_zero_local = s.local_active - (int64_t)loc[1];
       s.fixed_count += at_zero;
       s.active -= at_zero;
+      s.fixed_local += at_zero_local;
+      s.local_active -= at_zero_local;
       s.cmd.fix_hi = lam;
     }
   }
@@ -538,7 +548,7 @@ DEVI void s_after_scan(SpxState& s, const double* tot, double* trace) {
   s.cmd.phase = PH_SCAN;
   s.cmd.compact = 0;
   if (s.fixing) {
-    const int64_t present = s.fixed_count - s.fixed_removed;
+    const int64_t present = s.fixed_local - s.fixed_removed;
     if (present > 0 && (double)present >= s.compact_ratio * (double)s.phys_count) {
       s.cmd.compact = 1;
       s.pending_phys = s.phys_count - present;
@@ -723,10 +733,14 @@ __global__ void __launch_bounds__(kThreads, 1) spx_solve_kernel(SpxParams<T> p) 
     const bool is_master = grid_step<3>(p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort);
     if (threadIdx.x == 0) {
       if (is_master) {
-        tl_record(p.sync, epoch, c.phase, mode == 0 ? s_st.n : s_st.phys_count, s_st.cmd.compact);
-        if (mode == 0) s_after_init(s_st, s_tot);
-        else if (mode == 1) s_after_scan(s_st, s_tot, p.trace);
-        else s_after_snap(s_st, s_tot);
+        tl_record(p.sync, epoch, c.phase, mode == 0 ? p.n : s_st.phys_count, s_st.cmd.compact);
+        double loc[3] = {s_tot[0], s_tot[1], s_tot[2]}, glob[3];
+        if (!exchange_totals(p.ex, epoch, 3, ops, loc, glob)) {
+          s_st.status = ST_TIMEOUT;
+          s_st.cmd.phase = PH_DONE;
+        } else if (mode == 0) s_after_init(s_st, glob);
+        else if (mode == 1) s_after_scan(s_st, glob, loc, p.trace);
+        else s_after_snap(s_st, glob);
         const int ph = s_st.cmd.phase;
         if (ph == PH_FINAL || ph == PH_DONE || ph == PH_COPY) *p.st = s_st;
         s_cmd = s_st.cmd;

@@ -68,8 +68,9 @@ struct CqkState {
   double r_res, r_orig, fixed_abs, tau;
   double lam0, compact_ratio;
   int64_t fixed_count, fixed_removed, iterations, phi_evals, max_iter;
-  int64_t n, phys_count, pending_phys;
-  int64_t elems_scan, elems_written, elems_bp;  // byte-model counters
+  int64_t n, phys_count, pending_phys;  // n: global size; phys_count: this rank
+  int64_t fixed_local;                  // logically fixed elements of this rank
+  int64_t elems_scan, elems_written, elems_bp;  // byte-model counters (this rank)
   int64_t domain_index;
   int32_t has_plo, has_phi, fixing, variant, status, has_xbar, check, domain_field;
   int32_t trace_len, trace_cap, lam0_given, pad;
@@ -81,11 +82,13 @@ struct CqkParams {
   T *sd, *sa, *sb, *sl, *su;  // compaction scratch (n each) or null
   T* x;                       // output or null
   double* trace;              // 4 doubles per phi evaluation
-  int64_t n;
+  int64_t n;                  // elements of this rank's shard
+  int64_t offset;             // global index of the shard's first element
   double r;
   CqkState* st;
   double* partials;           // [gridDim.x][kMaxK]
   GridSync sync;
+  Exchange ex;                // cross-GPU partial exchange (world 1: none)
 };
 
 // ------------------------------------------------------------ master logic
@@ -127,8 +130,8 @@ DEVI void m_post_step(CqkState& s, double next) {
   if (s.iterations > s.max_iter) { m_stop(s, ST_MAXITER); return; }
   s.cmd.phase = PH_SCAN;
   s.cmd.compact = 0;
-  if (s.fixing) {
-    const int64_t present = s.fixed_count - s.fixed_removed;
+  if (s.fixing) {  // a purely local (per-rank) byte decision
+    const int64_t present = s.fixed_local - s.fixed_removed;
     if (present > 0 && (double)present >= s.compact_ratio * (double)s.phys_count) {
       s.cmd.compact = 1;
       s.pending_phys = s.phys_count - present;
@@ -143,8 +146,9 @@ DEVI void m_secant_or_fail(CqkState& s) {
 }
 
 // tot: 0 value, 1 abs_bx, 2 core, 3 tie_lo, 4 tie_hi, 5..7 lower-fix
-// (sum, abs, count), 8..10 upper-fix (sum, abs, count)
-DEVI void m_after_scan(CqkState& s, const double* tot, double* trace) {
+// (sum, abs, count), 8..10 upper-fix (sum, abs, count) -- summed over all
+// ranks; loc: the same vector of this rank alone (local bookkeeping only).
+DEVI void m_after_scan(CqkState& s, const double* tot, const double* loc, double* trace) {
   s.phi_evals += 1;
   s.elems_scan += s.phys_count;
   if (s.cmd.compact) {
@@ -182,6 +186,7 @@ DEVI void m_after_scan(CqkState& s, const double* tot, double* trace) {
         s.r_res -= total;
         s.fixed_abs += tabs;
         s.fixed_count += cnt;
+        s.fixed_local += (int64_t)(dir > 0 ? loc[7] : loc[10]);
         if (s.has_plo) s.phi_lo -= total;
         if (s.has_phi) s.phi_hi -= total;
         if (dir > 0) s.cmd.fix_hi = lam;

@@ -223,48 +223,68 @@ static double dot_pairwise(const double *b, const double *v, int64_t n) {
 #endif
 #define U01() ((double)(xo_next(&st) >> 11) * (1.0 / 9007199254740992.0))
 
-/* instances.py:43-70 */
+/* Elements [lo, hi) of gen_cqk(family, n, seed) (instances.py:43-70) into
+ * arrays of length hi - lo, plus the shard's pairwise b.l and b.u sums.  The
+ * draw offsets follow the reference's order: the (d, a, b) tuple of element
+ * i at draws per*i.., the (lo, hi) bound pair at 3n (n for correlated) + 2i,
+ * and the r draw at that offset + 2n. */
+int cqk_gen_cqk_range(int family, int64_t n, uint64_t seed, int64_t lo, int64_t hi, double *d,
+                      double *a, double *b, double *l, double *u, double *bl, double *bu) {
+  if (n < 1 || family < 0 || family > 2 || lo < 0 || hi > n || lo > hi) return -1;
+  const int64_t m = hi - lo;
+  const uint64_t per = family == CQK_FAMILY_CORRELATED ? 1 : 3;
+  const uint64_t off = per * (uint64_t)n;
+  if (m > 0) {
+    if (family == CQK_FAMILY_UNCORRELATED) {
+      /* flat = uniform(10, 25, 3n); d, a, b = flat[0::3], flat[1::3], flat[2::3] */
+      TUPLE_LOOP(seed, 3 * (uint64_t)lo, m, 3, {
+        d[k] = 10.0 + U01() * (25.0 - 10.0);
+        a[k] = 10.0 + U01() * (25.0 - 10.0);
+        b[k] = 10.0 + U01() * (25.0 - 10.0);
+      });
+    } else if (family == CQK_FAMILY_WEAKLY) {
+      TUPLE_LOOP(seed, 3 * (uint64_t)lo, m, 3, {
+        double f0 = U01(), f1 = U01(), f2 = U01();
+        double bk = 10.0 + 15.0 * f0;
+        b[k] = bk;
+        d[k] = (bk - 5.0) + 10.0 * f1;
+        a[k] = (bk - 5.0) + 10.0 * f2;
+      });
+    } else {
+      TUPLE_LOOP(seed, (uint64_t)lo, m, 1, {
+        double bk = 10.0 + U01() * (25.0 - 10.0);
+        b[k] = bk;
+        d[k] = bk + 5.0;
+        a[k] = bk + 5.0;
+      });
+    }
+    /* pair = uniform(10, 25, 2n); l = min(pair[0::2], pair[1::2]), u = max */
+    TUPLE_LOOP(seed, off + 2 * (uint64_t)lo, m, 2, {
+      double p0 = 10.0 + U01() * (25.0 - 10.0);
+      double p1 = 10.0 + U01() * (25.0 - 10.0);
+      l[k] = p0 < p1 ? p0 : p1;
+      u[k] = p0 > p1 ? p0 : p1;
+    });
+  }
+  if (bl) *bl = dot_pairwise(b, l, m);
+  if (bu) *bu = dot_pairwise(b, u, m);
+  return 0;
+}
+
+/* r = b.l + U * (b.u - b.l) with the reference's final draw (instances.py:64-66) */
+double cqk_gen_cqk_r(int family, int64_t n, uint64_t seed, double bl, double bu) {
+  const uint64_t per = family == CQK_FAMILY_CORRELATED ? 1 : 3;
+  double ur;
+  fill_draws(seed, per * (uint64_t)n + 2 * (uint64_t)n, 1, &ur, 1, K_U01, 0, 0);
+  return bl + ur * (bu - bl);
+}
+
 int cqk_gen_cqk(int family, int64_t n, uint64_t seed, double *d, double *a, double *b,
                 double *l, double *u, double *r_out) {
-  if (n < 1 || family < 0 || family > 2) return -1;
-  uint64_t off;
-  if (family == CQK_FAMILY_UNCORRELATED) {
-    /* flat = uniform(10, 25, 3n); d, a, b = flat[0::3], flat[1::3], flat[2::3] */
-    TUPLE_LOOP(seed, 0, n, 3, {
-      d[k] = 10.0 + U01() * (25.0 - 10.0);
-      a[k] = 10.0 + U01() * (25.0 - 10.0);
-      b[k] = 10.0 + U01() * (25.0 - 10.0);
-    });
-    off = 3 * (uint64_t)n;
-  } else if (family == CQK_FAMILY_WEAKLY) {
-    TUPLE_LOOP(seed, 0, n, 3, {
-      double f0 = U01(), f1 = U01(), f2 = U01();
-      double bk = 10.0 + 15.0 * f0;
-      b[k] = bk;
-      d[k] = (bk - 5.0) + 10.0 * f1;
-      a[k] = (bk - 5.0) + 10.0 * f2;
-    });
-    off = 3 * (uint64_t)n;
-  } else {
-    TUPLE_LOOP(seed, 0, n, 1, {
-      double bk = 10.0 + U01() * (25.0 - 10.0);
-      b[k] = bk;
-      d[k] = bk + 5.0;
-      a[k] = bk + 5.0;
-    });
-    off = (uint64_t)n;
-  }
-  /* pair = uniform(10, 25, 2n); l = min(pair[0::2], pair[1::2]), u = max */
-  TUPLE_LOOP(seed, off, n, 2, {
-    double lo = 10.0 + U01() * (25.0 - 10.0);
-    double hi = 10.0 + U01() * (25.0 - 10.0);
-    l[k] = lo < hi ? lo : hi;
-    u[k] = lo > hi ? lo : hi;
-  });
-  double bl = dot_pairwise(b, l, n), bu = dot_pairwise(b, u, n);
-  double ur;
-  fill_draws(seed, off + 2 * (uint64_t)n, 1, &ur, 1, K_U01, 0, 0);
-  *r_out = bl + ur * (bu - bl);
+  double bl, bu;
+  int rc = cqk_gen_cqk_range(family, n, seed, 0, n, d, a, b, l, u, &bl, &bu);
+  if (rc) return rc;
+  *r_out = cqk_gen_cqk_r(family, n, seed, bl, bu);
   return 0;
 }
 

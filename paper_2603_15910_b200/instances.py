@@ -38,6 +38,30 @@ def gen_cqk_arrays(family, n, seed, out=None):
     return (*arrs, float(r.value))
 
 
+def gen_cqk_shard(family, n, seed, lo, hi):
+    """Elements [lo, hi) of gen_cqk(family, n, seed) without generating the rest
+    (GF(2) skip-ahead): (d, a, b, l, u, bl, bu) with this shard's pairwise
+    b.l / b.u sums; combine the shards' sums with `cqk_r`."""
+    if family not in CQK_FAMILIES:
+        raise FamilyMismatch(f"not a CQK family: {family!r}")
+    m = int(hi) - int(lo)
+    arrs = [np.empty(m) for _ in range(5)]
+    bl, bu = ctypes.c_double(), ctypes.c_double()
+    rc = N.gen_library().cqk_gen_cqk_range(CQK_FAMILIES.index(family), int(n),
+                                           int(seed) & (2**64 - 1), int(lo), int(hi),
+                                           *[a.ctypes.data for a in arrs], ctypes.byref(bl),
+                                           ctypes.byref(bu))
+    if rc != 0:
+        raise ValueError(f"gen_cqk_shard failed ({rc})")
+    return (*arrs, float(bl.value), float(bu.value))
+
+
+def cqk_r(family, n, seed, bl, bu):
+    """r = b.l + U (b.u - b.l) with the stream's final draw (instances.py:64-66)."""
+    return float(N.gen_library().cqk_gen_cqk_r(CQK_FAMILIES.index(family), int(n),
+                                               int(seed) & (2**64 - 1), float(bl), float(bu)))
+
+
 def gen_cqk(family, n, seed, dtype=np.float64):
     """One random CQK instance of the given family (instances.py:43-70)."""
     d, a, b, l, u, r = gen_cqk_arrays(family, n, seed)
