@@ -728,7 +728,22 @@ extern "C" int spx_project_batched_f64(cqk_handle* h, int mem, const double* Y, 
   const int c = (int)cols;
   CUDA_TRY(cudaEventRecord(h->ev0, h->stream));
   cudaError_t e;
-  if (c <= kRowThreads) e = launch_rows<1>(h, Yd, Xd, Ld, Id, rows, c, r, tau, opts.max_iterations, fixing, opts.lambda0);
+  const size_t per_warp = ((size_t)c * 8 + 127) / 128 * 128 + kFreeCap * 8 + 128;
+  const size_t smem = per_warp * kRowWarps;
+  const char* force = getenv("CQK_ROWS_KERNEL");
+  const bool warp_kernel = smem <= 200 * 1024 && !(force && std::string(force) == "block");
+  if (warp_kernel) {
+    cudaFuncSetAttribute(spx_rows_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, spx_rows_warp_kernel, 32 * kRowWarps, smem);
+    int64_t grid = (int64_t)(occ > 0 ? occ : 1) * h->sm_count;
+    const int64_t need = (rows + kRowWarps - 1) / kRowWarps;
+    if (grid > need) grid = need;
+    spx_rows_warp_kernel<<<(unsigned)grid, 32 * kRowWarps, smem, h->stream>>>(
+        Yd, Xd, Ld, Id, rows, c, r, tau, opts.max_iterations, fixing, opts.lambda0);
+    e = cudaGetLastError();
+  } else if (c <= kRowThreads) e = launch_rows<1>(h, Yd, Xd, Ld, Id, rows, c, r, tau, opts.max_iterations, fixing, opts.lambda0);
   else if (c <= 2 * kRowThreads) e = launch_rows<2>(h, Yd, Xd, Ld, Id, rows, c, r, tau, opts.max_iterations, fixing, opts.lambda0);
   else if (c <= 4 * kRowThreads) e = launch_rows<4>(h, Yd, Xd, Ld, Id, rows, c, r, tau, opts.max_iterations, fixing, opts.lambda0);
   else if (c <= 8 * kRowThreads) e = launch_rows<8>(h, Yd, Xd, Ld, Id, rows, c, r, tau, opts.max_iterations, fixing, opts.lambda0);

@@ -875,6 +875,186 @@ __global__ void __launch_bounds__(kRowThreads) spx_rows_kernel(
   }
 }
 
+// ------------------------------------------------------------ warp-per-row
+// K8, Blackwell form: one warp owns one row at a time.  The row lands in
+// shared memory with ONE bulk TMA copy (cp.async.bulk + mbarrier complete_tx),
+// every reduction is a warp shuffle (no __syncthreads at all), the free set is
+// compacted into a small per-warp buffer once it fits (later Newton steps
+// touch only a few dozen values), and x = max(0, y + lam) is written back in
+// place and stored with one bulk TMA store.  Several warps per SM (bounded by
+// shared memory) keep HBM busy while others iterate.
+constexpr int kRowWarps = 2;      // warps per CTA
+constexpr int kFreeCap = 512;     // compacted free-set capacity per warp
+
+DEVI unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+DEVI void mbar_init(unsigned long long* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+}
+DEVI void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes) : "memory");
+}
+DEVI void tma_load_1d(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+DEVI void mbar_wait(unsigned long long* bar, unsigned phase) {
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(phase) : "memory");
+}
+DEVI void tma_store_1d(void* dst, const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+DEVI void tma_store_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+DEVI void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__global__ void __launch_bounds__(32 * kRowWarps) spx_rows_warp_kernel(
+    const double* __restrict__ Y, double* __restrict__ X, double* __restrict__ lam_out,
+    int32_t* __restrict__ it_out, int64_t rows, int cols, double r, double tau, int max_iter,
+    int fixing, double lam0_given) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const size_t a_bytes = ((size_t)cols * 8 + 127) / 128 * 128;
+  const size_t per_warp = a_bytes + kFreeCap * 8 + 128;
+  unsigned char* base = smem_raw + per_warp * w;
+  double* A = reinterpret_cast<double*>(base);
+  double* Bf = reinterpret_cast<double*>(base + a_bytes);
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(base + a_bytes + kFreeCap * 8);
+  const bool tma = (cols % 2) == 0 && (((uintptr_t)Y | (uintptr_t)X) & 15) == 0;
+  const unsigned bytes = (unsigned)cols * 8u;
+  if (lane == 0 && tma) mbar_init(bar);
+  __syncwarp();
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  unsigned phase = 0;
+  const int64_t gw = (int64_t)blockIdx.x * kRowWarps + w, W = (int64_t)gridDim.x * kRowWarps;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int64_t row = gw; row < rows; row += W) {
+    const double* y = Y + row * (int64_t)cols;
+    double* x = X + row * (int64_t)cols;
+    if (tma) {
+      if (lane == 0) {
+        tma_store_wait_read();  // the previous row's store has read A
+        mbar_expect_tx(bar, bytes);
+        tma_load_1d(A, y, bytes, bar);
+      }
+      mbar_wait(bar, phase);
+      phase ^= 1u;
+    } else {
+      for (int i = lane; i < cols; i += 32) A[i] = __ldcs(y + i);
+      __syncwarp();
+    }
+    // sum / max -> formula start (simplex.py:246-250 route)
+    double sum = 0.0, mx = -HUGE_VAL;
+    for (int i = lane; i < cols; i += 32) {
+      const double v = A[i];
+      sum += v;
+      mx = fmax(mx, v);
+    }
+    sum = warp_sum(sum);
+    mx = warp_max(mx);
+    double lam = isnan(lam0_given) ? (r - sum) / (double)cols : lam0_given;
+    lam = lam >= -mx ? lam : -mx;
+    double lo = -HUGE_VAL, hi = HUGE_VAL, fix_hi = HUGE_VAL;
+    int iterations = 0;
+    const double* F = A;  // current free-set storage
+    int m = cols;         // its length
+    bool compacted = false;
+    for (;;) {
+      double val = 0.0, npos = 0.0, nzero = 0.0;
+      for (int i = lane; i < m; i += 32) {
+        const double v = F[i];
+        const double t = __dadd_rn(v, lam);
+        if (!compacted && fixing && !(t > 0) && !(__dadd_rn(v, fix_hi) > 0)) continue;
+        if (t > 0) { val += t; npos += 1.0; }
+        else if (t == 0) nzero += 1.0;
+      }
+      const double value = warp_sum(val), dminus = warp_sum(npos), dplus = dminus + warp_sum(nzero);
+      double deriv;
+      if (iterations == 0) {
+        if (value == r) break;
+        deriv = value < r ? dplus : dminus;
+      } else {
+        if (value <= r) break;
+        deriv = dminus;
+      }
+      if (value < r) lo = lam;
+      else {
+        hi = lam;
+        if (fixing) {
+          fix_hi = lam;
+          // keep exactly the survivors (t > 0); compact them once they fit
+          if (dminus <= kFreeCap) {
+            int out = 0;
+            for (int i0 = 0; i0 < m; i0 += 32) {
+              const int i = i0 + lane;
+              double v = 0.0;
+              bool keep = false;
+              if (i < m) {
+                v = F[i];
+                keep = __dadd_rn(v, lam) > 0;
+              }
+              const unsigned mask = __ballot_sync(0xffffffffu, keep);
+              __syncwarp();  // all reads of this block precede the writes (in-place on Bf)
+              if (keep) Bf[out + __popc(mask & lt)] = v;
+              out += __popc(mask);
+            }
+            __syncwarp();
+            F = Bf;
+            m = out;
+            compacted = true;
+          }
+        }
+      }
+      if (deriv <= 0) {  // snap to the largest remaining breakpoint (simplex.py:276-281)
+        double mneg = -HUGE_VAL;
+        for (int i = lane; i < m; i += 32) {
+          const double v = F[i];
+          if (!compacted && fixing && !(__dadd_rn(v, fix_hi) > 0)) continue;
+          mneg = fmax(mneg, -v);
+        }
+        lam = warp_max(mneg);
+        ++iterations;
+        continue;
+      }
+      const double step = -(value - r) / deriv;
+      const double next = lam + step;
+      if (fabs(step) < tau || next == lam) { lam = next; break; }
+      if (isfinite(lo) && isfinite(hi) && hi - lo < tau * fmax(fabs(hi), fabs(lo))) {
+        lam = next;
+        break;
+      }
+      lam = next;
+      ++iterations;
+      if (iterations > max_iter) break;
+    }
+    // x = max(0, y + lam) in place, then one bulk store
+    for (int i = lane; i < cols; i += 32) {
+      const double t = __dadd_rn(A[i], lam);
+      const double xv = t > 0 ? t : 0.0;
+      if (tma) A[i] = xv;
+      else __stcs(x + i, xv);
+    }
+    if (tma) {
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) tma_store_1d(x, A, bytes);
+    }
+    if (lane == 0) {
+      if (lam_out) lam_out[row] = lam;
+      if (it_out) it_out[row] = iterations;
+    }
+    __syncwarp();
+  }
+  if (lane == 0 && tma) tma_store_wait_read();
+  // outstanding bulk stores complete before the grid exits (bulk_group semantics)
+  if (lane == 0 && tma) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 // ------------------------------------------------------------ utilities
 // Grid-stride kernels with per-block partials + a fixed-order finalize; used
 // by the component-level entry points (eval_phi, eval_x, breakpoints,

@@ -1,0 +1,132 @@
+"""Pin the C oracle against golden vectors produced by the REAL reference
+(tests/golden/make_golden.py).  With the reference's own lambda0 injected the
+oracle must reproduce the reference bit for bit (statuses, multipliers, x,
+iteration / evaluation / fixing counts); lambda0 itself (a BLAS ddot in the
+reference) agrees to ~1e-16."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+G = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+@pytest.fixture(scope="module")
+def small():
+    O.build()
+    return np.load(os.path.join(G, "small.npz"))
+
+
+@pytest.fixture(scope="module")
+def generated():
+    with open(os.path.join(G, "generated.json")) as f:
+        return json.load(f)
+
+
+def cqk_case(z, k):
+    p = f"c{k}_"
+    return [z[p + nm] for nm in ("d", "a", "b", "l", "u")], float(z[p + "r"][0]), p
+
+
+def test_solve_cqk_bitexact(small):
+    z = small
+    exact = 0
+    for k in range(int(z["n_cqk"][0])):
+        arrs, r, p = cqk_case(z, k)
+        lam0 = float(z[p + "lam0"][0])
+        for tag, fix in (("fix", True), ("nofix", False)):
+            ref = z[p + tag + "_out"]
+            o = O.solve_cqk(*arrs, r, fixing=fix, lam0=lam0)
+            st = {0: O.SOLVED, 1: O.INFEASIBLE}[int(ref[0])]
+            assert o["status"] == st, (k, tag)
+            assert o["iterations"] == int(ref[2]) and o["phi_evals"] == int(ref[3]), (k, tag)
+            assert o["fixed_count"] == int(ref[4]), (k, tag)
+            if st == O.SOLVED:
+                assert o["lam"] == ref[1], (k, tag, o["lam"], ref[1])
+                assert np.array_equal(o["x"], z[p + tag + "_x"]), (k, tag)
+                exact += 1
+    assert exact > 500
+
+
+def test_solve_cqk_own_lambda0_close(small):
+    z = small
+    for k in range(int(z["n_cqk"][0])):
+        arrs, r, p = cqk_case(z, k)
+        lam0 = O.initial_multiplier(*arrs, r)
+        ref0 = float(z[p + "lam0"][0])
+        assert abs(lam0 - ref0) <= 1e-14 * max(1.0, abs(ref0)), k
+        ref = z[p + "fix_out"]
+        o = O.solve_cqk(*arrs, r)
+        if int(ref[0]) == 0:
+            assert abs(o["lam"] - ref[1]) <= 1e-12 * max(1.0, abs(ref[1])), k
+
+
+def test_jacobi_bitexact(small):
+    z = small
+    for k in range(int(z["n_cqk"][0])):
+        arrs, r, p = cqk_case(z, k)
+        ref = z[p + "jac_out"]
+        o = O.jacobi_solve(*arrs, r, workers=3, lam0=float(z[p + "lam0"][0]))
+        assert o["status"] == {0: O.SOLVED, 1: O.INFEASIBLE}[int(ref[0])]
+        assert o["iterations"] == int(ref[2])
+        if int(ref[0]) == 0:
+            assert o["lam"] == ref[1], k
+
+
+def test_phi_scan_bitexact(small):
+    z = small
+    for k in range(int(z["n_cqk"][0])):
+        arrs, r, p = cqk_case(z, k)
+        for lam, ref in zip(z[p + "phi_lams"], z[p + "phi"]):
+            got = O.phi_scan(*arrs, float(lam))[:4]
+            assert np.array_equal(np.array(got), ref), (k, lam)
+
+
+def test_simplex_bitexact(small):
+    z = small
+    for k in range(int(z["n_spx"][0])):
+        p = f"s{k}_"
+        y, r = z[p + "y"], float(z[p + "r"][0])
+        o = O.newton_project_simplex(y, r)
+        ref = z[p + "newton"]
+        assert o["lam"] == ref[0] and o["iterations"] == int(ref[1]), k
+        assert o["phi_evals"] == int(ref[2]) and o["fixed_count"] == int(ref[3]), k
+        assert np.array_equal(o["x"], z[p + "x"]), k
+        f = z[p + "formula"]
+        o2 = O.newton_project_simplex(y, r, lam0=float(f[4]))
+        assert o2["lam"] == f[0] and o2["iterations"] == int(f[1]), k
+        lam, free, fixed, _ = O.simplex_init_lambda(y, r)
+        assert lam == z[p + "init_lam"][0] and np.array_equal(free, z[p + "init_free"]), k
+        x1 = O.project_l1(y, r)["x"]
+        assert np.array_equal(x1, z[p + "l1_x"]), k
+
+
+def test_generated_instances(generated):
+    import paper_2603_15910_b200 as P
+
+    for rec in generated["cqk"]:
+        if rec["n"] > 10**7:
+            continue  # the 1e8 fixtures are exercised by the GPU suite
+        d, a, b, l, u, r_ours = P.instances.gen_cqk_arrays(rec["family"], rec["n"], rec["seed"])
+        from tests_util import sha
+
+        assert sha(d, a, b, l, u) == rec["sha"], rec["family"]
+        assert abs(r_ours - rec["r"]) <= 1e-14 * abs(rec["r"])  # BLAS vs pairwise dot
+        for tag, fix in (("solve", True), ("nofix", False)):
+            o = O.solve_cqk(d, a, b, l, u, rec["r"], fixing=fix, lam0=rec["lam0"])
+            ref = rec[tag]
+            assert o["lam"] == ref["lam"], (rec["family"], rec["n"], tag)
+            assert o["iterations"] == ref["iterations"] and o["fixed_count"] == ref["fixed_count"]
+            assert sha(o["x"]) == ref["x_sha"]
+    for rec in generated["simplex"]:
+        y = P.gen_simplex_y(rec["family"], rec["n"], rec["seed"])
+        from tests_util import sha
+
+        assert sha(y) == rec["sha"]
+        o = O.newton_project_simplex(y, 1.0)
+        assert o["lam"] == rec["lam"] and o["iterations"] == rec["iterations"]
+        o2 = O.newton_project_simplex(y, 1.0, lam0=rec["formula_lam0"])
+        assert o2["lam"] == rec["formula_lam"] and o2["iterations"] == rec["formula_iterations"]
