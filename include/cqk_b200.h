@@ -62,7 +62,9 @@ typedef struct {
   double compact_ratio;     /* physical compaction when fixed/present >= ratio;
                                NaN = default 0.25, >1 = never */
   int32_t record_trace;     /* keep (lam, phi, dminus, dplus) per phi evaluation */
-  int32_t reserved;
+  int32_t simplex_start;    /* simplex / l1 start when lambda0 is NaN: 0 = (r - sum y)/n,
+                               1 = min((r - sum y)/n, r - max y) (both upper bounds;
+                               the reference's `lambda0=` route, simplex.py:246-250) */
 } cqk_options;
 
 /* SolveOutcome (newton.py:93-103) plus measurement counters. */
@@ -140,9 +142,10 @@ int cqk_solve_f64(cqk_handle *h, int mem, const double *d, const double *a,
 
 /* Simplex / l1 ---------------------------------------------------------------- */
 /* newton_project_simplex(y, r, opts, lambda0)  simplex.py:218-308.  The device
-   initializer is the formula lambda0 = (r - sum y)/n clamped to >= min(-y)
-   (the reference's `lambda0=` route, simplex.py:246-250) unless opts->lambda0
-   is given.  x may be NULL. */
+   initializer is lambda0 = min((r - sum y)/n, r - max y) (opts->simplex_start
+   = 1) or the plain formula (0), clamped to >= min(-y) -- the reference's
+   `lambda0=` route, simplex.py:246-250 -- unless opts->lambda0 is given.
+   x may be NULL. */
 int spx_project_f64(cqk_handle *h, int mem, const double *y, int64_t n, double r,
                     const cqk_options *opts, double *x, cqk_result *res);
 /* project_l1(y, r)  simplex.py:311-333 (dense).  res->iterations = -1 when y is

@@ -43,7 +43,7 @@ class Options(ctypes.Structure):
         ("lambda0", ctypes.c_double),
         ("compact_ratio", ctypes.c_double),
         ("record_trace", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("simplex_start", ctypes.c_int32),
     ]
 
 
@@ -246,7 +246,7 @@ def handle(device=None):
 
 
 def make_options(opts=None, variant=VARIANT_SOLVE, check=True, lambda0=None,
-                 compact_ratio=None, trace=False, fixing=None):
+                 compact_ratio=None, trace=False, fixing=None, start="tight"):
     o = Options()
     fix = getattr(opts, "variable_fixing", True) if fixing is None else fixing
     o.variable_fixing = 1 if fix else 0
@@ -258,4 +258,5 @@ def make_options(opts=None, variant=VARIANT_SOLVE, check=True, lambda0=None,
     o.lambda0 = math.nan if lambda0 is None else float(lambda0)
     o.compact_ratio = math.nan if compact_ratio is None else float(compact_ratio)
     o.record_trace = 1 if trace else 0
+    o.simplex_start = {"formula": 0, "tight": 1}[start]
     return o

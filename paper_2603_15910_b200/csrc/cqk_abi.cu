@@ -239,6 +239,7 @@ cqk_options default_opts() {
   o.check = 1;
   o.lambda0 = NAN;
   o.compact_ratio = NAN;
+  o.simplex_start = 1;
   return o;
 }
 
@@ -596,6 +597,7 @@ int spx_common(cqk_handle* h, int mem, const double* y, int64_t n, int64_t n_tot
   s.lam0_value = opts.lambda0;
   s.trace_cap = opts.record_trace ? kTraceCap : 0;
   s.compact_ratio = std::isnan(opts.compact_ratio) ? 0.25 : opts.compact_ratio;
+  s.start = opts.simplex_start;
   if (fixing) CUDA_TRY(h->scratch.ensure(((size_t)n * sizeof(double) + 255) / 256 * 256));
   std::memcpy(h->host_state, &s, sizeof s);  // pinned staging: fully asynchronous
   CUDA_TRY(cudaMemcpyAsync(h->state, h->host_state, sizeof s, cudaMemcpyHostToDevice, h->stream));
@@ -682,13 +684,14 @@ namespace {
 template <int EPT>
 cudaError_t launch_rows(cqk_handle* h, const double* Y, double* X, double* lam, int32_t* it,
                         int64_t rows, int cols, double r, double tau, int max_iter, int fixing,
-                        double lam0) {
+                        double lam0, int start) {
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, spx_rows_kernel<EPT>, kRowThreads, 0);
   int64_t grid = (int64_t)(occ > 0 ? occ : 1) * h->sm_count;
   if (grid > rows) grid = rows;
   spx_rows_kernel<EPT><<<(unsigned)grid, kRowThreads, 0, h->stream>>>(Y, X, lam, it, rows, cols, r,
-                                                                       tau, max_iter, fixing, lam0);
+                                                                       tau, max_iter, fixing, lam0,
+                                                                       start);
   return cudaGetLastError();
 }
 }  // namespace
@@ -728,10 +731,9 @@ extern "C" int spx_project_batched_f64(cqk_handle* h, int mem, const double* Y, 
   const int c = (int)cols;
   CUDA_TRY(cudaEventRecord(h->ev0, h->stream));
   cudaError_t e;
-  const size_t per_warp = ((size_t)c * 8 + 127) / 128 * 128 + kFreeCap * 8 + 128;
-  const size_t smem = per_warp * kRowWarps;
+  const size_t smem = rows_smem_per_warp(c) * kRowWarps;
   const char* force = getenv("CQK_ROWS_KERNEL");
-  const bool warp_kernel = smem <= 200 * 1024 && !(force && std::string(force) == "block");
+  const bool warp_kernel = smem <= 220 * 1024 && !(force && std::string(force) == "block");
   if (warp_kernel) {
     cudaFuncSetAttribute(spx_rows_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
@@ -741,14 +743,15 @@ extern "C" int spx_project_batched_f64(cqk_handle* h, int mem, const double* Y, 
     const int64_t need = (rows + kRowWarps - 1) / kRowWarps;
     if (grid > need) grid = need;
     spx_rows_warp_kernel<<<(unsigned)grid, 32 * kRowWarps, smem, h->stream>>>(
-        Yd, Xd, Ld, Id, rows, c, r, tau, opts.max_iterations, fixing, opts.lambda0);
+        Yd, Xd, Ld, Id, rows, c, r, tau, opts.max_iterations, fixing, opts.lambda0,
+        opts.simplex_start);
     e = cudaGetLastError();
-  } else if (c <= kRowThreads) e = launch_rows<1>(h, Yd, Xd, Ld, Id, rows, c, r, tau, opts.max_iterations, fixing, opts.lambda0);
-  else if (c <= 2 * kRowThreads) e = launch_rows<2>(h, Yd, Xd, Ld, Id, rows, c, r, tau, opts.max_iterations, fixing, opts.lambda0);
-  else if (c <= 4 * kRowThreads) e = launch_rows<4>(h, Yd, Xd, Ld, Id, rows, c, r, tau, opts.max_iterations, fixing, opts.lambda0);
-  else if (c <= 8 * kRowThreads) e = launch_rows<8>(h, Yd, Xd, Ld, Id, rows, c, r, tau, opts.max_iterations, fixing, opts.lambda0);
-  else if (c <= 16 * kRowThreads) e = launch_rows<16>(h, Yd, Xd, Ld, Id, rows, c, r, tau, opts.max_iterations, fixing, opts.lambda0);
-  else e = launch_rows<32>(h, Yd, Xd, Ld, Id, rows, c, r, tau, opts.max_iterations, fixing, opts.lambda0);
+  } else if (c <= kRowThreads) e = launch_rows<1>(h, Yd, Xd, Ld, Id, rows, c, r, tau, opts.max_iterations, fixing, opts.lambda0, opts.simplex_start);
+  else if (c <= 2 * kRowThreads) e = launch_rows<2>(h, Yd, Xd, Ld, Id, rows, c, r, tau, opts.max_iterations, fixing, opts.lambda0, opts.simplex_start);
+  else if (c <= 4 * kRowThreads) e = launch_rows<4>(h, Yd, Xd, Ld, Id, rows, c, r, tau, opts.max_iterations, fixing, opts.lambda0, opts.simplex_start);
+  else if (c <= 8 * kRowThreads) e = launch_rows<8>(h, Yd, Xd, Ld, Id, rows, c, r, tau, opts.max_iterations, fixing, opts.lambda0, opts.simplex_start);
+  else if (c <= 16 * kRowThreads) e = launch_rows<16>(h, Yd, Xd, Ld, Id, rows, c, r, tau, opts.max_iterations, fixing, opts.lambda0, opts.simplex_start);
+  else e = launch_rows<32>(h, Yd, Xd, Ld, Id, rows, c, r, tau, opts.max_iterations, fixing, opts.lambda0, opts.simplex_start);
   if (e != cudaSuccess) return set_err(CQK_E_CUDA, std::string("rows kernel: ") + cudaGetErrorString(e));
   CUDA_TRY(cudaEventRecord(h->ev1, h->stream));
   if (mem == CQK_MEM_HOST) {

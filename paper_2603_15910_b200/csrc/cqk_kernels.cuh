@@ -460,7 +460,7 @@ struct SpxState {
   int64_t n, active, phys_count, pending_phys, fixed_count, fixed_removed;
   int64_t local_active, fixed_local;  // this rank's share (multi-GPU)
   int64_t iterations, phi_evals, max_iter, elems_scan, elems_written;
-  int32_t fixing, status, l1, lam0_given, trace_len, trace_cap, compact_always, pad;
+  int32_t fixing, status, l1, lam0_given, trace_len, trace_cap, start, pad;
   double compact_ratio;
 };
 
@@ -492,7 +492,14 @@ DEVI void s_after_init(SpxState& s, const double* tot) {
     s.cmd.phase = PH_COPY;
     return;
   }
-  const double lam0 = s.lam0_given ? s.lam0_value : (s.r - tot[0]) / (double)s.n;
+  // start: 0 = the formula (r - sum y)/n; 1 (default) = min(formula, r - max y),
+  // both upper bounds of the root (phi(lam) >= sum(y) + n lam and
+  // phi(lam) >= max(y) + lam), the second far tighter on spread data -- the
+  // reference's own `lambda0=` route with a better start (simplex.py:246-250).
+  const double formula = (s.r - tot[0]) / (double)s.n;
+  const double tight = s.r - tot[1];
+  const double lam0 = s.lam0_given ? s.lam0_value
+                                   : (s.start && tight < formula ? tight : formula);
   const double mn = -tot[1];
   s.lam0 = lam0 >= mn ? lam0 : mn;  // max(lambda0, min(-y)), simplex.py:250
   s.cmd.lam = s.lam0;
@@ -764,7 +771,7 @@ template <int EPT>
 __global__ void __launch_bounds__(kRowThreads) spx_rows_kernel(
     const double* __restrict__ Y, double* __restrict__ X, double* __restrict__ lam_out,
     int32_t* __restrict__ it_out, int64_t rows, int cols, double r, double tau, int max_iter,
-    int fixing, double lam0_given) {
+    int fixing, double lam0_given, int start) {
   __shared__ double s_part[2][kRowThreads / 32][3];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int NW = kRowThreads / 32;
@@ -801,7 +808,8 @@ __global__ void __launch_bounds__(kRowThreads) spx_rows_kernel(
       if (live[k]) { sum += v[k]; mx = fmax(mx, v[k]); }
     double tsum, tmax;
     reduce3(sum, mx, 0.0, tsum, tmax, unused, true);
-    double lam = isnan(lam0_given) ? (r - tsum) / (double)cols : lam0_given;
+    const double formula = (r - tsum) / (double)cols, tight = r - tmax;
+    double lam = !isnan(lam0_given) ? lam0_given : (start && tight < formula ? tight : formula);
     lam = lam >= -tmax ? lam : -tmax;
     double lo = -HUGE_VAL, hi = HUGE_VAL;
     int iterations = 0;
@@ -884,7 +892,6 @@ __global__ void __launch_bounds__(kRowThreads) spx_rows_kernel(
 // place and stored with one bulk TMA store.  Several warps per SM (bounded by
 // shared memory) keep HBM busy while others iterate.
 constexpr int kRowWarps = 2;      // warps per CTA
-constexpr int kFreeCap = 512;     // compacted free-set capacity per warp
 
 DEVI unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 DEVI void mbar_init(unsigned long long* bar) {
@@ -913,18 +920,63 @@ DEVI void tma_store_1d(void* dst, const void* src, unsigned bytes) {
 DEVI void tma_store_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 DEVI void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+// Free-set capacity of the per-warp compaction buffer: half a row (at the
+// first fixing step the survivors are the positives at lambda0 ~ half the row
+// for symmetric data); while the survivors exceed it the full row is scanned
+// with the stateless drop test instead.
+__host__ __device__ inline int free_cap(int cols) { return ((cols + 1) / 2 + 1) & ~1; }
+__host__ __device__ inline size_t rows_smem_per_warp(int cols) {
+  return ((size_t)cols * 8 + 127) / 128 * 128 + ((size_t)free_cap(cols) * 8 + 127) / 128 * 128 + 128;
+}
+
+// phi over a contiguous smem range: sum of positive t = v + lam, #(t > 0),
+// #(t == 0); branch-free, two elements per 16-byte shared load, split
+// accumulators to break the DADD dependency chains.
+DEVI void rows_phi(const double* F, int m, double lam, bool drop_test, double fix_hi, int lane,
+                   double& val, int& npos, int& nzero) {
+  double v0 = 0.0, v1 = 0.0;
+  int p = 0, z = 0;
+  const int m2 = m & ~1;
+  for (int i = 2 * lane; i < m2; i += 64) {
+    const double2 v = *reinterpret_cast<const double2*>(F + i);
+    const double t0 = __dadd_rn(v.x, lam), t1 = __dadd_rn(v.y, lam);
+    v0 += t0 > 0 ? t0 : 0.0;
+    v1 += t1 > 0 ? t1 : 0.0;
+    p += (t0 > 0) + (t1 > 0);
+    // a zero t of a dropped variable is not in the free set (simplex.py:214)
+    z += (t0 == 0 && (!drop_test || __dadd_rn(v.x, fix_hi) > 0)) +
+         (t1 == 0 && (!drop_test || __dadd_rn(v.y, fix_hi) > 0));
+  }
+  if ((m & 1) && lane == 0) {
+    const double t = __dadd_rn(F[m - 1], lam);
+    v0 += t > 0 ? t : 0.0;
+    p += t > 0;
+    z += t == 0 && (!drop_test || __dadd_rn(F[m - 1], fix_hi) > 0);
+  }
+  val = v0 + v1;
+  npos = p;
+  nzero = z;
+}
+
+DEVI int warp_sum_i(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 __global__ void __launch_bounds__(32 * kRowWarps) spx_rows_warp_kernel(
     const double* __restrict__ Y, double* __restrict__ X, double* __restrict__ lam_out,
     int32_t* __restrict__ it_out, int64_t rows, int cols, double r, double tau, int max_iter,
-    int fixing, double lam0_given) {
+    int fixing, double lam0_given, int start) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const size_t a_bytes = ((size_t)cols * 8 + 127) / 128 * 128;
-  const size_t per_warp = a_bytes + kFreeCap * 8 + 128;
-  unsigned char* base = smem_raw + per_warp * w;
+  const size_t b_bytes = ((size_t)free_cap(cols) * 8 + 127) / 128 * 128;
+  unsigned char* base = smem_raw + rows_smem_per_warp(cols) * w;
   double* A = reinterpret_cast<double*>(base);
   double* Bf = reinterpret_cast<double*>(base + a_bytes);
-  unsigned long long* bar = reinterpret_cast<unsigned long long*>(base + a_bytes + kFreeCap * 8);
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(base + a_bytes + b_bytes);
+  const int cap = free_cap(cols);
   const bool tma = (cols % 2) == 0 && (((uintptr_t)Y | (uintptr_t)X) & 15) == 0;
   const unsigned bytes = (unsigned)cols * 8u;
   if (lane == 0 && tma) mbar_init(bar);
@@ -949,15 +1001,22 @@ __global__ void __launch_bounds__(32 * kRowWarps) spx_rows_warp_kernel(
       __syncwarp();
     }
     // sum / max -> formula start (simplex.py:246-250 route)
-    double sum = 0.0, mx = -HUGE_VAL;
-    for (int i = lane; i < cols; i += 32) {
-      const double v = A[i];
-      sum += v;
-      mx = fmax(mx, v);
+    double s0 = 0.0, s1 = 0.0, m0 = -HUGE_VAL, m1 = -HUGE_VAL;
+    const int c2 = cols & ~1;
+    for (int i = 2 * lane; i < c2; i += 64) {
+      const double2 v = *reinterpret_cast<const double2*>(A + i);
+      s0 += v.x;
+      s1 += v.y;
+      m0 = fmax(m0, v.x);
+      m1 = fmax(m1, v.y);
     }
-    sum = warp_sum(sum);
-    mx = warp_max(mx);
-    double lam = isnan(lam0_given) ? (r - sum) / (double)cols : lam0_given;
+    if ((cols & 1) && lane == 0) {
+      s0 += A[cols - 1];
+      m0 = fmax(m0, A[cols - 1]);
+    }
+    const double sum = warp_sum(s0 + s1), mx = warp_max(fmax(m0, m1));
+    const double formula = (r - sum) / (double)cols, tight = r - mx;
+    double lam = !isnan(lam0_given) ? lam0_given : (start && tight < formula ? tight : formula);
     lam = lam >= -mx ? lam : -mx;
     double lo = -HUGE_VAL, hi = HUGE_VAL, fix_hi = HUGE_VAL;
     int iterations = 0;
@@ -965,15 +1024,12 @@ __global__ void __launch_bounds__(32 * kRowWarps) spx_rows_warp_kernel(
     int m = cols;         // its length
     bool compacted = false;
     for (;;) {
-      double val = 0.0, npos = 0.0, nzero = 0.0;
-      for (int i = lane; i < m; i += 32) {
-        const double v = F[i];
-        const double t = __dadd_rn(v, lam);
-        if (!compacted && fixing && !(t > 0) && !(__dadd_rn(v, fix_hi) > 0)) continue;
-        if (t > 0) { val += t; npos += 1.0; }
-        else if (t == 0) nzero += 1.0;
-      }
-      const double value = warp_sum(val), dminus = warp_sum(npos), dplus = dminus + warp_sum(nzero);
+      double val;
+      int np, nz;
+      rows_phi(F, m, lam, fixing && !compacted && isfinite(fix_hi), fix_hi, lane, val, np, nz);
+      const double value = warp_sum(val);
+      const int npos = warp_sum_i(np), nzero = warp_sum_i(nz);
+      const double dminus = (double)npos, dplus = (double)(npos + nzero);
       double deriv;
       if (iterations == 0) {
         if (value == r) break;
@@ -988,7 +1044,7 @@ __global__ void __launch_bounds__(32 * kRowWarps) spx_rows_warp_kernel(
         if (fixing) {
           fix_hi = lam;
           // keep exactly the survivors (t > 0); compact them once they fit
-          if (dminus <= kFreeCap) {
+          if (npos <= cap) {
             int out = 0;
             for (int i0 = 0; i0 < m; i0 += 32) {
               const int i = i0 + lane;
@@ -999,8 +1055,7 @@ __global__ void __launch_bounds__(32 * kRowWarps) spx_rows_warp_kernel(
                 keep = __dadd_rn(v, lam) > 0;
               }
               const unsigned mask = __ballot_sync(0xffffffffu, keep);
-              __syncwarp();  // all reads of this block precede the writes (in-place on Bf)
-              if (keep) Bf[out + __popc(mask & lt)] = v;
+              if (keep) Bf[out + __popc(mask & lt)] = v;  // out <= i0: in-place safe
               out += __popc(mask);
             }
             __syncwarp();
@@ -1033,16 +1088,22 @@ __global__ void __launch_bounds__(32 * kRowWarps) spx_rows_warp_kernel(
       if (iterations > max_iter) break;
     }
     // x = max(0, y + lam) in place, then one bulk store
-    for (int i = lane; i < cols; i += 32) {
-      const double t = __dadd_rn(A[i], lam);
-      const double xv = t > 0 ? t : 0.0;
-      if (tma) A[i] = xv;
-      else __stcs(x + i, xv);
-    }
     if (tma) {
+      for (int i = 2 * lane; i < cols; i += 64) {
+        double2 v = *reinterpret_cast<double2*>(A + i);
+        const double t0 = __dadd_rn(v.x, lam), t1 = __dadd_rn(v.y, lam);
+        v.x = t0 > 0 ? t0 : 0.0;
+        v.y = t1 > 0 ? t1 : 0.0;
+        *reinterpret_cast<double2*>(A + i) = v;
+      }
       fence_async_smem();
       __syncwarp();
       if (lane == 0) tma_store_1d(x, A, bytes);
+    } else {
+      for (int i = lane; i < cols; i += 32) {
+        const double t = __dadd_rn(A[i], lam);
+        __stcs(x + i, t > 0 ? t : 0.0);
+      }
     }
     if (lane == 0) {
       if (lam_out) lam_out[row] = lam;
@@ -1050,7 +1111,6 @@ __global__ void __launch_bounds__(32 * kRowWarps) spx_rows_warp_kernel(
     }
     __syncwarp();
   }
-  if (lane == 0 && tma) tma_store_wait_read();
   // outstanding bulk stores complete before the grid exits (bulk_group semantics)
   if (lane == 0 && tma) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }

@@ -163,7 +163,7 @@ class ShardedProjection:
         self.x = torch.empty_like(self.y)
         torch.cuda.synchronize(self.y.device)
 
-    def solve(self, r, l1=False, opts=None):
+    def solve(self, r, l1=False, opts=None, start="tight"):
         import torch
 
         from .newton import SolveOutcome, Status
@@ -174,7 +174,7 @@ class ShardedProjection:
             opts = SolverOptions()
         h = self.handle
         h.set_stream(torch.cuda.current_stream(self.y.device).cuda_stream)
-        o = N.make_options(opts, compact_ratio=getattr(opts, "compact_ratio", None))
+        o = N.make_options(opts, compact_ratio=getattr(opts, "compact_ratio", None), start=start)
         o.tolerance_scale = opts.tau(np.float64)
         res = N.Result()
         fn = h.lib.l1_project_sharded_f64 if l1 else h.lib.spx_project_sharded_f64

@@ -1,12 +1,13 @@
 """Projections onto the simplex and the l1 ball (drop-in for cqksolve.simplex).
 
-Device route: the formula start lambda0 = (r - sum y)/n clamped to >= min(-y)
--- the reference's own `lambda0=` route of newton_project_simplex
-(simplex.py:246-250) -- followed by Algorithm 4's streamlined Newton
-iteration with variable fixing (simplex.py:256-294), all inside one
-persistent kernel.  The result equals the reference's Algorithm-2-initialised
-projection to rounding (the root does not depend on the start); iteration
-counts match the reference's `lambda0=` route.  `sharpened` and `xbar` only
+Device route: the reference's own `lambda0=` route of newton_project_simplex
+(simplex.py:246-250) with the start lambda0 = min((r - sum y)/n, r - max y)
+(both are upper bounds of the root; "formula" selects the first alone),
+followed by Algorithm 4's streamlined Newton iteration with variable fixing
+(simplex.py:256-294), all inside one persistent kernel.  The result equals the
+reference's Algorithm-2-initialised projection to rounding (the root does not
+depend on the start); iteration counts match the reference's `lambda0=` route
+with the same start.  `sharpened` and `xbar` only
 steer the reference's sequential Gauss-Seidel initialiser and therefore do
 not change the device result.
 """
@@ -55,7 +56,7 @@ def _prep(y):
     return np.ascontiguousarray(y, dtype=np.float64), y.dtype, False
 
 
-def _project(y, r, opts, lambda0, trace, l1):
+def _project(y, r, opts, lambda0, trace, l1, start="tight"):
     if opts is None:
         opts = SolverOptions()
     yv, dt, dev = _prep(y)
@@ -76,7 +77,7 @@ def _project(y, r, opts, lambda0, trace, l1):
         yp, xp = yv.ctypes.data, x.ctypes.data
         mem = N.MEM_HOST
     o = N.make_options(opts, lambda0=lambda0, trace=trace is not None,
-                       compact_ratio=getattr(opts, "compact_ratio", None))
+                       compact_ratio=getattr(opts, "compact_ratio", None), start=start)
     o.tolerance_scale = opts.tau(dt)
     res = N.Result()
     fn = h.lib.l1_project_f64 if l1 else h.lib.spx_project_f64
@@ -106,11 +107,14 @@ def _sparse(x, dev):
 
 
 def newton_project_simplex(y, r, opts=None, xbar=None, output="dense", sharpened=False,
-                           lambda0=None, trace=None):
-    """Streamlined Newton projection of y onto the level-r simplex (simplex.py:218-308)."""
+                           lambda0=None, trace=None, start="tight"):
+    """Streamlined Newton projection of y onto the level-r simplex (simplex.py:218-308).
+
+    start (B200 extension, used when lambda0 is None): "tight" =
+    min((r - sum y)/n, r - max y), "formula" = (r - sum y)/n."""
     if not r > 0:
         raise DomainError("r", None, "simplex level r must be positive")
-    x, res = _project(y, r, opts, lambda0, trace, l1=False)
+    x, res = _project(y, r, opts, lambda0, trace, l1=False, start=start)
     dev = _is_torch(x)
     sparse = None
     if output == "sparse":
@@ -121,11 +125,11 @@ def newton_project_simplex(y, r, opts=None, xbar=None, output="dense", sharpened
                         fixed_count=int(res.fixed_count), sparse=sparse, stats=res.stats())
 
 
-def project_l1(y, r, opts=None, output="dense", xbar=None):
+def project_l1(y, r, opts=None, output="dense", xbar=None, start="tight"):
     """Project y onto the l1 ball of radius r (simplex.py:311-333)."""
     if not r > 0:
         raise DomainError("r", None, "l1 radius r must be positive")
-    x, res = _project(y, r, opts, None, None, l1=True)
+    x, res = _project(y, r, opts, None, None, l1=True, start=start)
     if output == "sparse":
         dev = _is_torch(x)
         if dev:
@@ -138,16 +142,16 @@ def project_l1(y, r, opts=None, output="dense", xbar=None):
     return x
 
 
-def project_l1_outcome(y, r, opts=None):
+def project_l1_outcome(y, r, opts=None, start="tight"):
     """project_l1 with the solver statistics (B200 extension)."""
-    x, res = _project(y, r, opts, None, None, l1=True)
+    x, res = _project(y, r, opts, None, None, l1=True, start=start)
     inside = int(res.iterations) < 0
     return SolveOutcome(status=Status.SOLVED, lam=None if inside else float(res.lam), x=x,
                         iterations=int(res.iterations), phi_evals=int(res.phi_evals),
                         fixed_count=int(res.fixed_count), stats=res.stats())
 
 
-def project_simplex_rows(Y, r, opts=None, lambda0=None):
+def project_simplex_rows(Y, r, opts=None, lambda0=None, start="tight"):
     """Row-wise newton_project_simplex(Y[i], r) for a 2-d array (B200 extension, K8).
 
     Returns (X, lam[rows], iterations[rows], stats)."""
@@ -180,7 +184,7 @@ def project_simplex_rows(Y, r, opts=None, lambda0=None):
         its = np.empty(rows, np.int32)
         ptrs = (Yv.ctypes.data, X.ctypes.data, lam.ctypes.data, its.ctypes.data)
         mem = N.MEM_HOST
-    o = N.make_options(opts, lambda0=lambda0)
+    o = N.make_options(opts, lambda0=lambda0, start=start)
     o.tolerance_scale = opts.tau(np.float64)
     res = N.Result()
     rc = h.lib.spx_project_batched_f64(h.ptr, mem, ptrs[0], rows, cols, float(r), o, ptrs[1],

@@ -71,8 +71,10 @@ def test_simplex_vs_reference(rec):
 
     y = P.gen_simplex_y(rec["family"], rec["n"], rec["seed"])
     assert sha(y) == rec["sha"]
-    o = P.newton_project_simplex(y, 1.0)
-    # the device route is the reference's formula-start route: same iterations
+    tight = P.newton_project_simplex(y, 1.0)
+    assert abs(tight.lam - rec["lam"]) <= 1e-12 * max(1.0, abs(rec["lam"]))
+    o = P.newton_project_simplex(y, 1.0, start="formula")
+    # the formula-start route replays the reference's `lambda0=` route exactly
     assert o.iterations == rec["formula_iterations"]
     assert o.fixed_count == rec["formula_fixed_count"]
     assert abs(o.lam - rec["formula_lam"]) <= 1e-12 * max(1.0, abs(rec["formula_lam"]))

@@ -211,10 +211,14 @@ def test_simplex_random_vs_oracle():
         n = int(rng.integers(1, 400))
         y = rng.normal(0, 1, n)
         r = float(rng.uniform(0.1, 3))
-        out = p.newton_project_simplex(y, r)
-        lam0 = (r - O.pairwise_sum(y)) / n
-        ref = O.newton_project_simplex(y, r, lam0=lam0)
-        assert close(out.lam, ref["lam"]), (out.lam, ref["lam"])
+        for start in ("formula", "tight"):
+            out = p.newton_project_simplex(y, r, start=start)
+            lam0 = (r - O.pairwise_sum(y)) / n
+            if start == "tight":
+                lam0 = min(lam0, r - float(y.max()))
+            ref = O.newton_project_simplex(y, r, lam0=lam0)
+            assert close(out.lam, ref["lam"]), (out.lam, ref["lam"])
+            assert out.iterations == ref["iterations"], (start, out.iterations, ref["iterations"])
         assert float(np.abs(out.x - ref["x"]).max()) <= TOL * max(1.0, float(np.abs(y).max()))
         lam_star = O.exact_simplex_lambda(y, r)
         assert abs(out.lam - lam_star) <= 1e-10 * max(1.0, abs(lam_star))
@@ -267,7 +271,7 @@ def test_rows_vs_oracle():
         Y = rng.normal(0, 1, (17, cols))
         X, lam, its, _ = p.project_simplex_rows(Y, 1.0)
         for i in range(Y.shape[0]):
-            lam0 = (1.0 - O.pairwise_sum(Y[i])) / cols
+            lam0 = min((1.0 - O.pairwise_sum(Y[i])) / cols, 1.0 - float(Y[i].max()))
             ref = O.newton_project_simplex(Y[i], 1.0, lam0=lam0)
             assert close(lam[i], ref["lam"]), (cols, i, lam[i], ref["lam"])
             assert its[i] == ref["iterations"]
