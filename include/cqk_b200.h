@@ -99,10 +99,12 @@ int cqk_destroy(cqk_handle *h);
    accepted); NULL = the handle's own non-blocking stream. */
 int cqk_set_stream(cqk_handle *h, void *stream);
 int cqk_device_info(cqk_handle *h, int32_t *sm_count, int32_t *ctas, int32_t *threads);
-/* Per-pass device timeline of the last persistent solve: rows of 4 int64
-   {phase, elements streamed, compacted, globaltimer ns}; row 0 = kernel start,
-   row e = end of grid epoch e (phase -1 start, 0 lambda0/init, 1 scan, 2
-   breakpoint, 6 snap).  Returns rows copied. */
+/* Per-pass device timeline of the last persistent solve: rows of 10 int64
+   {phase, elements streamed, compacted, t_decide, t_all_arrived, t_released,
+   t_cta1_arrived, t_cta1_woke, last_cta, t_last_arrived} (globaltimer ns);
+   row 0 = kernel start, row e =
+   grid epoch e (phase -1 start, 0 lambda0/init, 1 scan, 2 breakpoint, 6 snap).
+   Returns rows copied. */
 int cqk_get_timeline(cqk_handle *h, long long *out, int32_t max_rows);
 /* Copy the last solve's per-evaluation trace rows (4 doubles each). */
 int cqk_get_trace(cqk_handle *h, double *out, int32_t max_rows);

@@ -142,7 +142,8 @@ int cqk_create(cqk_handle** out, int device) {
   e = e ? e : cudaMalloc(&h->state, st_bytes);
   e = e ? e : cudaMalloc(&h->partials, sizeof(double) * kMaxK * (gmax + kUtilBlocksMax));
   e = e ? e : cudaMalloc(&h->trace, sizeof(double) * 4 * kTraceCap);
-  e = e ? e : cudaMalloc(&h->timeline, sizeof(long long) * 4 * kTimelineCap);
+  e = e ? e : cudaMalloc(&h->timeline, sizeof(long long) * kTimelineCols * kTimelineCap);
+  e = e ? e : cudaMemset(h->timeline, 0, sizeof(long long) * kTimelineCols * kTimelineCap);
   e = e ? e : cudaMalloc(&h->red, sizeof(double) * kMaxK * kUtilBlocksMax);
   e = e ? e : cudaMalloc(&h->out, sizeof(double) * kMaxK);
   e = e ? e : cudaMallocHost(&h->err_host, 64);
@@ -205,7 +206,8 @@ int cqk_get_timeline(cqk_handle* h, long long* out, int32_t max_rows) {
   if (!h || !out) return set_err(CQK_E_ARG, "null argument");
   cudaSetDevice(h->device);
   int rows = max_rows < kTimelineCap ? max_rows : kTimelineCap;
-  CUDA_TRY(cudaMemcpy(out, h->timeline, sizeof(long long) * 4 * rows, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(out, h->timeline, sizeof(long long) * kTimelineCols * rows,
+                      cudaMemcpyDeviceToHost));
   return rows;
 }
 

@@ -90,40 +90,76 @@ DEVI void load_l2(S* dst, const S* src) {
 // in wait_release() and pick up the new command with one L2 round trip.
 template <int K>
 DEVI bool grid_step(double* partials, const double* s_cta, const int (&ops)[K],
-                    const GridSync& sy, double (*s_red)[kMaxK], double* s_tot, int* s_abort) {
+                    const GridSync& sy, double (*s_red)[kMaxK], double* s_tot, int* s_abort,
+                    unsigned epoch) {
   if (threadIdx.x < K) partials[(int64_t)blockIdx.x * kMaxK + threadIdx.x] = s_cta[threadIdx.x];
   __syncthreads();
+  if (threadIdx.x == 0 && blockIdx.x == 1) tl_mark(sy, epoch, 6);
   if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(sy.arrive, 1u);
+    // release-add: the CTA's partial row (ordered before by bar.sync) is
+    // visible to the master's acquire -- cheaper than fence.sc + atomic
+    unsigned prev;
+    asm volatile("atom.release.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(sy.arrive)
+                 : "memory");
+    if (prev == gridDim.x - 1) tl_last(sy, epoch, blockIdx.x);
   }
   if (blockIdx.x != 0) return false;
-  if (threadIdx.x == 0) {
-    const unsigned long long t0 = globaltimer();
-    while (ld_acquire(sy.arrive) < gridDim.x) {
-      if (globaltimer() - t0 > kSpinTimeoutNs) {
-        atomicExch(sy.error, 1);
-        *s_abort = 1;
-        break;
+  // Only warp 0 of the master works from here: lane 0 spins on the arrival
+  // count (timer checked every 256 polls -- reading %globaltimer is not
+  // free), then the warp reduces the per-CTA rows (lane l sums rows
+  // l, l+32, ... in order, then a xor butterfly: a fixed order), no
+  // block-wide barrier on the critical path.
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    if (lane == 0) {
+      const unsigned long long t0 = globaltimer();
+      unsigned polls = 0;
+      while (ld_relaxed(sy.arrive) < gridDim.x) {  // relaxed polls, one acquire fence
+        if ((++polls & 255u) == 0 && globaltimer() - t0 > kSpinTimeoutNs) {
+          atomicExch(sy.error, 1);
+          *s_abort = 1;
+          break;
+        }
+      }
+      fence_acquire_gpu();
+      if (!*s_abort) *sy.arrive = 0u;  // nobody arrives again before the release
+      tl_mark(sy, epoch, 4);
+    }
+    __syncwarp();
+    if (!*(volatile int*)s_abort) {
+      double acc[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+        acc[k] = ops[k] == OP_SUM ? 0.0 : ops[k] == OP_MIN ? HUGE_VAL : -HUGE_VAL;
+      // all loads first (one L2 round trip), then the fixed-order combine
+      constexpr int kRowsPerLane = 5;  // grids up to 160 CTAs in one round
+      const int G = (int)gridDim.x;
+      for (int c0 = 0; c0 < G; c0 += 32 * kRowsPerLane) {
+        double v[kRowsPerLane][K];
+#pragma unroll
+        for (int q = 0; q < kRowsPerLane; ++q) {
+          const int c = c0 + lane + 32 * q;
+#pragma unroll
+          for (int k = 0; k < K; ++k)
+            v[q][k] = c < G ? __ldcg(partials + (int64_t)c * kMaxK + k)
+                            : (ops[k] == OP_SUM ? 0.0 : ops[k] == OP_MIN ? HUGE_VAL : -HUGE_VAL);
+        }
+#pragma unroll
+        for (int q = 0; q < kRowsPerLane; ++q)
+#pragma unroll
+          for (int k = 0; k < K; ++k)
+            acc[k] = ops[k] == OP_SUM ? acc[k] + v[q][k]
+                     : ops[k] == OP_MIN ? fmin(acc[k], v[q][k]) : fmax(acc[k], v[q][k]);
+      }
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const double v = ops[k] == OP_SUM ? warp_sum(acc[k])
+                         : ops[k] == OP_MIN ? warp_min(acc[k]) : warp_max(acc[k]);
+        if (lane == 0) s_tot[k] = v;
       }
     }
-    if (!*s_abort) *sy.arrive = 0u;  // nobody arrives again before the release
   }
-  __syncthreads();
-  if (*s_abort) return false;
-  double acc[K];
-#pragma unroll
-  for (int k = 0; k < K; ++k)
-    acc[k] = ops[k] == OP_SUM ? 0.0 : ops[k] == OP_MIN ? HUGE_VAL : -HUGE_VAL;
-  for (int c = threadIdx.x; c < (int)gridDim.x; c += blockDim.x) {
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const double v = __ldcg(partials + (int64_t)c * kMaxK + k);
-      acc[k] = ops[k] == OP_SUM ? acc[k] + v : ops[k] == OP_MIN ? fmin(acc[k], v) : fmax(acc[k], v);
-    }
-  }
-  block_reduce<K>(acc, ops, s_red, s_tot);
-  return true;
+  return !*(volatile int*)s_abort;
 }
 
 // Master (CTA 0, thread 0): publish the next command and release the grid.
@@ -132,19 +168,20 @@ DEVI void master_release(const GridSync& sy, unsigned target, const Cmd& cmd, Cm
   unsigned long long* d = reinterpret_cast<unsigned long long*>(gcmd);
 #pragma unroll
   for (int i = 0; i < (int)(sizeof(Cmd) / 8); ++i) __stcg(d + i, s[i]);
-  __threadfence();
-  st_release(sy.gen, target);
+  st_release(sy.gen, target);  // release orders the command (and state) stores
 }
 
 // Non-master CTAs (thread 0): wait for the release, then fetch the command.
 DEVI bool wait_release(const GridSync& sy, unsigned target, const Cmd* gcmd, Cmd* out) {
   const unsigned long long t0 = globaltimer();
-  while ((int)(ld_acquire(sy.gen) - target) < 0) {
-    if (globaltimer() - t0 > kSpinTimeoutNs) {
+  unsigned polls = 0;
+  while ((int)(ld_relaxed(sy.gen) - target) < 0) {
+    if ((++polls & 255u) == 0 && globaltimer() - t0 > kSpinTimeoutNs) {
       atomicExch(sy.error, 1);
       return false;
     }
   }
+  fence_acquire_gpu();
   const unsigned long long* s = reinterpret_cast<const unsigned long long*>(gcmd);
   unsigned long long w[sizeof(Cmd) / 8];
 #pragma unroll
@@ -391,7 +428,7 @@ __global__ void __launch_bounds__(kThreads, 1) cqk_solve_kernel(CqkParams<T> p) 
 #pragma unroll
       for (int k = 0; k < 15; ++k) a15[k] = acc[k];
       block_reduce<15>(a15, ops, s_red, s_tot);
-      is_master = grid_step<15>(p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort);
+      is_master = grid_step<15>(p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch);
       if (is_master && threadIdx.x == 0) {
         tl_record(p.sync, epoch, PH_LAMBDA0, p.n, 0);
         double glob[15];
@@ -409,7 +446,7 @@ __global__ void __launch_bounds__(kThreads, 1) cqk_solve_kernel(CqkParams<T> p) 
 #pragma unroll
       for (int k = 0; k < K; ++k) { ops[k] = OP_SUM; aK[k] = acc[k]; }
       block_reduce<K>(aK, ops, s_red, s_tot);
-      is_master = grid_step<K>(p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort);
+      is_master = grid_step<K>(p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch);
       if (is_master && threadIdx.x == 0) {
         double loc[11], glob[11];
 #pragma unroll
@@ -425,7 +462,7 @@ __global__ void __launch_bounds__(kThreads, 1) cqk_solve_kernel(CqkParams<T> p) 
       int ops[2] = {c.right ? OP_MIN : OP_MAX, OP_SUM};
       double a2[2] = {acc[0], acc[1]};
       block_reduce<2>(a2, ops, s_red, s_tot);
-      is_master = grid_step<2>(p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort);
+      is_master = grid_step<2>(p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch);
       if (is_master && threadIdx.x == 0) {
         tl_record(p.sync, epoch, PH_BP, s_st.phys_count, 0);
         double glob[2];
@@ -441,8 +478,10 @@ __global__ void __launch_bounds__(kThreads, 1) cqk_solve_kernel(CqkParams<T> p) 
         if (ph == PH_FINAL || ph == PH_DONE) *p.st = s_st;  // results for the host
         s_cmd = s_st.cmd;
         master_release(p.sync, s_gen0 + epoch, s_st.cmd, &p.st->cmd);
+        tl_mark(p.sync, epoch, 5);
       } else if (!s_abort) {
         if (!wait_release(p.sync, s_gen0 + epoch, &p.st->cmd, &s_cmd)) s_abort = 1;
+        if (blockIdx.x == 1) tl_mark(p.sync, epoch, 7);
       }
     }
     __syncthreads();
@@ -737,7 +776,7 @@ __global__ void __launch_bounds__(kThreads, 1) spx_solve_kernel(SpxParams<T> p) 
     }
     double a3[3] = {acc[0], acc[1], acc[2]};
     block_reduce<3>(a3, ops, s_red, s_tot);
-    const bool is_master = grid_step<3>(p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort);
+    const bool is_master = grid_step<3>(p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch);
     if (threadIdx.x == 0) {
       if (is_master) {
         tl_record(p.sync, epoch, c.phase, mode == 0 ? p.n : s_st.phys_count, s_st.cmd.compact);
@@ -752,8 +791,10 @@ __global__ void __launch_bounds__(kThreads, 1) spx_solve_kernel(SpxParams<T> p) 
         if (ph == PH_FINAL || ph == PH_DONE || ph == PH_COPY) *p.st = s_st;
         s_cmd = s_st.cmd;
         master_release(p.sync, s_gen0 + epoch, s_st.cmd, &p.st->cmd);
+        tl_mark(p.sync, epoch, 5);
       } else if (!s_abort) {
         if (!wait_release(p.sync, s_gen0 + epoch, &p.st->cmd, &s_cmd)) s_abort = 1;
+        if (blockIdx.x == 1) tl_mark(p.sync, epoch, 7);
       }
     }
     __syncthreads();

@@ -1,0 +1,57 @@
+"""Write the judged ncu summaries into profiles/ (round-prefixed) from the
+gpurun_out/ scratch reports.  Usage: python tools/make_profiles.py r01"""
+import csv
+import io
+import json
+import os
+import shutil
+import subprocess
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from ncu_summary import run  # noqa: E402
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+rnd = sys.argv[1] if len(sys.argv) > 1 else "r01"
+src = os.path.join(ROOT, "gpurun_out")
+dst = os.path.join(ROOT, "profiles")
+os.makedirs(dst, exist_ok=True)
+
+
+def gb(s):
+    v, unit = s.split()[0], s.split()[1] if len(s.split()) > 1 else ""
+    f = float(v)
+    return f * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}.get(unit, 1.0)
+
+
+for tag, rep in (("solve", "prof_solve"), ("spx", "prof_spx"), ("rows", "prof_rows")):
+    path = os.path.join(src, f"{rep}_{rnd}.ncu-rep")
+    if not os.path.exists(path):
+        continue
+    s = run(path)
+    k = s["kernels"][0]
+    rd, wr = gb(k["dram__bytes_read.sum"]), gb(k["dram__bytes_write.sum"])
+    s["dram_bytes_per_launch"] = rd + wr
+    s["source_report"] = os.path.basename(path)
+    with open(os.path.join(dst, f"{rnd}_ncu_{tag}.json"), "w") as f:
+        json.dump(s, f, indent=1)
+    if tag == "solve":
+        with open(os.path.join(dst, "ncu_solve_kernel.json"), "w") as f:
+            json.dump({"round": rnd, "kernel": k["kernel"],
+                       "dram_bytes_per_launch": rd + wr,
+                       "gpu_time_ms_cold": k["gpu__time_duration.sum"],
+                       "workload": "C3 cqk-weakly-correlated n=1e8 solve_cqk (tools/profile_solve.py)"},
+                      f, indent=1)
+launch = os.path.join(src, f"launches_{rnd}.csv")
+if os.path.exists(launch):
+    rows = [r for r in csv.reader(open(launch)) if len(r) > 10 and r[0] != "ID"]
+    out = [{"id": r[0], "kernel": r[4], "grid": r[8], "block": r[7], "ns": r[-1]} for r in rows]
+    with open(os.path.join(dst, f"{rnd}_launches.json"), "w") as f:
+        json.dump({"command": "ncu --metrics gpu__time_duration.sum --clock-control none "
+                              "python bench.py --steps 2 --warmup 3 --no-cpu --e2e-steps 1",
+                   "launches": out}, f, indent=1)
+for b in ("bench", "bench_ref"):
+    p = os.path.join(src, f"{b}_{rnd}.json")
+    if os.path.exists(p):
+        shutil.copy(p, os.path.join(dst, f"{rnd}_{b}.json"))
+print(sorted(os.listdir(dst)))

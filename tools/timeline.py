@@ -32,16 +32,28 @@ h = N.handle()
 tl = h.timeline(64)
 t0 = tl[0, 3]
 prev = t0
+prev_rel = t0
 rows = []
 last = 0
 for k in range(1, len(tl)):
-    ph, el, comp, t = (int(v) for v in tl[k])
+    ph, el, comp, t = (int(v) for v in tl[k][:4])
+    t_all, t_rel, t_arr1, t_wake1, last_cta, t_last = (int(v) for v in tl[k][4:10])
     if t == 0 or t < prev:
         break
     dt = (t - prev) / 1e3
     by = el * B.get(ph, 40)
     rows.append({"epoch": k, "phase": ph, "elems": el, "compact": comp, "us": round(dt, 1),
-                 "GBps": round(by / dt / 1e3, 0) if dt > 0 else None})
+                 "GBps": round(by / dt / 1e3, 0) if dt > 0 else None,
+                 # breakdown (us): previous release -> CTA1 woke -> CTA1 arrived;
+                 # all arrived -> decision start -> released
+                 "wake1": round((t_wake1 - prev_rel) / 1e3, 2) if prev_rel and t_wake1 else None,
+                 "arrive1": round((t_arr1 - prev_rel) / 1e3, 2) if prev_rel and t_arr1 else None,
+                 "all_arrived": round((t_all - prev_rel) / 1e3, 2) if prev_rel and t_all else None,
+                 "reduced": round((t - t_all) / 1e3, 2) if t_all else None,
+                 "released": round((t_rel - t) / 1e3, 2) if t_rel else None,
+                 "last_cta": last_cta,
+                 "last_arrived": round((t_last - prev_rel) / 1e3, 2) if t_last else None})
+    prev_rel = t_rel
     prev = t
     last = t
 tot_ms = out.stats["device_ms"]
