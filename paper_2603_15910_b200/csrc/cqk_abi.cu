@@ -538,7 +538,7 @@ static int solve_impl(cqk_handle* h, int mem, const double* d, const double* a, 
   res->bracket_lo = s.lo;
   res->bracket_hi = s.hi;
   const int64_t pass0 = (opts.check || !lam0_given) ? n : 0;
-  const int64_t bytes0 = (opts.check || xbar) ? (xbar ? 48 : 40) : 24;
+  const int64_t bytes0 = xbar ? 48 : 24;  // l, u are validated on the first scan
   const int64_t fin = (s.status == ST_SOLVED && xo) ? n : 0;
   res->elems_read = pass0 + s.elems_scan + s.elems_bp + fin;
   res->elems_written = s.elems_written + fin;

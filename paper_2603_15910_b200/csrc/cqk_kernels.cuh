@@ -200,17 +200,17 @@ DEVI void lambda0_pass(const CqkParams<T>& p, int64_t seg_lo, int64_t m, double 
   const int lane = threadIdx.x & 31;
   const T* const pf[5] = {p.d + seg_lo, p.a + seg_lo, p.b + seg_lo, p.l + seg_lo, p.u + seg_lo};
   const T* const pf3[3] = {pf[0], pf[1], pf[2]};
-  if (CHECK || XBAR) prefetch_chunks<T, 5>(pf, 0, c_prefetch[0], m, lane);
+  if (XBAR) prefetch_chunks<T, 5>(pf, 0, c_prefetch[0], m, lane);
   else prefetch_chunks<T, 3>(pf3, 0, c_prefetch[0], m, lane);
   for (int64_t base = 0; base < m; base += CH) {
-    if (CHECK || XBAR) prefetch_chunks<T, 5>(pf, base / CH + c_prefetch[0], c_prefetch[0] > 0 ? 1 : 0, m, lane);
+    if (XBAR) prefetch_chunks<T, 5>(pf, base / CH + c_prefetch[0], c_prefetch[0] > 0 ? 1 : 0, m, lane);
     else prefetch_chunks<T, 3>(pf3, base / CH + c_prefetch[0], c_prefetch[0] > 0 ? 1 : 0, m, lane);
     const bool full = base + CH <= m;
     T D[E], A[E], B[E], L[E], U[E], X[E];
     load_chunk<T, false>(p.d + seg_lo, base, m, lane, full, T(1), D);
     load_chunk<T, false>(p.a + seg_lo, base, m, lane, full, T(0), A);
     load_chunk<T, false>(p.b + seg_lo, base, m, lane, full, T(1), B);
-    if (CHECK || XBAR) {
+    if (XBAR) {  // l, u are otherwise validated during the first scan
       load_chunk<T, false>(p.l + seg_lo, base, m, lane, full, T(0), L);
       load_chunk<T, false>(p.u + seg_lo, base, m, lane, full, T(0), U);
     }
@@ -231,19 +231,34 @@ DEVI void lambda0_pass(const CqkParams<T>& p, int64_t seg_lo, int64_t m, double 
         if (!isfinite((double)d)) acc[5] = fmin(acc[5], gi);
         if (!isfinite((double)a)) acc[6] = fmin(acc[6], gi);
         if (!isfinite((double)b)) acc[7] = fmin(acc[7], gi);
-        if (isnan((double)l)) acc[8] = fmin(acc[8], gi);
-        if (isnan((double)u)) acc[9] = fmin(acc[9], gi);
         if (!(d > T(0))) acc[10] = fmin(acc[10], gi);
         if (!(b > T(0))) acc[11] = fmin(acc[11], gi);
-        if (!(l <= u)) acc[12] = fmin(acc[12], gi);
-        if ((double)l == HUGE_VAL) acc[13] = fmin(acc[13], gi);
-        if ((double)u == -HUGE_VAL) acc[14] = fmin(acc[14], gi);
+        if (XBAR) {
+          if (isnan((double)l)) acc[8] = fmin(acc[8], gi);
+          if (isnan((double)u)) acc[9] = fmin(acc[9], gi);
+          if (!(l <= u)) acc[12] = fmin(acc[12], gi);
+          if ((double)l == HUGE_VAL) acc[13] = fmin(acc[13], gi);
+          if ((double)u == -HUGE_VAL) acc[14] = fmin(acc[14], gi);
+        }
       }
     }
   }
 }
 
-template <typename T, bool FIX, bool SRC_SCRATCH>
+// validate()'s l / u checks on the first scan: segment-local first index per
+// check in 32-bit registers (cheap in the register-tight scan loop), turned
+// into global double indices in slots 11..15 after the loop.
+constexpr int kCheckLuSlot = 11;  // slots 11..15: l NaN, u NaN, l<=u, l!=+inf, u!=-inf
+template <typename T>
+DEVI void check_lu(T l, T u, unsigned li, unsigned (&first)[5]) {
+  if (isnan((double)l)) first[0] = min(first[0], li);
+  if (isnan((double)u)) first[1] = min(first[1], li);
+  if (!(l <= u)) first[2] = min(first[2], li);
+  if ((double)l == HUGE_VAL) first[3] = min(first[3], li);
+  if ((double)u == -HUGE_VAL) first[4] = min(first[4], li);
+}
+
+template <typename T, bool FIX, bool SRC_SCRATCH, bool CHK = false>
 DEVI void scan_pass(const CqkParams<T>& p, const Cmd& c, int64_t seg_lo, int64_t& m,
                     bool compact, double (&acc)[kMaxK]) {
   constexpr int E = Vec<T>::n * kUnroll, CH = 32 * E;
@@ -258,6 +273,7 @@ DEVI void scan_pass(const CqkParams<T>& p, const Cmd& c, int64_t seg_lo, int64_t
   const unsigned lt = (1u << lane) - 1u;
   const T* const pf[5] = {sd, sa, sb, sl, su};
   prefetch_chunks<T, 5>(pf, 0, c_prefetch[0], m, lane);
+  unsigned first[5] = {~0u, ~0u, ~0u, ~0u, ~0u};
   int64_t out_m = 0;
   for (int64_t base = 0; base < m; base += CH) {
     prefetch_chunks<T, 5>(pf, base / CH + c_prefetch[0], c_prefetch[0] > 0 ? 1 : 0, m, lane);
@@ -272,6 +288,7 @@ DEVI void scan_pass(const CqkParams<T>& p, const Cmd& c, int64_t seg_lo, int64_t
 #pragma unroll
     for (int j = 0; j < E; ++j) {
       const bool valid = full || chunk_index<T>(base, lane, j) < m;
+      if (CHK && valid) check_lu<T>(L[j], U[j], (unsigned)chunk_index<T>(base, lane, j), first);
       keep[j] = valid && elem_scan<T, FIX>(D[j], A[j], B[j], L[j], U[j], lam, fhi, flo, chk_lo,
                                            chk_hi, acc);
     }
@@ -290,6 +307,11 @@ DEVI void scan_pass(const CqkParams<T>& p, const Cmd& c, int64_t seg_lo, int64_t
     }
   }
   if (FIX && compact) m = out_m;
+  if (CHK) {
+#pragma unroll
+    for (int k = 0; k < 5; ++k)
+      if (first[k] != ~0u) acc[kCheckLuSlot + k] = (double)(p.offset + seg_lo + (int64_t)first[k]);
+  }
 }
 
 template <typename T, bool SRC_SCRATCH>
@@ -434,6 +456,33 @@ __global__ void __launch_bounds__(kThreads, 1) cqk_solve_kernel(CqkParams<T> p) 
         double glob[15];
         if (exchange_totals(p.ex, epoch, 15, ops, s_tot, glob)) m_after_lambda0(s_st, glob);
         else m_stop(s_st, ST_TIMEOUT);
+      }
+    } else if (c.phase == PH_SCAN && c.check_lu) {
+      // first scan (original arrays, never compacting) with validate()'s l / u checks
+#pragma unroll
+      for (int k = kCheckLuSlot; k < kMaxK; ++k) acc[k] = HUGE_VAL;
+      scan_pass<T, FIX, false, true>(p, c, seg_lo, m, false, acc);
+      int ops[kMaxK];
+#pragma unroll
+      for (int k = 0; k < kMaxK; ++k) ops[k] = k < kCheckLuSlot ? OP_SUM : OP_MIN;
+      block_reduce<kMaxK>(acc, ops, s_red, s_tot);
+      is_master = grid_step<kMaxK>(p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch);
+      if (is_master && threadIdx.x == 0) {
+        double loc[kMaxK], glob[kMaxK];
+#pragma unroll
+        for (int k = 0; k < kMaxK; ++k) loc[k] = s_tot[k];
+        tl_record(p.sync, epoch, PH_SCAN, s_st.phys_count, 0);
+        if (!exchange_totals(p.ex, epoch, kMaxK, ops, loc, glob)) {
+          m_stop(s_st, ST_TIMEOUT);
+        } else {
+          s_st.cmd.check_lu = 0;
+          s_st.vidx[3] = glob[11];  // l NaN
+          s_st.vidx[4] = glob[12];  // u NaN
+          s_st.vidx[7] = glob[13];  // l <= u
+          s_st.vidx[8] = glob[14];  // l == +inf
+          s_st.vidx[9] = glob[15];  // u == -inf
+          if (m_validate(s_st, 3, 10)) m_after_scan(s_st, glob, loc, p.trace);
+        }
       }
     } else if (c.phase == PH_SCAN) {
       const bool compact = FIX && c.compact;

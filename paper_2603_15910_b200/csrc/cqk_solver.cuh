@@ -58,7 +58,7 @@ struct Cmd {
   int32_t phase;
   int32_t compact;  // this scan writes the survivors into scratch
   int32_t right;    // PH_BP direction
-  int32_t pad;
+  int32_t check_lu; // this (first) scan also validates l and u
 };
 
 // Master-side solver state (SolveState, newton.py:70-90, plus counters).
@@ -72,6 +72,7 @@ struct CqkState {
   int64_t fixed_local;                  // logically fixed elements of this rank
   int64_t elems_scan, elems_written, elems_bp;  // byte-model counters (this rank)
   int64_t domain_index;
+  double vidx[10];  // first offending index per validate() check (pass 0 / first scan)
   int32_t has_plo, has_phi, fixing, variant, status, has_xbar, check, domain_field;
   int32_t trace_len, trace_cap, lam0_given, pad;
 };
@@ -236,19 +237,39 @@ DEVI void m_after_bp(CqkState& s, const double* tot) {
 // tot: 0 s_all, 1 q_all, 2 s_J, 3 q_J, 4 |J|, 5..14 first offending index of
 // the ten validate() checks in the reference's order (core.py:186-216).
 constexpr int kValidateSlot = 5;
+// The checks in the reference's order: d,a,b finite; l,u NaN; r finite;
+// d>0; b>0; l<=u; l!=+inf; u!=-inf.  Classes c0 <= c < c1 are decided.
+DEVI bool m_validate(CqkState& s, int c0, int c1) {
+  const int32_t field_of[10] = {0, 1, 2, 3, 4, 0, 2, 6, 3, 4};
+  for (int c = c0; c < c1; ++c) {
+    if (c == 5 && !isfinite(s.r_orig)) {
+      s.domain_field = 5;
+      s.domain_index = -1;
+      m_stop(s, ST_DOMAIN);
+      return false;
+    }
+    if (s.vidx[c] < (double)s.n) {
+      s.domain_field = field_of[c];
+      s.domain_index = (int64_t)s.vidx[c];
+      m_stop(s, ST_DOMAIN);
+      return false;
+    }
+  }
+  return true;
+}
+
+// pass 0 checked d, a, b (and l, u only when xbar made it read them); the
+// l / u checks otherwise ride on the first phi scan, which reads l and u
+// anyway -- the verdict (the first failing check in the reference's order)
+// is identical, 16 B/element cheaper.
 DEVI void m_after_lambda0(CqkState& s, const double* tot) {
   if (s.check) {
-    // order: d,a,b finite; l,u NaN; r finite; d>0; b>0; l<=u; l!=+inf; u!=-inf
-    const int32_t field_of[10] = {0, 1, 2, 3, 4, 0, 2, 6, 3, 4};
-    for (int c = 0; c < 10; ++c) {
-      if (c == 5 && !isfinite(s.r_orig)) { s.domain_field = 5; s.domain_index = -1; m_stop(s, ST_DOMAIN); return; }
-      const double i = tot[kValidateSlot + c];
-      if (i < (double)s.n) {
-        s.domain_field = field_of[c];
-        s.domain_index = (int64_t)i;
-        m_stop(s, ST_DOMAIN);
-        return;
-      }
+    for (int c = 0; c < 10; ++c) s.vidx[c] = tot[kValidateSlot + c];
+    if (s.has_xbar) {
+      if (!m_validate(s, 0, 10)) return;
+    } else {
+      if (!m_validate(s, 0, 3)) return;  // d, a, b finiteness precede everything
+      s.cmd.check_lu = 1;
     }
   }
   if (!s.lam0_given) {
