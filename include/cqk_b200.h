@@ -64,7 +64,9 @@ typedef struct {
   int32_t record_trace;     /* keep (lam, phi, dminus, dplus) per phi evaluation */
   int32_t simplex_start;    /* simplex / l1 start when lambda0 is NaN: 0 = (r - sum y)/n,
                                1 = min((r - sum y)/n, r - max y) (both upper bounds;
-                               the reference's `lambda0=` route, simplex.py:246-250) */
+                               the reference's `lambda0=` route, simplex.py:246-250),
+                               2 = chunked Algorithm 2 (simplex.py:243-245 route with
+                               par_simplex_init, parallel.py:330-368) */
 } cqk_options;
 
 /* SolveOutcome (newton.py:93-103) plus measurement counters. */
@@ -154,6 +156,17 @@ int spx_project_f64(cqk_handle *h, int mem, const double *y, int64_t n, double r
    already inside the ball (x = copy of y). */
 int l1_project_f64(cqk_handle *h, int mem, const double *y, int64_t n, double r,
                    const cqk_options *opts, double *x, cqk_result *res);
+/* simplex_init_lambda (simplex.py:114-154; workers = 1) and par_simplex_init
+   (parallel.py:330-368; workers = W chunks as _chunk_ranges): Algorithm 2 per
+   chunk on the device (one thread per chunk, bit-exact recurrence) merged in
+   _tree_sum order.  idx (length p) selects candidates (NULL = all n); xbar and
+   sharpened as the reference.  Outputs: lambda0, |free|, free indices
+   (concatenated J; may be NULL), fixed_mask (length n; may be NULL), sum over
+   the free set, total jplus (for the xbar fallback; may be NULL). */
+int spx_init_alg2_f64(cqk_handle *h, int mem, const double *y, int64_t n, double r,
+                      const int64_t *idx, int64_t p, int64_t workers, const double *xbar,
+                      int sharpened, double *lam0, int64_t *nfree, int64_t *free_idx,
+                      uint8_t *fixed_mask, double *sum_free, int64_t *jplus);
 /* Row-wise newton_project_simplex(Y[i], r) for `rows` independent rows of
    length `cols` (row-major).  lam/iters per row may be NULL. */
 int spx_project_batched_f64(cqk_handle *h, int mem, const double *Y, int64_t rows,

@@ -81,6 +81,8 @@ def lib():
         L.orc_newton_project_simplex.argtypes = [_D, i64, dbl, i32, i64, dbl, _D, i32, dbl,
                                                  _D, _D, i64, R]
         L.orc_project_l1.argtypes = [_D, i64, dbl, i32, i64, dbl, _D, _D, R]
+        L.orc_par_simplex_init.argtypes = [_D, i64, dbl, i32, _D, _I64, _I64, _U8, _D]
+        L.orc_newton_simplex_from.argtypes = [_D, i64, dbl, i32, i64, dbl, dbl, _I64, i64, _D, R]
         L.orc_exact_simplex_lambda.argtypes = [_D, i64, dbl]
         L.orc_exact_simplex_lambda.restype = dbl
         _lib = L
@@ -257,3 +259,29 @@ def project_l1(y, r, fixing=True, max_iter=100, tau=TAU64, xbar=None):
 def exact_simplex_lambda(y, r):
     y = _f64(y)
     return lib().orc_exact_simplex_lambda(_p(y), y.size, float(r))
+
+
+def par_simplex_init(y, r, workers=1):
+    """parallel.py:330-368 -> (lambda0, free, fixed_mask, sum_free)."""
+    y = _f64(y)
+    n = y.size
+    free = np.empty(n, np.int64)
+    nf = ctypes.c_int64()
+    fixed = np.zeros(n, np.uint8)
+    lam = ctypes.c_double()
+    sj = ctypes.c_double()
+    lib().orc_par_simplex_init(_p(y), n, float(r), int(workers), ctypes.byref(lam), _p(free, _I64),
+                               ctypes.byref(nf), _p(fixed, _U8), ctypes.byref(sj))
+    return lam.value, free[: nf.value].copy(), fixed.astype(bool), sj.value
+
+
+def newton_simplex_from(y, r, lam0, free, fixing=True, max_iter=100, tau=TAU64, want_x=True):
+    """Algorithm 4 from (lam0, free set) without the lambda0= clamp."""
+    y = _f64(y)
+    f = np.ascontiguousarray(free, dtype=np.int64)
+    x = np.empty(y.size) if want_x else None
+    res = Result()
+    st = lib().orc_newton_simplex_from(_p(y), y.size, float(r), int(fixing), int(max_iter),
+                                       float(tau), float(lam0), _p(f, _I64), f.size, _p(x),
+                                       ctypes.byref(res))
+    return _finish(st, res, x)

@@ -763,6 +763,51 @@ int orc_simplex_init_lambda(const double *y, int64_t n, double r,
   return 0;
 }
 
+/* parallel.py:330-368 par_simplex_init: Algorithm 2 per contiguous chunk
+ * (chunks as _chunk_ranges), merged with _tree_sum; free = concatenated J. */
+int orc_par_simplex_init(const double *y, int64_t n, double r, int workers, double *lam,
+                         int64_t *free_out, int64_t *nfree, uint8_t *fixed_mask, double *sumJ) {
+  if (workers < 1) workers = 1;
+  int64_t *clo = xmalloc(sizeof(int64_t) * workers), *chi = xmalloc(sizeof(int64_t) * workers);
+  int nch = chunk_ranges(n, workers, clo, chi);
+  double *sums = xmalloc(sizeof(double) * nch);
+  int64_t *cnt = xmalloc(sizeof(int64_t) * nch);
+  memset(fixed_mask, 0, n);
+  int64_t *J = xmalloc(sizeof(int64_t) * n), *Jt = xmalloc(sizeof(int64_t) * n);
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int k = 0; k < nch; ++k) {
+    int64_t p = chi[k] - clo[k], *idx = xmalloc(sizeof(int64_t) * p), jp;
+    for (int64_t j = 0; j < p; ++j) idx[j] = clo[k] + j;
+    init_kernel(y, r, idx, p, NULL, 0, J + clo[k], fixed_mask, Jt + clo[k], &cnt[k], &sums[k], &jp);
+    free(idx);
+  }
+  int64_t tot = 0;
+  for (int k = 0; k < nch; ++k) {
+    memmove(free_out + tot, J + clo[k], sizeof(int64_t) * cnt[k]);
+    tot += cnt[k];
+  }
+  double s = tree_sum(sums, nch);
+  *sumJ = s;
+  *nfree = tot;
+  *lam = (r - s) / (double)tot;
+  free(clo); free(chi); free(sums); free(cnt); free(J); free(Jt);
+  return 0;
+}
+
+static int newton_simplex_loop(const double *y, int64_t n, double r, int fixing,
+                               int64_t max_iter, double tau, double lam, int64_t *free_,
+                               int64_t m, double *x, double *trace, int64_t trace_cap,
+                               orc_result *res);
+
+/* Algorithm 4 from a given start and free set (the loop of simplex.py:252-308) */
+int orc_newton_simplex_from(const double *y, int64_t n, double r, int fixing, int64_t max_iter,
+                            double tau, double lam0, const int64_t *free_idx, int64_t m,
+                            double *x, orc_result *res) {
+  int64_t *f = xmalloc(sizeof(int64_t) * n);
+  memcpy(f, free_idx, sizeof(int64_t) * m);
+  return newton_simplex_loop(y, n, r, fixing, max_iter, tau, lam0, f, m, x, NULL, 0, res);
+}
+
 /* simplex.py:218-308, dense output. */
 int orc_newton_project_simplex(const double *y, int64_t n, double r,
                                int fixing, int64_t max_iter, double tau,
@@ -786,6 +831,15 @@ int orc_newton_project_simplex(const double *y, int64_t n, double r,
     for (int64_t i = 0; i < n; ++i) free_[i] = i;
     m = n;
   }
+  return newton_simplex_loop(y, n, r, fixing, max_iter, tau, lam, free_, m, x, trace, trace_cap,
+                             res);
+}
+
+/* takes ownership of free_ */
+static int newton_simplex_loop(const double *y, int64_t n, double r, int fixing,
+                               int64_t max_iter, double tau, double lam, int64_t *free_,
+                               int64_t m, double *x, double *trace, int64_t trace_cap,
+                               orc_result *res) {
   double lam_init = lam;
   int64_t fixed_count = n - m, iterations = 0, phi_evals = 0;
   double lo = -INFINITY, hi = INFINITY;

@@ -116,6 +116,17 @@ int orc_newton_project_simplex(const double *y, int64_t n, double r,
                                double *x, double *trace, int64_t trace_cap,
                                orc_result *res);
 
+/* parallel.py:330-368 par_simplex_init (chunked Algorithm 2 + merge). */
+int orc_par_simplex_init(const double *y, int64_t n, double r, int workers, double *lam,
+                         int64_t *free_out, int64_t *nfree, uint8_t *fixed_mask, double *sumJ);
+
+/* The Newton loop of simplex.py:252-308 from a given start lam0 (no clamp)
+   and free index set (the route newton_project_simplex takes after its
+   initializer). */
+int orc_newton_simplex_from(const double *y, int64_t n, double r, int fixing, int64_t max_iter,
+                            double tau, double lam0, const int64_t *free_idx, int64_t m,
+                            double *x, orc_result *res);
+
 /* simplex.py:311-333 project_l1 (dense).  Returns status; res->iterations = -1
    when y is inside the ball (copy). */
 int orc_project_l1(const double *y, int64_t n, double r, int fixing,

@@ -87,7 +87,7 @@ EXPORTS = (
     "spx_project_f64", "l1_project_f64", "spx_project_batched_f64", "cqk_selftest_division",
     "cqk_comm_ipc_handle_size", "cqk_comm_create", "cqk_comm_connect", "cqk_comm_connect_local",
     "cqk_set_grid_limit", "cqk_reserve", "cqk_solve_sharded_f64", "spx_project_sharded_f64",
-    "l1_project_sharded_f64",
+    "l1_project_sharded_f64", "spx_init_alg2_f64",
 )
 
 _lib = None
@@ -137,6 +137,9 @@ def _declare(L):
                                         _P, _RES]
     L.spx_project_sharded_f64.argtypes = [_P, ctypes.c_int, _P, _I64, _I64, _D, _OPT, _P, _RES]
     L.l1_project_sharded_f64.argtypes = [_P, ctypes.c_int, _P, _I64, _I64, _D, _OPT, _P, _RES]
+    L.spx_init_alg2_f64.argtypes = [_P, ctypes.c_int, _P, _I64, _D, _P, _I64, _I64, _P,
+                                    ctypes.c_int, ctypes.POINTER(_D), ctypes.POINTER(_I64), _P,
+                                    _P, ctypes.POINTER(_D), ctypes.POINTER(_I64)]
     L.spx_project_batched_f64.argtypes = [_P, ctypes.c_int, _P, _I64, _I64, _D, _OPT, _P, _P,
                                           _P, _RES]
 
@@ -258,5 +261,5 @@ def make_options(opts=None, variant=VARIANT_SOLVE, check=True, lambda0=None,
     o.lambda0 = math.nan if lambda0 is None else float(lambda0)
     o.compact_ratio = math.nan if compact_ratio is None else float(compact_ratio)
     o.record_trace = 1 if trace else 0
-    o.simplex_start = {"formula": 0, "tight": 1}[start]
+    o.simplex_start = {"formula": 0, "tight": 1, "alg2": 2}[start]
     return o

@@ -13,6 +13,7 @@
 #include <limits>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/cqk_b200.h"
 #include "cqk_kernels.cuh"
@@ -81,7 +82,11 @@ struct cqk_handle {
   long long* timeline = nullptr;
   double* red = nullptr;     // utility partials
   double* out = nullptr;     // utility outputs (kMaxK doubles)
-  Buf scratch, stage, idxbuf, flags;
+  Buf scratch, stage, idxbuf, flags, alg2;
+  double* alg2_vals = nullptr;        // gathered free values of the last Algorithm-2 run
+  int64_t* alg2_idx = nullptr;        // ... and their global indices
+  int64_t* alg2_jplus = nullptr;
+  int64_t alg2_w = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int trace_len = 0;
   int grid_limit = 0;                 // 0: full device (virtual ranks share a GPU)
@@ -169,6 +174,7 @@ int cqk_destroy(cqk_handle* h) {
   h->stage.release();
   h->idxbuf.release();
   h->flags.release();
+  h->alg2.release();
   for (int q = 0; q < kMaxRanks; ++q)
     if (h->ipc_opened[q] && h->peers[q]) cudaIpcCloseMemHandle(h->peers[q]);
   if (h->mbox) cudaFree(h->mbox);
@@ -552,6 +558,103 @@ static int solve_impl(cqk_handle* h, int mem, const double* d, const double* a, 
 // ------------------------------------------------------------ simplex / l1
 namespace {
 
+// Enqueue one persistent simplex / l1 solve (state H2D, launch, state and
+// timeout flag D2H) on the handle's stream; the caller synchronises.
+int launch_spx(cqk_handle* h, SpxState& s, const double* yv, int64_t n, double* xo, bool l1,
+               bool sharded) {
+  if (s.fixing) CUDA_TRY(h->scratch.ensure(((size_t)n * sizeof(double) + 255) / 256 * 256));
+  std::memcpy(h->host_state, &s, sizeof s);  // pinned staging: fully asynchronous
+  CUDA_TRY(cudaMemcpyAsync(h->state, h->host_state, sizeof s, cudaMemcpyHostToDevice, h->stream));
+  SpxParams<double> p;
+  std::memset(&p, 0, sizeof p);
+  p.y = yv;
+  p.sy = s.fixing ? (double*)h->scratch.p : nullptr;
+  p.x = xo;
+  p.trace = h->trace;
+  p.n = n;
+  p.st = (SpxState*)h->state;
+  p.ex = make_exchange(h, sharded);
+  p.partials = h->partials;
+  p.sync.arrive = h->sync;
+  p.sync.gen = h->sync + 1;
+  p.sync.error = (int*)(h->sync + 2);
+  p.sync.timeline = h->timeline;
+  void* args[] = {&p};
+  const int grid = limit_grid(h, l1 ? h->grid_l1 : h->grid_spx);
+  const void* fn = l1 ? (const void*)spx_solve_kernel<double, true>
+                      : (const void*)spx_solve_kernel<double, false>;
+  CUDA_TRY(cudaLaunchCooperativeKernel(fn, grid, kThreads, args, 0, h->stream));
+  CUDA_TRY(cudaMemcpyAsync(h->host_state, h->state, sizeof s, cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(cudaMemcpyAsync(h->err_host, h->sync + 2, sizeof(unsigned), cudaMemcpyDeviceToHost,
+                           h->stream));
+  return 0;
+}
+
+// Chunked Algorithm 2 (par_simplex_init semantics) on the device: W chunks,
+// merged lambda0, gathered free set.  Results stay in h->alg2; `out` is the
+// merged summary (copied back, stream synchronised).
+int run_alg2(cqk_handle* h, const double* yv, const int64_t* idx, int64_t p, double r, int64_t W,
+             const double* xbar, int sharpened, bool l1, bool want_vals, bool want_idx,
+             uint8_t* fixed_dev, Alg2Out* out) {
+  if (W < 1) {  // auto: chunks of >= 256 elements (a chunk must be long enough
+                // for its multiplier to prove zeros), at most one per GPU thread
+    int64_t chunk = 256;
+    if (const char* e = getenv("CQK_ALG2_CHUNK")) chunk = atoll(e) > 0 ? atoll(e) : 256;
+    W = p / chunk;
+    if (W > (int64_t)h->sm_count * 1024) W = (int64_t)h->sm_count * 1024;
+    if (W < 1) W = 1;
+  }
+  if (W > p) W = p;
+  const size_t nb = ((size_t)p * 4 + 255) / 256 * 256, wb = ((size_t)W * 8 + 255) / 256 * 256;
+  const size_t vb = ((size_t)p * 8 + 255) / 256 * 256;
+  const size_t total = 2 * nb + 8 * wb + (want_vals ? vb : 0) + (want_idx ? vb : 0) + 256;
+  CUDA_TRY(h->alg2.ensure(total));
+  char* base = (char*)h->alg2.p;
+  int32_t* J = (int32_t*)base;
+  int32_t* Jt = (int32_t*)(base + nb);
+  double* sums = (double*)(base + 2 * nb);
+  double* sumabs = (double*)(base + 2 * nb + wb);
+  double* scratch = (double*)(base + 2 * nb + 2 * wb);  // 2 W doubles
+  int64_t* cards = (int64_t*)(base + 2 * nb + 4 * wb);
+  int64_t* jplus = (int64_t*)(base + 2 * nb + 5 * wb);
+  int64_t* offsets = (int64_t*)(base + 2 * nb + 6 * wb);
+  double* lams = (double*)(base + 2 * nb + 7 * wb);
+  char* tail = base + 2 * nb + 8 * wb;
+  double* vals = want_vals ? (double*)tail : nullptr;
+  if (want_vals) tail += vb;
+  int64_t* gidx = want_idx ? (int64_t*)tail : nullptr;
+  if (want_idx) tail += vb;
+  Alg2Out* dout = (Alg2Out*)tail;
+  h->alg2_vals = vals;
+  h->alg2_idx = gidx;
+  const int blocks = (int)((W + 255) / 256);
+  if (l1)
+    alg2_chunks_kernel<true><<<blocks, 256, 0, h->stream>>>(yv, idx, p, r, W, xbar, sharpened, J,
+                                                            Jt, fixed_dev, sums, cards, jplus, sumabs, lams);
+  else
+    alg2_chunks_kernel<false><<<blocks, 256, 0, h->stream>>>(yv, idx, p, r, W, xbar, sharpened, J,
+                                                             Jt, fixed_dev, sums, cards, jplus, sumabs,
+                                                             lams);
+  alg2_merge_kernel<<<1, 1024, 0, h->stream>>>(sums, l1 ? sumabs : nullptr, cards, lams, W, r,
+                                               scratch, offsets, dout);
+  if (want_vals || want_idx) {
+    if (l1)
+      alg2_gather_kernel<true><<<blocks, 256, 0, h->stream>>>(yv, idx, p, W, J, cards, offsets,
+                                                              vals, gidx);
+    else
+      alg2_gather_kernel<false><<<blocks, 256, 0, h->stream>>>(yv, idx, p, W, J, cards, offsets,
+                                                               vals, gidx);
+  }
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpyAsync(h->host_state, dout, sizeof(Alg2Out), cudaMemcpyDeviceToHost, h->stream));
+  // total jplus (for the xbar fallback of simplex_init_lambda) into host_state tail
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  std::memcpy(out, h->host_state, sizeof(Alg2Out));
+  h->alg2_w = W;
+  h->alg2_jplus = jplus;
+  return 0;
+}
+
 int spx_common(cqk_handle* h, int mem, const double* y, int64_t n, int64_t n_total, double r,
                const cqk_options* opts_in, double* x, cqk_result* res, bool l1, bool sharded) {
   if (!h || !y || !res) return set_err(CQK_E_ARG, "null argument");
@@ -578,6 +681,7 @@ int spx_common(cqk_handle* h, int mem, const double* y, int64_t n, int64_t n_tot
   if (!aligned16(yv) || (xo && !aligned16(xo)))
     return set_err(CQK_E_ARG, "device arrays must be 16-byte aligned");
   const bool fixing = opts.variable_fixing != 0;
+  const bool alg2 = opts.simplex_start == 2 && !sharded && std::isnan(opts.lambda0);
   SpxState s;
   std::memset(&s, 0, sizeof s);
   s.cmd.fix_hi = INFINITY;
@@ -600,38 +704,55 @@ int spx_common(cqk_handle* h, int mem, const double* y, int64_t n, int64_t n_tot
   s.trace_cap = opts.record_trace ? kTraceCap : 0;
   s.compact_ratio = std::isnan(opts.compact_ratio) ? 0.25 : opts.compact_ratio;
   s.start = opts.simplex_start;
-  if (fixing) CUDA_TRY(h->scratch.ensure(((size_t)n * sizeof(double) + 255) / 256 * 256));
-  std::memcpy(h->host_state, &s, sizeof s);  // pinned staging: fully asynchronous
-  CUDA_TRY(cudaMemcpyAsync(h->state, h->host_state, sizeof s, cudaMemcpyHostToDevice, h->stream));
-  SpxParams<double> p;
-  std::memset(&p, 0, sizeof p);
-  p.y = yv;
-  p.sy = fixing ? (double*)h->scratch.p : nullptr;
-  p.x = xo;
-  p.trace = h->trace;
-  p.n = n;
-  p.st = (SpxState*)h->state;
-  p.ex = make_exchange(h, sharded);
-  p.partials = h->partials;
-  p.sync.arrive = h->sync;
-  p.sync.gen = h->sync + 1;
-  p.sync.error = (int*)(h->sync + 2);
-  p.sync.timeline = h->timeline;
-  void* args[] = {&p};
-  const int grid = limit_grid(h, l1 ? h->grid_l1 : h->grid_spx);
-  const void* fn = l1 ? (const void*)spx_solve_kernel<double, true>
-                      : (const void*)spx_solve_kernel<double, false>;
+  int launches = 1;
+  int64_t extra_read = 0;
   CUDA_TRY(cudaEventRecord(h->ev0, h->stream));
-  CUDA_TRY(cudaLaunchCooperativeKernel(fn, grid, kThreads, args, 0, h->stream));
+  if (alg2) {
+    // simplex.py:243-245 with the chunked initializer: Algorithm 4 then runs
+    // on the gathered free set (values only) and x is one dense pass.
+    Alg2Out a2;
+    int rc = run_alg2(h, yv, nullptr, n, r, 0, nullptr, l1 ? 1 : 0, l1, true, false, nullptr, &a2);
+    if (rc) return rc;
+    launches = 5;
+    extra_read = n;
+    if (l1 && a2.inside) {
+      if (xo) spx_x_kernel<false><<<h->sm_count * 4, 256, 0, h->stream>>>(yv, n, 0.0, 1, xo);
+      s.status = ST_SOLVED;
+      s.iterations = -1;
+      s.cmd.phase = PH_COPY;
+    } else {
+      const int64_t m = a2.n_free;
+      s.cmd.phase = PH_LAMBDA0;  // one pass over the free set: r - max(w) tightens the start
+      s.lam0_given = 1;
+      s.lam0_value = a2.lam0;
+      s.start = 3;
+      s.n = m;
+      s.active = m;
+      s.local_active = m;
+      s.phys_count = m;
+      s.fixed_count = n - m;  // proven zero by the initializer (simplex.py:251)
+      s.fixed_local = n - m;
+      s.fixed_removed = n - m;
+      rc = launch_spx(h, s, h->alg2_vals, m, nullptr, false, false);
+      if (rc) return rc;
+      if (xo) {
+        CUDA_TRY(cudaStreamSynchronize(h->stream));
+        std::memcpy(&s, h->host_state, sizeof s);
+        if (l1) spx_x_kernel<true><<<h->sm_count * 4, 256, 0, h->stream>>>(yv, n, s.cmd.lam, 0, xo);
+        else spx_x_kernel<false><<<h->sm_count * 4, 256, 0, h->stream>>>(yv, n, s.cmd.lam, 0, xo);
+        CUDA_TRY(cudaGetLastError());
+      }
+    }
+  } else {
+    int rc = launch_spx(h, s, yv, n, xo, l1, sharded);
+    if (rc) return rc;
+  }
   CUDA_TRY(cudaEventRecord(h->ev1, h->stream));
-  CUDA_TRY(cudaMemcpyAsync(h->host_state, h->state, sizeof s, cudaMemcpyDeviceToHost, h->stream));
-  CUDA_TRY(cudaMemcpyAsync(h->err_host, h->sync + 2, sizeof(unsigned), cudaMemcpyDeviceToHost,
-                           h->stream));
   if (mem == CQK_MEM_HOST && x && xo)
     CUDA_TRY(cudaMemcpyAsync(x, xo, sizeof(double) * n, cudaMemcpyDeviceToHost, h->stream));
   int rc = finish_sync(h);
   if (rc) return rc;
-  std::memcpy(&s, h->host_state, sizeof s);
+  if (!(alg2 && s.iterations < 0)) std::memcpy(&s, h->host_state, sizeof s);
   rc = check_timeout(h);
   if (rc) return rc;
   float ms = 0.f;
@@ -646,11 +767,12 @@ int spx_common(cqk_handle* h, int mem, const double* y, int64_t n, int64_t n_tot
   res->bracket_lo = s.lo;
   res->bracket_hi = s.hi;
   const int64_t fin = (s.status == ST_SOLVED && xo) ? n : 0;
-  res->elems_read = n + s.elems_scan + fin;
+  const int64_t pass0 = alg2 ? extra_read : n;
+  res->elems_read = pass0 + s.elems_scan + fin;
   res->elems_written = s.elems_written + fin;
-  res->bytes_model = 8 * (n + s.elems_scan + s.elems_written) + 16 * fin;
+  res->bytes_model = 8 * (pass0 + s.elems_scan + s.elems_written) + 16 * fin;
   res->device_ms = ms;
-  res->launches = 1;
+  res->launches = launches;
   res->trace_len = s.trace_len;
   return res->status;
 }
@@ -961,4 +1083,57 @@ extern "C" int cqk_selftest_division(cqk_handle* h, uint64_t seed, int64_t count
   *mismatches = m;
   if (example2) { example2[0] = ex[0]; example2[1] = ex[1]; }
   return 0;
+}
+
+// ------------------------------------------------------------ Algorithm 2
+extern "C" int spx_init_alg2_f64(cqk_handle* h, int mem, const double* y, int64_t n, double r,
+                                 const int64_t* idx, int64_t p, int64_t workers,
+                                 const double* xbar, int sharpened, double* lam0, int64_t* nfree,
+                                 int64_t* free_idx, uint8_t* fixed_mask, double* sum_free,
+                                 int64_t* jplus) {
+  if (!h || !y || !lam0 || !nfree) return set_err(CQK_E_ARG, "null argument");
+  CUDA_TRY(cudaSetDevice(h->device));
+  if (!idx) p = n;
+  if (p < 1) return set_err(CQK_E_EMPTY, "initializer needs at least one candidate index");
+  const double* dv[2];
+  {
+    const double* in[2] = {y, xbar};
+    int rc = stage_inputs<double>(h, mem, n, in, 2, dv, 0, nullptr);
+    if (rc) return rc;
+  }
+  const int64_t* ix;
+  int rc = stage_idx(h, mem, idx, p, &ix);
+  if (rc) return rc;
+  uint8_t* fdev = nullptr;
+  if (fixed_mask) {
+    if (mem == CQK_MEM_DEVICE) fdev = fixed_mask;
+    else {
+      CUDA_TRY(h->flags.ensure(n));
+      fdev = (uint8_t*)h->flags.p;
+    }
+    CUDA_TRY(cudaMemsetAsync(fdev, 0, n, h->stream));
+  }
+  Alg2Out a2;
+  rc = run_alg2(h, dv[0], ix, p, r, workers < 1 ? 0 : workers, xbar ? dv[1] : nullptr, sharpened,
+                false, false, free_idx != nullptr, fdev, &a2);
+  if (rc) return rc;
+  *lam0 = a2.lam0;
+  *nfree = a2.n_free;
+  if (sum_free) *sum_free = a2.sum_free;
+  if (free_idx)
+    CUDA_TRY(cudaMemcpyAsync(free_idx, h->alg2_idx, sizeof(int64_t) * a2.n_free,
+                             mem == CQK_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice,
+                             h->stream));
+  if (fixed_mask && mem == CQK_MEM_HOST)
+    CUDA_TRY(cudaMemcpyAsync(fixed_mask, fdev, n, cudaMemcpyDeviceToHost, h->stream));
+  if (jplus) {
+    std::vector<int64_t> jp(h->alg2_w);
+    CUDA_TRY(cudaMemcpyAsync(jp.data(), h->alg2_jplus, sizeof(int64_t) * h->alg2_w,
+                             cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    int64_t t = 0;
+    for (int64_t v : jp) t += v;
+    *jplus = t;
+  }
+  return finish_sync(h);
 }

@@ -584,10 +584,12 @@ DEVI void s_after_init(SpxState& s, const double* tot) {
   // both upper bounds of the root (phi(lam) >= sum(y) + n lam and
   // phi(lam) >= max(y) + lam), the second far tighter on spread data -- the
   // reference's own `lambda0=` route with a better start (simplex.py:246-250).
+  // start 3: a given upper bound (the Algorithm-2 merge) tightened the same way
   const double formula = (s.r - tot[0]) / (double)s.n;
   const double tight = s.r - tot[1];
-  const double lam0 = s.lam0_given ? s.lam0_value
-                                   : (s.start && tight < formula ? tight : formula);
+  double lam0;
+  if (s.start == 3) lam0 = tight < s.lam0_value ? tight : s.lam0_value;
+  else lam0 = s.lam0_given ? s.lam0_value : (s.start && tight < formula ? tight : formula);
   const double mn = -tot[1];
   s.lam0 = lam0 >= mn ? lam0 : mn;  // max(lambda0, min(-y)), simplex.py:250
   s.cmd.lam = s.lam0;
@@ -1203,6 +1205,218 @@ __global__ void __launch_bounds__(32 * kRowWarps) spx_rows_warp_kernel(
   }
   // outstanding bulk stores complete before the grid exits (bulk_group semantics)
   if (lane == 0 && tma) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// ------------------------------------------------------------ Algorithm 2
+// The reference's Gauss-Seidel initializer (simplex.py:47-111) run per
+// contiguous chunk -- par_simplex_init semantics (parallel.py:330-368): chunk
+// k = [floor(k n/W), floor((k+1) n/W)) exactly as np.linspace(...).astype(int64)
+// (parallel.py:82-85), one GPU thread per chunk replaying the sequential
+// recurrence bit for bit, then a one-block merge in _tree_sum order
+// (parallel.py:62-72).  Every zero proven inside a chunk is valid globally
+// (the chunk's multiplier bounds the full problem's from above), so the free
+// set that Algorithm 4 iterates on collapses to a tiny fraction of n.
+struct Alg2Out {
+  double lam0, sum_free, sum_abs;
+  int64_t n_free;
+  int32_t inside;  // l1: sum |y| <= r
+  int32_t pad;
+};
+
+DEVI void chunk_bounds(int64_t n, int64_t W, int64_t k, int64_t& lo, int64_t& hi) {
+  const double step = (double)n / (double)W;
+  lo = (int64_t)((double)k * step);
+  hi = k + 1 == W ? n : (int64_t)((double)(k + 1) * step);
+}
+
+template <bool L1>
+__global__ void __launch_bounds__(256) alg2_chunks_kernel(
+    const double* __restrict__ y, const int64_t* __restrict__ idx, int64_t p, double r,
+    int64_t W, const double* __restrict__ xbar, int sharpened, int32_t* __restrict__ J,
+    int32_t* __restrict__ Jt, uint8_t* __restrict__ fixed, double* __restrict__ sums,
+    int64_t* __restrict__ cards, int64_t* __restrict__ jplus_out, double* __restrict__ sumabs,
+    double* __restrict__ lams) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= W) return;
+  int64_t lo, hi;
+  chunk_bounds(p, W, k, lo, hi);
+  auto w_of = [&](int64_t pos) -> double {
+    const int64_t i = idx ? idx[pos] : pos;
+    const double v = __ldg(y + i);
+    return L1 ? fabs(v) : v;
+  };
+  auto orig = [&](int64_t pos) -> int64_t { return idx ? idx[pos] : pos; };
+  const bool use_xbar = xbar != nullptr;
+  int32_t* Jc = J + lo;
+  int32_t* Jtc = Jt + lo;
+  double sabs = 0.0;
+  // simplex.py:58-111 with local offsets (pos - lo) in J / Jt
+  const double y1 = w_of(lo);
+  sabs += y1;
+  int64_t nJ = 1, nJt = 0, jplus = 0;
+  Jc[0] = 0;
+  double sumJ = y1, lam = r - y1;
+  if (!use_xbar || xbar[orig(lo)] > 0.0) jplus = 1;
+  for (int64_t pos = lo + 1; pos < hi; ++pos) {
+    const double yi = w_of(pos);
+    sabs += yi;
+    if (use_xbar && xbar[orig(pos)] <= 0.0) continue;
+    bool ok = __dadd_rn(yi, lam) > 0.0;
+    if (sharpened && yi <= 0.0) ok = false;
+    if (!ok) {
+      if (fixed) fixed[orig(pos)] = 1;
+      continue;
+    }
+    const double cand = __ddiv_rn(__dsub_rn(__dsub_rn(r, sumJ), yi), (double)(nJ + 1));
+    if (cand < __dsub_rn(r, yi)) {
+      Jc[nJ++] = (int32_t)(pos - lo);
+      sumJ = __dadd_rn(sumJ, yi);
+      lam = cand;
+    } else {
+      for (int64_t q = 0; q < nJ; ++q) Jtc[nJt++] = Jc[q];
+      Jc[0] = (int32_t)(pos - lo);
+      nJ = 1;
+      sumJ = yi;
+      lam = __dsub_rn(r, yi);
+      jplus = 0;
+    }
+    if (!use_xbar || xbar[orig(pos)] > 0.0) ++jplus;
+  }
+  for (int64_t q = 0; q < nJt; ++q) {
+    const int64_t pos = lo + Jtc[q];
+    const double yi = w_of(pos);
+    bool ok = __dadd_rn(yi, lam) > 0.0;
+    if (sharpened && yi <= 0.0) ok = false;
+    if (!ok) {
+      if (fixed) fixed[orig(pos)] = 1;
+      continue;
+    }
+    lam = __ddiv_rn(__dsub_rn(__dsub_rn(r, sumJ), yi), (double)(nJ + 1));
+    Jc[nJ++] = Jtc[q];
+    sumJ = __dadd_rn(sumJ, yi);
+    if (!use_xbar || xbar[orig(pos)] > 0.0) ++jplus;
+  }
+  sums[k] = sumJ;
+  cards[k] = nJ;
+  jplus_out[k] = jplus;
+  lams[k] = lam;  // simplex_init_lambda returns the recurrence's own lam
+  if (sumabs) sumabs[k] = sabs;
+}
+
+// One block: _tree_sum of the chunk sums (and of sum|y| for the l1 test) in
+// the reference's pairwise order, and exclusive offsets of the chunk cards.
+__global__ void __launch_bounds__(1024) alg2_merge_kernel(const double* __restrict__ sums,
+                                                          const double* __restrict__ sumabs,
+                                                          const int64_t* __restrict__ cards,
+                                                          const double* __restrict__ lams,
+                                                          int64_t W, double r, double* scratch,
+                                                          int64_t* offsets, Alg2Out* out) {
+  __shared__ int64_t s_part[1024];
+  // exclusive scan of cards: contiguous ranges per thread
+  const int64_t per = (W + blockDim.x - 1) / blockDim.x;
+  const int64_t c0 = threadIdx.x * per, c1 = c0 + per < W ? c0 + per : W;
+  int64_t loc = 0;
+  for (int64_t c = c0; c < c1; ++c) loc += cards[c];
+  s_part[threadIdx.x] = loc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t run = 0;
+    for (int t = 0; t < (int)blockDim.x; ++t) {
+      const int64_t v = s_part[t];
+      s_part[t] = run;
+      run += v;
+    }
+    out->n_free = run;
+  }
+  __syncthreads();
+  int64_t run = s_part[threadIdx.x];
+  for (int64_t c = c0; c < c1; ++c) {
+    offsets[c] = run;
+    run += cards[c];
+  }
+  // _tree_sum: adjacent pairs level by level, odd tail carried (ping-pong)
+  for (int pass = 0; pass < (sumabs ? 2 : 1); ++pass) {
+    const double* src = pass == 0 ? sums : sumabs;
+    double* bufA = scratch;
+    double* bufB = scratch + W;
+    for (int64_t i = threadIdx.x; i < W; i += blockDim.x) bufA[i] = src[i];
+    __syncthreads();
+    int64_t k = W;
+    while (k > 1) {
+      const int64_t half = k / 2;
+      for (int64_t j = threadIdx.x; j < half; j += blockDim.x) bufB[j] = bufA[2 * j] + bufA[2 * j + 1];
+      if ((k & 1) && threadIdx.x == 0) bufB[half] = bufA[k - 1];
+      __syncthreads();
+      k = half + (k & 1);
+      double* t = bufA;
+      bufA = bufB;
+      bufB = t;
+    }
+    if (threadIdx.x == 0) {
+      if (pass == 0) out->sum_free = bufA[0];
+      else out->sum_abs = bufA[0];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    // one chunk: simplex_init_lambda's lam (simplex.py:111); else the merge
+    // of par_simplex_init (parallel.py:365)
+    out->lam0 = W == 1 ? lams[0] : (r - out->sum_free) / (double)out->n_free;
+    out->inside = sumabs ? out->sum_abs <= r : 0;
+  }
+}
+
+// Gather the free set: values (w = y or |y|) and, optionally, global indices.
+template <bool L1>
+__global__ void __launch_bounds__(256) alg2_gather_kernel(
+    const double* __restrict__ y, const int64_t* __restrict__ idx, int64_t p, int64_t W,
+    const int32_t* __restrict__ J, const int64_t* __restrict__ cards,
+    const int64_t* __restrict__ offsets, double* __restrict__ vals, int64_t* __restrict__ gidx) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= W) return;
+  int64_t lo, hi;
+  chunk_bounds(p, W, k, lo, hi);
+  const int64_t c = cards[k], o = offsets[k];
+  for (int64_t q = 0; q < c; ++q) {
+    const int64_t pos = lo + J[lo + q];
+    const int64_t i = idx ? idx[pos] : pos;
+    if (vals) {
+      const double v = y[i];
+      vals[o + q] = L1 ? fabs(v) : v;
+    }
+    if (gidx) gidx[o + q] = i;
+  }
+}
+
+// x = max(0, y + lam) (simplex.py:303) / sign(y) max(0, |y| + lam) (simplex.py:333)
+template <bool L1>
+__global__ void __launch_bounds__(256) spx_x_kernel(const double* __restrict__ y, int64_t n,
+                                                    double lam, int copy, double* __restrict__ x) {
+  const int64_t n2 = n / 2;
+  const double2* y2 = reinterpret_cast<const double2*>(y);
+  double2* x2 = reinterpret_cast<double2*>(x);
+  const bool vec = (((uintptr_t)y | (uintptr_t)x) & 15) == 0;
+  auto f = [&](double v) {
+    if (copy) return v;
+    const double w = L1 ? fabs(v) : v;
+    const double t = __dadd_rn(w, lam);
+    const double pos = t > 0 ? t : 0.0;
+    if (!L1) return pos;
+    const double sg = v > 0 ? 1.0 : (v < 0 ? -1.0 : 0.0);
+    return __dmul_rn(sg, pos);
+  };
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  if (vec) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2; i += stride) {
+      double2 v = ld_stream(y2 + i);
+      v.x = f(v.x);
+      v.y = f(v.y);
+      __stcs(x2 + i, v);
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) x[n - 1] = f(y[n - 1]);
+  } else {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) x[i] = f(y[i]);
+  }
 }
 
 // ------------------------------------------------------------ utilities

@@ -23,6 +23,8 @@ from .newton import ContractViolation, SolveOutcome, SolverOptions, Status
 __all__ = [
     "InitResult",
     "EmptyIndexSet",
+    "simplex_init_lambda",
+    "par_simplex_init",
     "newton_project_simplex",
     "project_l1",
     "project_simplex_rows",
@@ -39,6 +41,78 @@ class InitResult:
     free: np.ndarray
     fixed_mask: np.ndarray
     sum_free: float
+
+
+def _alg2(y, r, idx, xbar, sharpened, workers):
+    import ctypes
+
+    yv, dt, dev = _prep(y)
+    n = int(yv.shape[0])
+    h = N.handle(yv.device.index if dev else None)
+    import torch
+
+    if dev:
+        h.set_stream(torch.cuda.current_stream(yv.device).cuda_stream)
+        mem = N.MEM_DEVICE
+        ix = None if idx is None else torch.as_tensor(idx, device=yv.device).to(torch.int64).contiguous()
+        xb = None if xbar is None else xbar.to(torch.float64).contiguous()
+        p = n if ix is None else int(ix.numel())
+        free = torch.empty(max(p, 1), dtype=torch.int64, device=yv.device)
+        fixed = torch.zeros(n, dtype=torch.uint8, device=yv.device)
+        ptr = lambda t: None if t is None else t.data_ptr()  # noqa: E731
+        yp = yv.data_ptr()
+    else:
+        h.set_stream(torch.cuda.current_stream(h.device).cuda_stream)
+        mem = N.MEM_HOST
+        ix = None if idx is None else np.ascontiguousarray(idx, dtype=np.int64)
+        xb = None if xbar is None else np.ascontiguousarray(xbar, dtype=np.float64)
+        p = n if ix is None else int(ix.size)
+        free = np.empty(max(p, 1), np.int64)
+        fixed = np.zeros(n, np.uint8)
+        ptr = lambda a: None if a is None else a.ctypes.data  # noqa: E731
+        yp = yv.ctypes.data
+    if p == 0:
+        raise EmptyIndexSet("initializer needs at least one candidate index")
+    lam, nf, sj, jp = ctypes.c_double(), ctypes.c_int64(), ctypes.c_double(), ctypes.c_int64()
+    rc = h.lib.spx_init_alg2_f64(h.ptr, mem, yp, n, float(r), ptr(ix), p, int(workers), ptr(xb),
+                                 int(bool(sharpened)), lam, nf, ptr(free), ptr(fixed), sj, jp)
+    if rc == N.E_EMPTY:
+        raise EmptyIndexSet("initializer needs at least one candidate index")
+    if rc != 0:
+        raise N.NativeError(f"Algorithm-2 initializer failed ({rc}): {N.last_error()}")
+    lam0 = lam.value
+    if xbar is not None and jp.value == 0:  # simplex.py:151-152
+        y0 = float(yv[0])
+        lam0 = max(float(r) / n, -y0)
+    fm = fixed.bool() if dev else fixed.astype(bool)
+    return InitResult(lambda0=float(lam0), free=free[: nf.value], fixed_mask=fm,
+                      sum_free=float(sj.value))
+
+
+def simplex_init_lambda(y, r, idx=None, xbar=None, sharpened=False):
+    """Algorithm 2, the sequential Gauss-Seidel initializer (simplex.py:114-154).
+
+    Runs the exact recurrence on one device thread (it is inherently serial;
+    see par_simplex_init for the chunked form)."""
+    if xbar is not None:
+        xa = xbar.cpu().numpy() if _is_torch(xbar) else np.asarray(xbar)
+        n = int(y.shape[0])
+        if xa.shape[0] != n:
+            raise DomainError("xbar", None, "xbar must have length n")
+        if np.any(xa < 0):
+            raise DomainError("xbar", None, "warm-start estimate must be >= 0")
+    if idx is not None and len(idx) == 0:
+        raise EmptyIndexSet("initializer needs at least one candidate index")
+    return _alg2(y, r, idx, xbar, sharpened, workers=1)
+
+
+def par_simplex_init(y, r, workers=None):
+    """Algorithm 2 per contiguous chunk, merged (parallel.py:330-368); one
+    device thread per chunk, bit-identical to the reference for the same
+    `workers`."""
+    from .parallel import resolve_workers
+
+    return _alg2(y, r, None, None, False, workers=resolve_workers(workers))
 
 
 def _prep(y):
@@ -111,7 +185,9 @@ def newton_project_simplex(y, r, opts=None, xbar=None, output="dense", sharpened
     """Streamlined Newton projection of y onto the level-r simplex (simplex.py:218-308).
 
     start (B200 extension, used when lambda0 is None): "tight" =
-    min((r - sum y)/n, r - max y), "formula" = (r - sum y)/n."""
+    min((r - sum y)/n, r - max y), "formula" = (r - sum y)/n, "alg2" = the
+    chunked Algorithm-2 initializer (par_simplex_init) with Algorithm 4 on its
+    free set."""
     if not r > 0:
         raise DomainError("r", None, "simplex level r must be positive")
     x, res = _project(y, r, opts, lambda0, trace, l1=False, start=start)

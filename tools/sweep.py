@@ -55,24 +55,28 @@ for w in which:
         res[w] = cqk("cqk-uncorrelated", 10**7)
     elif w == "jac":
         res[w] = cqk("cqk-weakly-correlated", 10**8, jac=True)
-    elif w in ("spx", "l1"):
+    elif w.split("_")[0] in ("spx", "l1") and not w.startswith("spx1e6"):
         n = 10**8
+        start = w.split("_")[1] if "_" in w else "tight"
         y = torch.from_numpy(P.gen_simplex_y("simplex-n01", n, 1)).cuda()
-        if w == "spx":
-            ms, out = timeit(lambda: P.newton_project_simplex(y, 1.0))
+        if w.startswith("spx"):
+            ms, out = timeit(lambda: P.newton_project_simplex(y, 1.0, start=start))
             st = out.stats
             ev = out.phi_evals
         else:
-            ms, out = timeit(lambda: P.simplex.project_l1_outcome(y, 1.0))
+            ms, out = timeit(lambda: P.simplex.project_l1_outcome(y, 1.0, start=start))
             st = out.stats
             ev = out.phi_evals
         res[w] = {"ms": ms, "kernel_ms": st["device_ms"], "GBps": st["bytes_model"] / st["device_ms"] / 1e6,
                   "frac": st["bytes_model"] / st["device_ms"] / 1e6 / PEAK, "evals": ev,
                   "elem_per_s": n / ms * 1e3, "bytes_per_elem": st["bytes_model"] / n}
-    elif w == "spx1e6":
-        y = torch.from_numpy(P.gen_simplex_y("simplex-u01", 10**6, 1)).cuda()
-        ms, out = timeit(lambda: P.newton_project_simplex(y, 1.0), reps=50)
-        res[w] = {"ms": ms, "kernel_ms": out.stats["device_ms"], "evals": out.phi_evals}
+    elif w.startswith("spx1e6"):
+        start = w.split("_")[1] if "_" in w else "tight"
+        fam = "simplex-n01" if "n01" in w else "simplex-u01"
+        y = torch.from_numpy(P.gen_simplex_y(fam, 10**6, 1)).cuda()
+        ms, out = timeit(lambda: P.newton_project_simplex(y, 1.0, start=start), reps=50)
+        res[w] = {"ms": ms, "kernel_ms": out.stats["device_ms"], "evals": out.phi_evals,
+                  "launches": out.stats["launches"]}
     elif w == "rows":
         rows, cols = 65536, 4096
         Y = torch.from_numpy(P.gen_simplex_y("simplex-n01", rows * cols, 1)).cuda().view(rows, cols)
