@@ -856,9 +856,29 @@ extern "C" int spx_project_batched_f64(cqk_handle* h, int mem, const double* Y, 
   CUDA_TRY(cudaEventRecord(h->ev0, h->stream));
   cudaError_t e;
   const size_t smem = rows_smem_per_warp(c) * kRowWarps;
+  const size_t smem_cta = rows_cta_smem<4, 8>(c);
   const char* force = getenv("CQK_ROWS_KERNEL");
-  const bool warp_kernel = smem <= 220 * 1024 && !(force && std::string(force) == "block");
-  if (warp_kernel) {
+  const std::string fk = force ? force : "";
+  const bool cta_kernel = smem_cta <= 220 * 1024 && c >= 256 && fk != "block" && fk != "warp";
+  const bool warp_kernel = !cta_kernel && smem <= 220 * 1024 && fk != "block";
+  if (cta_kernel) {
+    auto go = [&](auto kern, int threads, size_t sm) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      int occ = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, sm);
+      int64_t grid = (int64_t)(occ > 0 ? occ : 1) * h->sm_count;
+      if (grid > rows) grid = rows;
+      kern<<<(unsigned)grid, threads, sm, h->stream>>>(Yd, Xd, Ld, Id, rows, c, r, tau,
+                                                       opts.max_iterations, fixing, opts.lambda0,
+                                                       opts.simplex_start);
+      return cudaGetLastError();
+    };
+    // measured on B200 (65536 x 4096): 4 warps/row with a cols/8 free-set
+    // buffer (6 CTAs/SM) 1.09 ms; cols/2 buffer 1.28 ms; 8 warps/row 1.6 ms
+    if (fk == "cta4") e = go(spx_rows_cta_kernel<4, 2>, 128, rows_cta_smem<4, 2>(c));
+    else if (fk == "cta8") e = go(spx_rows_cta_kernel<8, 8>, 256, rows_cta_smem<8, 8>(c));
+    else e = go(spx_rows_cta_kernel<4, 8>, 128, rows_cta_smem<4, 8>(c));
+  } else if (warp_kernel) {
     cudaFuncSetAttribute(spx_rows_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     int occ = 0;
