@@ -142,7 +142,8 @@ def gen_shard(n_total, world, rank):
     from paper_2603_15910_b200.distributed import allgather_bytes, shard_bounds
 
     lo, hi = shard_bounds(n_total, world, rank)
-    d, a, b, l, u, bl, bu = P.instances.gen_cqk_shard(FAMILY, n_total, SEED, lo, hi)
+    # the shard is generated straight into this rank's HBM (bit-identical stream)
+    dev, bl, bu = P.instances.gen_cqk_shard_device(FAMILY, n_total, SEED, lo, hi)
     parts = [np.frombuffer(x, dtype=np.float64) for x in
              allgather_bytes(np.array([bl, bu]).tobytes())]
     sbl = sbu = 0.0
@@ -150,7 +151,7 @@ def gen_shard(n_total, world, rank):
         sbl += pbl
         sbu += pbu
     r = P.instances.cqk_r(FAMILY, n_total, SEED, sbl, sbu)
-    return [d, a, b, l, u], r, lo, hi
+    return dev, r, lo, hi
 
 
 def cpu_baseline_sample(arrs, r, cores):
@@ -235,9 +236,12 @@ def main():
     arrs, r, lo, hi = gen_shard(args.n, world, rank)
     n_local = hi - lo
     stream = torch.cuda.Stream()
-    with torch.cuda.stream(stream):
-        dev = [torch.from_numpy(v).cuda() for v in arrs]
-    stream.synchronize()
+    if world == 1:
+        with torch.cuda.stream(stream):
+            dev = [torch.from_numpy(v).cuda() for v in arrs]
+        stream.synchronize()
+    else:
+        dev = arrs  # already resident (generated on the device)
     if world > 1:
         from paper_2603_15910_b200 import distributed as D
 

@@ -212,6 +212,21 @@ int l1_project_sharded_f64(cqk_handle *h, int mem, const double *y, int64_t n_lo
                            int64_t n_total, double r, const cqk_options *opts, double *x,
                            cqk_result *res);
 
+/* On-device instances --------------------------------------
+   gen_cqk(family, n, seed) (instances.py:43-70) straight into device arrays,
+   bit-identical to the reference's stream (GF(2) jump per thread); r from
+   device sums of b.l and b.u.  family: 0 uncorrelated, 1 weakly, 2 correlated. */
+int cqk_gen_cqk_device(cqk_handle *h, int family, int64_t n, uint64_t seed, double *d,
+                       double *a, double *b, double *l, double *u, double *r);
+/* Elements [lo, hi) of the same instance (a rank's shard), with the shard's
+   b.l and b.u sums; combine the shards' sums (rank order) with
+   cqk_gen_cqk_r of include/cqk_instances.h. */
+int cqk_gen_cqk_device_range(cqk_handle *h, int family, int64_t n, uint64_t seed, int64_t lo,
+                             int64_t hi, double *d, double *a, double *b, double *l, double *u,
+                             double *bl, double *bu);
+/* gen_simplex_y("simplex-u01", n, seed) (instances.py:73-86) into device y. */
+int cqk_gen_simplex_u01_device(cqk_handle *h, int64_t n, uint64_t seed, double *y);
+
 /* Diagnostics ------------------------------------------------------------------ */
 /* Bitwise check of the solver's shared-reciprocal division against the IEEE
    library division on `count` random operand pairs (mode 0: exponents in

@@ -87,7 +87,8 @@ EXPORTS = (
     "spx_project_f64", "l1_project_f64", "spx_project_batched_f64", "cqk_selftest_division",
     "cqk_comm_ipc_handle_size", "cqk_comm_create", "cqk_comm_connect", "cqk_comm_connect_local",
     "cqk_set_grid_limit", "cqk_reserve", "cqk_solve_sharded_f64", "spx_project_sharded_f64",
-    "l1_project_sharded_f64", "spx_init_alg2_f64",
+    "l1_project_sharded_f64", "spx_init_alg2_f64", "cqk_gen_cqk_device",
+    "cqk_gen_cqk_device_range", "cqk_gen_simplex_u01_device",
 )
 
 _lib = None
@@ -140,6 +141,12 @@ def _declare(L):
     L.spx_init_alg2_f64.argtypes = [_P, ctypes.c_int, _P, _I64, _D, _P, _I64, _I64, _P,
                                     ctypes.c_int, ctypes.POINTER(_D), ctypes.POINTER(_I64), _P,
                                     _P, ctypes.POINTER(_D), ctypes.POINTER(_I64)]
+    L.cqk_gen_cqk_device.argtypes = [_P, ctypes.c_int, _I64, ctypes.c_uint64, _P, _P, _P, _P,
+                                     _P, ctypes.POINTER(_D)]
+    L.cqk_gen_simplex_u01_device.argtypes = [_P, _I64, ctypes.c_uint64, _P]
+    L.cqk_gen_cqk_device_range.argtypes = [_P, ctypes.c_int, _I64, ctypes.c_uint64, _I64, _I64,
+                                           _P, _P, _P, _P, _P, ctypes.POINTER(_D),
+                                           ctypes.POINTER(_D)]
     L.spx_project_batched_f64.argtypes = [_P, ctypes.c_int, _P, _I64, _I64, _D, _OPT, _P, _P,
                                           _P, _RES]
 

@@ -25,7 +25,8 @@ NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-f
               "-shared", "--expt-relaxed-constexpr"]
 
 CUDA_SOURCES = ["cqk_abi.cu"]
-CUDA_DEPS = ["cqk_abi.cu", "cqk_device.cuh", "cqk_solver.cuh", "cqk_kernels.cuh"]
+CUDA_DEPS = ["cqk_abi.cu", "cqk_device.cuh", "cqk_solver.cuh", "cqk_kernels.cuh", "gen_kernels.cuh",
+             "xoshiro_jump.h"]
 
 
 def _nvcc():
@@ -64,7 +65,7 @@ def build_cuda(force=False, verbose=False):
 
 def build_instances(force=False):
     src = os.path.join(CSRC, "instances.c")
-    deps = [src, os.path.join(ROOT, "include", "cqk_instances.h")]
+    deps = [src, os.path.join(CSRC, "xoshiro_jump.h"), os.path.join(ROOT, "include", "cqk_instances.h")]
     if not force and not _stale(GEN_LIB, deps):
         return GEN_LIB
     os.makedirs(LIBDIR, exist_ok=True)

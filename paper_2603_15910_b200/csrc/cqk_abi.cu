@@ -1157,3 +1157,96 @@ extern "C" int spx_init_alg2_f64(cqk_handle* h, int mem, const double* y, int64_
   }
   return finish_sync(h);
 }
+
+// ------------------------------------------------------------ device generators
+#include "gen_kernels.cuh"
+extern "C" {
+#include "xoshiro_jump.h"
+}
+
+namespace {
+// per-thread states of a stream of `count` tuples of `per_elem` draws from `base`
+int upload_states(cqk_handle* h, uint64_t seed, uint64_t base, int64_t per, int64_t per_elem,
+                  int64_t T, XoState* dst) {
+  std::vector<xo_state> st((size_t)T);
+  xo_jump_states(seed, base, (uint64_t)(per * per_elem), T, st.data());
+  CUDA_TRY(cudaMemcpyAsync(dst, st.data(), sizeof(XoState) * T, cudaMemcpyHostToDevice, h->stream));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));  // st is pageable and dies here
+  return 0;
+}
+}  // namespace
+
+extern "C" int cqk_gen_cqk_device_range(cqk_handle* h, int family, int64_t n, uint64_t seed,
+                                        int64_t lo, int64_t hi, double* d, double* a, double* b,
+                                        double* l, double* u, double* bl, double* bu) {
+  if (!h || !d || !a || !b || !l || !u || n < 1 || family < 0 || family > 2 || lo < 0 ||
+      hi > n || lo >= hi)
+    return set_err(CQK_E_ARG, "bad generator arguments");
+  CUDA_TRY(cudaSetDevice(h->device));
+  const int64_t m = hi - lo;
+  const int64_t T = m < 16384 ? m : 16384;
+  const int64_t per = (m + T - 1) / T;
+  const int64_t Tn = (m + per - 1) / per;
+  CUDA_TRY(h->idxbuf.ensure(sizeof(XoState) * 2 * Tn));
+  XoState* st1 = (XoState*)h->idxbuf.p;
+  XoState* st2 = st1 + Tn;
+  const int64_t tup = family == 2 ? 1 : 3;
+  const uint64_t off = (uint64_t)tup * (uint64_t)n;
+  int rc = upload_states(h, seed, (uint64_t)tup * lo, per, tup, Tn, st1);
+  if (rc) return rc;
+  rc = upload_states(h, seed, off + 2 * (uint64_t)lo, per, 2, Tn, st2);
+  if (rc) return rc;
+  gen_cqk_kernel<<<(unsigned)((Tn + 255) / 256), 256, 0, h->stream>>>(family, m, per, st1, st2, d,
+                                                                      a, b, l, u);
+  const int nb = util_blocks(h, m);
+  dot_bl_bu_kernel<<<nb, 256, 0, h->stream>>>(b, l, u, m, h->red);
+  finalize_kernel<<<1, kUtilThreads, 0, h->stream>>>(h->red, nb, 2, 0, 0, h->out);
+  CUDA_TRY(cudaGetLastError());
+  double t[2];
+  CUDA_TRY(cudaMemcpyAsync(t, h->out, sizeof t, cudaMemcpyDeviceToHost, h->stream));
+  rc = finish_sync(h);
+  if (rc) return rc;
+  if (bl) *bl = t[0];
+  if (bu) *bu = t[1];
+  return 0;
+}
+
+static double gen_cqk_r(int family, int64_t n, uint64_t seed, double bl, double bu) {
+  const uint64_t off = (uint64_t)(family == 2 ? 1 : 3) * (uint64_t)n;
+  xo_state s = xo_jump(xo_seed(seed), off + 2 * (uint64_t)n);  // instances.py:66
+  const double ur = (double)(xo_next(&s) >> 11) * 0x1p-53;
+  return bl + ur * (bu - bl);
+}
+
+extern "C" int cqk_gen_cqk_device(cqk_handle* h, int family, int64_t n, uint64_t seed, double* d,
+                                  double* a, double* b, double* l, double* u, double* r_out) {
+  if (!r_out) return set_err(CQK_E_ARG, "null r");
+  double bl, bu;
+  int rc = cqk_gen_cqk_device_range(h, family, n, seed, 0, n, d, a, b, l, u, &bl, &bu);
+  if (rc) return rc;
+  *r_out = gen_cqk_r(family, n, seed, bl, bu);
+  return 0;
+}
+
+extern "C" int cqk_gen_simplex_u01_device(cqk_handle* h, int64_t n, uint64_t seed, double* y) {
+  if (!h || !y || n < 1) return set_err(CQK_E_ARG, "bad generator arguments");
+  CUDA_TRY(cudaSetDevice(h->device));
+  const int64_t T = n < 16384 ? n : 16384;
+  const int64_t per = (n + T - 1) / T;
+  const int64_t Tn = (n + per - 1) / per;
+  CUDA_TRY(h->idxbuf.ensure(sizeof(XoState) * Tn + 64));
+  XoState* st = (XoState*)h->idxbuf.p;
+  unsigned long long* zeros = (unsigned long long*)(st + Tn);
+  for (uint64_t attempt = 0;; ++attempt) {  // instances.py:78-86: redraw while any zero
+    int rc = upload_states(h, seed, attempt * (uint64_t)n, per, 1, Tn, st);
+    if (rc) return rc;
+    CUDA_TRY(cudaMemsetAsync(zeros, 0, 8, h->stream));
+    gen_u01_kernel<<<(unsigned)((Tn + 255) / 256), 256, 0, h->stream>>>(n, per, st, y, zeros);
+    CUDA_TRY(cudaGetLastError());
+    unsigned long long z = 0;
+    CUDA_TRY(cudaMemcpyAsync(&z, zeros, 8, cudaMemcpyDeviceToHost, h->stream));
+    rc = finish_sync(h);
+    if (rc) return rc;
+    if (!z) return 0;
+  }
+}

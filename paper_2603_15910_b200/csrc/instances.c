@@ -24,90 +24,7 @@
 
 #include "../../include/cqk_instances.h"
 
-typedef struct { uint64_t s[4]; } xo_state;
-
-static inline uint64_t rotl(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
-
-static inline uint64_t xo_next(xo_state *st) {
-  uint64_t *s = st->s;
-  uint64_t result = rotl(s[0] + s[3], 23) + s[0];
-  uint64_t t = s[1] << 17;
-  s[2] ^= s[0];
-  s[3] ^= s[1];
-  s[1] ^= s[2];
-  s[0] ^= s[3];
-  s[2] ^= t;
-  s[3] = rotl(s[3], 45);
-  return result;
-}
-
-static xo_state xo_seed(uint64_t seed) {
-  xo_state st;
-  uint64_t z = seed;
-  for (int i = 0; i < 4; ++i) {
-    z += 0x9E3779B97F4A7C15ULL;
-    uint64_t o = z;
-    o = (o ^ (o >> 30)) * 0xBF58476D1CE4E5B9ULL;
-    o = (o ^ (o >> 27)) * 0x94D049BB133111EBULL;
-    st.s[i] = o ^ (o >> 31);
-  }
-  return st;
-}
-
-/* ---- GF(2) skip-ahead: the state transition is linear on 256 bits. ---- */
-typedef struct { uint64_t col[256][4]; } gf2mat; /* column j = image of e_j */
-
-static void mat_apply(const gf2mat *m, const uint64_t v[4], uint64_t out[4]) {
-  uint64_t r0 = 0, r1 = 0, r2 = 0, r3 = 0;
-  for (int w = 0; w < 4; ++w) {
-    uint64_t bits = v[w];
-    while (bits) {
-      int b = __builtin_ctzll(bits);
-      bits &= bits - 1;
-      const uint64_t *c = m->col[w * 64 + b];
-      r0 ^= c[0]; r1 ^= c[1]; r2 ^= c[2]; r3 ^= c[3];
-    }
-  }
-  out[0] = r0; out[1] = r1; out[2] = r2; out[3] = r3;
-}
-
-static void mat_mul(const gf2mat *a, const gf2mat *b, gf2mat *out) {
-  for (int j = 0; j < 256; ++j) mat_apply(a, b->col[j], out->col[j]);
-}
-
-static void transition_matrix(gf2mat *m) {
-  for (int j = 0; j < 256; ++j) {
-    xo_state st = {{0, 0, 0, 0}};
-    st.s[j / 64] = 1ULL << (j % 64);
-    xo_next(&st);
-    memcpy(m->col[j], st.s, sizeof st.s);
-  }
-}
-
-/* state advanced by k draws */
-static xo_state xo_jump(xo_state st, uint64_t k) {
-  if (k == 0) return st;
-  gf2mat *base = malloc(sizeof(gf2mat)), *tmp = malloc(sizeof(gf2mat));
-  transition_matrix(base);
-  uint64_t v[4];
-  memcpy(v, st.s, sizeof v);
-  while (k) {
-    if (k & 1) {
-      uint64_t o[4];
-      mat_apply(base, v, o);
-      memcpy(v, o, sizeof v);
-    }
-    k >>= 1;
-    if (k) {
-      mat_mul(base, base, tmp);
-      gf2mat *sw = base; base = tmp; tmp = sw;
-    }
-  }
-  memcpy(st.s, v, sizeof v);
-  free(base);
-  free(tmp);
-  return st;
-}
+#include "xoshiro_jump.h"
 
 static int nthreads_for(int64_t count) {
 #ifdef _OPENMP

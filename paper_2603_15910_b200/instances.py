@@ -15,7 +15,7 @@ from . import _native as N
 from .core import CqkInstance
 
 __all__ = ["CQK_FAMILIES", "SIMPLEX_FAMILIES", "FamilyMismatch", "gen_cqk", "gen_simplex_y",
-           "Xoshiro256pp"]
+           "gen_cqk_device", "gen_simplex_y_device", "Xoshiro256pp"]
 
 CQK_FAMILIES = ("cqk-uncorrelated", "cqk-weakly-correlated", "cqk-correlated")
 SIMPLEX_FAMILIES = ("simplex-u01", "simplex-n01", "simplex-n0m3")
@@ -108,3 +108,64 @@ class Xoshiro256pp:
     def integers(self, upper, size):
         u = self.uniform01(size)
         return np.minimum((u * upper).astype(np.int64), upper - 1)
+
+
+def gen_cqk_device(family, n, seed, device=None):
+    """gen_cqk straight into CUDA memory: bit-identical arrays (per-thread
+    GF(2) jumps of the Xoshiro256++ stream), r from device b.l / b.u sums.
+    Returns a CqkInstance of CUDA tensors."""
+    import torch
+
+    if family not in CQK_FAMILIES:
+        raise FamilyMismatch(f"not a CQK family: {family!r}")
+    h = N.handle(device)
+    h.set_stream(torch.cuda.current_stream(h.device).cuda_stream)
+    arrs = [torch.empty(int(n), dtype=torch.float64, device=f"cuda:{h.device}") for _ in range(5)]
+    r = ctypes.c_double()
+    rc = h.lib.cqk_gen_cqk_device(h.ptr, CQK_FAMILIES.index(family), int(n),
+                                  int(seed) & (2**64 - 1), *[t.data_ptr() for t in arrs],
+                                  ctypes.byref(r))
+    if rc != 0:
+        raise N.NativeError(f"device generator failed ({rc}): {N.last_error()}")
+    return CqkInstance(*arrs, r=float(r.value))
+
+
+def gen_cqk_shard_device(family, n, seed, lo, hi, device=None):
+    """Elements [lo, hi) of gen_cqk(family, n, seed) generated in CUDA memory:
+    ([d, a, b, l, u] tensors, bl, bu) -- combine the shards' b.l / b.u with
+    cqk_r to get the instance's r."""
+    import torch
+
+    if family not in CQK_FAMILIES:
+        raise FamilyMismatch(f"not a CQK family: {family!r}")
+    h = N.handle(device)
+    h.set_stream(torch.cuda.current_stream(h.device).cuda_stream)
+    arrs = [torch.empty(int(hi) - int(lo), dtype=torch.float64, device=f"cuda:{h.device}")
+            for _ in range(5)]
+    bl, bu = ctypes.c_double(), ctypes.c_double()
+    rc = h.lib.cqk_gen_cqk_device_range(h.ptr, CQK_FAMILIES.index(family), int(n),
+                                        int(seed) & (2**64 - 1), int(lo), int(hi),
+                                        *[t.data_ptr() for t in arrs], ctypes.byref(bl),
+                                        ctypes.byref(bu))
+    if rc != 0:
+        raise N.NativeError(f"device generator failed ({rc}): {N.last_error()}")
+    return arrs, float(bl.value), float(bu.value)
+
+
+def gen_simplex_y_device(family, n, seed, device=None):
+    """gen_simplex_y into CUDA memory: simplex-u01 is generated on the device
+    (bit-identical); the normal families use the host generator (their
+    Box-Muller log/cos must be glibc's to stay bit-identical) and one copy."""
+    import torch
+
+    if family not in SIMPLEX_FAMILIES:
+        raise FamilyMismatch(f"not a simplex family: {family!r}")
+    h = N.handle(device)
+    if family != "simplex-u01":
+        return torch.from_numpy(gen_simplex_y(family, n, seed)).to(f"cuda:{h.device}")
+    h.set_stream(torch.cuda.current_stream(h.device).cuda_stream)
+    y = torch.empty(int(n), dtype=torch.float64, device=f"cuda:{h.device}")
+    rc = h.lib.cqk_gen_simplex_u01_device(h.ptr, int(n), int(seed) & (2**64 - 1), y.data_ptr())
+    if rc != 0:
+        raise N.NativeError(f"device generator failed ({rc}): {N.last_error()}")
+    return y
