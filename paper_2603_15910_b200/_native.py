@@ -156,7 +156,7 @@ def load_library(path=None):
     global _lib
     with _lock:
         if _lib is None:
-            p = path or LIB_PATH
+            p = path or os.environ.get("CQK_LIB") or LIB_PATH
             if not os.path.exists(p):
                 raise NativeUnavailable(
                     f"{p} is missing: run `python -m paper_2603_15910_b200.build` "

@@ -59,6 +59,8 @@ struct Cmd {
   int32_t compact;  // this scan writes the survivors into scratch
   int32_t right;    // PH_BP direction
   int32_t check_lu; // this (first) scan also validates l and u
+  int32_t live_lo;  // a lower-fixed element may still be physically present
+  int32_t live_hi;  // ... an upper-fixed one
 };
 
 // Master-side solver state (SolveState, newton.py:70-90, plus counters).
@@ -67,6 +69,7 @@ struct CqkState {
   double lo, hi, phi_lo, phi_hi;
   double r_res, r_orig, fixed_abs, tau;
   double lam0, compact_ratio;
+  double fhi_phys, flo_phys;  // fixing multipliers the working set was last compacted at
   int64_t fixed_count, fixed_removed, iterations, phi_evals, max_iter;
   int64_t n, phys_count, pending_phys;  // n: global size; phys_count: this rank
   int64_t fixed_local;                  // logically fixed elements of this rank
@@ -131,6 +134,11 @@ DEVI void m_post_step(CqkState& s, double next) {
   if (s.iterations > s.max_iter) { m_stop(s, ST_MAXITER); return; }
   s.cmd.phase = PH_SCAN;
   s.cmd.compact = 0;
+  // The fixed tests are needed only while some element fixed at the current
+  // multipliers can still be physically present: the last compaction (if
+  // any) removed everything fixed at fhi_phys / flo_phys.
+  s.cmd.live_lo = s.fixing && s.cmd.fix_hi != s.fhi_phys;
+  s.cmd.live_hi = s.fixing && s.cmd.fix_lo != s.flo_phys;
   if (s.fixing) {  // a purely local (per-rank) byte decision
     const int64_t present = s.fixed_local - s.fixed_removed;
     if (present > 0 && (double)present >= s.compact_ratio * (double)s.phys_count) {
@@ -157,6 +165,8 @@ DEVI void m_after_scan(CqkState& s, const double* tot, const double* loc, double
     s.fixed_removed += s.phys_count - s.pending_phys;
     s.phys_count = s.pending_phys;
     s.cmd.compact = 0;
+    s.fhi_phys = s.cmd.fix_hi;  // everything fixed at these multipliers is gone
+    s.flo_phys = s.cmd.fix_lo;
   }
   const double lam = s.cmd.lam;
   const double value = tot[0], abs_bx = tot[1];

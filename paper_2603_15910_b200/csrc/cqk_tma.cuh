@@ -1,0 +1,676 @@
+// cqk_tma.cuh -- TMA-pipelined persistent CQK solve (sm_100a, fp64).
+//
+// Same single-launch solve as cqk_solve_kernel (the Newton state machine of
+// cqk_solver.cuh, replayed on CTA 0's thread 0), with a Blackwell streaming
+// engine underneath every pass:
+//
+//   * tiles of kTileC elements; CTA c owns tiles c, c+G, c+2G, ... so at any
+//     moment the whole grid streams one contiguous window of every array;
+//   * one producer warp per CTA (one elected lane) keeps kStagesC tiles of
+//     all streamed arrays in flight into shared memory with 1-D bulk TMA
+//     copies (cp.async.bulk ... mbarrier::complete_tx) -- ~160 KB in flight
+//     per SM without spending registers on it;
+//   * kConsW consumer warps evaluate the element math out of shared memory
+//     and release each stage with one mbarrier arrive per warp;
+//   * compaction writes the survivors of CTA c densely into CTA c's own tile
+//     slots of the scratch arrays (slot q = tile c + qG), so later passes
+//     stream the same tile layout, from the front of scratch, with the same
+//     producer; a CTA only ever rewrites slots it has already fully loaded
+//     (in place is safe) and a proxy fence orders those generic stores before
+//     the next pass's bulk loads.
+//
+// Per-element arithmetic (elem_scan / elem_bp / elem_final), the fixed-order
+// reductions and the grid step are those of the warp-segment kernel, so the
+// decisions, counters and tolerances are unchanged; only the summation order
+// (and hence rounding-level bits) differs between the two engines.
+#pragma once
+#include "cqk_kernels.cuh"
+
+namespace cqk {
+
+#ifndef CQK_TMA_TILE
+#define CQK_TMA_TILE 960
+#endif
+#ifndef CQK_TMA_STAGES
+#define CQK_TMA_STAGES 4
+#endif
+#ifndef CQK_TMA_CONSW
+#define CQK_TMA_CONSW 15
+#endif
+constexpr int kTileC = CQK_TMA_TILE;      // elements per array per tile
+constexpr int kStagesC = CQK_TMA_STAGES;
+constexpr int kArrMaxC = 6;               // d, a, b, l, u, xbar
+constexpr int kConsW = CQK_TMA_CONSW;     // consumer warps
+constexpr int kConsT = 32 * kConsW;
+constexpr int kTmaThreads = kConsT + 32;  // + one producer warp
+constexpr int kStageElemsC = kArrMaxC * kTileC;
+constexpr size_t kSmemC = (size_t)kStagesC * kStageElemsC * sizeof(double);
+constexpr int kEptC = kTileC / kConsT;    // elements per consumer thread per tile
+constexpr int kVpt = kEptC / 2;           // double2 vectors per thread per array
+static_assert(kEptC % 2 == 0 && kEptC * kConsT == kTileC, "tile must split into double2 per thread");
+
+DEVI void mbar_init_count(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+DEVI void mbar_arrive1(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+DEVI void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+DEVI void consumer_bar() { asm volatile("bar.sync 1, %0;" ::"n"(kConsT) : "memory"); }
+
+// Tile / slot geometry.  Every tile of kTileC elements is split into kConsW
+// warp sub-segments of kSeg = 32 * kEptC elements; lane l of warp w owns the
+// sub-segment elements 64u + 2l + v (u < kVpt, v < 2), i.e. conflict-free
+// 16-byte shared loads.  Original layout: tile t covers [t*T, min((t+1)*T, n)).
+// Scratch layout: slot q of CTA c is tile index c + q*G, and warp w's
+// survivors fill sub-segment w of the CTA's slots 0, 1, ... densely -- so
+// compaction needs no CTA-wide prefix (no barrier), stays deterministic, and a
+// warp only ever rewrites sub-segments it has already consumed.
+constexpr int kSeg = 32 * kEptC;
+static_assert(kSeg * kConsW == kTileC, "warp sub-segments tile the tile");
+
+DEVI int e_loc(int lane, int j) { return 64 * (j >> 1) + 2 * lane + (j & 1); }
+
+// Tiles (original arrays, nslots < 0: tile t = c + qG covers
+// [t*T, min((t+1)*T, n))) or the nslots scratch slots of this CTA.
+struct TileWalk {
+  int64_t n, ntiles;
+  int nslots;
+};
+
+// Streamed array set, passed by value so the pointers live in registers.
+struct Src {
+  const double* p[kArrMaxC];
+};
+
+struct TPipe {
+  double* buf;
+  unsigned long long* full;
+  unsigned long long* empty;
+  unsigned pc;  // tiles through the pipeline since kernel start (same on both sides)
+};
+
+// Producer (one lane): NA arrays of every tile of the walk, 16-byte granular
+// (the odd last element of an odd-length array is read by its consumer
+// straight from global memory).
+// Pipeline geometry: ST stages of STRIDE elements (NA arrays of kTileC each).
+// The 5/6-array passes use kStagesC stages of kArrMaxC arrays; the 3-array
+// lambda0 pass re-cuts the same shared memory into twice as many stages (its
+// own mbarriers and counter), keeping the same bytes in flight.
+constexpr int kStages3 = kStagesC * 2;
+constexpr int kStride3 = 3 * kTileC;
+
+template <int NA, int ST = kStagesC, int STRIDE = kStageElemsC>
+DEVI void produce(const Src src, const TileWalk& tw, TPipe& pp) {
+  const int64_t step = (int64_t)gridDim.x * kTileC;
+  const int64_t end = tw.nslots < 0 ? tw.n : ((int64_t)blockIdx.x + (int64_t)tw.nslots * gridDim.x) * kTileC;
+  int s = pp.pc % ST;
+  unsigned ph = ((pp.pc / ST) & 1) ^ 1;  // parity of the previous use of stage s
+  bool first_round = pp.pc < (unsigned)ST;
+  for (int64_t base = (int64_t)blockIdx.x * kTileC; base < end; base += step) {
+    if (!first_round) mbar_wait(&pp.empty[s], ph);
+    const int64_t left = tw.n - base;
+    const int cnt = tw.nslots < 0 && left < kTileC ? (int)left : kTileC;
+    const unsigned bytes = ((unsigned)cnt * 8u) & ~15u;
+    mbar_expect_tx(&pp.full[s], NA * bytes);
+    if (bytes) {
+#pragma unroll
+      for (int k = 0; k < NA; ++k)
+        tma_load_1d(pp.buf + (size_t)s * STRIDE + k * kTileC, src.p[k] + base, bytes, &pp.full[s]);
+    }
+    ++pp.pc;
+    if (++s == ST) { s = 0; ph ^= 1; first_round = false; }
+  }
+}
+
+// What a consumer warp sees of one tile: its sub-segment of every array in
+// shared memory (sm + k*T), the matching global sub-segment (base of the
+// warp's elements) and how many of its kSeg elements are valid.
+struct WTile {
+  const double* sm;   // stage + kSeg * warp
+  int64_t gbase;      // element index of the sub-segment's first element
+  int wcnt;           // valid elements of this warp's sub-segment (0..kSeg)
+  bool patch;         // odd original tile: element wcnt-1 is not in the stage
+  int q;              // slot / tile ordinal of this CTA in the pass
+};
+
+// Consumer warps: body(WTile) per tile, then release the stage.
+// m_w >= 0: scratch walk with this warp's element count m_w.
+template <int ST = kStagesC, int STRIDE = kStageElemsC, typename Body>
+DEVI void consume(const TileWalk& tw, TPipe& pp, int64_t m_w, Body&& body) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t step = (int64_t)gridDim.x * kTileC;
+  const bool scratch = tw.nslots >= 0;
+  const int64_t end = scratch ? ((int64_t)blockIdx.x + (int64_t)tw.nslots * gridDim.x) * kTileC : tw.n;
+  int s = pp.pc % ST;
+  unsigned ph = (pp.pc / ST) & 1;
+  // valid elements of this warp's sub-segment still ahead (scratch walk)
+  int64_t left_w = m_w;
+  WTile wt;
+  wt.q = 0;
+  for (int64_t base = (int64_t)blockIdx.x * kTileC; base < end; base += step, ++wt.q) {
+    wt.sm = pp.buf + (size_t)s * STRIDE + kSeg * warp;
+    wt.gbase = base + kSeg * warp;
+    const int64_t left = scratch ? left_w : tw.n - wt.gbase;
+    wt.wcnt = left <= 0 ? 0 : (left < kSeg ? (int)left : kSeg);
+    wt.patch = !scratch && (wt.wcnt & 1) && wt.wcnt < kSeg;
+    left_w -= kSeg;
+    mbar_wait(&pp.full[s], ph);
+    if (wt.wcnt > 0) body(wt);
+    __syncwarp();
+    if (lane == 0) mbar_arrive1(&pp.empty[s]);
+    ++pp.pc;
+    if (++s == ST) { s = 0; ph ^= 1; }
+  }
+}
+
+template <bool FULL = false>
+DEVI void tile_load(const WTile& wt, int k, const double* garr, double (&v)[kEptC],
+                    double fill = 0.0) {
+  const int lane = threadIdx.x & 31;
+  const double* sarr = wt.sm + k * kTileC;
+#pragma unroll
+  for (int u = 0; u < kVpt; ++u) {
+    const double2 w = *reinterpret_cast<const double2*>(sarr + 64 * u + 2 * lane);
+    v[2 * u] = w.x;
+    v[2 * u + 1] = w.y;
+  }
+  if (!FULL) {
+#pragma unroll
+    for (int j = 0; j < kEptC; ++j)
+      if (e_loc(lane, j) >= wt.wcnt) v[j] = fill;  // neutral values beyond the data
+    if (wt.patch) {
+      const int e = wt.wcnt - 1;  // even: the (v = 0) element of pair e / 2
+#pragma unroll
+      for (int u = 0; u < kVpt; ++u)
+        if (64 * u + 2 * lane == e) v[2 * u] = ld_scratch(garr + wt.gbase + e);
+    }
+  }
+}
+
+// ------------------------------------------------------------ fast element math
+// The fast division of div_y (cqk_device.cuh) is bit-identical to __ddiv_rn
+// whenever numerator and divisor lie in [2^-500, 2^500).  The range test
+// runs on the exponent bits with integer ops (no FP64 compares, no branch per
+// division); a warp whose tile holds any operand outside it recomputes its
+// quotients with __ddiv_rn in one warp-uniform (practically never taken)
+// branch -- so the per-element path is straight-line code.
+DEVI bool exp_ok(double x) {
+  const unsigned e = ((unsigned)__double2hiint(x) >> 20) & 0x7ffu;
+  return e - 523u < 1000u;
+}
+DEVI double div_fast(double a, double b, double y) {
+  const double q0 = __dmul_rn(a, y);
+  const double r = fma(q0, -b, a);
+  return fma(y, r, q0);
+}
+
+// t, w = b*b/d and the stateless fixed tests (t(fix_hi) <= l, t(fix_lo) >= u,
+// cqk_solver.cuh elem_scan) for the kEptC elements of this thread.
+template <bool FIX>
+DEVI void tile_t(const double (&D)[kEptC], const double (&A)[kEptC], const double (&B)[kEptC],
+                 const double (&L)[kEptC], const double (&U)[kEptC], double lam, double fhi,
+                 double flo, bool chk_lo, bool chk_hi, double (&T)[kEptC], double (&W)[kEptC],
+                 bool (&FXL)[kEptC], bool (&FXH)[kEptC]) {
+  bool ok = true;
+#pragma unroll
+  for (int j = 0; j < kEptC; ++j) {
+    const double yd = rcp_div(D[j]);
+    const double num = add_rn(mul_rn(B[j], lam), A[j]);
+    T[j] = div_fast(num, D[j], yd);
+    W[j] = (double)(mul_rn(B[j], B[j]) * yd);
+    ok = ok && exp_ok(num) && exp_ok(D[j]);
+    FXL[j] = FXH[j] = false;
+    if (FIX && chk_lo) {
+      const double nh = add_rn(mul_rn(B[j], fhi), A[j]);
+      FXL[j] = div_fast(nh, D[j], yd) <= L[j];
+      ok = ok && exp_ok(nh);
+    }
+    if (FIX && chk_hi) {
+      const double nl = add_rn(mul_rn(B[j], flo), A[j]);
+      FXH[j] = div_fast(nl, D[j], yd) >= U[j];
+      ok = ok && exp_ok(nl);
+    }
+  }
+  if (!__all_sync(0xffffffffu, ok)) {
+#pragma unroll
+    for (int j = 0; j < kEptC; ++j) {
+      T[j] = div_rn(add_rn(mul_rn(B[j], lam), A[j]), D[j]);
+      if (FIX && chk_lo) FXL[j] = div_rn(add_rn(mul_rn(B[j], fhi), A[j]), D[j]) <= L[j];
+      if (FIX && chk_hi) FXH[j] = div_rn(add_rn(mul_rn(B[j], flo), A[j]), D[j]) >= U[j];
+    }
+  }
+}
+
+// ------------------------------------------------------------ consumer passes
+template <bool CHECK, bool XBAR>
+DEVI void t_lambda0(const CqkParams<double>& p, const TileWalk& tw, TPipe& pp,
+                    double (&acc)[kMaxK]) {
+  const int lane = threadIdx.x & 31;
+  constexpr int ST = XBAR ? kStagesC : kStages3;
+  constexpr int STRIDE = XBAR ? kStageElemsC : kStride3;
+  consume<ST, STRIDE>(tw, pp, -1, [&](const WTile& wt) {
+    double D[kEptC], A[kEptC], B[kEptC], L[kEptC], U[kEptC], X[kEptC];
+    tile_load(wt, 0, p.d, D, 1.0);
+    tile_load(wt, 1, p.a, A);
+    tile_load(wt, 2, p.b, B, 1.0);
+    if (XBAR) {
+      tile_load(wt, 3, p.l, L);
+      tile_load(wt, 4, p.u, U);
+      tile_load(wt, 5, p.xbar, X);
+    }
+    bool bad = false;
+#pragma unroll
+    for (int j = 0; j < kEptC; ++j) {
+      const bool valid = e_loc(lane, j) < wt.wcnt;
+      const double y = rcp_nr(D[j]);
+      const double s = mul_rn(B[j], A[j] * y);
+      const double q = mul_rn(B[j], B[j] * y);
+      if (valid) { acc[0] += s; acc[1] += q; }
+      if (XBAR && valid && L[j] < X[j] && X[j] < U[j]) { acc[2] += s; acc[3] += q; acc[4] += 1.0; }
+      if (CHECK) {
+        bool b_ = !(D[j] > 0.0 && D[j] < HUGE_VAL) || !(fabs(A[j]) < HUGE_VAL) ||
+                  !(B[j] > 0.0 && B[j] < HUGE_VAL);
+        if (XBAR) b_ = b_ || !(L[j] <= U[j]) || L[j] == HUGE_VAL || U[j] == -HUGE_VAL;
+        bad = bad || (valid && b_);
+      }
+    }
+    if (CHECK && __any_sync(0xffffffffu, bad)) {  // rare: locate the first offenders
+#pragma unroll
+      for (int j = 0; j < kEptC; ++j) {
+        const int e = e_loc(lane, j);
+        if (e >= wt.wcnt) continue;
+        const double gi = (double)(p.offset + wt.gbase + e);
+        const double d = D[j], a = A[j], b = B[j];
+        if (!isfinite(d)) acc[5] = fmin(acc[5], gi);
+        if (!isfinite(a)) acc[6] = fmin(acc[6], gi);
+        if (!isfinite(b)) acc[7] = fmin(acc[7], gi);
+        if (!(d > 0.0)) acc[10] = fmin(acc[10], gi);
+        if (!(b > 0.0)) acc[11] = fmin(acc[11], gi);
+        if (XBAR) {
+          const double l = L[j], u = U[j];
+          if (isnan(l)) acc[8] = fmin(acc[8], gi);
+          if (isnan(u)) acc[9] = fmin(acc[9], gi);
+          if (!(l <= u)) acc[12] = fmin(acc[12], gi);
+          if (l == HUGE_VAL) acc[13] = fmin(acc[13], gi);
+          if (u == -HUGE_VAL) acc[14] = fmin(acc[14], gi);
+        }
+      }
+    }
+  });
+}
+
+// One tile of the phi scan (core.py:233-263 per element, as elem_scan in
+// cqk_solver.cuh) for this thread's kEptC elements; keep[j]: the element is
+// (logically) active.  Straight-line: predicated accumulation, counts in
+// integer registers, the l / u validation on one warp-uniform branch.
+template <bool FIX, bool CHK, bool FULL>
+DEVI void scan_tile(const CqkParams<double>& p, const WTile& wt, const Src& src, double lam,
+                    double fhi, double flo, bool chk_lo, bool chk_hi, double (&acc)[kMaxK],
+                    int (&nfix)[2], bool (&keep)[kEptC]) {
+  const int lane = threadIdx.x & 31;
+  double D[kEptC], A[kEptC], B[kEptC], L[kEptC], U[kEptC];
+  tile_load<FULL>(wt, 0, src.p[0], D, 1.0);
+  tile_load<FULL>(wt, 1, src.p[1], A);
+  tile_load<FULL>(wt, 2, src.p[2], B, 1.0);
+  tile_load<FULL>(wt, 3, src.p[3], L);
+  tile_load<FULL>(wt, 4, src.p[4], U);
+  if (CHK) {  // validate()'s l / u checks ride on the first scan
+    bool bad = false;
+#pragma unroll
+    for (int j = 0; j < kEptC; ++j) {
+      const bool valid = FULL || e_loc(lane, j) < wt.wcnt;
+      bad = bad || (valid && (!(L[j] <= U[j]) || L[j] == HUGE_VAL || U[j] == -HUGE_VAL));
+    }
+    if (__any_sync(0xffffffffu, bad)) {
+#pragma unroll
+      for (int j = 0; j < kEptC; ++j) {
+        const int e = e_loc(lane, j);
+        if (!FULL && e >= wt.wcnt) continue;
+        const double gi = (double)(p.offset + wt.gbase + e);
+        const double l = L[j], u = U[j];
+        if (isnan(l)) acc[kCheckLuSlot] = fmin(acc[kCheckLuSlot], gi);
+        if (isnan(u)) acc[kCheckLuSlot + 1] = fmin(acc[kCheckLuSlot + 1], gi);
+        if (!(l <= u)) acc[kCheckLuSlot + 2] = fmin(acc[kCheckLuSlot + 2], gi);
+        if (l == HUGE_VAL) acc[kCheckLuSlot + 3] = fmin(acc[kCheckLuSlot + 3], gi);
+        if (u == -HUGE_VAL) acc[kCheckLuSlot + 4] = fmin(acc[kCheckLuSlot + 4], gi);
+      }
+    }
+  }
+  double T[kEptC], W[kEptC];
+  bool FXL[kEptC], FXH[kEptC];
+  tile_t<FIX>(D, A, B, L, U, lam, fhi, flo, chk_lo, chk_hi, T, W, FXL, FXH);
+#pragma unroll
+  for (int j = 0; j < kEptC; ++j) {
+    const bool valid = FULL || e_loc(lane, j) < wt.wcnt;
+    const double t = T[j], l = L[j], u = U[j];
+    const bool alo = t <= l, ahi = t >= u;
+    bool fixed = false;
+    if (FIX) fixed = (alo && FXL[j]) || (ahi && FXH[j]);
+    const bool kp = valid && !fixed;
+    keep[j] = kp;
+    const double bx = mul_rn(B[j], clip(t, l, u));
+    const double w = W[j];
+    const bool lt = l < u;
+    if (kp) { acc[0] += bx; acc[1] += fabs(bx); }
+    if (kp && !(alo || ahi)) acc[2] += w;
+    if (kp && alo && lt && t == l) acc[3] += w;
+    if (kp && ahi && lt && t == u) acc[4] += w;
+    if (FIX) {
+      if (kp && alo) { acc[5] += bx; acc[6] += fabs(bx); nfix[0] += 1; }
+      if (kp && ahi) { acc[8] += bx; acc[9] += fabs(bx); nfix[1] += 1; }
+    }
+  }
+}
+
+// phi scan over the walk (m_w >= 0: this warp's scratch count); with
+// `compact` every warp appends its survivors to its own scratch
+// sub-segments.  Returns this warp's new element count.
+template <bool FIX, bool CHK>
+DEVI int64_t t_scan(const CqkParams<double>& p, const Cmd& c, const TileWalk& tw, int64_t m_w,
+                    const Src src, bool compact, TPipe& pp, double (&acc)[kMaxK]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned ltm = (1u << lane) - 1u;
+  const double lam = c.lam, fhi = c.fix_hi, flo = c.fix_lo;
+  const bool chk_lo = FIX && c.live_lo, chk_hi = FIX && c.live_hi;
+  int nfix[2] = {0, 0};
+  int64_t out_m = 0;  // survivors so far: slots [0, q_out) full plus off_out in slot q_out
+  int64_t q_out = 0;
+  int off_out = 0;
+  const int64_t g = gridDim.x;
+  consume(tw, pp, m_w, [&](const WTile& wt) {
+    bool keep[kEptC];
+    if (wt.wcnt == kSeg)
+      scan_tile<FIX, CHK, true>(p, wt, src, lam, fhi, flo, chk_lo, chk_hi, acc, nfix, keep);
+    else
+      scan_tile<FIX, CHK, false>(p, wt, src, lam, fhi, flo, chk_lo, chk_hi, acc, nfix, keep);
+    if (FIX && compact) {
+      // survivor r of this tile (r < kSeg) lands at sub-segment offset
+      // off_out + r: slot q_out or, after one wrap, q_out + 1
+      const int64_t b0 = ((int64_t)blockIdx.x + q_out * g) * kTileC + kSeg * warp;
+      const int64_t b1 = b0 + g * kTileC;
+      // the survivors' values come back from the (still held) stage
+      double D[kEptC], A[kEptC], B[kEptC], L[kEptC], U[kEptC];
+      tile_load(wt, 0, src.p[0], D);
+      tile_load(wt, 1, src.p[1], A);
+      tile_load(wt, 2, src.p[2], B);
+      tile_load(wt, 3, src.p[3], L);
+      tile_load(wt, 4, src.p[4], U);
+      int r = off_out;
+#pragma unroll
+      for (int j = 0; j < kEptC; ++j) {
+        const unsigned bal = __ballot_sync(0xffffffffu, keep[j]);
+        if (keep[j]) {
+          const int o = r + __popc(bal & ltm);
+          const int64_t pos = o < kSeg ? b0 + o : b1 + (o - kSeg);
+          p.sd[pos] = D[j]; p.sa[pos] = A[j]; p.sb[pos] = B[j]; p.sl[pos] = L[j]; p.su[pos] = U[j];
+        }
+        r += __popc(bal);
+      }
+      out_m += r - off_out;
+      off_out = r;
+      if (off_out >= kSeg) { off_out -= kSeg; ++q_out; }
+    }
+  });
+  if (FIX) { acc[7] += (double)nfix[0]; acc[10] += (double)nfix[1]; }
+  if (FIX && compact) fence_proxy_async_global();  // generic stores -> next pass's bulk loads
+  return out_m;
+}
+
+DEVI void t_bp(const CqkParams<double>& p, const Cmd& c, bool fix, const TileWalk& tw,
+               int64_t m_w, const Src src, TPipe& pp, double (&acc)[kMaxK]) {
+  const int lane = threadIdx.x & 31;
+  const double lam = c.lam, fhi = c.fix_hi, flo = c.fix_lo;
+  const bool right = c.right != 0;
+  consume(tw, pp, m_w, [&](const WTile& wt) {
+    double D[kEptC], A[kEptC], B[kEptC], L[kEptC], U[kEptC];
+    tile_load(wt, 0, src.p[0], D, 1.0);
+    tile_load(wt, 1, src.p[1], A);
+    tile_load(wt, 2, src.p[2], B, 1.0);
+    tile_load(wt, 3, src.p[3], L);
+    tile_load(wt, 4, src.p[4], U);
+#pragma unroll
+    for (int j = 0; j < kEptC; ++j) {
+      if (e_loc(lane, j) >= wt.wcnt) continue;
+      if (fix) {  // only the logically active set takes part
+        const double yd = rcp_div(D[j]);
+        const double t = t_of_y(D[j], A[j], B[j], lam, yd);
+        if (isfinite(c.fix_hi) && t <= L[j] && t_of_y(D[j], A[j], B[j], fhi, yd) <= L[j]) continue;
+        if (isfinite(c.fix_lo) && t >= U[j] && t_of_y(D[j], A[j], B[j], flo, yd) >= U[j]) continue;
+      }
+      elem_bp<double>(D[j], A[j], B[j], L[j], U[j], c.edge, right, acc[0], acc[1]);
+    }
+  });
+}
+
+template <bool FIX, bool FULL>
+DEVI void final_tile(const CqkParams<double>& p, const WTile& wt, double lam, double fhi,
+                     double flo, bool chk_lo, bool chk_hi) {
+  const int lane = threadIdx.x & 31;
+  double D[kEptC], A[kEptC], B[kEptC], L[kEptC], U[kEptC];
+  tile_load<FULL>(wt, 0, p.d, D, 1.0);
+  tile_load<FULL>(wt, 1, p.a, A);
+  tile_load<FULL>(wt, 2, p.b, B, 1.0);
+  tile_load<FULL>(wt, 3, p.l, L);
+  tile_load<FULL>(wt, 4, p.u, U);
+  double T[kEptC], W[kEptC], X[kEptC];
+  bool FXL[kEptC], FXH[kEptC];
+  tile_t<FIX>(D, A, B, L, U, lam, fhi, flo, chk_lo, chk_hi, T, W, FXL, FXH);
+#pragma unroll
+  for (int j = 0; j < kEptC; ++j) {  // elem_final: fixed variables keep their bound
+    double x = clip(T[j], L[j], U[j]);
+    if (FIX) {
+      if (FXL[j]) x = L[j];
+      else if (FXH[j]) x = U[j];
+    }
+    X[j] = x;
+  }
+#pragma unroll
+  for (int u = 0; u < kVpt; ++u) {
+    const int e = 64 * u + 2 * lane;
+    double* xp = p.x + wt.gbase + e;
+    if (FULL || e + 1 < wt.wcnt) store_out(reinterpret_cast<double2*>(xp), make_double2(X[2 * u], X[2 * u + 1]));
+    else if (e < wt.wcnt) *xp = X[2 * u];
+  }
+}
+
+template <bool FIX>
+DEVI void t_final(const CqkParams<double>& p, const Cmd& c, const TileWalk& tw, TPipe& pp) {
+  const double lam = c.lam, fhi = c.fix_hi, flo = c.fix_lo;
+  // fixed variables need an explicit test only if lam* left the side of the
+  // fixing multiplier (the criterion-2 finish(lam + step) edge)
+  const bool chk_lo = FIX && c.lam > c.fix_hi, chk_hi = FIX && c.lam < c.fix_lo;
+  consume(tw, pp, -1, [&](const WTile& wt) {
+    if (wt.wcnt == kSeg) final_tile<FIX, true>(p, wt, lam, fhi, flo, chk_lo, chk_hi);
+    else final_tile<FIX, false>(p, wt, lam, fhi, flo, chk_lo, chk_hi);
+  });
+}
+
+// ------------------------------------------------------------ the kernel
+template <bool FIX>
+__global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<double> p) {
+  extern __shared__ __align__(128) unsigned char s_dyn[];
+  __shared__ __align__(8) unsigned long long s_full[kStagesC], s_empty[kStagesC];
+  __shared__ __align__(8) unsigned long long s_full3[kStages3], s_empty3[kStages3];
+  __shared__ double s_red[kConsW + 1][kMaxK];
+  __shared__ double s_tot[kMaxK];
+  __shared__ Cmd s_cmd;
+  __shared__ CqkState s_st;  // master (CTA 0) only
+  __shared__ unsigned s_gen0;
+  __shared__ int s_abort;
+  __shared__ int s_nslots;   // scratch slots of this CTA (max over its warps)
+  __shared__ int s_nsl_new;  // ... being formed by a compacting pass
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool producer = warp == kConsW;
+  const bool master = blockIdx.x == 0;
+  TPipe pp{reinterpret_cast<double*>(s_dyn), s_full, s_empty, 0u};
+  TPipe pp3{reinterpret_cast<double*>(s_dyn), s_full3, s_empty3, 0u};  // 3-array lambda0 pass
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStagesC; ++s) {
+      mbar_init_count(&s_full[s], 1);
+      mbar_init_count(&s_empty[s], kConsW);
+    }
+    for (int s = 0; s < kStages3; ++s) {
+      mbar_init_count(&s_full3[s], 1);
+      mbar_init_count(&s_empty3[s], kConsW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    s_gen0 = ld_acquire(p.sync.gen);
+    s_abort = 0;
+    s_nslots = 0;
+    s_nsl_new = 0;
+    if (master) {
+      s_st = *p.st;  // host-initialised before the launch
+      s_cmd = s_st.cmd;
+      tl_record(p.sync, 0, -1, p.n, 0);
+    } else {
+      load_l2(&s_cmd, &p.st->cmd);
+    }
+  }
+  __syncthreads();
+  const int64_t ntiles = (p.n + kTileC - 1) / kTileC;
+  const TileWalk orig{p.n, ntiles, -1};
+  const Src src_orig{{p.d, p.a, p.b, p.l, p.u, nullptr}};
+  const Src src_scr{{p.sd, p.sa, p.sb, p.sl, p.su, nullptr}};
+  const Src src_l0x{{p.d, p.a, p.b, p.l, p.u, p.xbar}};
+  const bool prod_lane = producer && lane == 0;
+  const int has_xbar = p.xbar != nullptr;
+  const int check = p.st->check;  // immutable during the solve
+  bool in_scratch = false;
+  int64_t m_w = -1;  // this warp's scratch element count (consumers, once in scratch)
+  for (unsigned epoch = 1;; ++epoch) {
+    const Cmd c = s_cmd;
+    if (c.phase == PH_DONE || s_abort) break;
+    const TileWalk work{p.n, ntiles, in_scratch ? s_nslots : -1};
+    const Src wsrc = in_scratch ? src_scr : src_orig;
+    if (c.phase == PH_FINAL) {
+      if (p.x) {
+        if (prod_lane) produce<5>(src_orig, orig, pp);
+        else if (!producer) t_final<FIX>(p, c, orig, pp);
+      }
+      break;
+    }
+    double acc[kMaxK];
+#pragma unroll
+    for (int k = 0; k < kMaxK; ++k) acc[k] = 0.0;
+    bool is_master = false;
+    if (c.phase == PH_LAMBDA0) {
+#pragma unroll
+      for (int k = kValidateSlot; k < kValidateSlot + 10; ++k) acc[k] = HUGE_VAL;
+      if (prod_lane) {
+        if (has_xbar) produce<6>(src_l0x, orig, pp);
+        else produce<3, kStages3, kStride3>(src_l0x, orig, pp3);
+      } else if (!producer) {
+        if (check && has_xbar) t_lambda0<true, true>(p, orig, pp, acc);
+        else if (check) t_lambda0<true, false>(p, orig, pp3, acc);
+        else if (has_xbar) t_lambda0<false, true>(p, orig, pp, acc);
+        else t_lambda0<false, false>(p, orig, pp3, acc);
+      }
+      const int ops[15] = {OP_SUM, OP_SUM, OP_SUM, OP_SUM, OP_SUM, OP_MIN, OP_MIN, OP_MIN,
+                           OP_MIN, OP_MIN, OP_MIN, OP_MIN, OP_MIN, OP_MIN, OP_MIN};
+      double a15[15];
+#pragma unroll
+      for (int k = 0; k < 15; ++k) a15[k] = acc[k];
+      block_reduce<15>(a15, ops, s_red, s_tot);
+      is_master = grid_step<15>(p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch);
+      if (is_master && threadIdx.x == 0) {
+        tl_record(p.sync, epoch, PH_LAMBDA0, p.n, 0);
+        double glob[15];
+        if (exchange_totals(p.ex, epoch, 15, ops, s_tot, glob)) m_after_lambda0(s_st, glob);
+        else m_stop(s_st, ST_TIMEOUT);
+      }
+    } else if (c.phase == PH_SCAN && c.check_lu) {
+#pragma unroll
+      for (int k = kCheckLuSlot; k < kMaxK; ++k) acc[k] = HUGE_VAL;
+      if (prod_lane) produce<5>(src_orig, orig, pp);
+      else if (!producer) t_scan<FIX, true>(p, c, orig, -1, src_orig, false, pp, acc);
+      int ops[kMaxK];
+#pragma unroll
+      for (int k = 0; k < kMaxK; ++k) ops[k] = k < kCheckLuSlot ? OP_SUM : OP_MIN;
+      block_reduce<kMaxK>(acc, ops, s_red, s_tot);
+      is_master = grid_step<kMaxK>(p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch);
+      if (is_master && threadIdx.x == 0) {
+        double loc[kMaxK], glob[kMaxK];
+#pragma unroll
+        for (int k = 0; k < kMaxK; ++k) loc[k] = s_tot[k];
+        tl_record(p.sync, epoch, PH_SCAN, s_st.phys_count, 0);
+        if (!exchange_totals(p.ex, epoch, kMaxK, ops, loc, glob)) {
+          m_stop(s_st, ST_TIMEOUT);
+        } else {
+          s_st.cmd.check_lu = 0;
+          s_st.vidx[3] = glob[11];  // l NaN
+          s_st.vidx[4] = glob[12];  // u NaN
+          s_st.vidx[7] = glob[13];  // l <= u
+          s_st.vidx[8] = glob[14];  // l == +inf
+          s_st.vidx[9] = glob[15];  // u == -inf
+          if (m_validate(s_st, 3, 10)) m_after_scan(s_st, glob, loc, p.trace);
+        }
+      }
+    } else if (c.phase == PH_SCAN) {
+      const bool compact = FIX && c.compact;
+      if (prod_lane) {
+        produce<5>(wsrc, work, pp);
+      } else if (!producer) {
+        const int64_t mm = t_scan<FIX, false>(p, c, work, m_w, wsrc, compact, pp, acc);
+        if (compact) {
+          m_w = mm;
+          if (lane == 0) atomicMax(&s_nsl_new, (int)((mm + kSeg - 1) / kSeg));
+        }
+      }
+      if (compact) in_scratch = true;
+      constexpr int K = FIX ? 11 : 5;
+      int ops[K];
+      double aK[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) { ops[k] = OP_SUM; aK[k] = acc[k]; }
+      block_reduce<K>(aK, ops, s_red, s_tot);  // (its barrier orders the atomicMax above)
+      if (compact && threadIdx.x == 0) {   // nobody reads s_nslots before the next epoch
+        s_nslots = s_nsl_new;
+        s_nsl_new = 0;
+      }
+      is_master = grid_step<K>(p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch);
+      if (is_master && threadIdx.x == 0) {
+        double loc[11], glob[11];
+#pragma unroll
+        for (int k = 0; k < 11; ++k) loc[k] = glob[k] = k < K ? s_tot[k] : 0.0;
+        tl_record(p.sync, epoch, PH_SCAN, s_st.phys_count, s_st.cmd.compact);
+        if (exchange_totals(p.ex, epoch, K, ops, loc, glob)) m_after_scan(s_st, glob, loc, p.trace);
+        else m_stop(s_st, ST_TIMEOUT);
+      }
+    } else if (c.phase == PH_BP) {
+      acc[0] = c.right ? HUGE_VAL : -HUGE_VAL;
+      if (prod_lane) produce<5>(wsrc, work, pp);
+      else if (!producer) t_bp(p, c, FIX, work, m_w, wsrc, pp, acc);
+      int ops[2] = {c.right ? OP_MIN : OP_MAX, OP_SUM};
+      double a2[2] = {acc[0], acc[1]};
+      block_reduce<2>(a2, ops, s_red, s_tot);
+      is_master = grid_step<2>(p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch);
+      if (is_master && threadIdx.x == 0) {
+        tl_record(p.sync, epoch, PH_BP, s_st.phys_count, 0);
+        double glob[2];
+        if (exchange_totals(p.ex, epoch, 2, ops, s_tot, glob)) m_after_bp(s_st, glob);
+        else m_stop(s_st, ST_TIMEOUT);
+      }
+    } else {
+      break;
+    }
+    if (threadIdx.x == 0) {
+      if (is_master) {
+        const int ph = s_st.cmd.phase;
+        if (ph == PH_FINAL || ph == PH_DONE) *p.st = s_st;  // results for the host
+        s_cmd = s_st.cmd;
+        master_release(p.sync, s_gen0 + epoch, s_st.cmd, &p.st->cmd);
+        tl_mark(p.sync, epoch, 5);
+      } else if (!s_abort) {
+        if (!wait_release(p.sync, s_gen0 + epoch, &p.st->cmd, &s_cmd)) s_abort = 1;
+        if (blockIdx.x == 1) tl_mark(p.sync, epoch, 7);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Scratch elements per array for the tile-slot layout (whole tiles).
+inline int64_t tma_scratch_elems(int64_t n) { return (n + kTileC - 1) / kTileC * kTileC; }
+
+}  // namespace cqk
