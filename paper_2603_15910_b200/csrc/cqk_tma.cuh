@@ -55,6 +55,25 @@ DEVI void mbar_init_count(unsigned long long* bar, unsigned count) {
 DEVI void mbar_arrive1(unsigned long long* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// Shared-window (u32) forms: the addresses are converted once per kernel.
+DEVI void mbar_wait_s(unsigned bar, unsigned phase) {
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n}" ::"r"(bar), "r"(phase) : "memory");
+}
+DEVI void mbar_arrive_s(unsigned bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+DEVI void mbar_expect_tx_s(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+DEVI void tma_load_1d_s(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
 DEVI void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 DEVI void consumer_bar() { asm volatile("bar.sync 1, %0;" ::"n"(kConsT) : "memory"); }
 
@@ -85,8 +104,7 @@ struct Src {
 
 struct TPipe {
   double* buf;
-  unsigned long long* full;
-  unsigned long long* empty;
+  unsigned full, empty;  // shared-window addresses of the mbarrier arrays (8 B each)
   unsigned pc;  // tiles through the pipeline since kernel start (same on both sides)
 };
 
@@ -108,15 +126,16 @@ DEVI void produce(const Src src, const TileWalk& tw, TPipe& pp) {
   unsigned ph = ((pp.pc / ST) & 1) ^ 1;  // parity of the previous use of stage s
   bool first_round = pp.pc < (unsigned)ST;
   for (int64_t base = (int64_t)blockIdx.x * kTileC; base < end; base += step) {
-    if (!first_round) mbar_wait(&pp.empty[s], ph);
+    if (!first_round) mbar_wait_s(pp.empty + 8 * s, ph);
     const int64_t left = tw.n - base;
     const int cnt = tw.nslots < 0 && left < kTileC ? (int)left : kTileC;
     const unsigned bytes = ((unsigned)cnt * 8u) & ~15u;
-    mbar_expect_tx(&pp.full[s], NA * bytes);
+    const unsigned fb = pp.full + 8 * s;
+    mbar_expect_tx_s(fb, NA * bytes);
     if (bytes) {
+      const unsigned dst = smem_u32(pp.buf) + (unsigned)(s * STRIDE) * 8u;
 #pragma unroll
-      for (int k = 0; k < NA; ++k)
-        tma_load_1d(pp.buf + (size_t)s * STRIDE + k * kTileC, src.p[k] + base, bytes, &pp.full[s]);
+      for (int k = 0; k < NA; ++k) tma_load_1d_s(dst + k * kTileC * 8u, src.p[k] + base, bytes, fb);
     }
     ++pp.pc;
     if (++s == ST) { s = 0; ph ^= 1; first_round = false; }
@@ -155,10 +174,10 @@ DEVI void consume(const TileWalk& tw, TPipe& pp, int64_t m_w, Body&& body) {
     wt.wcnt = left <= 0 ? 0 : (left < kSeg ? (int)left : kSeg);
     wt.patch = !scratch && (wt.wcnt & 1) && wt.wcnt < kSeg;
     left_w -= kSeg;
-    mbar_wait(&pp.full[s], ph);
+    mbar_wait_s(pp.full + 8 * s, ph);
     if (wt.wcnt > 0) body(wt);
     __syncwarp();
-    if (lane == 0) mbar_arrive1(&pp.empty[s]);
+    if (lane == 0) mbar_arrive_s(pp.empty + 8 * s);
     ++pp.pc;
     if (++s == ST) { s = 0; ph ^= 1; }
   }
@@ -195,9 +214,8 @@ DEVI void tile_load(const WTile& wt, int k, const double* garr, double (&v)[kEpt
 // division); a warp whose tile holds any operand outside it recomputes its
 // quotients with __ddiv_rn in one warp-uniform (practically never taken)
 // branch -- so the per-element path is straight-line code.
-DEVI bool exp_ok(double x) {
-  const unsigned e = ((unsigned)__double2hiint(x) >> 20) & 0x7ffu;
-  return e - 523u < 1000u;
+DEVI bool exp_ok(double x) {  // biased exponent in [523, 1522]
+  return (((unsigned)__double2hiint(x) & 0x7ff00000u) - (523u << 20)) < (1000u << 20);
 }
 DEVI double div_fast(double a, double b, double y) {
   const double q0 = __dmul_rn(a, y);
@@ -206,12 +224,13 @@ DEVI double div_fast(double a, double b, double y) {
 }
 
 // t, w = b*b/d and the stateless fixed tests (t(fix_hi) <= l, t(fix_lo) >= u,
-// cqk_solver.cuh elem_scan) for the kEptC elements of this thread.
-template <bool FIX>
+// cqk_solver.cuh elem_scan) for the kEptC elements of this thread; CLO / CHI
+// (warp-uniform, dispatched at compile time): which fixed tests are live.
+template <bool CLO, bool CHI>
 DEVI void tile_t(const double (&D)[kEptC], const double (&A)[kEptC], const double (&B)[kEptC],
                  const double (&L)[kEptC], const double (&U)[kEptC], double lam, double fhi,
-                 double flo, bool chk_lo, bool chk_hi, double (&T)[kEptC], double (&W)[kEptC],
-                 bool (&FXL)[kEptC], bool (&FXH)[kEptC]) {
+                 double flo, double (&T)[kEptC], double (&W)[kEptC], bool (&FXL)[kEptC],
+                 bool (&FXH)[kEptC]) {
   bool ok = true;
 #pragma unroll
   for (int j = 0; j < kEptC; ++j) {
@@ -221,12 +240,12 @@ DEVI void tile_t(const double (&D)[kEptC], const double (&A)[kEptC], const doubl
     W[j] = (double)(mul_rn(B[j], B[j]) * yd);
     ok = ok && exp_ok(num) && exp_ok(D[j]);
     FXL[j] = FXH[j] = false;
-    if (FIX && chk_lo) {
+    if (CLO) {
       const double nh = add_rn(mul_rn(B[j], fhi), A[j]);
       FXL[j] = div_fast(nh, D[j], yd) <= L[j];
       ok = ok && exp_ok(nh);
     }
-    if (FIX && chk_hi) {
+    if (CHI) {
       const double nl = add_rn(mul_rn(B[j], flo), A[j]);
       FXH[j] = div_fast(nl, D[j], yd) >= U[j];
       ok = ok && exp_ok(nl);
@@ -236,11 +255,23 @@ DEVI void tile_t(const double (&D)[kEptC], const double (&A)[kEptC], const doubl
 #pragma unroll
     for (int j = 0; j < kEptC; ++j) {
       T[j] = div_rn(add_rn(mul_rn(B[j], lam), A[j]), D[j]);
-      if (FIX && chk_lo) FXL[j] = div_rn(add_rn(mul_rn(B[j], fhi), A[j]), D[j]) <= L[j];
-      if (FIX && chk_hi) FXH[j] = div_rn(add_rn(mul_rn(B[j], flo), A[j]), D[j]) >= U[j];
+      if (CLO) FXL[j] = div_rn(add_rn(mul_rn(B[j], fhi), A[j]), D[j]) <= L[j];
+      if (CHI) FXH[j] = div_rn(add_rn(mul_rn(B[j], flo), A[j]), D[j]) >= U[j];
     }
   }
 }
+
+// Compile-time dispatch of the two fixed-test flags.
+#define CQK_DISPATCH_FIXED(CLO_RT, CHI_RT, CALL)          \
+  do {                                                    \
+    if (CLO_RT) {                                         \
+      if (CHI_RT) { constexpr bool CLO = true, CHI = true; CALL; }   \
+      else { constexpr bool CLO = true, CHI = false; CALL; }         \
+    } else {                                              \
+      if (CHI_RT) { constexpr bool CLO = false, CHI = true; CALL; }  \
+      else { constexpr bool CLO = false, CHI = false; CALL; }        \
+    }                                                     \
+  } while (0)
 
 // ------------------------------------------------------------ consumer passes
 template <bool CHECK, bool XBAR>
@@ -251,13 +282,24 @@ DEVI void t_lambda0(const CqkParams<double>& p, const TileWalk& tw, TPipe& pp,
   constexpr int STRIDE = XBAR ? kStageElemsC : kStride3;
   consume<ST, STRIDE>(tw, pp, -1, [&](const WTile& wt) {
     double D[kEptC], A[kEptC], B[kEptC], L[kEptC], U[kEptC], X[kEptC];
-    tile_load(wt, 0, p.d, D, 1.0);
-    tile_load(wt, 1, p.a, A);
-    tile_load(wt, 2, p.b, B, 1.0);
-    if (XBAR) {
-      tile_load(wt, 3, p.l, L);
-      tile_load(wt, 4, p.u, U);
-      tile_load(wt, 5, p.xbar, X);
+    if (wt.wcnt == kSeg) {
+      tile_load<true>(wt, 0, p.d, D);
+      tile_load<true>(wt, 1, p.a, A);
+      tile_load<true>(wt, 2, p.b, B);
+      if (XBAR) {
+        tile_load<true>(wt, 3, p.l, L);
+        tile_load<true>(wt, 4, p.u, U);
+        tile_load<true>(wt, 5, p.xbar, X);
+      }
+    } else {
+      tile_load(wt, 0, p.d, D, 1.0);
+      tile_load(wt, 1, p.a, A);
+      tile_load(wt, 2, p.b, B, 1.0);
+      if (XBAR) {
+        tile_load(wt, 3, p.l, L);
+        tile_load(wt, 4, p.u, U);
+        tile_load(wt, 5, p.xbar, X);
+      }
     }
     bool bad = false;
 #pragma unroll
@@ -304,10 +346,10 @@ DEVI void t_lambda0(const CqkParams<double>& p, const TileWalk& tw, TPipe& pp,
 // cqk_solver.cuh) for this thread's kEptC elements; keep[j]: the element is
 // (logically) active.  Straight-line: predicated accumulation, counts in
 // integer registers, the l / u validation on one warp-uniform branch.
-template <bool FIX, bool CHK, bool FULL>
+template <bool FIX, bool CHK, bool FULL, bool CLO, bool CHI>
 DEVI void scan_tile(const CqkParams<double>& p, const WTile& wt, const Src& src, double lam,
-                    double fhi, double flo, bool chk_lo, bool chk_hi, double (&acc)[kMaxK],
-                    int (&nfix)[2], bool (&keep)[kEptC]) {
+                    double fhi, double flo, double (&acc)[kMaxK], int (&nfix)[2],
+                    bool (&keep)[kEptC]) {
   const int lane = threadIdx.x & 31;
   double D[kEptC], A[kEptC], B[kEptC], L[kEptC], U[kEptC];
   tile_load<FULL>(wt, 0, src.p[0], D, 1.0);
@@ -339,26 +381,45 @@ DEVI void scan_tile(const CqkParams<double>& p, const WTile& wt, const Src& src,
   }
   double T[kEptC], W[kEptC];
   bool FXL[kEptC], FXH[kEptC];
-  tile_t<FIX>(D, A, B, L, U, lam, fhi, flo, chk_lo, chk_hi, T, W, FXL, FXH);
+  tile_t<CLO, CHI>(D, A, B, L, U, lam, fhi, flo, T, W, FXL, FXH);
+  bool tie_any = false;
 #pragma unroll
   for (int j = 0; j < kEptC; ++j) {
     const bool valid = FULL || e_loc(lane, j) < wt.wcnt;
     const double t = T[j], l = L[j], u = U[j];
     const bool alo = t <= l, ahi = t >= u;
     bool fixed = false;
-    if (FIX) fixed = (alo && FXL[j]) || (ahi && FXH[j]);
+    if (CLO) fixed = fixed || (alo && FXL[j]);
+    if (CHI) fixed = fixed || (ahi && FXH[j]);
     const bool kp = valid && !fixed;
     keep[j] = kp;
-    const double bx = mul_rn(B[j], clip(t, l, u));
-    const double w = W[j];
-    const bool lt = l < u;
-    if (kp) { acc[0] += bx; acc[1] += fabs(bx); }
-    if (kp && !(alo || ahi)) acc[2] += w;
-    if (kp && alo && lt && t == l) acc[3] += w;
-    if (kp && ahi && lt && t == u) acc[4] += w;
+    const double x = clip(t, l, u);
+    const double bx = mul_rn(B[j], x);
+    const double bxk = kp ? bx : 0.0;
+    acc[0] += bxk;
+    acc[1] += fabs(bxk);
+    const bool interior = !(alo || ahi);
+    acc[2] += (kp && interior) ? W[j] : 0.0;
+    // an exact tie t == l or t == u (the one-sided slopes) -- rare
+    tie_any = tie_any || (kp && !interior && t == x);
     if (FIX) {
-      if (kp && alo) { acc[5] += bx; acc[6] += fabs(bx); nfix[0] += 1; }
-      if (kp && ahi) { acc[8] += bx; acc[9] += fabs(bx); nfix[1] += 1; }
+      const bool lo = kp && alo, hi = kp && ahi;
+      const double bl = lo ? bx : 0.0, bh = hi ? bx : 0.0;
+      acc[5] += bl;
+      acc[6] += fabs(bl);
+      acc[8] += bh;
+      acc[9] += fabs(bh);
+      nfix[0] += lo;
+      nfix[1] += hi;
+    }
+  }
+  if (__any_sync(0xffffffffu, tie_any)) {
+#pragma unroll
+    for (int j = 0; j < kEptC; ++j) {
+      const double t = T[j], l = L[j], u = U[j];
+      const bool lt = l < u;
+      if (keep[j] && t <= l && lt && t == l) acc[3] += W[j];
+      if (keep[j] && t >= u && lt && t == u) acc[4] += W[j];
     }
   }
 }
@@ -381,9 +442,11 @@ DEVI int64_t t_scan(const CqkParams<double>& p, const Cmd& c, const TileWalk& tw
   consume(tw, pp, m_w, [&](const WTile& wt) {
     bool keep[kEptC];
     if (wt.wcnt == kSeg)
-      scan_tile<FIX, CHK, true>(p, wt, src, lam, fhi, flo, chk_lo, chk_hi, acc, nfix, keep);
+      CQK_DISPATCH_FIXED(chk_lo, chk_hi, (scan_tile<FIX, CHK, true, CLO, CHI>(
+                                             p, wt, src, lam, fhi, flo, acc, nfix, keep)));
     else
-      scan_tile<FIX, CHK, false>(p, wt, src, lam, fhi, flo, chk_lo, chk_hi, acc, nfix, keep);
+      CQK_DISPATCH_FIXED(chk_lo, chk_hi, (scan_tile<FIX, CHK, false, CLO, CHI>(
+                                             p, wt, src, lam, fhi, flo, acc, nfix, keep)));
     if (FIX && compact) {
       // survivor r of this tile (r < kSeg) lands at sub-segment offset
       // off_out + r: slot q_out or, after one wrap, q_out + 1
@@ -391,11 +454,19 @@ DEVI int64_t t_scan(const CqkParams<double>& p, const Cmd& c, const TileWalk& tw
       const int64_t b1 = b0 + g * kTileC;
       // the survivors' values come back from the (still held) stage
       double D[kEptC], A[kEptC], B[kEptC], L[kEptC], U[kEptC];
-      tile_load(wt, 0, src.p[0], D);
-      tile_load(wt, 1, src.p[1], A);
-      tile_load(wt, 2, src.p[2], B);
-      tile_load(wt, 3, src.p[3], L);
-      tile_load(wt, 4, src.p[4], U);
+      if (wt.wcnt == kSeg) {
+        tile_load<true>(wt, 0, src.p[0], D);
+        tile_load<true>(wt, 1, src.p[1], A);
+        tile_load<true>(wt, 2, src.p[2], B);
+        tile_load<true>(wt, 3, src.p[3], L);
+        tile_load<true>(wt, 4, src.p[4], U);
+      } else {
+        tile_load(wt, 0, src.p[0], D);
+        tile_load(wt, 1, src.p[1], A);
+        tile_load(wt, 2, src.p[2], B);
+        tile_load(wt, 3, src.p[3], L);
+        tile_load(wt, 4, src.p[4], U);
+      }
       int r = off_out;
 #pragma unroll
       for (int j = 0; j < kEptC; ++j) {
@@ -443,9 +514,9 @@ DEVI void t_bp(const CqkParams<double>& p, const Cmd& c, bool fix, const TileWal
   });
 }
 
-template <bool FIX, bool FULL>
+template <bool FIX, bool FULL, bool CLO, bool CHI>
 DEVI void final_tile(const CqkParams<double>& p, const WTile& wt, double lam, double fhi,
-                     double flo, bool chk_lo, bool chk_hi) {
+                     double flo) {
   const int lane = threadIdx.x & 31;
   double D[kEptC], A[kEptC], B[kEptC], L[kEptC], U[kEptC];
   tile_load<FULL>(wt, 0, p.d, D, 1.0);
@@ -455,14 +526,12 @@ DEVI void final_tile(const CqkParams<double>& p, const WTile& wt, double lam, do
   tile_load<FULL>(wt, 4, p.u, U);
   double T[kEptC], W[kEptC], X[kEptC];
   bool FXL[kEptC], FXH[kEptC];
-  tile_t<FIX>(D, A, B, L, U, lam, fhi, flo, chk_lo, chk_hi, T, W, FXL, FXH);
+  tile_t<CLO, CHI>(D, A, B, L, U, lam, fhi, flo, T, W, FXL, FXH);
 #pragma unroll
   for (int j = 0; j < kEptC; ++j) {  // elem_final: fixed variables keep their bound
     double x = clip(T[j], L[j], U[j]);
-    if (FIX) {
-      if (FXL[j]) x = L[j];
-      else if (FXH[j]) x = U[j];
-    }
+    if (CLO && FXL[j]) x = L[j];
+    else if (CHI && FXH[j]) x = U[j];
     X[j] = x;
   }
 #pragma unroll
@@ -481,8 +550,10 @@ DEVI void t_final(const CqkParams<double>& p, const Cmd& c, const TileWalk& tw, 
   // fixing multiplier (the criterion-2 finish(lam + step) edge)
   const bool chk_lo = FIX && c.lam > c.fix_hi, chk_hi = FIX && c.lam < c.fix_lo;
   consume(tw, pp, -1, [&](const WTile& wt) {
-    if (wt.wcnt == kSeg) final_tile<FIX, true>(p, wt, lam, fhi, flo, chk_lo, chk_hi);
-    else final_tile<FIX, false>(p, wt, lam, fhi, flo, chk_lo, chk_hi);
+    if (wt.wcnt == kSeg)
+      CQK_DISPATCH_FIXED(chk_lo, chk_hi, (final_tile<FIX, true, CLO, CHI>(p, wt, lam, fhi, flo)));
+    else
+      CQK_DISPATCH_FIXED(chk_lo, chk_hi, (final_tile<FIX, false, CLO, CHI>(p, wt, lam, fhi, flo)));
   });
 }
 
@@ -503,8 +574,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool producer = warp == kConsW;
   const bool master = blockIdx.x == 0;
-  TPipe pp{reinterpret_cast<double*>(s_dyn), s_full, s_empty, 0u};
-  TPipe pp3{reinterpret_cast<double*>(s_dyn), s_full3, s_empty3, 0u};  // 3-array lambda0 pass
+  TPipe pp{reinterpret_cast<double*>(s_dyn), smem_u32(s_full), smem_u32(s_empty), 0u};
+  TPipe pp3{reinterpret_cast<double*>(s_dyn), smem_u32(s_full3), smem_u32(s_empty3), 0u};  // lambda0
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStagesC; ++s) {
       mbar_init_count(&s_full[s], 1);
