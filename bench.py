@@ -301,13 +301,19 @@ def main():
         host = [t.numpy() for t in pinned]
         inst_h = P.CqkInstance(*host, r=r)
         with torch.cuda.stream(stream):
-            out = P.solve_cqk(inst_h)
+            # warm-up: the caching host allocator ends up holding the two
+            # pinned x blocks a steady-state caller cycles through
+            for _ in range(3):
+                out = P.solve_cqk(inst_h)
+                del out
             torch.cuda.synchronize()
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             for _ in range(args.e2e_steps):
-                out = P.solve_cqk(inst_h)
+                out = P.solve_cqk(inst_h)  # H2D of d,a,b,l,u + solve + D2H of x
+                assert out.status is P.Status.SOLVED
+                del out
             e1.record(stream)
             torch.cuda.synchronize()
         ems = e0.elapsed_time(e1)
@@ -336,7 +342,7 @@ def main():
             },
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "cqk_solve_kernel<double,true> (persistent, 1 launch/solve)",
+                         "kernel": "cqk_tma_kernel<true> (persistent TMA-pipelined solve, 1 launch/solve)",
                          "bytes_per_launch": bpl, "kernel_ms": kms},
             "cpu_baseline": cpu,
             "e2e": e2e,

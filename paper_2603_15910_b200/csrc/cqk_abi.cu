@@ -18,6 +18,7 @@
 #include "../../include/cqk_b200.h"
 #include "cqk_kernels.cuh"
 #include "cqk_tma.cuh"
+#include "cqk_tma_spx.cuh"
 
 using namespace cqk;
 
@@ -77,6 +78,7 @@ struct cqk_handle {
   cudaStream_t stream = nullptr;
   int grid_cqk_fix = 0, grid_cqk_jac = 0, grid_spx = 0, grid_l1 = 0;
   int grid_tma_fix = 0, grid_tma_jac = 0;  // TMA-pipelined CQK kernels (0: unavailable)
+  int grid_tma_spx = 0, grid_tma_l1 = 0;    // TMA-pipelined simplex / l1 kernels
   bool use_tma = true;                     // CQK_ENGINE=seg selects the warp-segment kernel
   unsigned* sync = nullptr;  // [0] arrive, [1] gen, [2] error
   void* state = nullptr;     // CqkState / SpxState
@@ -145,9 +147,12 @@ int cqk_create(cqk_handle** out, int device) {
     };
     h->grid_tma_fix = occ_tma((const void*)cqk_tma_kernel<true>);
     h->grid_tma_jac = occ_tma((const void*)cqk_tma_kernel<false>);
+    h->grid_tma_spx = occ_tma((const void*)spx_tma_kernel<false>);
+    h->grid_tma_l1 = occ_tma((const void*)spx_tma_kernel<true>);
     cudaGetLastError();
     const char* eng = getenv("CQK_ENGINE");
-    h->use_tma = !(eng && std::strcmp(eng, "seg") == 0) && h->grid_tma_fix > 0 && h->grid_tma_jac > 0;
+    h->use_tma = !(eng && std::strcmp(eng, "seg") == 0) && h->grid_tma_fix > 0 &&
+                 h->grid_tma_jac > 0 && h->grid_tma_spx > 0 && h->grid_tma_l1 > 0;
   }
   int gmax = h->grid_cqk_fix;
   gmax = gmax > h->grid_cqk_jac ? gmax : h->grid_cqk_jac;
@@ -601,7 +606,10 @@ namespace {
 // timeout flag D2H) on the handle's stream; the caller synchronises.
 int launch_spx(cqk_handle* h, SpxState& s, const double* yv, int64_t n, double* xo, bool l1,
                bool sharded) {
-  if (s.fixing) CUDA_TRY(h->scratch.ensure(((size_t)n * sizeof(double) + 255) / 256 * 256));
+  const bool tma = h->use_tma;
+  if (s.fixing)
+    CUDA_TRY(h->scratch.ensure(((size_t)(tma ? tma_scratch_elems_y(n) : n) * sizeof(double) + 255) /
+                               256 * 256));
   std::memcpy(h->host_state, &s, sizeof s);  // pinned staging: fully asynchronous
   CUDA_TRY(cudaMemcpyAsync(h->state, h->host_state, sizeof s, cudaMemcpyHostToDevice, h->stream));
   SpxParams<double> p;
@@ -619,10 +627,17 @@ int launch_spx(cqk_handle* h, SpxState& s, const double* yv, int64_t n, double* 
   p.sync.error = (int*)(h->sync + 2);
   p.sync.timeline = h->timeline;
   void* args[] = {&p};
-  const int grid = limit_grid(h, l1 ? h->grid_l1 : h->grid_spx);
-  const void* fn = l1 ? (const void*)spx_solve_kernel<double, true>
-                      : (const void*)spx_solve_kernel<double, false>;
-  CUDA_TRY(cudaLaunchCooperativeKernel(fn, grid, kThreads, args, 0, h->stream));
+  int grid;
+  const void* fn;
+  if (tma) {
+    grid = limit_grid(h, l1 ? h->grid_tma_l1 : h->grid_tma_spx);
+    fn = l1 ? (const void*)spx_tma_kernel<true> : (const void*)spx_tma_kernel<false>;
+  } else {
+    grid = limit_grid(h, l1 ? h->grid_l1 : h->grid_spx);
+    fn = l1 ? (const void*)spx_solve_kernel<double, true> : (const void*)spx_solve_kernel<double, false>;
+  }
+  CUDA_TRY(cudaLaunchCooperativeKernel(fn, grid, tma ? kTmaThreads : kThreads, args,
+                                       tma ? kSmemC : 0, h->stream));
   CUDA_TRY(cudaMemcpyAsync(h->host_state, h->state, sizeof s, cudaMemcpyDeviceToHost, h->stream));
   CUDA_TRY(cudaMemcpyAsync(h->err_host, h->sync + 2, sizeof(unsigned), cudaMemcpyDeviceToHost,
                            h->stream));

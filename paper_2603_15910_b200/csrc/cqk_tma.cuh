@@ -118,24 +118,24 @@ struct TPipe {
 constexpr int kStages3 = kStagesC * 2;
 constexpr int kStride3 = 3 * kTileC;
 
-template <int NA, int ST = kStagesC, int STRIDE = kStageElemsC>
+template <int NA, int ST = kStagesC, int STRIDE = kStageElemsC, int TT = kTileC>
 DEVI void produce(const Src src, const TileWalk& tw, TPipe& pp) {
-  const int64_t step = (int64_t)gridDim.x * kTileC;
-  const int64_t end = tw.nslots < 0 ? tw.n : ((int64_t)blockIdx.x + (int64_t)tw.nslots * gridDim.x) * kTileC;
+  const int64_t step = (int64_t)gridDim.x * TT;
+  const int64_t end = tw.nslots < 0 ? tw.n : ((int64_t)blockIdx.x + (int64_t)tw.nslots * gridDim.x) * TT;
   int s = pp.pc % ST;
   unsigned ph = ((pp.pc / ST) & 1) ^ 1;  // parity of the previous use of stage s
   bool first_round = pp.pc < (unsigned)ST;
-  for (int64_t base = (int64_t)blockIdx.x * kTileC; base < end; base += step) {
+  for (int64_t base = (int64_t)blockIdx.x * TT; base < end; base += step) {
     if (!first_round) mbar_wait_s(pp.empty + 8 * s, ph);
     const int64_t left = tw.n - base;
-    const int cnt = tw.nslots < 0 && left < kTileC ? (int)left : kTileC;
+    const int cnt = tw.nslots < 0 && left < TT ? (int)left : TT;
     const unsigned bytes = ((unsigned)cnt * 8u) & ~15u;
     const unsigned fb = pp.full + 8 * s;
     mbar_expect_tx_s(fb, NA * bytes);
     if (bytes) {
       const unsigned dst = smem_u32(pp.buf) + (unsigned)(s * STRIDE) * 8u;
 #pragma unroll
-      for (int k = 0; k < NA; ++k) tma_load_1d_s(dst + k * kTileC * 8u, src.p[k] + base, bytes, fb);
+      for (int k = 0; k < NA; ++k) tma_load_1d_s(dst + k * TT * 8u, src.p[k] + base, bytes, fb);
     }
     ++pp.pc;
     if (++s == ST) { s = 0; ph ^= 1; first_round = false; }
@@ -155,19 +155,20 @@ struct WTile {
 
 // Consumer warps: body(WTile) per tile, then release the stage.
 // m_w >= 0: scratch walk with this warp's element count m_w.
-template <int ST = kStagesC, int STRIDE = kStageElemsC, typename Body>
+template <int ST = kStagesC, int STRIDE = kStageElemsC, int TT = kTileC, typename Body>
 DEVI void consume(const TileWalk& tw, TPipe& pp, int64_t m_w, Body&& body) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t step = (int64_t)gridDim.x * kTileC;
+  constexpr int kSeg = TT / kConsW;
+  const int64_t step = (int64_t)gridDim.x * TT;
   const bool scratch = tw.nslots >= 0;
-  const int64_t end = scratch ? ((int64_t)blockIdx.x + (int64_t)tw.nslots * gridDim.x) * kTileC : tw.n;
+  const int64_t end = scratch ? ((int64_t)blockIdx.x + (int64_t)tw.nslots * gridDim.x) * TT : tw.n;
   int s = pp.pc % ST;
   unsigned ph = (pp.pc / ST) & 1;
   // valid elements of this warp's sub-segment still ahead (scratch walk)
   int64_t left_w = m_w;
   WTile wt;
   wt.q = 0;
-  for (int64_t base = (int64_t)blockIdx.x * kTileC; base < end; base += step, ++wt.q) {
+  for (int64_t base = (int64_t)blockIdx.x * TT; base < end; base += step, ++wt.q) {
     wt.sm = pp.buf + (size_t)s * STRIDE + kSeg * warp;
     wt.gbase = base + kSeg * warp;
     const int64_t left = scratch ? left_w : tw.n - wt.gbase;
@@ -183,25 +184,26 @@ DEVI void consume(const TileWalk& tw, TPipe& pp, int64_t m_w, Body&& body) {
   }
 }
 
-template <bool FULL = false>
-DEVI void tile_load(const WTile& wt, int k, const double* garr, double (&v)[kEptC],
+template <bool FULL = false, int TT = kTileC>
+DEVI void tile_load(const WTile& wt, int k, const double* garr, double (&v)[TT / kConsT],
                     double fill = 0.0) {
+  constexpr int EPT = TT / kConsT, VPT = EPT / 2;
   const int lane = threadIdx.x & 31;
-  const double* sarr = wt.sm + k * kTileC;
+  const double* sarr = wt.sm + k * TT;
 #pragma unroll
-  for (int u = 0; u < kVpt; ++u) {
+  for (int u = 0; u < VPT; ++u) {
     const double2 w = *reinterpret_cast<const double2*>(sarr + 64 * u + 2 * lane);
     v[2 * u] = w.x;
     v[2 * u + 1] = w.y;
   }
   if (!FULL) {
 #pragma unroll
-    for (int j = 0; j < kEptC; ++j)
+    for (int j = 0; j < EPT; ++j)
       if (e_loc(lane, j) >= wt.wcnt) v[j] = fill;  // neutral values beyond the data
     if (wt.patch) {
       const int e = wt.wcnt - 1;  // even: the (v = 0) element of pair e / 2
 #pragma unroll
-      for (int u = 0; u < kVpt; ++u)
+      for (int u = 0; u < VPT; ++u)
         if (64 * u + 2 * lane == e) v[2 * u] = ld_scratch(garr + wt.gbase + e);
     }
   }
