@@ -11,7 +11,7 @@
  * Status codes mirror the reference's outcomes and exceptions:
  *   CQK_SOLVED / CQK_INFEASIBLE      -> Status.SOLVED / Status.INFEASIBLE
  *                                       (newton.py:33-35)
- *   CQK_E_DOMAIN (+field, index)     -> DomainError(field, index)  (core.py:81-87)
+ *   CQK_E_DOMAIN (+field, index)     -> DomainError(field, index)  (core.py:30-36)
  *   CQK_E_MAXITER                    -> MaxIterationsError          (newton.py:42-49)
  *   CQK_E_CONTRACT                   -> ContractViolation           (newton.py:38-39)
  *   CQK_E_EMPTY                      -> EmptyIndexSet               (simplex.py:33-34)
@@ -112,22 +112,22 @@ int cqk_get_timeline(cqk_handle *h, long long *out, int32_t max_rows);
 int cqk_get_trace(cqk_handle *h, double *out, int32_t max_rows);
 
 /* CQK ----------------------------------------------------------------------- */
-/* validate(inst)  core.py:177-216 */
+/* validate(inst)  core.py:126-165 */
 int cqk_validate_f64(cqk_handle *h, int mem, const double *d, const double *a,
                      const double *b, const double *l, const double *u, int64_t n,
                      double r, cqk_result *res);
-/* initial_multiplier(inst, xbar)  core.py:288-308 ; xbar may be NULL */
+/* initial_multiplier(inst, xbar)  core.py:237-257 ; xbar may be NULL */
 int cqk_initial_multiplier_f64(cqk_handle *h, int mem, const double *d, const double *a,
                                const double *b, const double *l, const double *u,
                                int64_t n, double r, const double *xbar, double *lam0);
-/* _phi_scan / eval_phi(inst, lam, idx)  core.py:233-276.  idx may be NULL (all
+/* _phi_scan / eval_phi(inst, lam, idx)  core.py:182-225.  idx may be NULL (all
    n).  out4 = {value, dminus, dplus, abs_bx}; at_lower/at_upper (length m) may
    be NULL. */
 int cqk_phi_f64(cqk_handle *h, int mem, const double *d, const double *a,
                 const double *b, const double *l, const double *u, int64_t n,
                 const int64_t *idx, int64_t m, double lam, double *out4,
                 uint8_t *at_lower, uint8_t *at_upper);
-/* eval_x(inst, lam, idx)  core.py:219-230 -> x[m] */
+/* eval_x(inst, lam, idx)  core.py:168-179 -> x[m] */
 int cqk_eval_x_f64(cqk_handle *h, int mem, const double *d, const double *a,
                    const double *b, const double *l, const double *u, int64_t n,
                    const int64_t *idx, int64_t m, double lam, double *x);

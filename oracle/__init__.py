@@ -125,7 +125,7 @@ def initial_multiplier(d, a, b, l, u, r, xbar=None):
 
 
 def phi_scan(d, a, b, l, u, lam, idx=None):
-    """core.py:233 _phi_scan -> (value, dminus, dplus, abs_bx, at_lower, at_upper)."""
+    """core.py:182 _phi_scan -> (value, dminus, dplus, abs_bx, at_lower, at_upper)."""
     arrs = _arrays(d, a, b, l, u)
     ix = None if idx is None else np.ascontiguousarray(idx, dtype=np.int64)
     m = arrs[0].size if ix is None else ix.size

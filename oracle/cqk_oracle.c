@@ -21,7 +21,7 @@
 /* numpy's pairwise summation of a contiguous double array: blocks of <= 128
  * summed with 8 interleaved accumulators, larger ranges split at a multiple
  * of 8 near the middle.  This is what `ndarray.sum()` does in the reference
- * (e.g. core.py:249-262), so reproducing it makes the oracle bit-faithful. */
+ * (e.g. core.py:198-211), so reproducing it makes the oracle bit-faithful. */
 double orc_pairwise_sum(const double *a, int64_t n) {
   if (n < 8) {
     double s = 0.0;
@@ -68,7 +68,7 @@ static int domain(orc_result *res, int field, int64_t index) {
   return ORC_E_DOMAIN;
 }
 
-/* core.py:177-216: checks in the reference's order, first offending index. */
+/* core.py:126-165: checks in the reference's order, first offending index. */
 int orc_validate(const double *d, const double *a, const double *b,
                  const double *l, const double *u, int64_t n, double r,
                  orc_result *res) {
@@ -112,7 +112,7 @@ static void sq_sums(const double *d, const double *a, const double *b,
   free(tq);
 }
 
-/* core.py:288-308: lambda0 = (r - s)/q over all indices, or over the strictly
+/* core.py:237-257: lambda0 = (r - s)/q over all indices, or over the strictly
  * interior components of xbar when there are any. */
 double orc_initial_multiplier(const double *d, const double *a, const double *b,
                               const double *l, const double *u, int64_t n,
@@ -139,7 +139,7 @@ typedef struct {
   double value, dminus, dplus, abs_bx;
 } scan4;
 
-/* core.py:233-263 _phi_scan: one pass over idx[0..m) (NULL = identity).
+/* core.py:182-212 _phi_scan: one pass over idx[0..m) (NULL = identity).
  * Temporaries mirror the numpy expression graph; masked sums sum the
  * compacted subsequence, as `w[mask].sum()` does. */
 static scan4 phi_scan(const double *d, const double *a, const double *b,
@@ -186,7 +186,7 @@ int orc_phi_scan(const double *d, const double *a, const double *b,
   return 0;
 }
 
-/* core.py:219-230 eval_x */
+/* core.py:168-179 eval_x */
 void orc_eval_x(const double *d, const double *a, const double *b,
                 const double *l, const double *u, const int64_t *idx,
                 int64_t m, double lam, double *x) {

@@ -13,7 +13,7 @@
  * Sums emulate numpy's pairwise summation (the reference's `ndarray.sum`), so
  * with the reference's own lambda0 injected (`lam0` argument, NaN = compute it)
  * the iterate sequence is reproduced bit for bit.  lambda0 itself is a BLAS
- * ddot in the reference (core.py:306-307) whose order is OpenBLAS-kernel
+ * ddot in the reference (core.py:255-256) whose order is OpenBLAS-kernel
  * specific; the oracle uses the pairwise sum there (agreement ~1e-16).
  */
 #ifndef CQK_ORACLE_H
@@ -48,24 +48,24 @@ typedef struct {
 /* numpy pairwise summation (numpy/_core/src/umath/loops_utils.h.src) */
 double orc_pairwise_sum(const double *a, int64_t n);
 
-/* core.py:177-216 validate; returns ORC_SOLVED or ORC_E_DOMAIN (+field/index) */
+/* core.py:126-165 validate; returns ORC_SOLVED or ORC_E_DOMAIN (+field/index) */
 int orc_validate(const double *d, const double *a, const double *b,
                  const double *l, const double *u, int64_t n, double r,
                  orc_result *res);
 
-/* core.py:288-308 initial_multiplier (xbar may be NULL) */
+/* core.py:237-257 initial_multiplier (xbar may be NULL) */
 double orc_initial_multiplier(const double *d, const double *a, const double *b,
                               const double *l, const double *u, int64_t n,
                               double r, const double *xbar);
 
-/* core.py:233-263 _phi_scan over idx (NULL = all).  out[4] = value, dminus,
+/* core.py:182-212 _phi_scan over idx (NULL = all).  out[4] = value, dminus,
    dplus, abs_bx.  at_lower/at_upper may be NULL. */
 int orc_phi_scan(const double *d, const double *a, const double *b,
                  const double *l, const double *u, const int64_t *idx,
                  int64_t m, double lam, double *out, uint8_t *at_lower,
                  uint8_t *at_upper);
 
-/* core.py:219-230 eval_x over idx (NULL = all) into x[m] */
+/* core.py:168-179 eval_x over idx (NULL = all) into x[m] */
 void orc_eval_x(const double *d, const double *a, const double *b,
                 const double *l, const double *u, const int64_t *idx,
                 int64_t m, double lam, double *x);

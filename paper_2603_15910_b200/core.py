@@ -30,7 +30,7 @@ __all__ = [
 
 
 class DomainError(ValueError):
-    """Problem data violates an invariant (bad sign, l > u, NaN, ...).  core.py:81-87"""
+    """Problem data violates an invariant (bad sign, l > u, NaN, ...).  core.py:30-36"""
 
     def __init__(self, field, index, message):
         self.field = field
@@ -62,7 +62,7 @@ def _dtype_of(v):
 
 @dataclass
 class CqkInstance:
-    """Data (d, a, b, l, u, r) of one CQK instance (core.py:90-127).
+    """Data (d, a, b, l, u, r) of one CQK instance (core.py:39-76).
 
     Arrays share a common length n and floating dtype; -inf in l and +inf in
     u are allowed.  Treated as immutable after construction.
@@ -99,7 +99,7 @@ class CqkInstance:
 
 @dataclass
 class SimplexInstance:
-    """A point y to project onto {x >= 0, sum x = r} (core.py:130-151)."""
+    """A point y to project onto {x >= 0, sum x = r} (core.py:79-100)."""
 
     y: object
     r: float
@@ -137,7 +137,7 @@ class SimplexInstance:
 
 @dataclass
 class PhiEval:
-    """phi(lam) together with both lateral derivatives at lam (core.py:154-160)."""
+    """phi(lam) together with both lateral derivatives at lam (core.py:103-109)."""
 
     value: float
     dminus: float
@@ -250,7 +250,7 @@ def raise_domain(res):
 
 # ------------------------------------------------------------- functions
 def validate(inst):
-    """Raise DomainError on the first violated invariant (core.py:177-216), on device."""
+    """Raise DomainError on the first violated invariant (core.py:126-165), on device."""
     if inst.n < 1:
         raise DomainError("d", None, "instance must have at least one variable")
     for name in ("d", "a", "b", "l", "u"):
@@ -268,7 +268,7 @@ def validate(inst):
 
 
 def eval_x(inst, lam, idx=None):
-    """The primal minimizer x(lam) clipped to [l, u] (core.py:219-230); idx selects components."""
+    """The primal minimizer x(lam) clipped to [l, u] (core.py:168-179); idx selects components."""
     m = Marshal(inst.d, inst.a, inst.b, inst.l, inst.u)
     ix, ixp, cnt = m.index(idx, inst.n)
     h = m.handle()
@@ -281,7 +281,7 @@ def eval_x(inst, lam, idx=None):
 
 
 def phi_scan(inst, lam, idx=None, masks=False):
-    """core.py:233-263 _phi_scan on device -> (value, dminus, dplus, abs_bx[, at_lower, at_upper])."""
+    """core.py:182-212 _phi_scan on device -> (value, dminus, dplus, abs_bx[, at_lower, at_upper])."""
     m = Marshal(inst.d, inst.a, inst.b, inst.l, inst.u)
     ix, ixp, cnt = m.index(idx, inst.n)
     h = m.handle()
@@ -310,13 +310,13 @@ def phi_scan(inst, lam, idx=None, masks=False):
 
 
 def eval_phi(inst, lam, idx=None):
-    """phi(lam) = b'x(lam) and both lateral derivatives (core.py:266-276)."""
+    """phi(lam) = b'x(lam) and both lateral derivatives (core.py:215-225)."""
     value, dminus, dplus, _ = phi_scan(inst, lam, idx)
     return PhiEval(value=value, dminus=dminus, dplus=dplus)
 
 
 def breakpoints(inst):
-    """All finite breakpoints (d*bound - a)/b with their variable indices (core.py:279-285).
+    """All finite breakpoints (d*bound - a)/b with their variable indices (core.py:228-234).
 
     Host-side utility (not on the Newton hot path)."""
     d, a, b, l, u = (np.asarray(v.cpu().numpy() if _is_torch(v) else v)
@@ -329,7 +329,7 @@ def breakpoints(inst):
 
 
 def initial_multiplier(inst, xbar=None):
-    """(r - sum b*a/d) / sum b^2/d over all indices or the interior of xbar (core.py:288-308)."""
+    """(r - sum b*a/d) / sum b^2/d over all indices or the interior of xbar (core.py:237-257)."""
     if xbar is not None:
         shape = tuple(xbar.shape) if hasattr(xbar, "shape") else np.asarray(xbar).shape
         if shape != (inst.n,):
@@ -351,7 +351,7 @@ def ctypes_double():
 
 
 def simplex_as_cqk(y, r):
-    """Embed a simplex projection as a CQK instance (d=b=1, l=0, u=inf); core.py:311-325."""
+    """Embed a simplex projection as a CQK instance (d=b=1, l=0, u=inf); core.py:260-274."""
     if _is_torch(y):
         import torch
 

@@ -193,7 +193,7 @@ DEVI bool wait_release(const GridSync& sy, unsigned target, const Cmd* gcmd, Cmd
 }
 
 // ------------------------------------------------------------ CQK passes
-// pass 0: lambda0 sums (core.py:288-308) fused with validate (core.py:177-216)
+// pass 0: lambda0 sums (core.py:237-257) fused with validate (core.py:126-165)
 template <typename T, bool CHECK, bool XBAR>
 DEVI void lambda0_pass(const CqkParams<T>& p, int64_t seg_lo, int64_t m, double (&acc)[kMaxK]) {
   constexpr int E = Vec<T>::n * kUnroll, CH = 32 * E;

@@ -4,9 +4,9 @@
 // (newton.py:209-342) / parallel.jacobi_solve (parallel.py:371-500) /
 // parallel.par_solve_cqk (parallel.py:174-327):
 //
-//   pass 0   validate (core.py:177-216) fused with the lambda0 sums
-//            (core.py:288-308)                                  24..48 B/elem
-//   pass k   phi scan at lambda_k (core.py:233-263) over the warp-owned
+//   pass 0   validate (core.py:126-165) fused with the lambda0 sums
+//            (core.py:237-257)                                  24..48 B/elem
+//   pass k   phi scan at lambda_k (core.py:182-212) over the warp-owned
 //            physical working set, K = 5 (Jacobi) or 11 (fixing) partials;
 //            optional in-place compaction of the survivors        40 B/elem
 //            (+40 B per survivor written)
@@ -245,7 +245,7 @@ DEVI void m_after_bp(CqkState& s, const double* tot) {
 }
 
 // tot: 0 s_all, 1 q_all, 2 s_J, 3 q_J, 4 |J|, 5..14 first offending index of
-// the ten validate() checks in the reference's order (core.py:186-216).
+// the ten validate() checks in the reference's order (core.py:135-165).
 constexpr int kValidateSlot = 5;
 // The checks in the reference's order: d,a,b finite; l,u NaN; r finite;
 // d>0; b>0; l<=u; l!=+inf; u!=-inf.  Classes c0 <= c < c1 are decided.
@@ -293,7 +293,7 @@ DEVI void m_after_lambda0(CqkState& s, const double* tot) {
 }
 
 // ------------------------------------------------------------ element ops
-// core.py:246-262 for one element; returns false if the element is already
+// core.py:195-211 for one element; returns false if the element is already
 // (logically) fixed and therefore not part of the active set.
 // chk_lo / chk_hi: a lower / upper fixing multiplier exists (finite), so
 // the stateless fixed test is needed at all (never divide by infinities).

@@ -344,7 +344,7 @@ DEVI void t_lambda0(const CqkParams<double>& p, const TileWalk& tw, TPipe& pp,
   });
 }
 
-// One tile of the phi scan (core.py:233-263 per element, as elem_scan in
+// One tile of the phi scan (core.py:182-212 per element, as elem_scan in
 // cqk_solver.cuh) for this thread's kEptC elements; keep[j]: the element is
 // (logically) active.  Straight-line: predicated accumulation, counts in
 // integer registers, the l / u validation on one warp-uniform branch.
