@@ -88,6 +88,7 @@ struct cqk_handle {
   double* red = nullptr;     // utility partials
   double* out = nullptr;     // utility outputs (kMaxK doubles)
   Buf scratch, stage, idxbuf, flags, alg2;
+  int32_t* wcnt = nullptr;            // per-warp scratch counts (simplex tail mode)
   double* alg2_vals = nullptr;        // gathered free values of the last Algorithm-2 run
   int64_t* alg2_idx = nullptr;        // ... and their global indices
   int64_t* alg2_jplus = nullptr;
@@ -174,6 +175,7 @@ int cqk_create(cqk_handle** out, int device) {
   e = e ? e : cudaMemset(h->timeline, 0, sizeof(long long) * kTimelineCols * kTimelineCap);
   e = e ? e : cudaMalloc(&h->red, sizeof(double) * kMaxK * kUtilBlocksMax);
   e = e ? e : cudaMalloc(&h->out, sizeof(double) * kMaxK);
+  e = e ? e : cudaMalloc(&h->wcnt, sizeof(int32_t) * kConsW * (h->sm_count + 8));
   e = e ? e : cudaMallocHost(&h->err_host, 64);
   e = e ? e : cudaMallocHost(&h->host_state, st_bytes);
   e = e ? e : set_prefetch();
@@ -208,6 +210,7 @@ int cqk_destroy(cqk_handle* h) {
   cudaFree(h->timeline);
   cudaFree(h->red);
   cudaFree(h->out);
+  if (h->wcnt) cudaFree(h->wcnt);
   if (h->err_host) cudaFreeHost(h->err_host);
   if (h->host_state) cudaFreeHost(h->host_state);
   if (h->ev0) cudaEventDestroy(h->ev0);
@@ -626,6 +629,10 @@ int launch_spx(cqk_handle* h, SpxState& s, const double* yv, int64_t n, double* 
   p.sync.gen = h->sync + 1;
   p.sync.error = (int*)(h->sync + 2);
   p.sync.timeline = h->timeline;
+  {
+    const char* te = getenv("CQK_TAIL");
+    p.wcnt = (tma && !sharded && !(te && te[0] == '0')) ? h->wcnt : nullptr;
+  }
   void* args[] = {&p};
   int grid;
   const void* fn;

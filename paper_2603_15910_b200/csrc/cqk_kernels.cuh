@@ -104,61 +104,56 @@ DEVI bool grid_step(double* partials, const double* s_cta, const int (&ops)[K],
     if (prev == gridDim.x - 1) tl_last(sy, epoch, blockIdx.x);
   }
   if (blockIdx.x != 0) return false;
-  // Only warp 0 of the master works from here: lane 0 spins on the arrival
-  // count (timer checked every 256 polls -- reading %globaltimer is not
-  // free), then the warp reduces the per-CTA rows (lane l sums rows
-  // l, l+32, ... in order, then a xor butterfly: a fixed order), no
-  // block-wide barrier on the critical path.
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    if (lane == 0) {
-      const unsigned long long t0 = globaltimer();
-      unsigned polls = 0;
-      while (ld_relaxed(sy.arrive) < gridDim.x) {  // relaxed polls, one acquire fence
-        if ((++polls & 255u) == 0 && globaltimer() - t0 > kSpinTimeoutNs) {
-          atomicExch(sy.error, 1);
-          *s_abort = 1;
-          break;
-        }
-      }
-      fence_acquire_gpu();
-      if (!*s_abort) *sy.arrive = 0u;  // nobody arrives again before the release
-      tl_mark(sy, epoch, 4);
-    }
-    __syncwarp();
-    if (!*(volatile int*)s_abort) {
-      double acc[K];
-#pragma unroll
-      for (int k = 0; k < K; ++k)
-        acc[k] = ops[k] == OP_SUM ? 0.0 : ops[k] == OP_MIN ? HUGE_VAL : -HUGE_VAL;
-      // all loads first (one L2 round trip), then the fixed-order combine
-      constexpr int kRowsPerLane = 5;  // grids up to 160 CTAs in one round
-      const int G = (int)gridDim.x;
-      for (int c0 = 0; c0 < G; c0 += 32 * kRowsPerLane) {
-        double v[kRowsPerLane][K];
-#pragma unroll
-        for (int q = 0; q < kRowsPerLane; ++q) {
-          const int c = c0 + lane + 32 * q;
-#pragma unroll
-          for (int k = 0; k < K; ++k)
-            v[q][k] = c < G ? __ldcg(partials + (int64_t)c * kMaxK + k)
-                            : (ops[k] == OP_SUM ? 0.0 : ops[k] == OP_MIN ? HUGE_VAL : -HUGE_VAL);
-        }
-#pragma unroll
-        for (int q = 0; q < kRowsPerLane; ++q)
-#pragma unroll
-          for (int k = 0; k < K; ++k)
-            acc[k] = ops[k] == OP_SUM ? acc[k] + v[q][k]
-                     : ops[k] == OP_MIN ? fmin(acc[k], v[q][k]) : fmax(acc[k], v[q][k]);
-      }
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        const double v = ops[k] == OP_SUM ? warp_sum(acc[k])
-                         : ops[k] == OP_MIN ? warp_min(acc[k]) : warp_max(acc[k]);
-        if (lane == 0) s_tot[k] = v;
+  // The whole master CTA reduces: thread 0 spins on the arrival count (timer
+  // checked every 256 polls -- reading %globaltimer is not free); then
+  // thread t folds rows t, t+blockDim, ... (one L2 round trip: K loads of one
+  // 128-byte row each), warps combine with xor butterflies and warp 0 takes
+  // the warp totals in order -- a fixed order, no float atomics.
+  if (threadIdx.x == 0) {
+    const unsigned long long t0 = globaltimer();
+    unsigned polls = 0;
+    while (ld_relaxed(sy.arrive) < gridDim.x) {  // relaxed polls, one acquire fence
+      if ((++polls & 255u) == 0 && globaltimer() - t0 > kSpinTimeoutNs) {
+        atomicExch(sy.error, 1);
+        *s_abort = 1;
+        break;
       }
     }
+    fence_acquire_gpu();
+    if (!*s_abort) *sy.arrive = 0u;  // nobody arrives again before the release
+    tl_mark(sy, epoch, 4);
   }
+  __syncthreads();
+  if (*(volatile int*)s_abort) return false;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double acc[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) acc[k] = ops[k] == OP_SUM ? 0.0 : ops[k] == OP_MIN ? HUGE_VAL : -HUGE_VAL;
+  for (int c = threadIdx.x; c < (int)gridDim.x; c += blockDim.x) {
+    double v[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) v[k] = __ldcg(partials + (int64_t)c * kMaxK + k);
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      acc[k] = ops[k] == OP_SUM ? acc[k] + v[k] : ops[k] == OP_MIN ? fmin(acc[k], v[k]) : fmax(acc[k], v[k]);
+  }
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const double v = ops[k] == OP_SUM ? warp_sum(acc[k]) : ops[k] == OP_MIN ? warp_min(acc[k])
+                                                                           : warp_max(acc[k]);
+    if (lane == 0) s_red[warp][k] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < K) {
+    const int k = threadIdx.x;
+    double v = s_red[0][k];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      const double o = s_red[w][k];
+      v = ops[k] == OP_SUM ? v + o : ops[k] == OP_MIN ? fmin(v, o) : fmax(v, o);
+    }
+    s_tot[k] = v;
+  }
+  __syncthreads();
   return !*(volatile int*)s_abort;
 }
 
@@ -563,6 +558,7 @@ struct SpxParams {
   double* partials;
   GridSync sync;
   Exchange ex;
+  int32_t* wcnt;  // [grid][consumer warps] scratch counts: enables the TMA kernel's tail mode
 };
 
 DEVI void s_finish(SpxState& s, double lam) {

@@ -119,13 +119,15 @@ constexpr int kStages3 = kStagesC * 2;
 constexpr int kStride3 = 3 * kTileC;
 
 template <int NA, int ST = kStagesC, int STRIDE = kStageElemsC, int TT = kTileC>
-DEVI void produce(const Src src, const TileWalk& tw, TPipe& pp) {
+DEVI int produce(const Src src, const TileWalk& tw, TPipe& pp, int skip = 0, int maxn = 1 << 30) {
   const int64_t step = (int64_t)gridDim.x * TT;
   const int64_t end = tw.nslots < 0 ? tw.n : ((int64_t)blockIdx.x + (int64_t)tw.nslots * gridDim.x) * TT;
   int s = pp.pc % ST;
   unsigned ph = ((pp.pc / ST) & 1) ^ 1;  // parity of the previous use of stage s
   bool first_round = pp.pc < (unsigned)ST;
-  for (int64_t base = (int64_t)blockIdx.x * TT; base < end; base += step) {
+  int issued = 0;
+  for (int64_t base = ((int64_t)blockIdx.x + (int64_t)skip * gridDim.x) * TT; base < end && issued < maxn;
+       base += step) {
     if (!first_round) mbar_wait_s(pp.empty + 8 * s, ph);
     const int64_t left = tw.n - base;
     const int cnt = tw.nslots < 0 && left < TT ? (int)left : TT;
@@ -138,7 +140,23 @@ DEVI void produce(const Src src, const TileWalk& tw, TPipe& pp) {
       for (int k = 0; k < NA; ++k) tma_load_1d_s(dst + k * TT * 8u, src.p[k] + base, bytes, fb);
     }
     ++pp.pc;
+    ++issued;
     if (++s == ST) { s = 0; ph ^= 1; first_round = false; }
+  }
+  return issued;
+}
+
+// Consumers: wait for and release n issued tiles without using them (a
+// speculative prefetch the next phase did not want).
+template <int ST = kStagesC>
+DEVI void drain(TPipe& pp, int n) {
+  const int lane = threadIdx.x & 31;
+  for (int i = 0; i < n; ++i) {
+    const int s = pp.pc % ST;
+    mbar_wait_s(pp.full + 8 * s, (pp.pc / ST) & 1);
+    __syncwarp();
+    if (lane == 0) mbar_arrive_s(pp.empty + 8 * s);
+    ++pp.pc;
   }
 }
 
@@ -573,6 +591,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
   __shared__ int s_abort;
   __shared__ int s_nslots;   // scratch slots of this CTA (max over its warps)
   __shared__ int s_nsl_new;  // ... being formed by a compacting pass
+  __shared__ int s_spec;     // tiles of the next pass issued across the grid step
+  __shared__ int s_spec_scr; // ... and whether they came from scratch
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool producer = warp == kConsW;
   const bool master = blockIdx.x == 0;
@@ -592,6 +612,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
     s_abort = 0;
     s_nslots = 0;
     s_nsl_new = 0;
+    s_spec = 0;
+    s_spec_scr = 0;
     if (master) {
       s_st = *p.st;  // host-initialised before the launch
       s_cmd = s_st.cmd;
@@ -611,15 +633,35 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
   const int check = p.st->check;  // immutable during the solve
   bool in_scratch = false;
   int64_t m_w = -1;  // this warp's scratch element count (consumers, once in scratch)
+  // The producer lane issues the first tiles of the most likely next pass (a
+  // phi scan / breakpoint pass over the current working set -- or, before
+  // any compaction, the final pass over the original arrays) while the grid
+  // step is in flight: the loads do not depend on lambda.
+  auto speculate = [&]() {
+    const TileWalk nw{p.n, ntiles, in_scratch ? s_nslots : -1};
+    s_spec = produce<5>(in_scratch ? src_scr : src_orig, nw, pp, 0, kStagesC);
+    s_spec_scr = in_scratch;
+  };
   for (unsigned epoch = 1;; ++epoch) {
     const Cmd c = s_cmd;
-    if (c.phase == PH_DONE || s_abort) break;
+    const int spec = s_spec;
+    if (c.phase == PH_DONE || s_abort) {
+      if (!producer) drain(pp, spec);  // never leave bulk copies in flight
+      break;
+    }
     const TileWalk work{p.n, ntiles, in_scratch ? s_nslots : -1};
     const Src wsrc = in_scratch ? src_scr : src_orig;
     if (c.phase == PH_FINAL) {
+      const bool reuse = spec > 0 && !s_spec_scr;  // the speculated tiles are the final's
       if (p.x) {
-        if (prod_lane) produce<5>(src_orig, orig, pp);
-        else if (!producer) t_final<FIX>(p, c, orig, pp);
+        if (prod_lane) {
+          produce<5>(src_orig, orig, pp, reuse ? spec : 0);
+        } else if (!producer) {
+          if (!reuse) drain(pp, spec);
+          t_final<FIX>(p, c, orig, pp);
+        }
+      } else if (!producer) {
+        drain(pp, spec);
       }
       break;
     }
@@ -645,6 +687,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
 #pragma unroll
       for (int k = 0; k < 15; ++k) a15[k] = acc[k];
       block_reduce<15>(a15, ops, s_red, s_tot);
+      if (prod_lane) speculate();
       is_master = grid_step<15>(p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch);
       if (is_master && threadIdx.x == 0) {
         tl_record(p.sync, epoch, PH_LAMBDA0, p.n, 0);
@@ -655,12 +698,13 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
     } else if (c.phase == PH_SCAN && c.check_lu) {
 #pragma unroll
       for (int k = kCheckLuSlot; k < kMaxK; ++k) acc[k] = HUGE_VAL;
-      if (prod_lane) produce<5>(src_orig, orig, pp);
+      if (prod_lane) produce<5>(src_orig, orig, pp, spec);
       else if (!producer) t_scan<FIX, true>(p, c, orig, -1, src_orig, false, pp, acc);
       int ops[kMaxK];
 #pragma unroll
       for (int k = 0; k < kMaxK; ++k) ops[k] = k < kCheckLuSlot ? OP_SUM : OP_MIN;
       block_reduce<kMaxK>(acc, ops, s_red, s_tot);
+      if (prod_lane) speculate();
       is_master = grid_step<kMaxK>(p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch);
       if (is_master && threadIdx.x == 0) {
         double loc[kMaxK], glob[kMaxK];
@@ -682,7 +726,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
     } else if (c.phase == PH_SCAN) {
       const bool compact = FIX && c.compact;
       if (prod_lane) {
-        produce<5>(wsrc, work, pp);
+        produce<5>(wsrc, work, pp, spec);
       } else if (!producer) {
         const int64_t mm = t_scan<FIX, false>(p, c, work, m_w, wsrc, compact, pp, acc);
         if (compact) {
@@ -697,9 +741,12 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
 #pragma unroll
       for (int k = 0; k < K; ++k) { ops[k] = OP_SUM; aK[k] = acc[k]; }
       block_reduce<K>(aK, ops, s_red, s_tot);  // (its barrier orders the atomicMax above)
-      if (compact && threadIdx.x == 0) {   // nobody reads s_nslots before the next epoch
-        s_nslots = s_nsl_new;
-        s_nsl_new = 0;
+      if (prod_lane) {
+        if (compact) {  // nobody else reads s_nslots before the next epoch
+          s_nslots = s_nsl_new;
+          s_nsl_new = 0;
+        }
+        speculate();
       }
       is_master = grid_step<K>(p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch);
       if (is_master && threadIdx.x == 0) {
@@ -712,11 +759,12 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
       }
     } else if (c.phase == PH_BP) {
       acc[0] = c.right ? HUGE_VAL : -HUGE_VAL;
-      if (prod_lane) produce<5>(wsrc, work, pp);
+      if (prod_lane) produce<5>(wsrc, work, pp, spec);
       else if (!producer) t_bp(p, c, FIX, work, m_w, wsrc, pp, acc);
       int ops[2] = {c.right ? OP_MIN : OP_MAX, OP_SUM};
       double a2[2] = {acc[0], acc[1]};
       block_reduce<2>(a2, ops, s_red, s_tot);
+      if (prod_lane) speculate();
       is_master = grid_step<2>(p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch);
       if (is_master && threadIdx.x == 0) {
         tl_record(p.sync, epoch, PH_BP, s_st.phys_count, 0);

@@ -21,6 +21,60 @@ static_assert(kStagesY >= 2, "pipeline needs at least two stages");
 template <bool L1>
 DEVI double spx_wv(double y) { return L1 ? fabs(y) : y; }
 
+// Tail mode: once the physical working set fits one SM's shared memory, the
+// master CTA gathers it (from the warp sub-segments, whose counts every warp
+// published in its last compacting pass, or from y itself) and runs the
+// remaining Newton iterations alone -- a block reduction and the state
+// machine per iteration, no grid barrier -- then releases the grid into the
+// final pass.  Single-GPU solves only.
+constexpr int kTailY = 16384;  // elements (128 KB of the stage memory)
+static_assert(kTailY * sizeof(double) <= kSmemC, "tail set must fit the stage memory");
+
+// Gather the working set into V[0, m) (master CTA, all threads).
+template <bool L1>
+DEVI int tail_gather(const SpxParams<double>& p, bool in_scratch, double* V, int* s_scan) {
+  const int nt = blockDim.x, tid = threadIdx.x;
+  if (!in_scratch) {
+    const int m = (int)p.n;
+    for (int i = tid; i < m; i += nt) V[i] = spx_wv<L1>(p.y[i]);
+    return m;
+  }
+  // pairs k = c * kConsW + w, a contiguous block of them per thread, in order
+  const int pairs = (int)gridDim.x * kConsW;
+  const int per = (pairs + nt - 1) / nt;
+  const int k0 = tid * per, k1 = min(k0 + per, pairs);
+  int mine = 0;
+  for (int k = k0; k < k1; ++k) mine += __ldcg(p.wcnt + k);
+  // block exclusive scan of `mine` (warp inclusive scans + warp totals)
+  const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  int incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) s_scan[warp] = incl;
+  __syncthreads();
+  int wpre = 0, total = 0;
+  for (int w = 0; w < nw; ++w) {
+    const int v = s_scan[w];
+    wpre += w < warp ? v : 0;
+    total += v;
+  }
+  int off = wpre + incl - mine;
+  const int64_t g = gridDim.x;
+  for (int k = k0; k < k1; ++k) {
+    const int c = k / kConsW, w = k % kConsW, cnt = __ldcg(p.wcnt + k);
+    for (int i = 0; i < cnt; ++i) {
+      const int64_t q = i / kSegY;
+      V[off + i] = __ldcg(p.sy + ((int64_t)c + q * g) * kTileY + kSegY * w + (i % kSegY));
+    }
+    off += cnt;
+  }
+  __syncthreads();
+  return total;
+}
+
 // MODE 0: sum / max of w; 1: phi scan (+ compaction); 2: max(-w) snap.
 template <bool L1, int MODE, bool FULL>
 DEVI void spx_tile(const WTile& wt, const double* src, bool scratch, double lam, bool fix,
@@ -134,6 +188,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
   __shared__ unsigned s_gen0;
   __shared__ int s_abort;
   __shared__ int s_nslots, s_nsl_new;
+  __shared__ int s_spec, s_spec_scr;  // next-pass tiles issued across the grid step
+  __shared__ int s_tail;              // master: finish the iterations in this CTA
+  __shared__ int s_scan[kConsW + 1];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool producer = warp == kConsW;
   const bool prod_lane = producer && lane == 0;
@@ -148,6 +205,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
     s_gen0 = ld_acquire(p.sync.gen);
     s_abort = 0;
     s_nslots = s_nsl_new = 0;
+    s_spec = s_spec_scr = 0;
+    s_tail = 0;
     if (master) {
       s_st = *p.st;
       s_cmd = s_st.cmd;
@@ -162,22 +221,37 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
   const TileWalk orig{p.n, ntiles, -1};
   bool in_scratch = false;
   int64_t m_w = -1;
+  // first tiles of the likely next pass, issued while the grid step runs
+  // (cqk_tma.cuh: the loads do not depend on lambda)
+  auto speculate = [&]() {
+    const TileWalk nw{p.n, ntiles, in_scratch ? s_nslots : -1};
+    s_spec = produce<1, kStagesY, kTileY, kTileY>(Src{{in_scratch ? p.sy : p.y}}, nw, pp, 0, kStagesY);
+    s_spec_scr = in_scratch;
+  };
   for (unsigned epoch = 1;; ++epoch) {
     const Cmd c = s_cmd;
-    if (c.phase == PH_DONE || s_abort) break;
+    const int spec = s_spec;
+    if (c.phase == PH_DONE || s_abort) {
+      if (!producer) drain<kStagesY>(pp, spec);
+      break;
+    }
     const TileWalk work{p.n, ntiles, in_scratch ? s_nslots : -1};
     if (c.phase == PH_FINAL || c.phase == PH_COPY) {
+      const bool reuse = spec > 0 && !s_spec_scr;
       if (p.x) {
         const bool copy = c.phase == PH_COPY;
         if (prod_lane) {
-          produce<1, kStagesY, kTileY, kTileY>(Src{{p.y}}, orig, pp);
+          produce<1, kStagesY, kTileY, kTileY>(Src{{p.y}}, orig, pp, reuse ? spec : 0);
         } else if (!producer) {
+          if (!reuse) drain<kStagesY>(pp, spec);
           const double lam = c.lam;
           consume<kStagesY, kTileY, kTileY>(orig, pp, -1, [&](const WTile& wt) {
             if (wt.wcnt == kSegY) spx_final_tile<L1, true>(p, wt, copy, lam);
             else spx_final_tile<L1, false>(p, wt, copy, lam);
           });
         }
+      } else if (!producer) {
+        drain<kStagesY>(pp, spec);
       }
       break;
     }
@@ -191,18 +265,21 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
       mode = 0;
       acc[1] = -HUGE_VAL;
       ops[1] = OP_MAX;
-      if (prod_lane) produce<1, kStagesY, kTileY, kTileY>(Src{{p.y}}, orig, pp);
+      if (prod_lane) produce<1, kStagesY, kTileY, kTileY>(Src{{p.y}}, orig, pp, spec);
       else if (!producer) t_spx<L1, 0>(p, c, false, orig, -1, false, pp, acc);
     } else if (c.phase == PH_SCAN) {
       mode = 1;
       const bool compact = fix && c.compact;
       if (prod_lane) {
-        produce<1, kStagesY, kTileY, kTileY>(wsrc, work, pp);
+        produce<1, kStagesY, kTileY, kTileY>(wsrc, work, pp, spec);
       } else if (!producer) {
         const int64_t mm = t_spx<L1, 1>(p, c, fix, work, m_w, compact, pp, acc);
         if (compact) {
           m_w = mm;
-          if (lane == 0) atomicMax(&s_nsl_new, (int)((mm + kSegY - 1) / kSegY));
+          if (lane == 0) {
+            atomicMax(&s_nsl_new, (int)((mm + kSegY - 1) / kSegY));
+            if (p.wcnt) p.wcnt[blockIdx.x * kConsW + warp] = (int32_t)(mm < kTailY ? mm : kTailY);
+          }
         }
       }
       if (compact) in_scratch = true;
@@ -210,16 +287,19 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
       mode = 2;
       acc[0] = -HUGE_VAL;
       ops[0] = OP_MAX;
-      if (prod_lane) produce<1, kStagesY, kTileY, kTileY>(wsrc, work, pp);
+      if (prod_lane) produce<1, kStagesY, kTileY, kTileY>(wsrc, work, pp, spec);
       else if (!producer) t_spx<L1, 2>(p, c, fix, work, m_w, false, pp, acc);
     } else {
       break;
     }
     double a3[3] = {acc[0], acc[1], acc[2]};
     block_reduce<3>(a3, ops, s_red, s_tot);  // (its barrier orders the atomicMax above)
-    if (mode == 1 && fix && c.compact && threadIdx.x == 0) {
-      s_nslots = s_nsl_new;
-      s_nsl_new = 0;
+    if (prod_lane) {
+      if (mode == 1 && fix && c.compact) {  // nobody else reads s_nslots before the next epoch
+        s_nslots = s_nsl_new;
+        s_nsl_new = 0;
+      }
+      speculate();
     }
     const bool is_master = grid_step<3>(p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch);
     if (threadIdx.x == 0) {
@@ -233,16 +313,71 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
         else if (mode == 1) s_after_scan(s_st, glob, loc, p.trace);
         else s_after_snap(s_st, glob);
         const int ph = s_st.cmd.phase;
-        if (ph == PH_FINAL || ph == PH_DONE || ph == PH_COPY) *p.st = s_st;
-        s_cmd = s_st.cmd;
-        master_release(p.sync, s_gen0 + epoch, s_st.cmd, &p.st->cmd);
-        tl_mark(p.sync, epoch, 5);
+        s_tail = p.wcnt && p.ex.world <= 1 && (ph == PH_SCAN || ph == PH_SNAP) &&
+                 s_st.phys_count <= kTailY && (in_scratch || p.n <= kTailY);
+        if (!s_tail) {
+          if (ph == PH_FINAL || ph == PH_DONE || ph == PH_COPY) *p.st = s_st;
+          s_cmd = s_st.cmd;
+          master_release(p.sync, s_gen0 + epoch, s_st.cmd, &p.st->cmd);
+          tl_mark(p.sync, epoch, 5);
+        }
       } else if (!s_abort) {
         if (!wait_release(p.sync, s_gen0 + epoch, &p.st->cmd, &s_cmd)) s_abort = 1;
         if (blockIdx.x == 1) tl_mark(p.sync, epoch, 7);
       }
     }
     __syncthreads();
+    if (master && s_tail) {  // uniform in the master CTA; the other CTAs wait for the release
+      if (!producer) drain<kStagesY>(pp, s_spec);  // the stage memory becomes the tail set
+      __syncthreads();
+      double* V = reinterpret_cast<double*>(s_dyn);
+      const int m = tail_gather<L1>(p, in_scratch, V, s_scan);
+      for (unsigned it = 1;; ++it) {
+        const Cmd tc = s_st.cmd;
+        if (tc.phase != PH_SCAN && tc.phase != PH_SNAP) break;
+        const bool scan = tc.phase == PH_SCAN;
+        const double lam = tc.lam, fhi = tc.fix_hi;
+        double a3[3] = {scan ? 0.0 : -HUGE_VAL, 0.0, 0.0};
+        int n0 = 0, n1 = 0;
+        // contiguous runs per thread (>= 2: tiny sets sum pairwise-sequentially,
+        // as the tiled passes do), then the fixed-order block reduction
+        const int per = max(2, (m + (int)blockDim.x - 1) / (int)blockDim.x);
+        const int i0 = min(m, (int)threadIdx.x * per), i1 = min(m, i0 + per);
+        for (int i = i0; i < i1; ++i) {
+          const double w = V[i];
+          const double v = add_rn(w, lam);
+          const bool kp = !(fix && !(v > 0.0) && !(add_rn(w, fhi) > 0.0));
+          if (scan) {
+            a3[0] += (kp && v > 0.0) ? v : 0.0;
+            n0 += kp && v > 0.0;
+            n1 += kp && v == 0.0;
+          } else {
+            a3[0] = kp ? fmax(a3[0], -w) : a3[0];
+            n0 += kp;
+          }
+        }
+        a3[1] = (double)n0;
+        a3[2] = (double)n1;
+        int tops[3] = {scan ? OP_SUM : OP_MAX, OP_SUM, OP_SUM};
+        block_reduce<3>(a3, tops, s_red, s_tot);
+        if (threadIdx.x == 0) {
+          tl_record(p.sync, epoch + it, tc.phase, m, 0);
+          if (scan) s_after_scan(s_st, s_tot, s_tot, p.trace);
+          else s_after_snap(s_st, s_tot);
+        }
+        __syncthreads();
+      }
+      if (threadIdx.x == 0) {
+        const int ph = s_st.cmd.phase;
+        if (ph == PH_FINAL || ph == PH_DONE || ph == PH_COPY) *p.st = s_st;
+        s_cmd = s_st.cmd;
+        s_spec = 0;
+        s_tail = 0;
+        master_release(p.sync, s_gen0 + epoch, s_st.cmd, &p.st->cmd);
+        tl_mark(p.sync, epoch, 5);
+      }
+      __syncthreads();
+    }
   }
 }
 
