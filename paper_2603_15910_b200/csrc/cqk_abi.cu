@@ -920,10 +920,28 @@ extern "C" int spx_project_batched_f64(cqk_handle* h, int mem, const double* Y, 
   const size_t smem_cta = rows_cta_smem<4, 8>(c);
   const char* force = getenv("CQK_ROWS_KERNEL");
   const std::string fk = force ? force : "";
-  const bool cta_kernel = smem_cta <= 220 * 1024 && c >= 256 && fk != "block" && fk != "warp";
+  const bool aligned_rows = (c % 2) == 0 && aligned16(Yd) && aligned16(Xd);
+  const bool pipe_kernel = aligned_rows && rows_pipe_smem<4, 8>(c) <= 220 * 1024 && c >= 256 &&
+                           (fk == "" || fk == "pipe" || fk == "pipe8" || fk == "fused");
+  const bool cta_kernel = !pipe_kernel && smem_cta <= 220 * 1024 && c >= 256 && fk != "block" && fk != "warp";
   const bool warp_kernel = !cta_kernel && smem <= 220 * 1024 && fk != "block";
-  if (cta_kernel) {
-    auto go = [&](auto kern, int threads, size_t sm) {
+  auto go = [&](auto kern, int threads, size_t sm) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, sm);
+    int64_t grid = (int64_t)(occ > 0 ? occ : 1) * h->sm_count;
+    if (grid > rows) grid = rows;
+    kern<<<(unsigned)grid, threads, sm, h->stream>>>(Yd, Xd, Ld, Id, rows, c, r, tau,
+                                                     opts.max_iterations, fixing, opts.lambda0,
+                                                     opts.simplex_start);
+    return cudaGetLastError();
+  };
+  if (pipe_kernel) {
+    if (fk == "pipe8") e = go(spx_rows_pipe_kernel<8, 8, 2>, 256, rows_pipe_smem<8, 8, 2>(c));
+    else if (fk == "pipe") e = go(spx_rows_pipe_kernel<4, 8, 2>, 128, rows_pipe_smem<4, 8, 2>(c));
+    else e = go(spx_rows_pipe_kernel<4, 8, 1>, 128, rows_pipe_smem<4, 8, 1>(c));
+  } else if (cta_kernel) {
+    auto go_ = [&](auto kern, int threads, size_t sm) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       int occ = 0;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, sm);
@@ -936,9 +954,9 @@ extern "C" int spx_project_batched_f64(cqk_handle* h, int mem, const double* Y, 
     };
     // measured on B200 (65536 x 4096): 4 warps/row with a cols/8 free-set
     // buffer (6 CTAs/SM) 1.09 ms; cols/2 buffer 1.28 ms; 8 warps/row 1.6 ms
-    if (fk == "cta4") e = go(spx_rows_cta_kernel<4, 2>, 128, rows_cta_smem<4, 2>(c));
-    else if (fk == "cta8") e = go(spx_rows_cta_kernel<8, 8>, 256, rows_cta_smem<8, 8>(c));
-    else e = go(spx_rows_cta_kernel<4, 8>, 128, rows_cta_smem<4, 8>(c));
+    if (fk == "cta4") e = go_(spx_rows_cta_kernel<4, 2>, 128, rows_cta_smem<4, 2>(c));
+    else if (fk == "cta8") e = go_(spx_rows_cta_kernel<8, 8>, 256, rows_cta_smem<8, 8>(c));
+    else e = go_(spx_rows_cta_kernel<4, 8>, 128, rows_cta_smem<4, 8>(c));
   } else if (warp_kernel) {
     cudaFuncSetAttribute(spx_rows_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);

@@ -1395,6 +1395,366 @@ __global__ void __launch_bounds__(32 * WPR) spx_rows_cta_kernel(
   if (threadIdx.x == 0 && tma) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// ------------------------------------------------------------ rows, pipelined
+// The CTA-per-row algorithm with (1) the next row's bulk load issued while the
+// current row iterates (two row buffers), and (2) the first phi evaluation
+// fused with the compaction it almost always triggers: the survivors
+// (t > 0) are written to the warp's free-set buffer during the phi pass
+// itself (ballot positions preserve the element order; writes stop at the
+// buffer capacity) and adopted only if the decision then fixes (phi >= r)
+// and they fit -- one pass over the row instead of two.
+template <int WPR, int CAPDIV = 8, int NB = 2>
+__host__ __device__ inline size_t rows_pipe_smem(int cols) {
+  return NB * (((size_t)cols * 8 + 127) / 128 * 128) +
+         (size_t)rows_cap_part<WPR, CAPDIV>(cols) * 10 * WPR + 2 * WPR * 4 * 8 + 128;
+}
+
+// phi over the warp's slice with speculative survivor capture into Bw (values)
+// and BI (slice positions, for the zero-fill + scatter final pass).
+// t = y + lam >= 0 exactly when y >= -lam (the rounded sum of two doubles is
+// negative iff the exact one is), so the common path is one compare per
+// element and one vote per 256-element step; the bookkeeping (sums, counts,
+// ballot positions in element order) runs only in steps holding a t >= 0.
+DEVI void rows_capture_step(const double* F, int i0, int m2, double lam, int lane, unsigned lt,
+                            double* Bw, uint16_t* BI, int cap, double& v0, double& v1, int& z,
+                            int& o) {
+  const int i = i0 + 2 * lane;
+  double2 v = make_double2(0.0, 0.0);
+  const bool in = i < m2;
+  if (in) v = *reinterpret_cast<const double2*>(F + i);
+  const double t0 = __dadd_rn(v.x, lam), t1 = __dadd_rn(v.y, lam);
+  const bool k0 = in && t0 > 0, k1 = in && t1 > 0;
+  v0 += k0 ? t0 : 0.0;
+  v1 += k1 ? t1 : 0.0;
+  z += (in && t0 == 0) + (in && t1 == 0);
+  const unsigned b0 = __ballot_sync(0xffffffffu, k0), b1 = __ballot_sync(0xffffffffu, k1);
+  const int pos0 = o + __popc(b0 & lt) + __popc(b1 & lt);
+  if (k0 && pos0 < cap) { Bw[pos0] = v.x; BI[pos0] = (uint16_t)i; }
+  if (k1 && pos0 + k0 < cap) { Bw[pos0 + k0] = v.y; BI[pos0 + k0] = (uint16_t)(i + 1); }
+  o += __popc(b0) + __popc(b1);
+}
+
+DEVI void rows_phi_capture(const double* F, int m, double lam, int lane, unsigned lt, double* Bw,
+                           uint16_t* BI, int cap, double& val, int& npos, int& nzero) {
+  double v0 = 0.0, v1 = 0.0;
+  int z = 0, o = 0;
+  const int m2 = m & ~1;
+  const double nl = -lam;
+  for (int i0 = 0; i0 < m2; i0 += 64) {
+    const int i = i0 + 2 * lane;
+    const bool in = i < m2;
+    double2 v = make_double2(-HUGE_VAL, -HUGE_VAL);
+    if (in) v = *reinterpret_cast<const double2*>(F + i);
+    if (!__any_sync(0xffffffffu, v.x >= nl || v.y >= nl)) continue;  // no t >= 0 here
+    rows_capture_step(F, i0, m2, lam, lane, lt, Bw, BI, cap, v0, v1, z, o);
+  }
+  if (m & 1) {  // odd slice: the last element, lane 0
+    const double v = F[m - 1];
+    const double t = __dadd_rn(v, lam);
+    const bool k = lane == 0 && t > 0;
+    v0 += k ? t : 0.0;
+    z += lane == 0 && t == 0;
+    if (__ballot_sync(0xffffffffu, k)) {
+      if (lane == 0 && o < cap) { Bw[o] = v; BI[o] = (uint16_t)(m - 1); }
+      ++o;
+    }
+  }
+  val = v0 + v1;
+  npos = o;  // warp-uniform: the survivors of the whole slice
+  nzero = z;
+}
+
+DEVI double __int_as_double_lo(int v) { return __hiloint2double(0, v); }
+DEVI int __double_lo_as_int(double d) { return __double2loint(d); }
+
+template <int WPR, int CAPDIV = 8, int NB = 2>
+__global__ void __launch_bounds__(32 * WPR) spx_rows_pipe_kernel(
+    const double* __restrict__ Y, double* __restrict__ X, double* __restrict__ lam_out,
+    int32_t* __restrict__ it_out, int64_t rows, int cols, double r, double tau, int max_iter,
+    int fixing, double lam0_given, int start) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const size_t a_bytes = ((size_t)cols * 8 + 127) / 128 * 128;
+  const int capw = rows_cap_part<WPR, CAPDIV>(cols);
+  double* Abuf[2] = {reinterpret_cast<double*>(smem_raw),
+                     reinterpret_cast<double*>(smem_raw + (NB - 1) * a_bytes)};
+  double* Bw = reinterpret_cast<double*>(smem_raw + NB * a_bytes) + (size_t)capw * w;
+  double* red = reinterpret_cast<double*>(smem_raw + NB * a_bytes + (size_t)capw * 8 * WPR);
+  uint16_t* BI = reinterpret_cast<uint16_t*>(red + 2 * WPR * 4 + 2) + (size_t)capw * w;
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(red + 2 * WPR * 4);  // [2]
+  const unsigned bytes = (unsigned)cols * 8u;
+  const int q0 = (int)(((int64_t)cols * w / WPR) & ~1LL);
+  const int q1 = w + 1 == WPR ? cols : (int)(((int64_t)cols * (w + 1) / WPR) & ~1LL);
+  const int64_t G = gridDim.x;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0]);
+    mbar_init(&bar[1]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if ((int64_t)blockIdx.x < rows) {  // prologue: the first row
+      mbar_expect_tx(&bar[0], bytes);
+      tma_load_1d(Abuf[0], Y + (int64_t)blockIdx.x * cols, bytes, &bar[0]);
+    }
+  }
+  __syncthreads();
+  unsigned phase[2] = {0u, 0u};
+  int rb = 0;
+  const unsigned lt = (1u << lane) - 1u;
+  auto cta3 = [&](double v0, double v1, double v2, bool max1, double& t0, double& t1,
+                  double& t2) {
+    v0 = warp_sum(v0);
+    v1 = max1 ? warp_max(v1) : warp_sum(v1);
+    v2 = warp_sum(v2);
+    double* slot = red + (rb * WPR + w) * 4;
+    if (lane == 0) { slot[0] = v0; slot[1] = v1; slot[2] = v2; }
+    __syncthreads();
+    const double* s0 = red + rb * WPR * 4;
+    t0 = s0[0]; t1 = s0[1]; t2 = s0[2];
+#pragma unroll
+    for (int q = 1; q < WPR; ++q) {
+      t0 += s0[q * 4 + 0];
+      t1 = max1 ? fmax(t1, s0[q * 4 + 1]) : t1 + s0[q * 4 + 1];
+      t2 += s0[q * 4 + 2];
+    }
+    rb ^= 1;
+  };
+  // (value, #pos, #zero) over the CTA: one double and one packed integer
+  // butterfly per warp (counts <= cols < 2^16), one __syncthreads
+  // (plus how many warps' survivors overflow their free-set buffer, so the
+  // compaction decision is CTA-uniform)
+  auto cta_phi = [&](double v, int npos_lane, int nz_lane, int ovf, double& tv, int& tpos, int& tz,
+                     int& tovf) {
+    v = warp_sum(v);
+    const int pk = warp_sum_i((npos_lane << 16) + nz_lane);
+    double* slot = red + (rb * WPR + w) * 4;
+    if (lane == 0) { slot[0] = v; slot[1] = __int_as_double_lo(pk); slot[2] = __int_as_double_lo(ovf); }
+    __syncthreads();
+    const double* s0 = red + rb * WPR * 4;
+    tv = s0[0];
+    int tp = __double_lo_as_int(s0[1]), to = __double_lo_as_int(s0[2]);
+#pragma unroll
+    for (int q = 1; q < WPR; ++q) {
+      tv += s0[q * 4 + 0];
+      tp += __double_lo_as_int(s0[q * 4 + 1]);
+      to += __double_lo_as_int(s0[q * 4 + 2]);
+    }
+    tpos = tp >> 16;
+    tz = tp & 0xffff;
+    tovf = to;
+    rb ^= 1;
+  };
+  bool next_issued = false;  // NB == 1: this row's buffer was refilled early
+  int k = 0;
+  for (int64_t row = blockIdx.x; row < rows; row += G, ++k) {
+    const int b = NB == 2 ? (k & 1) : 0;
+    double* A = Abuf[b];
+    double* x = X + row * (int64_t)cols;
+    if (NB == 1 && k > 0 && !next_issued && threadIdx.x == 0) {  // reload after the store read it
+      tma_store_wait_read();
+      mbar_expect_tx(&bar[0], bytes);
+      tma_load_1d(A, Y + row * (int64_t)cols, bytes, &bar[0]);
+    }
+    next_issued = false;
+    mbar_wait(&bar[b], phase[b]);
+    phase[b] ^= 1u;
+    double s0 = 0.0, s1 = 0.0, m0 = -HUGE_VAL, m1 = -HUGE_VAL;
+    for (int i = q0 + 2 * lane; i + 1 < q1; i += 64) {
+      const double2 v = *reinterpret_cast<const double2*>(A + i);
+      s0 += v.x;
+      s1 += v.y;
+      m0 = fmax(m0, v.x);
+      m1 = fmax(m1, v.y);
+    }
+    if (((q1 - q0) & 1) && lane == 0) {
+      s0 += A[q1 - 1];
+      m0 = fmax(m0, A[q1 - 1]);
+    }
+    double sum, mx, unused;
+    cta3(s0 + s1, fmax(m0, m1), 0.0, true, sum, mx, unused);
+    // the next row streams into the other buffer while this one iterates;
+    // that buffer's previous row was stored one row ago (its read is done
+    // or nearly so by now)
+    if (NB == 2 && threadIdx.x == 0 && row + G < rows) {
+      tma_store_wait_read();
+      mbar_expect_tx(&bar[b ^ 1], bytes);
+      tma_load_1d(Abuf[b ^ 1], Y + (row + G) * (int64_t)cols, bytes, &bar[b ^ 1]);
+    }
+    const double formula = (r - sum) / (double)cols, tight = r - mx;
+    double lam = !isnan(lam0_given) ? lam0_given : (start && tight < formula ? tight : formula);
+    lam = lam >= -mx ? lam : -mx;
+    double lo = -HUGE_VAL, hi = HUGE_VAL, fix_hi = HUGE_VAL;
+    int iterations = 0;
+    const double* F = A + q0;
+    int m = q1 - q0;
+    bool compacted = false;
+    for (;;) {
+      double val;
+      int np, nz;
+      const bool capture = fixing && !compacted;
+      if (capture) {
+        // no variable is dropped yet (nothing compacted, fix_hi = +inf at the
+        // first evaluation; later evaluations reach here only while the
+        // survivors did not fit -- then the drop test applies as in rows_phi)
+        if (isfinite(fix_hi)) rows_phi(F, m, lam, true, fix_hi, lane, val, np, nz);
+        else rows_phi_capture(F, m, lam, lane, lt, Bw, BI, capw, val, np, nz);
+      } else {
+        rows_phi(F, m, lam, false, fix_hi, lane, val, np, nz);
+      }
+      const bool captured_now = capture && !isfinite(fix_hi);
+      const int npw = captured_now ? np : warp_sum_i(np);
+      const int npl = captured_now ? (lane == 0 ? np : 0) : np;
+      double value;
+      int tpos, tz, tovf;
+      cta_phi(val, npl, nz, lane == 0 && npw > capw, value, tpos, tz, tovf);
+      const double dminus = (double)tpos, dplus = (double)(tpos + tz);
+      double deriv;
+      if (iterations == 0) {
+        if (value == r) break;
+        deriv = value < r ? dplus : dminus;
+      } else {
+        if (value <= r) break;
+        deriv = dminus;
+      }
+      if (value < r) lo = lam;
+      else {
+        hi = lam;
+        if (fixing) {
+          const bool captured = capture && !isfinite(fix_hi);
+          fix_hi = lam;
+          if (tovf == 0 && !compacted) {  // every warp's survivors fit: CTA-uniform
+            if (!captured) {  // compact now (values + slice positions), in place
+              int out = 0;
+              for (int i0 = 0; i0 < m; i0 += 32) {
+                const int i = i0 + lane;
+                double v = 0.0;
+                int ix = 0;
+                bool keep = false;
+                if (i < m) {
+                  v = F[i];
+                  ix = compacted ? BI[i] : i;
+                  keep = __dadd_rn(v, lam) > 0;
+                }
+                const unsigned mask = __ballot_sync(0xffffffffu, keep);
+                __syncwarp();  // every lane has read F[i] / BI[i] before anyone writes
+                if (keep) {
+                  Bw[out + __popc(mask & lt)] = v;  // out <= i0: in-place safe
+                  BI[out + __popc(mask & lt)] = (uint16_t)ix;
+                }
+                out += __popc(mask);
+              }
+            }
+            __syncwarp();
+            F = Bw;
+            m = npw;
+            compacted = true;
+            // single buffer: nobody reads the row again (x leaves through the
+            // zero-fill + scatter below), so the next row can stream in now
+            if (NB == 1 && threadIdx.x == 0 && row + G < rows) {
+              tma_store_wait_read();
+              mbar_expect_tx(&bar[0], bytes);
+              tma_load_1d(A, Y + (row + G) * (int64_t)cols, bytes, &bar[0]);
+            }
+            next_issued = NB == 1;
+          } else if (tovf == 0 && compacted && npw <= capw) {  // re-compact the free set
+            int out = 0;
+            for (int i0 = 0; i0 < m; i0 += 32) {
+              const int i = i0 + lane;
+              double v = 0.0;
+              int ix = 0;
+              bool keep = false;
+              if (i < m) {
+                v = F[i];
+                ix = BI[i];
+                keep = __dadd_rn(v, lam) > 0;
+              }
+              const unsigned mask = __ballot_sync(0xffffffffu, keep);
+              __syncwarp();
+              if (keep) {
+                Bw[out + __popc(mask & lt)] = v;
+                BI[out + __popc(mask & lt)] = (uint16_t)ix;
+              }
+              out += __popc(mask);
+            }
+            __syncwarp();
+            m = npw;
+          }
+        }
+      }
+      if (deriv <= 0) {  // simplex.py:276-281
+        double mneg = -HUGE_VAL;
+        for (int i = lane; i < m; i += 32) {
+          const double v = F[i];
+          if (!compacted && fixing && !(__dadd_rn(v, fix_hi) > 0)) continue;
+          mneg = fmax(mneg, -v);
+        }
+        double t0, t2;
+        cta3(0.0, mneg, 0.0, true, t0, lam, t2);
+        ++iterations;
+        continue;
+      }
+      const double step = -(value - r) / deriv;
+      const double next = lam + step;
+      if (fabs(step) < tau || next == lam) { lam = next; break; }
+      if (isfinite(lo) && isfinite(hi) && hi - lo < tau * fmax(fabs(hi), fabs(lo))) {
+        lam = next;
+        break;
+      }
+      lam = next;
+      ++iterations;
+      if (iterations > max_iter) break;
+    }
+    if (compacted && NB == 1) {
+      // every variable outside the free set was dropped at some fix_hi >= lam,
+      // so its y + lam <= y + fix_hi <= 0 (rounded add is monotone): x = 0
+      // there; the free set scatters max(0, y + lam) to its positions --
+      // straight to global memory (the row buffer already holds the next row)
+      double* xs = x + q0;
+      for (int i = 2 * lane; i + 1 < q1 - q0; i += 64)
+        __stcs(reinterpret_cast<double2*>(xs + i), make_double2(0.0, 0.0));
+      if (((q1 - q0) & 1) && lane == 0) xs[q1 - q0 - 1] = 0.0;
+      __syncwarp();
+      for (int i = lane; i < m; i += 32) {
+        const double t = __dadd_rn(F[i], lam);
+        if (t > 0) xs[BI[i]] = t;
+      }
+      if (threadIdx.x == 0) {
+        if (lam_out) lam_out[row] = lam;
+        if (it_out) it_out[row] = iterations;
+      }
+      continue;
+    }
+    if (compacted) {
+      for (int i = q0 + 2 * lane; i + 1 < q1; i += 64)
+        *reinterpret_cast<double2*>(A + i) = make_double2(0.0, 0.0);
+      if (((q1 - q0) & 1) && lane == 0) A[q1 - 1] = 0.0;
+      __syncwarp();
+      for (int i = lane; i < m; i += 32) {
+        const double t = __dadd_rn(F[i], lam);
+        if (t > 0) A[q0 + BI[i]] = t;
+      }
+    } else {
+      for (int i = q0 + 2 * lane; i + 1 < q1; i += 64) {
+        double2 v = *reinterpret_cast<double2*>(A + i);
+        const double t0 = __dadd_rn(v.x, lam), t1 = __dadd_rn(v.y, lam);
+        v.x = t0 > 0 ? t0 : 0.0;
+        v.y = t1 > 0 ? t1 : 0.0;
+        *reinterpret_cast<double2*>(A + i) = v;
+      }
+      if (((q1 - q0) & 1) && lane == 0) {
+        const double t = __dadd_rn(A[q1 - 1], lam);
+        A[q1 - 1] = t > 0 ? t : 0.0;
+      }
+    }
+    fence_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      tma_store_1d(x, A, bytes);
+      if (lam_out) lam_out[row] = lam;
+      if (it_out) it_out[row] = iterations;
+    }
+  }
+  if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 // ------------------------------------------------------------ Algorithm 2
 // The reference's Gauss-Seidel initializer (simplex.py:47-111) run per
 // contiguous chunk -- par_simplex_init semantics (parallel.py:330-368): chunk
