@@ -156,6 +156,17 @@ int spx_project_f64(cqk_handle *h, int mem, const double *y, int64_t n, double r
    already inside the ball (x = copy of y). */
 int l1_project_f64(cqk_handle *h, int mem, const double *y, int64_t n, double r,
                    const cqk_options *opts, double *x, cqk_result *res);
+/* Warm-started projections: newton_project_simplex(y, r, xbar=, sharpened=)
+   (simplex.py:218-308 with the xbar-support initializer, simplex.py:65-109)
+   and project_l1(y, r, xbar=) (simplex.py:311-333, sharpened, xbar = |xbar|).
+   Algorithm 2 runs per chunk on the device from xbar's support (par_simplex_init
+   merge, parallel.py:330-368), Algorithm 4 on its free set.  xbar: n values or
+   NULL; sharpened: 0 / 1 (simplex only). */
+int spx_project_warm_f64(cqk_handle *h, int mem, const double *y, int64_t n, double r,
+                         const cqk_options *opts, const double *xbar, int sharpened, double *x,
+                         cqk_result *res);
+int l1_project_warm_f64(cqk_handle *h, int mem, const double *y, int64_t n, double r,
+                        const cqk_options *opts, const double *xbar, double *x, cqk_result *res);
 /* simplex_init_lambda (simplex.py:114-154; workers = 1) and par_simplex_init
    (parallel.py:330-368; workers = W chunks as _chunk_ranges): Algorithm 2 per
    chunk on the device (one thread per chunk, bit-exact recurrence) merged in

@@ -84,7 +84,8 @@ EXPORTS = (
     "cqk_abi_version", "cqk_last_error", "cqk_create", "cqk_destroy", "cqk_set_stream",
     "cqk_device_info", "cqk_get_trace", "cqk_get_timeline", "cqk_validate_f64", "cqk_initial_multiplier_f64",
     "cqk_phi_f64", "cqk_eval_x_f64", "cqk_nearest_breakpoint_f64", "cqk_solve_f64",
-    "spx_project_f64", "l1_project_f64", "spx_project_batched_f64", "cqk_selftest_division",
+    "spx_project_f64", "l1_project_f64", "spx_project_warm_f64", "l1_project_warm_f64",
+    "spx_project_batched_f64", "cqk_selftest_division",
     "cqk_comm_ipc_handle_size", "cqk_comm_create", "cqk_comm_connect", "cqk_comm_connect_local",
     "cqk_set_grid_limit", "cqk_reserve", "cqk_solve_sharded_f64", "spx_project_sharded_f64",
     "l1_project_sharded_f64", "spx_init_alg2_f64", "cqk_gen_cqk_device",
@@ -126,6 +127,9 @@ def _declare(L):
     L.cqk_solve_f64.argtypes = [_P, ctypes.c_int, *arr5, _I64, _D, _OPT, _P, _P, _RES]
     L.spx_project_f64.argtypes = [_P, ctypes.c_int, _P, _I64, _D, _OPT, _P, _RES]
     L.l1_project_f64.argtypes = [_P, ctypes.c_int, _P, _I64, _D, _OPT, _P, _RES]
+    L.spx_project_warm_f64.argtypes = [_P, ctypes.c_int, _P, _I64, _D, _OPT, _P, ctypes.c_int,
+                                       _P, _RES]
+    L.l1_project_warm_f64.argtypes = [_P, ctypes.c_int, _P, _I64, _D, _OPT, _P, _P, _RES]
     L.cqk_selftest_division.argtypes = [_P, ctypes.c_uint64, _I64, ctypes.c_int,
                                         ctypes.POINTER(ctypes.c_uint64), _P]
     L.cqk_comm_ipc_handle_size.restype = ctypes.c_int

@@ -6,6 +6,7 @@
 // H2D before and D2H after it.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -87,7 +88,7 @@ struct cqk_handle {
   long long* timeline = nullptr;
   double* red = nullptr;     // utility partials
   double* out = nullptr;     // utility outputs (kMaxK doubles)
-  Buf scratch, stage, idxbuf, flags, alg2;
+  Buf scratch, stage, idxbuf, flags, alg2, warm;
   int32_t* wcnt = nullptr;            // per-warp scratch counts (simplex tail mode)
   double* alg2_vals = nullptr;        // gathered free values of the last Algorithm-2 run
   int64_t* alg2_idx = nullptr;        // ... and their global indices
@@ -200,6 +201,7 @@ int cqk_destroy(cqk_handle* h) {
   h->idxbuf.release();
   h->flags.release();
   h->alg2.release();
+  h->warm.release();
   for (int q = 0; q < kMaxRanks; ++q)
     if (h->ipc_opened[q] && h->peers[q]) cudaIpcCloseMemHandle(h->peers[q]);
   if (h->mbox) cudaFree(h->mbox);
@@ -717,7 +719,8 @@ int run_alg2(cqk_handle* h, const double* yv, const int64_t* idx, int64_t p, dou
 }
 
 int spx_common(cqk_handle* h, int mem, const double* y, int64_t n, int64_t n_total, double r,
-               const cqk_options* opts_in, double* x, cqk_result* res, bool l1, bool sharded) {
+               const cqk_options* opts_in, double* x, cqk_result* res, bool l1, bool sharded,
+               const double* xbar = nullptr, int sharpened = -1) {
   if (!h || !y || !res) return set_err(CQK_E_ARG, "null argument");
   std::memset(res, 0, sizeof *res);
   res->domain_index = -1;
@@ -731,18 +734,23 @@ int spx_common(cqk_handle* h, int mem, const double* y, int64_t n, int64_t n_tot
   }
   if (n_total < 1 || (!sharded && n < 1)) return set_err(CQK_E_ARG, "n must be >= 1");
   const double* yv;
+  const double* xbv = nullptr;
   double* xdev = nullptr;
   double* xo = x;
   {
-    const double* in[1] = {y};
-    int rc = stage_inputs<double>(h, mem, n, in, 1, &yv, (mem == CQK_MEM_HOST && x) ? 1 : 0, &xdev);
+    const double* in[2] = {y, xbar};
+    const double* dv[2] = {nullptr, nullptr};
+    int rc = stage_inputs<double>(h, mem, n, in, 2, dv, (mem == CQK_MEM_HOST && x) ? 1 : 0, &xdev);
     if (rc) return rc;
+    yv = dv[0];
+    xbv = xbar ? dv[1] : nullptr;
     if (mem == CQK_MEM_HOST) xo = x ? xdev : nullptr;
   }
   if (!aligned16(yv) || (xo && !aligned16(xo)))
     return set_err(CQK_E_ARG, "device arrays must be 16-byte aligned");
   const bool fixing = opts.variable_fixing != 0;
-  const bool alg2 = opts.simplex_start == 2 && !sharded && std::isnan(opts.lambda0);
+  // the Algorithm-2 route: start "alg2", or a warm start (xbar, simplex.py:65-109)
+  const bool alg2 = (opts.simplex_start == 2 || xbv) && !sharded && std::isnan(opts.lambda0);
   SpxState s;
   std::memset(&s, 0, sizeof s);
   s.cmd.fix_hi = INFINITY;
@@ -772,8 +780,44 @@ int spx_common(cqk_handle* h, int mem, const double* y, int64_t n, int64_t n_tot
     // simplex.py:243-245 with the chunked initializer: Algorithm 4 then runs
     // on the gathered free set (values only) and x is one dense pass.
     Alg2Out a2;
-    int rc = run_alg2(h, yv, nullptr, n, r, 0, nullptr, l1 ? 1 : 0, l1, true, false, nullptr, &a2);
+    const int sharp = sharpened >= 0 ? sharpened : (l1 ? 1 : 0);
+    // chunks without a warm start (every chunk multiplier bounds the root,
+    // par_simplex_init); with xbar the sequential recurrence exactly as
+    // simplex_init_lambda runs it (its no-support fallback is global), and
+    // the free set is ~fixed_mask (wider than the initializer's set J)
+    uint8_t* mask = nullptr;
+    double* wvals = nullptr;
+    int64_t* wcount = nullptr;
+    if (xbv) {
+      const size_t mb = ((size_t)n + 255) / 256 * 256, vb = ((size_t)n * 8 + 255) / 256 * 256;
+      CUDA_TRY(h->warm.ensure(mb + vb + 256));
+      mask = (uint8_t*)h->warm.p;
+      wvals = (double*)((char*)h->warm.p + mb);
+      wcount = (int64_t*)((char*)h->warm.p + mb + vb);
+      CUDA_TRY(cudaMemsetAsync(mask, 0, n, h->stream));
+    }
+    int rc = run_alg2(h, yv, nullptr, n, r, xbv ? 1 : 0, xbv, sharp, l1, !xbv, false, mask, &a2);
     if (rc) return rc;
+    if (xbv) {
+      if (l1) spx_gather_free_kernel<true><<<1, 1024, 0, h->stream>>>(yv, mask, n, wvals, wcount);
+      else spx_gather_free_kernel<false><<<1, 1024, 0, h->stream>>>(yv, mask, n, wvals, wcount);
+      CUDA_TRY(cudaGetLastError());
+      int64_t m = 0;
+      CUDA_TRY(cudaMemcpyAsync(&m, wcount, sizeof m, cudaMemcpyDeviceToHost, h->stream));
+      CUDA_TRY(cudaStreamSynchronize(h->stream));
+      a2.n_free = m;
+      h->alg2_vals = wvals;
+    }
+    if (xbv) {  // simplex.py:151-152: no positive xbar component contributed
+      int64_t jp = 0;
+      CUDA_TRY(cudaMemcpy(&jp, h->alg2_jplus, sizeof jp, cudaMemcpyDeviceToHost));
+      if (jp == 0) {
+        double y0 = 0.0;
+        CUDA_TRY(cudaMemcpy(&y0, yv, sizeof y0, cudaMemcpyDeviceToHost));
+        if (l1) y0 = std::fabs(y0);
+        a2.lam0 = std::max(r / (double)n, -y0);
+      }
+    }
     launches = 5;
     extra_read = n;
     if (l1 && a2.inside) {
@@ -786,7 +830,7 @@ int spx_common(cqk_handle* h, int mem, const double* y, int64_t n, int64_t n_tot
       s.cmd.phase = PH_LAMBDA0;  // one pass over the free set: r - max(w) tightens the start
       s.lam0_given = 1;
       s.lam0_value = a2.lam0;
-      s.start = 3;
+      s.start = xbv ? 2 : 3;  // warm: the initializer's multiplier as is (simplex.py:243-245)
       s.n = m;
       s.active = m;
       s.local_active = m;
@@ -857,6 +901,25 @@ extern "C" int l1_project_sharded_f64(cqk_handle* h, int mem, const double* y, i
                                       double* x, cqk_result* res) {
   if (!h || !h->mbox) return set_err(CQK_E_ARG, "communicator not set up");
   return spx_common(h, mem, y, n_local, n_total, r, opts, x, res, true, true);
+}
+
+// Warm-started projections (simplex.py:218 / 311 with xbar): the Algorithm-2
+// initializer seeded by the support of xbar (device chunks, par_simplex_init
+// merge), Algorithm 4 on its free set.  xbar may be NULL (sharpened only).
+extern "C" int spx_project_warm_f64(cqk_handle* h, int mem, const double* y, int64_t n, double r,
+                                    const cqk_options* opts, const double* xbar, int sharpened,
+                                    double* x, cqk_result* res) {
+  cqk_options o = opts ? *opts : default_opts();
+  o.simplex_start = 2;
+  return spx_common(h, mem, y, n, n, r, &o, x, res, false, false, xbar, sharpened);
+}
+
+extern "C" int l1_project_warm_f64(cqk_handle* h, int mem, const double* y, int64_t n, double r,
+                                   const cqk_options* opts, const double* xbar, double* x,
+                                   cqk_result* res) {
+  cqk_options o = opts ? *opts : default_opts();
+  o.simplex_start = 2;
+  return spx_common(h, mem, y, n, n, r, &o, x, res, true, false, xbar, 1);
 }
 
 extern "C" int l1_project_f64(cqk_handle* h, int mem, const double* y, int64_t n, double r,

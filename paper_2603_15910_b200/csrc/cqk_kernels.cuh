@@ -1967,6 +1967,40 @@ __global__ void __launch_bounds__(256) spx_x_kernel(const double* __restrict__ y
   }
 }
 
+// Warm-started projections: the free set is every index the initializer did
+// not prove zero (simplex.py:244, ~fixed_mask -- with xbar that is more than
+// its running set J).  One CTA, chunks of 1024 in index order, warp-ballot
+// block scan: deterministic, np.flatnonzero order.
+template <bool L1>
+__global__ void __launch_bounds__(1024) spx_gather_free_kernel(const double* __restrict__ y,
+                                                               const uint8_t* __restrict__ fixed,
+                                                               int64_t n, double* __restrict__ vals,
+                                                               int64_t* __restrict__ count) {
+  __shared__ int s_w[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int64_t base_out = 0;
+  for (int64_t c0 = 0; c0 < n; c0 += 1024) {
+    const int64_t i = c0 + threadIdx.x;
+    const bool keep = i < n && !fixed[i];
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) s_w[warp] = __popc(bal);
+    __syncthreads();
+    int pre = 0, tot = 0;
+    for (int w = 0; w < 32; ++w) {
+      const int v = s_w[w];
+      pre += w < warp ? v : 0;
+      tot += v;
+    }
+    if (keep) {
+      const double v = y[i];
+      vals[base_out + pre + __popc(bal & ((1u << lane) - 1u))] = L1 ? fabs(v) : v;
+    }
+    base_out += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *count = base_out;
+}
+
 // ------------------------------------------------------------ utilities
 // Grid-stride kernels with per-block partials + a fixed-order finalize; used
 // by the component-level entry points (eval_phi, eval_x, breakpoints,

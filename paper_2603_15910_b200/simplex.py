@@ -7,9 +7,10 @@ followed by Algorithm 4's streamlined Newton iteration with variable fixing
 (simplex.py:256-294), all inside one persistent kernel.  The result equals the
 reference's Algorithm-2-initialised projection to rounding (the root does not
 depend on the start); iteration counts match the reference's `lambda0=` route
-with the same start.  `sharpened` and `xbar` only
-steer the reference's sequential Gauss-Seidel initialiser and therefore do
-not change the device result.
+with the same start.  A warm start (`xbar`, simplex.py:65-109) -- or
+start="alg2" -- runs the reference's Gauss-Seidel initializer per chunk on
+the device (par_simplex_init semantics, `sharpened` as given) and Algorithm 4
+on its free set.
 """
 
 from dataclasses import dataclass
@@ -130,10 +131,19 @@ def _prep(y):
     return np.ascontiguousarray(y, dtype=np.float64), y.dtype, False
 
 
-def _project(y, r, opts, lambda0, trace, l1, start="tight"):
+def _project(y, r, opts, lambda0, trace, l1, start="tight", xbar=None, sharpened=None):
     if opts is None:
         opts = SolverOptions()
     yv, dt, dev = _prep(y)
+    # warm start (simplex.py:65-109): Algorithm 2 seeded by xbar's support
+    warm = lambda0 is None and (xbar is not None or (start == "alg2" and sharpened))
+    xb = None
+    if warm and xbar is not None:
+        xb, _, xdev = _prep(xbar)
+        if xdev != dev or int(xb.shape[0]) != int(yv.shape[0]):
+            raise DomainError("xbar", None, "xbar must match y in length and placement")
+        if not bool((xb >= 0).all()) and not l1:
+            raise DomainError("xbar", None, "warm-start estimate must be >= 0")
     n = int(yv.shape[0])
     h = N.handle(yv.device.index if dev else None)
     if dev:
@@ -154,8 +164,16 @@ def _project(y, r, opts, lambda0, trace, l1, start="tight"):
                        compact_ratio=getattr(opts, "compact_ratio", None), start=start)
     o.tolerance_scale = opts.tau(dt)
     res = N.Result()
-    fn = h.lib.l1_project_f64 if l1 else h.lib.spx_project_f64
-    rc = fn(h.ptr, mem, yp, n, float(r), o, xp, res)
+    if warm:
+        xbp = None if xb is None else (xb.data_ptr() if dev else xb.ctypes.data)
+        if l1:
+            rc = h.lib.l1_project_warm_f64(h.ptr, mem, yp, n, float(r), o, xbp, xp, res)
+        else:
+            rc = h.lib.spx_project_warm_f64(h.ptr, mem, yp, n, float(r), o, xbp,
+                                            1 if sharpened else 0, xp, res)
+    else:
+        fn = h.lib.l1_project_f64 if l1 else h.lib.spx_project_f64
+        rc = fn(h.ptr, mem, yp, n, float(r), o, xp, res)
     if trace is not None:
         trace.extend(h.trace(res.trace_len))
     if rc == N.E_DOMAIN:
@@ -190,7 +208,8 @@ def newton_project_simplex(y, r, opts=None, xbar=None, output="dense", sharpened
     free set."""
     if not r > 0:
         raise DomainError("r", None, "simplex level r must be positive")
-    x, res = _project(y, r, opts, lambda0, trace, l1=False, start=start)
+    x, res = _project(y, r, opts, lambda0, trace, l1=False, start=start, xbar=xbar,
+                      sharpened=sharpened)
     dev = _is_torch(x)
     sparse = None
     if output == "sparse":
@@ -205,7 +224,7 @@ def project_l1(y, r, opts=None, output="dense", xbar=None, start="tight"):
     """Project y onto the l1 ball of radius r (simplex.py:311-333)."""
     if not r > 0:
         raise DomainError("r", None, "l1 radius r must be positive")
-    x, res = _project(y, r, opts, None, None, l1=True, start=start)
+    x, res = _project(y, r, opts, None, None, l1=True, start=start, xbar=xbar, sharpened=True)
     if output == "sparse":
         dev = _is_torch(x)
         if dev:
