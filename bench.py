@@ -104,12 +104,20 @@ def dist_init():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # CQK_BENCH_DEVICE / CQK_BENCH_BACKEND=gloo: run the N>1 code path with all
+    # ranks on one GPU (a smoke test of the sharded protocol, not a number)
+    if os.environ.get("CQK_BENCH_DEVICE") is not None:
+        local = int(os.environ["CQK_BENCH_DEVICE"])
     if world > 1:
         import torch
         import torch.distributed as dist
 
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("CQK_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     return world, rank, local
 
 
@@ -126,7 +134,8 @@ def max_over_ranks(v, world):
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -215,7 +224,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--n", type=int, default=N_FULL)
+    ap.add_argument("--n", "--size", dest="n", type=int, default=N_FULL)
     ap.add_argument("--variant", default="solve", choices=["solve", "jacobi"])
     ap.add_argument("--ref-sample", type=int, default=10**7)
     ap.add_argument("--e2e-steps", type=int, default=5)

@@ -188,6 +188,7 @@ int cqk_create(cqk_handle** out, int device) {
     return set_err(CQK_E_CUDA, std::string("cqk_create: ") + cudaGetErrorString(e));
   }
   h->stream = h->own;
+  if (const char* gl = getenv("CQK_GRID_LIMIT")) h->grid_limit = atoi(gl);  // shared-GPU runs
   *out = h;
   return 0;
 }
