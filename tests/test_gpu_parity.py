@@ -290,3 +290,19 @@ def test_device_tensors_zero_copy():
     assert out.x.is_cuda
     assert close(out.lam, ref["lam"])
     assert float((out.x.cpu().numpy() - ref["x"]).__abs__().max()) <= 1e-12 * 25
+
+
+def test_solve_pipeline_matches_sequential():
+    p = P()
+    from paper_2603_15910_b200.pipeline import SolvePipeline
+
+    insts = []
+    for seed in range(6):
+        d, a, b, l, u, r = random_arrays(900 + seed, 5000 + 997 * seed)
+        insts.append(p.CqkInstance(d=d, a=a, b=b, l=l, u=u, r=r))
+    seq = [p.solve_cqk(i) for i in insts]
+    with SolvePipeline(depth=3) as pipe:
+        outs = [f.result() for f in [pipe.submit(i) for i in insts]]
+    for s, o in zip(seq, outs):
+        assert o.status is s.status and o.lam == s.lam and o.iterations == s.iterations
+        assert np.array_equal(o.x, s.x)
