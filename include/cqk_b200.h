@@ -205,6 +205,10 @@ int cqk_comm_connect_local(cqk_handle *h, cqk_handle *const *ranks, int world);
 int cqk_reserve(cqk_handle *h, int64_t n);
 /* Cap the persistent grid (CTAs); 0 = the full device.  Lets several ranks
    share one GPU (virtual ranks) or leave SMs for other work. */
+/* CQK solve engine: 0 auto (TMA pipeline from 8e6 elements per rank,
+   CQK_TMA_MIN_N), 1 TMA pipeline, 2 warp-segment kernel.  Results agree to
+   rounding (summation order differs). */
+int cqk_set_engine(cqk_handle *h, int mode);
 int cqk_set_grid_limit(cqk_handle *h, int max_ctas);
 /* Sharded solve_cqk / jacobi_solve / par_solve_cqk: this rank's shard
    [offset, offset + n_local) of an n_total-element instance.  All ranks call

@@ -37,6 +37,10 @@ namespace cqk {
 #ifndef CQK_TMA_CONSW
 #define CQK_TMA_CONSW 15
 #endif
+// A/B switches for measurement (CQK_TMA_FLAGS): bit 0 disables the
+// next-pass prefetch across the grid step.
+__constant__ int c_tma_flags;
+
 constexpr int kTileC = CQK_TMA_TILE;      // elements per array per tile
 constexpr int kStagesC = CQK_TMA_STAGES;
 constexpr int kArrMaxC = 6;               // d, a, b, l, u, xbar
@@ -639,7 +643,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
   // step is in flight: the loads do not depend on lambda.
   auto speculate = [&]() {
     const TileWalk nw{p.n, ntiles, in_scratch ? s_nslots : -1};
-    s_spec = produce<5>(in_scratch ? src_scr : src_orig, nw, pp, 0, kStagesC);
+    s_spec = (c_tma_flags & 1) ? 0 : produce<5>(in_scratch ? src_scr : src_orig, nw, pp, 0, kStagesC);
     s_spec_scr = in_scratch;
   };
   for (unsigned epoch = 1;; ++epoch) {

@@ -225,7 +225,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
   // (cqk_tma.cuh: the loads do not depend on lambda)
   auto speculate = [&]() {
     const TileWalk nw{p.n, ntiles, in_scratch ? s_nslots : -1};
-    s_spec = produce<1, kStagesY, kTileY, kTileY>(Src{{in_scratch ? p.sy : p.y}}, nw, pp, 0, kStagesY);
+    s_spec = (c_tma_flags & 1) ? 0
+                               : produce<1, kStagesY, kTileY, kTileY>(Src{{in_scratch ? p.sy : p.y}}, nw,
+                                                                      pp, 0, kStagesY);
     s_spec_scr = in_scratch;
   };
   for (unsigned epoch = 1;; ++epoch) {

@@ -21,6 +21,17 @@ def P():
     return p
 
 
+@pytest.fixture(autouse=True, params=["tma", "seg"])
+def engine(request):
+    """Run every case on both CQK engines (auto picks by size)."""
+    from paper_2603_15910_b200 import _native as N
+
+    h = N.handle()
+    h.lib.cqk_set_engine(h.ptr, 1 if request.param == "tma" else 2)
+    yield request.param
+    h.lib.cqk_set_engine(h.ptr, 0)
+
+
 def inst_arrays(seed, n):
     rng = np.random.default_rng(seed)
     d = rng.uniform(0.5, 3.0, n)
