@@ -127,7 +127,11 @@ DEVI int64_t t_spx(const SpxParams<double>& p, const Cmd& c, bool fix, const Til
     double Wv[kEptY];
     if (wt.wcnt == kSegY) spx_tile<L1, MODE, true>(wt, src, scratch, lam, fix, fhi, acc, cnt, keep, Wv);
     else spx_tile<L1, MODE, false>(wt, src, scratch, lam, fix, fhi, acc, cnt, keep, Wv);
-    if (MODE == 1 && compact) {  // warp sub-segment compaction of the values w
+    bool any_keep = false;
+#pragma unroll
+    for (int j = 0; j < kEptY; ++j) any_keep = any_keep || keep[j];
+    // survivors are rare in projections: most tiles have none to write
+    if (MODE == 1 && compact && __any_sync(0xffffffffu, any_keep)) {  // warp sub-segment compaction
       const int64_t b0 = ((int64_t)blockIdx.x + q_out * g) * kTileY + kSegY * warp;
       const int64_t b1 = b0 + g * kTileY;
       int r = off_out;
