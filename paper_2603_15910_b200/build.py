@@ -21,7 +21,7 @@ GEN_LIB = os.path.join(LIBDIR, "libcqk_instances.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # -fmad=false: no FMA contraction anywhere, so every product/sum in the
 # element math and the scalar Newton logic rounds exactly like numpy/Python.
-NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC",
+NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC,-fopenmp", "-lgomp",
               "-shared", "--expt-relaxed-constexpr"]
 
 CUDA_SOURCES = ["cqk_abi.cu"]

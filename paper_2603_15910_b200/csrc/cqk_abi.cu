@@ -5,6 +5,7 @@
 // Every solve is ONE cooperative kernel launch; the small state struct goes
 // H2D before and D2H after it.
 #include <cuda_runtime.h>
+#include <omp.h>
 
 #include <algorithm>
 #include <cmath>
@@ -94,6 +95,12 @@ struct cqk_handle {
   double* red = nullptr;     // utility partials
   double* out = nullptr;     // utility outputs (kMaxK doubles)
   Buf scratch, stage, idxbuf, flags, alg2, warm;
+  // pageable host inputs / outputs: a ring of pinned chunk buffers filled /
+  // drained by OpenMP memcpy while the copy engine moves the previous chunk
+  static constexpr int kRing = 4;
+  static constexpr size_t kRingBytes = 32u << 20;
+  void* ring[kRing] = {};
+  cudaEvent_t ring_ev[kRing] = {};
   int32_t* wcnt = nullptr;            // per-warp scratch counts (simplex tail mode)
   double* alg2_vals = nullptr;        // gathered free values of the last Algorithm-2 run
   int64_t* alg2_idx = nullptr;        // ... and their global indices
@@ -220,6 +227,10 @@ int cqk_destroy(cqk_handle* h) {
   cudaFree(h->red);
   cudaFree(h->out);
   if (h->wcnt) cudaFree(h->wcnt);
+  for (int k = 0; k < cqk_handle::kRing; ++k) {
+    if (h->ring[k]) cudaFreeHost(h->ring[k]);
+    if (h->ring_ev[k]) cudaEventDestroy(h->ring_ev[k]);
+  }
   if (h->err_host) cudaFreeHost(h->err_host);
   if (h->host_state) cudaFreeHost(h->host_state);
   if (h->ev0) cudaEventDestroy(h->ev0);
@@ -286,6 +297,87 @@ cqk_options default_opts() {
   return o;
 }
 
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeManaged;
+}
+
+int ensure_ring(cqk_handle* h) {
+  for (int k = 0; k < cqk_handle::kRing; ++k) {
+    if (!h->ring[k]) CUDA_TRY(cudaMallocHost(&h->ring[k], cqk_handle::kRingBytes));
+    if (!h->ring_ev[k]) CUDA_TRY(cudaEventCreateWithFlags(&h->ring_ev[k], cudaEventDisableTiming));
+  }
+  return 0;
+}
+
+void par_memcpy(void* dst, const void* src, size_t bytes) {
+  const int64_t nt = omp_get_max_threads() < 8 ? omp_get_max_threads() : 8;
+  const size_t part = (bytes / nt + 63) / 64 * 64;
+#pragma omp parallel for num_threads(nt) schedule(static)
+  for (int64_t t = 0; t < nt; ++t) {
+    const size_t o = (size_t)t * part;
+    if (o < bytes) std::memcpy((char*)dst + o, (const char*)src + o, o + part < bytes ? part : bytes - o);
+  }
+}
+
+// Pageable host -> device: memcpy chunks into the pinned ring (several host
+// threads) while the copy engine moves the previous chunk (~3-4x the
+// driver's own pageable path on this class of host).  Pinned memory goes
+// straight to cudaMemcpyAsync.
+int h2d(cqk_handle* h, void* dst, const void* src, size_t bytes) {
+  if (bytes == 0) return 0;
+  if (bytes < (1u << 20) || is_pinned(src)) {
+    CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, h->stream));
+    return 0;
+  }
+  int rc = ensure_ring(h);
+  if (rc) return rc;
+  for (size_t off = 0, k = 0; off < bytes; off += cqk_handle::kRingBytes, ++k) {
+    const int s = (int)(k % cqk_handle::kRing);
+    const size_t len = bytes - off < cqk_handle::kRingBytes ? bytes - off : cqk_handle::kRingBytes;
+    CUDA_TRY(cudaEventSynchronize(h->ring_ev[s]));  // the slot's previous copy is done
+    par_memcpy(h->ring[s], (const char*)src + off, len);
+    CUDA_TRY(cudaMemcpyAsync((char*)dst + off, h->ring[s], len, cudaMemcpyHostToDevice, h->stream));
+    CUDA_TRY(cudaEventRecord(h->ring_ev[s], h->stream));
+  }
+  return 0;
+}
+
+// Device -> pageable host, the mirror image (enqueued work on the stream
+// completes first; the caller's buffer is complete on return).
+int d2h(cqk_handle* h, void* dst, const void* src, size_t bytes) {
+  if (bytes == 0) return 0;
+  if (bytes < (1u << 20) || is_pinned(dst)) {
+    CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, h->stream));
+    return 0;
+  }
+  int rc = ensure_ring(h);
+  if (rc) return rc;
+  const size_t R = cqk_handle::kRingBytes;
+  const size_t nchunks = (bytes + R - 1) / R;
+  auto launch = [&](size_t k) -> int {
+    const int s = (int)(k % cqk_handle::kRing);
+    const size_t off = k * R, len = bytes - off < R ? bytes - off : R;
+    CUDA_TRY(cudaMemcpyAsync(h->ring[s], (const char*)src + off, len, cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(cudaEventRecord(h->ring_ev[s], h->stream));
+    return 0;
+  };
+  for (size_t k = 0; k < nchunks && k < (size_t)cqk_handle::kRing; ++k)
+    if ((rc = launch(k))) return rc;
+  for (size_t k = 0; k < nchunks; ++k) {
+    const int s = (int)(k % cqk_handle::kRing);
+    const size_t off = k * R, len = bytes - off < R ? bytes - off : R;
+    CUDA_TRY(cudaEventSynchronize(h->ring_ev[s]));
+    par_memcpy((char*)dst + off, h->ring[s], len);
+    if (k + cqk_handle::kRing < nchunks && (rc = launch(k + cqk_handle::kRing))) return rc;
+  }
+  return 0;
+}
+
 // Host-mode staging: copy `count` host arrays of n T into one device slab.
 template <typename T>
 int stage_inputs(cqk_handle* h, int mem, int64_t n, const T* const* in, int count,
@@ -300,7 +392,8 @@ int stage_inputs(cqk_handle* h, int mem, int64_t n, const T* const* in, int coun
   for (int i = 0; i < count; ++i) {
     if (!in[i]) { dev[i] = nullptr; continue; }
     T* d = (T*)(base + per * i);
-    CUDA_TRY(cudaMemcpyAsync(d, in[i], (size_t)n * sizeof(T), cudaMemcpyHostToDevice, h->stream));
+    int rc = h2d(h, d, in[i], (size_t)n * sizeof(T));
+    if (rc) return rc;
     dev[i] = d;
   }
   for (int j = 0; j < extra_out; ++j) dev_out[j] = (T*)(base + per * (count + j));
@@ -589,7 +682,10 @@ static int solve_impl(cqk_handle* h, int mem, const double* d, const double* a, 
   CUDA_TRY(cudaMemcpyAsync(h->err_host, h->sync + 2, sizeof(unsigned), cudaMemcpyDeviceToHost,
                            h->stream));
   if (mem == CQK_MEM_HOST && x && xo)
-    CUDA_TRY(cudaMemcpyAsync(x, xo, sizeof(double) * n, cudaMemcpyDeviceToHost, h->stream));
+  {
+    int rc_ = d2h(h, x, xo, sizeof(double) * n);
+    if (rc_) return rc_;
+  }
   int rc = finish_sync(h);
   if (rc) return rc;
   std::memcpy(&s, h->host_state, sizeof s);
@@ -870,7 +966,10 @@ int spx_common(cqk_handle* h, int mem, const double* y, int64_t n, int64_t n_tot
   }
   CUDA_TRY(cudaEventRecord(h->ev1, h->stream));
   if (mem == CQK_MEM_HOST && x && xo)
-    CUDA_TRY(cudaMemcpyAsync(x, xo, sizeof(double) * n, cudaMemcpyDeviceToHost, h->stream));
+  {
+    int rc_ = d2h(h, x, xo, sizeof(double) * n);
+    if (rc_) return rc_;
+  }
   int rc = finish_sync(h);
   if (rc) return rc;
   if (!(alg2 && s.iterations < 0)) std::memcpy(&s, h->host_state, sizeof s);
@@ -984,7 +1083,10 @@ extern "C" int spx_project_batched_f64(cqk_handle* h, int mem, const double* Y, 
     const size_t rb = ((size_t)rows * 8 + 255) / 256 * 256;
     CUDA_TRY(h->stage.ensure(2 * per + 2 * rb));
     char* base = (char*)h->stage.p;
-    CUDA_TRY(cudaMemcpyAsync(base, Y, (size_t)tot * 8, cudaMemcpyHostToDevice, h->stream));
+    {
+      int rc_ = h2d(h, base, Y, (size_t)tot * 8);
+      if (rc_) return rc_;
+    }
     Yd = (const double*)base;
     Xd = (double*)(base + per);
     Ld = lam ? (double*)(base + 2 * per) : nullptr;
@@ -1057,7 +1159,10 @@ extern "C" int spx_project_batched_f64(cqk_handle* h, int mem, const double* Y, 
   if (e != cudaSuccess) return set_err(CQK_E_CUDA, std::string("rows kernel: ") + cudaGetErrorString(e));
   CUDA_TRY(cudaEventRecord(h->ev1, h->stream));
   if (mem == CQK_MEM_HOST) {
-    CUDA_TRY(cudaMemcpyAsync(X, Xd, (size_t)tot * 8, cudaMemcpyDeviceToHost, h->stream));
+    {
+      int rc_ = d2h(h, X, Xd, (size_t)tot * 8);
+      if (rc_) return rc_;
+    }
     if (lam) CUDA_TRY(cudaMemcpyAsync(lam, Ld, (size_t)rows * 8, cudaMemcpyDeviceToHost, h->stream));
     if (iters) CUDA_TRY(cudaMemcpyAsync(iters, Id, (size_t)rows * 4, cudaMemcpyDeviceToHost, h->stream));
   }
