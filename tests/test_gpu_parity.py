@@ -306,3 +306,22 @@ def test_solve_pipeline_matches_sequential():
     for s, o in zip(seq, outs):
         assert o.status is s.status and o.lam == s.lam and o.iterations == s.iterations
         assert np.array_equal(o.x, s.x)
+
+
+def test_rows_many_per_cta_mixed_paths():
+    """More rows than resident CTAs (the next row streams in while a row
+    iterates), alternating rows whose free set fits the warp buffers (zero-fill
+    + scatter output) with rows that overflow them (staged output)."""
+    p = P()
+    rng = np.random.default_rng(9)
+    rows, cols = 4001, 4096
+    Y = rng.normal(0, 1, (rows, cols))
+    Y[1::2] = rng.uniform(0, 1, (rows // 2, cols))  # u01 rows overflow at the tight start
+    X, lam, its, _ = p.project_simplex_rows(Y, 1.0)
+    for i in list(range(0, 40)) + list(range(rows - 40, rows)) + list(range(1000, 4000, 97)):
+        lam0 = min((1.0 - O.pairwise_sum(Y[i])) / cols, 1.0 - float(Y[i].max()))
+        ref = O.newton_project_simplex(Y[i], 1.0, lam0=lam0)
+        assert close(lam[i], ref["lam"]), (i, lam[i], ref["lam"])
+        assert its[i] == ref["iterations"]
+        assert float(np.abs(X[i] - ref["x"]).max()) <= TOL
+    np.testing.assert_allclose(X.sum(axis=1), 1.0, atol=1e-12)
