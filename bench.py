@@ -308,6 +308,28 @@ def main():
     # public SolvePipeline (depth 2: one step's H2D overlaps the previous
     # step's solve and D2H -- each step still moves all its bytes).
     e2e = None
+    if world > 1 and args.e2e_steps > 0:
+        # every rank: its shard's H2D from pinned host memory + the collective
+        # solve + D2H of its x, device-timed, max over ranks
+        host = [t.cpu().pin_memory().numpy() for t in dev]
+        xh = torch.empty(n_local, dtype=torch.float64, pin_memory=True).numpy()
+        with torch.cuda.stream(stream):
+            for _ in range(2):
+                assert solver.solve_host(host, xh).status is P.Status.SOLVED
+            torch.cuda.synchronize()
+            barrier(world)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(args.e2e_steps):
+                assert solver.solve_host(host, xh).status is P.Status.SOLVED
+            e1.record(stream)
+            torch.cuda.synchronize()
+        ems = max_over_ranks(e0.elapsed_time(e1) / args.e2e_steps, world)
+        e2e = {"value": args.n / (ems / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": 5 * 8 * args.n, "d2h_bytes_per_step": 8 * args.n,
+               "ms_per_step": ems, "api": "ShardedCQK.solve_host (each rank its shard)"}
+        del host
     if world == 1 and args.e2e_steps > 0:
         from paper_2603_15910_b200.pipeline import SolvePipeline
 

@@ -208,6 +208,9 @@ int cqk_reserve(cqk_handle *h, int64_t n);
 /* CQK solve engine: 0 auto (TMA pipeline from 8e6 elements per rank,
    CQK_TMA_MIN_N), 1 TMA pipeline, 2 warp-segment kernel.  Results agree to
    rounding (summation order differs). */
+/* Pre-allocate the host-mode staging of an n-element shard (collective solves
+   with CQK_MEM_HOST must not allocate while peers wait inside the kernel). */
+int cqk_reserve_host(cqk_handle *h, int64_t n);
 int cqk_set_engine(cqk_handle *h, int mode);
 int cqk_set_grid_limit(cqk_handle *h, int max_ctas);
 /* Sharded solve_cqk / jacobi_solve / par_solve_cqk: this rank's shard

@@ -87,7 +87,7 @@ EXPORTS = (
     "spx_project_f64", "l1_project_f64", "spx_project_warm_f64", "l1_project_warm_f64",
     "spx_project_batched_f64", "cqk_selftest_division",
     "cqk_comm_ipc_handle_size", "cqk_comm_create", "cqk_comm_connect", "cqk_comm_connect_local",
-    "cqk_set_grid_limit", "cqk_set_engine", "cqk_reserve", "cqk_solve_sharded_f64", "spx_project_sharded_f64",
+    "cqk_set_grid_limit", "cqk_set_engine", "cqk_reserve", "cqk_reserve_host", "cqk_solve_sharded_f64", "spx_project_sharded_f64",
     "l1_project_sharded_f64", "spx_init_alg2_f64", "cqk_gen_cqk_device",
     "cqk_gen_cqk_device_range", "cqk_gen_simplex_u01_device",
 )
@@ -138,6 +138,7 @@ def _declare(L):
     L.cqk_comm_connect_local.argtypes = [_P, _P, ctypes.c_int]
     L.cqk_set_grid_limit.argtypes = [_P, ctypes.c_int]
     L.cqk_set_engine.argtypes = [_P, ctypes.c_int]
+    L.cqk_reserve_host.argtypes = [_P, _I64]
     L.cqk_reserve.argtypes = [_P, _I64]
     L.cqk_solve_sharded_f64.argtypes = [_P, ctypes.c_int, *arr5, _I64, _I64, _I64, _D, _OPT, _P,
                                         _P, _RES]

@@ -491,6 +491,16 @@ extern "C" int cqk_reserve(cqk_handle* h, int64_t n) {
   return 0;
 }
 
+extern "C" int cqk_reserve_host(cqk_handle* h, int64_t n) {
+  if (!h || n < 0) return set_err(CQK_E_ARG, "bad reserve");
+  CUDA_TRY(cudaSetDevice(h->device));
+  const size_t per = ((size_t)n * sizeof(double) + 255) / 256 * 256;
+  CUDA_TRY(h->stage.ensure(per * 7));  // d, a, b, l, u, xbar + x
+  if (int rc = ensure_ring(h)) return rc;
+  CUDA_TRY(cudaDeviceSynchronize());
+  return 0;
+}
+
 extern "C" int cqk_set_engine(cqk_handle* h, int mode) {
   if (!h || mode < 0 || mode > 2) return set_err(CQK_E_ARG, "engine: 0 auto, 1 tma, 2 segments");
   h->engine = mode;

@@ -144,6 +144,38 @@ class ShardedCQK:
 
         return _outcome(_I, res, rc, x, "sharded solve_cqk")
 
+    def solve_host(self, host_arrays, x_out=None, opts=None, variant="solve", check=True):
+        """Collective solve of this rank's shard given in HOST memory (numpy,
+        ideally page-locked): the library copies it to the device, solves and
+        writes x back into x_out (a host array of n_local, allocated if None)."""
+        import torch
+
+        if opts is None:
+            opts = SolverOptions()
+        h = self.handle
+        if not getattr(self, "_host_reserved", False):
+            rc = h.lib.cqk_reserve_host(h.ptr, self.n_local)
+            if rc != 0:
+                raise N.NativeError(f"cqk_reserve_host failed ({rc}): {N.last_error()}")
+            self._host_reserved = True
+        h.set_stream(torch.cuda.current_stream(self.device).cuda_stream)
+        arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in host_arrays]
+        if x_out is None:
+            x_out = torch.empty(self.n_local, dtype=torch.float64, pin_memory=True).numpy()
+        o = N.make_options(opts, variant=_VARIANTS[variant], check=check,
+                           compact_ratio=getattr(opts, "compact_ratio", None),
+                           fixing=False if variant == "jacobi" else None)
+        o.tolerance_scale = opts.tau(np.float64)
+        res = N.Result()
+        rc = h.lib.cqk_solve_sharded_f64(h.ptr, N.MEM_HOST, *[a.ctypes.data for a in arrs],
+                                         self.n_local, self.offset, self.n_total, self.r, o, None,
+                                         x_out.ctypes.data, res)
+
+        class _I:
+            dtype = np.dtype(np.float64)
+
+        return _outcome(_I, res, rc, x_out, "sharded solve_cqk")
+
 
 class ShardedProjection:
     """This rank's shard of y for collective simplex (l1=False) / l1-ball

@@ -40,6 +40,10 @@ def _worker(rank, world, port, q):
         sh = [torch.from_numpy(v[lo:hi].copy()).cuda() for v in (d, a, b, l, u)]
         solver = D.ShardedCQK(sh, r, n_total=n, offset=lo, comm=comm)
         out = solver.solve()
+        # the same collective solve from host memory (H2D / D2H in the library)
+        oh = solver.solve_host([v[lo:hi] for v in (d, a, b, l, u)])
+        assert oh.lam == out.lam and oh.iterations == out.iterations
+        assert np.array_equal(oh.x, out.x.cpu().numpy())
         q.put((rank, out.lam, out.iterations, out.fixed_count, lo, out.x.cpu().numpy()))
     except Exception as e:  # pragma: no cover
         q.put((rank, repr(e)))
