@@ -401,15 +401,16 @@ int stage_inputs(cqk_handle* h, int mem, int64_t n, const T* const* in, int coun
 }
 
 // Compact when the logically fixed, physically present elements reach this
-// share of the working set (CQK_COMPACT_RATIO overrides).  0.5 would stream
-// ~3-8% fewer bytes on the C3 families, but the extra full-width scan with
-// live fixed tests costs more than it saves (measured), so 0.25.
-double default_compact_ratio() {
+// share of the working set (CQK_COMPACT_RATIO overrides).  Measured on the C3
+// families (n = 1e8): with the TMA engine 0.5 streams 2-5% fewer bytes and is
+// fastest (weak 3.99 -> 3.88 ms, corr 4.26 -> 3.88 ms); the warp-segment
+// engine (small n) keeps 0.25.
+double default_compact_ratio(bool tma = false) {
   static double v = [] {
     const char* e = getenv("CQK_COMPACT_RATIO");
-    return e ? atof(e) : 0.25;
+    return e ? atof(e) : -1.0;
   }();
-  return v;
+  return v >= 0 ? v : (tma ? 0.5 : 0.25);
 }
 
 bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
@@ -630,7 +631,6 @@ static int solve_impl(cqk_handle* h, int mem, const double* d, const double* a, 
   s.r_orig = r;
   s.tau = tau_of(&opts, false);
   s.lam0 = s.cmd.lam;
-  s.compact_ratio = std::isnan(opts.compact_ratio) ? default_compact_ratio() : opts.compact_ratio;
   s.fhi_phys = INFINITY;  // the original arrays: nothing removed yet
   s.flo_phys = -INFINITY;
   s.max_iter = opts.max_iterations;
@@ -648,6 +648,7 @@ static int solve_impl(cqk_handle* h, int mem, const double* d, const double* a, 
   // per-epoch fill latency makes the warp-segment kernel faster (measured:
   // 1e6 0.16 vs 0.11 ms, 1e7 equal, 3e7 1.48 vs 1.71 ms)
   const bool tma = h->use_tma && (h->engine == 1 || (h->engine == 0 && n >= h->tma_min_n));
+  s.compact_ratio = std::isnan(opts.compact_ratio) ? default_compact_ratio(tma) : opts.compact_ratio;
   // scratch: n per array (warp segments) or whole tile slots (TMA engine)
   const size_t per = ((size_t)(tma ? tma_scratch_elems(n) : n) * sizeof(double) + 255) / 256 * 256;
   if (fixing) CUDA_TRY(h->scratch.ensure(per * 5));
