@@ -262,7 +262,7 @@ def handle(device=None):
 
 
 def make_options(opts=None, variant=VARIANT_SOLVE, check=True, lambda0=None,
-                 compact_ratio=None, trace=False, fixing=None, start="tight"):
+                 compact_ratio=None, trace=False, fixing=None, start="auto"):
     o = Options()
     fix = getattr(opts, "variable_fixing", True) if fixing is None else fixing
     o.variable_fixing = 1 if fix else 0
@@ -274,5 +274,5 @@ def make_options(opts=None, variant=VARIANT_SOLVE, check=True, lambda0=None,
     o.lambda0 = math.nan if lambda0 is None else float(lambda0)
     o.compact_ratio = math.nan if compact_ratio is None else float(compact_ratio)
     o.record_trace = 1 if trace else 0
-    o.simplex_start = {"formula": 0, "tight": 1, "alg2": 2}[start]
+    o.simplex_start = {"formula": 0, "tight": 1, "alg2": 2, "auto": 4}[start]
     return o

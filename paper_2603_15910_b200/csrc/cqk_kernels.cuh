@@ -543,8 +543,9 @@ struct SpxState {
   int64_t n, active, phys_count, pending_phys, fixed_count, fixed_removed;
   int64_t local_active, fixed_local;  // this rank's share (multi-GPU)
   int64_t iterations, phi_evals, max_iter, elems_scan, elems_written;
-  int32_t fixing, status, l1, lam0_given, trace_len, trace_cap, start, pad;
+  int32_t fixing, status, l1, lam0_given, trace_len, trace_cap, start, hist_ok;
   double compact_ratio;
+  double lam_hist;  // start "auto": histogram upper bound of the root after the first scan (or NaN)
 };
 
 template <typename T>
@@ -559,6 +560,7 @@ struct SpxParams {
   GridSync sync;
   Exchange ex;
   int32_t* wcnt;  // [grid][consumer warps] scratch counts: enables the TMA kernel's tail mode
+  int32_t* hist;  // [kHistB] bucket counts of the first scan (start "auto"), zeroed by the host
 };
 
 DEVI void s_finish(SpxState& s, double lam) {
@@ -590,6 +592,8 @@ DEVI void s_after_init(SpxState& s, const double* tot) {
   s.lam0 = lam0 >= mn ? lam0 : mn;  // max(lambda0, min(-y)), simplex.py:250
   s.cmd.lam = s.lam0;
   s.cmd.phase = PH_SCAN;
+  s.cmd.hist = s.hist_ok && s.start == 4 && !s.lam0_given && s.fixing;
+  s.lam_hist = NAN;
 }
 
 // tot: 0 value, 1 #(v>0), 2 #(v==0)   (simplex.py:207-215, 256-294)
@@ -630,10 +634,17 @@ DEVI void s_after_scan(SpxState& s, const double* tot, const double* loc, double
   }
   if (deriv <= 0) { s.cmd.phase = PH_SNAP; return; }
   const double step = -(value - s.r) / deriv;
-  const double next = lam + step;
+  double next = lam + step;
   if (fabs(step) < s.tau || next == lam) { s_finish(s, next); return; }
   if (isfinite(s.lo) && isfinite(s.hi)) {
     if (s.hi - s.lo < s.tau * fmax(fabs(s.hi), fabs(s.lo))) { s_finish(s, next); return; }
+  }
+  // start "auto": both the Newton iterate and the histogram bound lie above
+  // the root when phi > r; take the smaller (the first scan only)
+  if (s.cmd.hist) {
+    if (value > s.r && isfinite(s.lam_hist) && s.lam_hist < next && s.lam_hist > s.lo) next = s.lam_hist;
+    s.cmd.hist = 0;
+    s.lam_hist = NAN;
   }
   s.cmd.lam = next;
   s.iterations += 1;

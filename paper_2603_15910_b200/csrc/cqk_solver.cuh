@@ -61,6 +61,8 @@ struct Cmd {
   int32_t check_lu; // this (first) scan also validates l and u
   int32_t live_lo;  // a lower-fixed element may still be physically present
   int32_t live_hi;  // ... an upper-fixed one
+  int32_t hist;     // simplex: this scan also histograms t > 0 (start "auto")
+  int32_t pad_;
 };
 
 // Master-side solver state (SolveState, newton.py:70-90, plus counters).

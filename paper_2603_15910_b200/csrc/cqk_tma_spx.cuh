@@ -21,6 +21,18 @@ static_assert(kStagesY >= 2, "pipeline needs at least two stages");
 template <bool L1>
 DEVI double spx_wv(double y) { return L1 ? fabs(y) : y; }
 
+// Start "auto": the first scan (at the tight start lam0 = r - max w, an upper
+// bound of the root) also counts its positive t = w + lam0 in kHistB buckets of
+// width r / kHistB (integer counts: order-independent, hence deterministic).
+// With one bucket of margin for rounding, an element in bucket j has
+// t >= (j - 1) r / kHistB, so phi(lam0 - k r / kHistB) >= (r / kHistB)
+// sum_{j > k} c_j (j - 1 - k): the largest k making that >= r gives an upper
+// bound of the root within about a bucket of it.  The master takes it in
+// place of the first Newton step when smaller, which skips the linear
+// shrinking phase of Newton-from-above on spread data (u01: 8 grid epochs -> 4).
+constexpr int kHistB = 1024;
+static_assert(kHistB == 2 * kTmaThreads, "hist_bound: two buckets per thread");
+static_assert((kHistB & (kHistB - 1)) == 0, "power of two");
 // Tail mode: once the physical working set fits one SM's shared memory, the
 // master CTA gathers it (from the warp sub-segments, whose counts every warp
 // published in its last compacting pass, or from y itself) and runs the
@@ -76,10 +88,10 @@ DEVI int tail_gather(const SpxParams<double>& p, bool in_scratch, double* V, int
 }
 
 // MODE 0: sum / max of w; 1: phi scan (+ compaction); 2: max(-w) snap.
-template <bool L1, int MODE, bool FULL>
+template <bool L1, int MODE, bool FULL, bool HIST = false>
 DEVI void spx_tile(const WTile& wt, const double* src, bool scratch, double lam, bool fix,
                    double fhi, double (&acc)[kMaxK], int (&cnt)[2], bool (&keep)[kEptY],
-                   double (&Wv)[kEptY]) {
+                   double (&Wv)[kEptY], int* s_hist, double hscale) {
   const int lane = threadIdx.x & 31;
   double Y[kEptY];
   tile_load<FULL, kTileY>(wt, 0, src, Y);
@@ -103,6 +115,7 @@ DEVI void spx_tile(const WTile& wt, const double* src, bool scratch, double lam,
       acc[0] += (kp && pos) ? v : 0.0;
       cnt[0] += kp && pos;
       cnt[1] += kp && v == 0.0;
+      if (HIST && kp && pos) atomicAdd(&s_hist[min(kHistB - 1, (int)(v * hscale))], 1);
     } else {
       acc[0] = kp ? fmax(acc[0], -w) : acc[0];
       cnt[0] += kp;
@@ -112,7 +125,8 @@ DEVI void spx_tile(const WTile& wt, const double* src, bool scratch, double lam,
 
 template <bool L1, int MODE>
 DEVI int64_t t_spx(const SpxParams<double>& p, const Cmd& c, bool fix, const TileWalk& tw,
-                   int64_t m_w, bool compact, TPipe& pp, double (&acc)[kMaxK]) {
+                   int64_t m_w, bool compact, TPipe& pp, double (&acc)[kMaxK],
+                   int* s_hist = nullptr, double hscale = 0.0) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned ltm = (1u << lane) - 1u;
   const bool scratch = tw.nslots >= 0;
@@ -125,8 +139,17 @@ DEVI int64_t t_spx(const SpxParams<double>& p, const Cmd& c, bool fix, const Til
   consume<kStagesY, kTileY, kTileY>(tw, pp, m_w, [&](const WTile& wt) {
     bool keep[kEptY];
     double Wv[kEptY];
-    if (wt.wcnt == kSegY) spx_tile<L1, MODE, true>(wt, src, scratch, lam, fix, fhi, acc, cnt, keep, Wv);
-    else spx_tile<L1, MODE, false>(wt, src, scratch, lam, fix, fhi, acc, cnt, keep, Wv);
+    // the histogram (start "auto") rides on one scan per solve: its own instance
+    if (MODE == 1 && s_hist) {
+      if (wt.wcnt == kSegY)
+        spx_tile<L1, MODE, true, true>(wt, src, scratch, lam, fix, fhi, acc, cnt, keep, Wv, s_hist, hscale);
+      else
+        spx_tile<L1, MODE, false, true>(wt, src, scratch, lam, fix, fhi, acc, cnt, keep, Wv, s_hist, hscale);
+    } else if (wt.wcnt == kSegY) {
+      spx_tile<L1, MODE, true>(wt, src, scratch, lam, fix, fhi, acc, cnt, keep, Wv, s_hist, hscale);
+    } else {
+      spx_tile<L1, MODE, false>(wt, src, scratch, lam, fix, fhi, acc, cnt, keep, Wv, s_hist, hscale);
+    }
     bool any_keep = false;
 #pragma unroll
     for (int j = 0; j < kEptY; ++j) any_keep = any_keep || keep[j];
@@ -181,6 +204,45 @@ DEVI void spx_final_tile(const SpxParams<double>& p, const WTile& wt, bool copy,
   }
 }
 
+// Master CTA: sum the per-CTA bucket rows (integers, any order), suffix-scan
+// c_j and j c_j from the top, and take the largest k whose lower bound
+// (r / kHistB) sum_{j > k} c_j (j - 1 - k) reaches r.  Two buckets per
+// thread (kHistB == 2 * blockDim.x); all sums are exact integers.
+DEVI void hist_bound(const SpxParams<double>& p, double lam0, double r, int* s_hist, SpxState& st) {
+  __shared__ long long s_w1[32], s_w2[32];
+  __shared__ int s_kbest;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = blockDim.x >> 5;
+  const int G = (int)gridDim.x;
+  // thread t owns buckets kb = kHistB - 2 - 2t + {1, 0}: idx' = 2t, 2t+1 from the top
+  const int k_hi = kHistB - 1 - 2 * t, k_lo = k_hi - 1;
+  const long long c_hi = __ldcg(p.hist + k_hi), c_lo = __ldcg(p.hist + k_lo);
+  (void)G;
+  // inclusive scans (from the top) of c and j*c over this thread's pair
+  long long a1 = c_hi + c_lo, a2 = (long long)k_hi * c_hi + (long long)k_lo * c_lo;
+  long long i1 = a1, i2 = a2;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long v1 = __shfl_up_sync(0xffffffffu, i1, o), v2 = __shfl_up_sync(0xffffffffu, i2, o);
+    if (lane >= o) { i1 += v1; i2 += v2; }
+  }
+  if (lane == 31) { s_w1[warp] = i1; s_w2[warp] = i2; }
+  if (t == 0) s_kbest = -1;
+  __syncthreads();
+  long long b1 = 0, b2 = 0;
+  for (int w = 0; w < warp && w < nw; ++w) { b1 += s_w1[w]; b2 += s_w2[w]; }
+  // sums over j > k: for k_hi everything before this thread; for k_lo add c_hi
+  const long long S1_hi = b1 + i1 - a1, S2_hi = b2 + i2 - a2;
+  const long long S1_lo = S1_hi + c_hi, S2_lo = S2_hi + (long long)k_hi * c_hi;
+  const double bw = r / kHistB, need = r * (1.0 + 1e-12);
+  int kb = -1;
+  if (k_hi < kHistB - 1 && bw * (double)(S2_hi - (long long)(1 + k_hi) * S1_hi) >= need) kb = k_hi;
+  else if (bw * (double)(S2_lo - (long long)(1 + k_lo) * S1_lo) >= need) kb = k_lo;
+  if (kb >= 0) atomicMax(&s_kbest, kb);  // an integer max: order-independent
+  __syncthreads();
+  if (t == 0) st.lam_hist = s_kbest >= 0 ? lam0 - (double)s_kbest * bw : NAN;
+  (void)s_hist;
+}
+
 template <bool L1>
 __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<double> p) {
   extern __shared__ __align__(128) unsigned char s_dyn[];
@@ -195,6 +257,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
   __shared__ int s_spec, s_spec_scr;  // next-pass tiles issued across the grid step
   __shared__ int s_tail;              // master: finish the iterations in this CTA
   __shared__ int s_scan[kConsW + 1];
+  __shared__ int s_hist[kHistB];      // start "auto": first-scan bucket counts
+  __shared__ double s_lam_hist;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool producer = warp == kConsW;
   const bool prod_lane = producer && lane == 0;
@@ -219,6 +283,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
       load_l2(&s_cmd, &p.st->cmd);
     }
   }
+  for (int k = threadIdx.x; k < kHistB; k += blockDim.x) s_hist[k] = 0;
   __syncthreads();
   const bool fix = p.st->fixing != 0;
   const int64_t ntiles = (p.n + kTileY - 1) / kTileY;
@@ -279,7 +344,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
       if (prod_lane) {
         produce<1, kStagesY, kTileY, kTileY>(wsrc, work, pp, spec);
       } else if (!producer) {
-        const int64_t mm = t_spx<L1, 1>(p, c, fix, work, m_w, compact, pp, acc);
+        const bool hist = c.hist && p.hist;
+        const int64_t mm = t_spx<L1, 1>(p, c, fix, work, m_w, compact, pp, acc,
+                                        hist ? s_hist : nullptr, (double)kHistB / p.st->r);
         if (compact) {
           m_w = mm;
           if (lane == 0) {
@@ -307,7 +374,18 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
       }
       speculate();
     }
+    if (mode == 1 && c.hist && p.hist) {
+      // this CTA's nonzero counts into the global histogram (integer atomics:
+      // order-independent); each CTA starts at its own offset so the 148
+      // CTAs' atomics on a dense histogram do not queue on the same address
+      const int rot = (int)((blockIdx.x * 7u) % kHistB);
+      for (int i = threadIdx.x; i < kHistB; i += blockDim.x) {
+        const int k = (i + rot) & (kHistB - 1);
+        if (s_hist[k]) atomicAdd(&p.hist[k], s_hist[k]);
+      }
+    }
     const bool is_master = grid_step<3>(p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch);
+    if (is_master && mode == 1 && c.hist && p.hist) hist_bound(p, c.lam, s_st.r, s_hist, s_st);
     if (threadIdx.x == 0) {
       if (is_master) {
         tl_record(p.sync, epoch, c.phase, mode == 0 ? p.n : s_st.phys_count, s_st.cmd.compact);

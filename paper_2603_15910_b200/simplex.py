@@ -131,7 +131,7 @@ def _prep(y):
     return np.ascontiguousarray(y, dtype=np.float64), y.dtype, False
 
 
-def _project(y, r, opts, lambda0, trace, l1, start="tight", xbar=None, sharpened=None):
+def _project(y, r, opts, lambda0, trace, l1, start="auto", xbar=None, sharpened=None):
     if opts is None:
         opts = SolverOptions()
     yv, dt, dev = _prep(y)
@@ -199,13 +199,17 @@ def _sparse(x, dev):
 
 
 def newton_project_simplex(y, r, opts=None, xbar=None, output="dense", sharpened=False,
-                           lambda0=None, trace=None, start="tight"):
+                           lambda0=None, trace=None, start="auto"):
     """Streamlined Newton projection of y onto the level-r simplex (simplex.py:218-308).
 
-    start (B200 extension, used when lambda0 is None): "tight" =
-    min((r - sum y)/n, r - max y), "formula" = (r - sum y)/n, "alg2" = the
+    start (B200 extension, used when lambda0 is None): "auto" (default) =
+    the tight start with the first Newton step replaced by a histogram upper
+    bound of the root when smaller (fewest passes; the iterate count is this
+    route's own); "tight" = min((r - sum y)/n, r - max y) exactly as the
+    reference's `lambda0=` route would iterate from it; "formula" =
+    (r - sum y)/n (the reference's `lambda0=` formula route); "alg2" = the
     chunked Algorithm-2 initializer (par_simplex_init) with Algorithm 4 on its
-    free set."""
+    free set.  All routes return the same projection."""
     if not r > 0:
         raise DomainError("r", None, "simplex level r must be positive")
     x, res = _project(y, r, opts, lambda0, trace, l1=False, start=start, xbar=xbar,
@@ -220,7 +224,7 @@ def newton_project_simplex(y, r, opts=None, xbar=None, output="dense", sharpened
                         fixed_count=int(res.fixed_count), sparse=sparse, stats=res.stats())
 
 
-def project_l1(y, r, opts=None, output="dense", xbar=None, start="tight"):
+def project_l1(y, r, opts=None, output="dense", xbar=None, start="auto"):
     """Project y onto the l1 ball of radius r (simplex.py:311-333)."""
     if not r > 0:
         raise DomainError("r", None, "l1 radius r must be positive")
@@ -237,7 +241,7 @@ def project_l1(y, r, opts=None, output="dense", xbar=None, start="tight"):
     return x
 
 
-def project_l1_outcome(y, r, opts=None, start="tight"):
+def project_l1_outcome(y, r, opts=None, start="auto"):
     """project_l1 with the solver statistics (B200 extension)."""
     x, res = _project(y, r, opts, None, None, l1=True, start=start)
     inside = int(res.iterations) < 0

@@ -219,6 +219,9 @@ def test_simplex_random_vs_oracle():
             ref = O.newton_project_simplex(y, r, lam0=lam0)
             assert close(out.lam, ref["lam"]), (out.lam, ref["lam"])
             assert out.iterations == ref["iterations"], (start, out.iterations, ref["iterations"])
+        auto = p.newton_project_simplex(y, r)
+        assert close(auto.lam, ref["lam"]), (auto.lam, ref["lam"])
+        assert float(np.abs(auto.x - ref["x"]).max()) <= TOL * max(1.0, float(np.abs(y).max()))
         assert float(np.abs(out.x - ref["x"]).max()) <= TOL * max(1.0, float(np.abs(y).max()))
         lam_star = O.exact_simplex_lambda(y, r)
         assert abs(out.lam - lam_star) <= 1e-10 * max(1.0, abs(lam_star))

@@ -78,10 +78,14 @@ def test_simplex_and_l1_sizes_tail_mode(n, fam):
     y = rng.uniform(0, 1, n) if fam == "u01" else rng.normal(0, 1, n)
     lam0 = min((1.0 - float(O.pairwise_sum(y))) / n, 1.0 - float(y.max()))
     ref = O.newton_project_simplex(y, 1.0, lam0=lam0)
-    out = p.newton_project_simplex(y, 1.0)
+    out = p.newton_project_simplex(y, 1.0, start="tight")
     assert close(out.lam, ref["lam"]), (n, fam, out.lam, ref["lam"])
     assert np.abs(out.x - ref["x"]).max() <= TOL
     assert out.iterations == ref["iterations"]
+    auto = p.newton_project_simplex(y, 1.0)  # histogram-refined start: same projection
+    assert close(auto.lam, ref["lam"]), (n, fam, auto.lam, ref["lam"])
+    assert np.abs(auto.x - ref["x"]).max() <= TOL
+    assert auto.iterations <= ref["iterations"]
     x1 = p.project_l1(y - 0.5, 1.0)
     r1 = O.project_l1(y - 0.5, 1.0)
     assert np.abs(x1 - r1["x"]).max() <= TOL

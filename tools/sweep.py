@@ -57,7 +57,7 @@ for w in which:
         res[w] = cqk("cqk-weakly-correlated", 10**8, jac=True)
     elif w.split("_")[0] in ("spx", "l1") and not w.startswith("spx1e6"):
         n = 10**8
-        start = w.split("_")[1] if "_" in w else "tight"
+        start = w.split("_")[1] if "_" in w else "auto"
         y = torch.from_numpy(P.gen_simplex_y("simplex-n01", n, 1)).cuda()
         if w.startswith("spx"):
             ms, out = timeit(lambda: P.newton_project_simplex(y, 1.0, start=start))
@@ -71,8 +71,9 @@ for w in which:
                   "frac": st["bytes_model"] / st["device_ms"] / 1e6 / PEAK, "evals": ev,
                   "elem_per_s": n / ms * 1e3, "bytes_per_elem": st["bytes_model"] / n}
     elif w.startswith("spx1e6"):
-        start = w.split("_")[1] if "_" in w else "tight"
-        fam = "simplex-n01" if "n01" in w else "simplex-u01"
+        parts = w.split("_")[1:]
+        start = next((x for x in parts if x in ("tight", "formula", "alg2", "auto")), "auto")
+        fam = "simplex-n01" if "n01" in parts else "simplex-u01"
         y = torch.from_numpy(P.gen_simplex_y(fam, 10**6, 1)).cuda()
         ms, out = timeit(lambda: P.newton_project_simplex(y, 1.0, start=start), reps=50)
         res[w] = {"ms": ms, "kernel_ms": out.stats["device_ms"], "evals": out.phi_evals,

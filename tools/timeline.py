@@ -23,7 +23,9 @@ if kind in ("weak", "corr", "unc", "jac"):
 else:
     fam = "simplex-u01" if kind.endswith("u01") else "simplex-n01"
     y = torch.from_numpy(P.gen_simplex_y(fam, n, 1)).cuda()
-    f = (lambda: P.newton_project_simplex(y, 1.0)) if kind.startswith("spx") else (lambda: P.simplex.project_l1_outcome(y, 1.0))
+    start = os.environ.get("CQK_START", "auto")
+    f = ((lambda: P.newton_project_simplex(y, 1.0, start=start)) if kind.startswith("spx")
+         else (lambda: P.simplex.project_l1_outcome(y, 1.0, start=start)))
     B = {0: 8, 1: 8, 6: 8}
     fin = 16
 for _ in range(3):
