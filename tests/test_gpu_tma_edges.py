@@ -103,3 +103,40 @@ def test_misaligned_device_input_rejected():
         p.solve_cqk(p.CqkInstance(*mis, r=r))
     ok = p.solve_cqk(p.CqkInstance(*[t.clone() for t in mis], r=r))
     assert ok.status is p.Status.SOLVED
+
+
+@pytest.mark.parametrize("case", ["d_nonpos", "a_nan", "b_inf", "l_nan", "u_nan", "l_gt_u",
+                                  "l_posinf", "u_neginf", "two_faults", "tail_elem"])
+def test_validation_first_offender(case, engine):
+    """validate() inside the solve (pass 0 for d, a, b; the first scan for l, u)
+    reports the reference's first failing check and index on both engines."""
+    p = P()
+    n = 300001
+    d, a, b, l, u, r = inst_arrays(77, n)
+    if case == "d_nonpos":
+        d[123457] = 0.0
+    elif case == "a_nan":
+        a[200000] = np.nan
+    elif case == "b_inf":
+        b[5] = np.inf
+    elif case == "l_nan":
+        l[299999] = np.nan
+    elif case == "u_nan":
+        u[150001] = np.nan
+    elif case == "l_gt_u":
+        l[100001] = u[100001] + 1.0
+    elif case == "l_posinf":
+        l[70000] = np.inf
+        u[70000] = np.inf
+    elif case == "u_neginf":
+        l[80000] = -np.inf
+        u[80000] = -np.inf
+    elif case == "two_faults":  # a later check at a smaller index must not win
+        l[1000] = u[1000] + 1.0
+        d[250000] = -1.0
+    elif case == "tail_elem":
+        b[n - 1] = -2.0
+    ref = O.validate(d, a, b, l, u, r)
+    with pytest.raises(p.DomainError) as e:
+        p.solve_cqk(p.CqkInstance(d=d, a=a, b=b, l=l, u=u, r=r))
+    assert (e.value.field, e.value.index) == tuple(ref), (case, e.value.field, e.value.index, ref)
