@@ -71,6 +71,7 @@ cudaError_t set_prefetch() {
   int tf = 0;
   if (const char* e = getenv("CQK_TMA_FLAGS")) tf = atoi(e);
   cudaError_t err = cudaMemcpyToSymbol(c_tma_flags, &tf, sizeof tf);
+  err = err ? err : cudaMemcpyToSymbol(c_tma_flags_w, &tf, sizeof tf);
   return err ? err : cudaMemcpyToSymbol(c_prefetch, pf, sizeof pf);
 }
 

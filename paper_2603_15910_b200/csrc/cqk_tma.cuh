@@ -60,7 +60,15 @@ DEVI void mbar_arrive1(unsigned long long* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 // Shared-window (u32) forms: the addresses are converted once per kernel.
+__constant__ int c_tma_flags_w;  // bit 1 of CQK_TMA_FLAGS: spin with test_wait
 DEVI void mbar_wait_s(unsigned bar, unsigned phase) {
+  if (c_tma_flags_w & 2) {
+    asm volatile(
+        "{\n.reg .pred p;\nTWAIT_%=:\n"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra TWAIT_%=;\n}" ::"r"(bar), "r"(phase) : "memory");
+    return;
+  }
   asm volatile(
       "{\n.reg .pred p;\nWAIT_%=:\n"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
