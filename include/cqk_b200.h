@@ -101,9 +101,12 @@ int cqk_destroy(cqk_handle *h);
    accepted); NULL = the handle's own non-blocking stream. */
 int cqk_set_stream(cqk_handle *h, void *stream);
 int cqk_device_info(cqk_handle *h, int32_t *sm_count, int32_t *ctas, int32_t *threads);
-/* Per-pass device timeline of the last persistent solve: rows of 10 int64
+/* Per-pass device timeline of the last persistent solve: rows of 20 int64
    {phase, elements streamed, compacted, t_decide, t_all_arrived, t_released,
-   t_cta1_arrived, t_cta1_woke, last_cta, t_last_arrived} (globaltimer ns);
+   t_cta1_arrived, t_cta1_woke, last_cta, t_last_arrived, then for the TMA CQK kernel
+   CTA 1 pass start, consumer warp 0 done, block-reduced, producer done, last consumer
+   warp done, last warp at the block reduction, then the master's grid reduction:
+   started, rows loaded, warps combined, folded} (globaltimer ns);
    row 0 = kernel start, row e =
    grid epoch e (phase -1 start, 0 lambda0/init, 1 scan, 2 breakpoint, 6 snap).
    Returns rows copied. */
@@ -205,7 +208,7 @@ int cqk_comm_connect_local(cqk_handle *h, cqk_handle *const *ranks, int world);
 int cqk_reserve(cqk_handle *h, int64_t n);
 /* Cap the persistent grid (CTAs); 0 = the full device.  Lets several ranks
    share one GPU (virtual ranks) or leave SMs for other work. */
-/* CQK solve engine: 0 auto (TMA pipeline from 8e6 elements per rank,
+/* CQK solve engine: 0 auto (TMA pipeline from 1e6 elements per rank,
    CQK_TMA_MIN_N), 1 TMA pipeline, 2 warp-segment kernel.  Results agree to
    rounding (summation order differs). */
 /* Pre-allocate the host-mode staging of an n-element shard (collective solves

@@ -232,7 +232,7 @@ class Handle:
 
     def timeline(self, rows=64):
         """Per-pass device timeline of the last persistent solve (see cqk_b200.h)."""
-        out = np.zeros((rows, 10), dtype=np.int64)
+        out = np.zeros((rows, 20), dtype=np.int64)
         got = self.lib.cqk_get_timeline(self.ptr, out.ctypes.data, int(rows))
         return out[: max(got, 0)]
 

@@ -87,7 +87,7 @@ struct cqk_handle {
   int grid_tma_spx = 0, grid_tma_l1 = 0;    // TMA-pipelined simplex / l1 kernels
   bool use_tma = true;                     // CQK_ENGINE=seg selects the warp-segment kernel
   int engine = 0;                          // cqk_set_engine: 0 auto, 1 TMA, 2 warp segments
-  int64_t tma_min_n = 8000000;             // auto: CQK solves of >= this many elements per rank
+  int64_t tma_min_n = 1000000;             // auto: CQK solves of >= this many elements per rank
   unsigned* sync = nullptr;  // [0] arrive, [1] gen, [2] error
   void* state = nullptr;     // CqkState / SpxState
   double* partials = nullptr;

@@ -125,6 +125,7 @@ DEVI bool grid_step(double* partials, const double* s_cta, const int (&ops)[K],
   }
   __syncthreads();
   if (*(volatile int*)s_abort) return false;
+  if (threadIdx.x == 0) tl_mark(sy, epoch, 16);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double acc[K];
 #pragma unroll
@@ -137,23 +138,31 @@ DEVI bool grid_step(double* partials, const double* s_cta, const int (&ops)[K],
     for (int k = 0; k < K; ++k)
       acc[k] = ops[k] == OP_SUM ? acc[k] + v[k] : ops[k] == OP_MIN ? fmin(acc[k], v[k]) : fmax(acc[k], v[k]);
   }
+  if (threadIdx.x == 0) tl_mark(sy, epoch, 17);
+  // only the warps that hold rows combine (identities elsewhere; this also
+  // keeps a TMA producer warp out of the shuffles, see block_reduce)
+  const int nw = min((int)(blockDim.x >> 5), (int)((gridDim.x + 31) >> 5));
+  if (warp < nw) {
 #pragma unroll
-  for (int k = 0; k < K; ++k) {
-    const double v = ops[k] == OP_SUM ? warp_sum(acc[k]) : ops[k] == OP_MIN ? warp_min(acc[k])
-                                                                           : warp_max(acc[k]);
-    if (lane == 0) s_red[warp][k] = v;
+    for (int k = 0; k < K; ++k) {
+      const double v = ops[k] == OP_SUM ? warp_sum(acc[k]) : ops[k] == OP_MIN ? warp_min(acc[k])
+                                                                             : warp_max(acc[k]);
+      if (lane == 0) s_red[warp][k] = v;
+    }
   }
+  if (threadIdx.x == 0) tl_mark(sy, epoch, 18);
   __syncthreads();
   if (threadIdx.x < K) {
     const int k = threadIdx.x;
     double v = s_red[0][k];
-    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+    for (int w = 1; w < nw; ++w) {
       const double o = s_red[w][k];
       v = ops[k] == OP_SUM ? v + o : ops[k] == OP_MIN ? fmin(v, o) : fmax(v, o);
     }
     s_tot[k] = v;
   }
   __syncthreads();
+  if (threadIdx.x == 0) tl_mark(sy, epoch, 19);
   return !*(volatile int*)s_abort;
 }
 

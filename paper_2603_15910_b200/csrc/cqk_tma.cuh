@@ -605,6 +605,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
   __shared__ int s_nsl_new;  // ... being formed by a compacting pass
   __shared__ int s_spec;     // tiles of the next pass issued across the grid step
   __shared__ int s_spec_scr; // ... and whether they came from scratch
+  __shared__ unsigned long long s_probe_last;  // timeline probe: last consumer warp done
+  __shared__ unsigned long long s_probe_pre;   // ... last warp (incl. producer) at the reduction
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool producer = warp == kConsW;
   const bool master = blockIdx.x == 0;
@@ -626,6 +628,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
     s_nsl_new = 0;
     s_spec = 0;
     s_spec_scr = 0;
+    s_probe_last = 0;
+    s_probe_pre = 0;
     if (master) {
       s_st = *p.st;  // host-initialised before the launch
       s_cmd = s_st.cmd;
@@ -654,9 +658,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
     s_spec = (c_tma_flags & 1) ? 0 : produce<5>(in_scratch ? src_scr : src_orig, nw, pp, 0, kStagesC);
     s_spec_scr = in_scratch;
   };
+  const bool probe = blockIdx.x == 1 && p.sync.timeline;  // timeline detail columns 10-15
   for (unsigned epoch = 1;; ++epoch) {
     const Cmd c = s_cmd;
     const int spec = s_spec;
+    if (probe && threadIdx.x == 0) tl_mark(p.sync, epoch, 10);
     if (c.phase == PH_DONE || s_abort) {
       if (!producer) drain(pp, spec);  // never leave bulk copies in flight
       break;
@@ -698,7 +704,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
       double a15[15];
 #pragma unroll
       for (int k = 0; k < 15; ++k) a15[k] = acc[k];
-      block_reduce<15>(a15, ops, s_red, s_tot);
+      block_reduce<15, kConsW>(a15, ops, s_red, s_tot);
       if (prod_lane) speculate();
       is_master = grid_step<15>(p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch);
       if (is_master && threadIdx.x == 0) {
@@ -715,7 +721,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
       int ops[kMaxK];
 #pragma unroll
       for (int k = 0; k < kMaxK; ++k) ops[k] = k < kCheckLuSlot ? OP_SUM : OP_MIN;
-      block_reduce<kMaxK>(acc, ops, s_red, s_tot);
+      block_reduce<kMaxK, kConsW>(acc, ops, s_red, s_tot);
       if (prod_lane) speculate();
       is_master = grid_step<kMaxK>(p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch);
       if (is_master && threadIdx.x == 0) {
@@ -739,8 +745,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
       const bool compact = FIX && c.compact;
       if (prod_lane) {
         produce<5>(wsrc, work, pp, spec);
+        if (probe) tl_mark(p.sync, epoch, 13);
       } else if (!producer) {
         const int64_t mm = t_scan<FIX, false>(p, c, work, m_w, wsrc, compact, pp, acc);
+        if (probe && threadIdx.x == 0) tl_mark(p.sync, epoch, 11);
+        if (probe && lane == 0) atomicMax(&s_probe_last, (unsigned long long)globaltimer());
         if (compact) {
           m_w = mm;
           if (lane == 0) atomicMax(&s_nsl_new, (int)((mm + kSeg - 1) / kSeg));
@@ -752,7 +761,17 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
       double aK[K];
 #pragma unroll
       for (int k = 0; k < K; ++k) { ops[k] = OP_SUM; aK[k] = acc[k]; }
-      block_reduce<K>(aK, ops, s_red, s_tot);  // (its barrier orders the atomicMax above)
+      if (probe && lane == 0) atomicMax(&s_probe_pre, (unsigned long long)globaltimer());
+      block_reduce<K, kConsW>(aK, ops, s_red, s_tot);  // (its barrier orders the atomicMax above)
+      if (probe && threadIdx.x == 0) {
+        tl_mark(p.sync, epoch, 12);
+        if (p.sync.timeline && epoch < (unsigned)kTimelineCap) {
+          p.sync.timeline[kTimelineCols * epoch + 14] = (long long)s_probe_last;
+          p.sync.timeline[kTimelineCols * epoch + 15] = (long long)s_probe_pre;
+        }
+        s_probe_last = 0;
+        s_probe_pre = 0;
+      }
       if (prod_lane) {
         if (compact) {  // nobody else reads s_nslots before the next epoch
           s_nslots = s_nsl_new;
@@ -775,7 +794,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
       else if (!producer) t_bp(p, c, FIX, work, m_w, wsrc, pp, acc);
       int ops[2] = {c.right ? OP_MIN : OP_MAX, OP_SUM};
       double a2[2] = {acc[0], acc[1]};
-      block_reduce<2>(a2, ops, s_red, s_tot);
+      block_reduce<2, kConsW>(a2, ops, s_red, s_tot);
       if (prod_lane) speculate();
       is_master = grid_step<2>(p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch);
       if (is_master && threadIdx.x == 0) {

@@ -366,7 +366,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
       break;
     }
     double a3[3] = {acc[0], acc[1], acc[2]};
-    block_reduce<3>(a3, ops, s_red, s_tot);  // (its barrier orders the atomicMax above)
+    block_reduce<3, kConsW>(a3, ops, s_red, s_tot);  // (its barrier orders the atomicMax above)
     if (prod_lane) {
       if (mode == 1 && fix && c.compact) {  // nobody else reads s_nslots before the next epoch
         s_nslots = s_nsl_new;
@@ -443,7 +443,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
         a3[1] = (double)n0;
         a3[2] = (double)n1;
         int tops[3] = {scan ? OP_SUM : OP_MAX, OP_SUM, OP_SUM};
-        block_reduce<3>(a3, tops, s_red, s_tot);
+        block_reduce<3>(a3, tops, s_red, s_tot);  // all 16 warps hold tail elements
         if (threadIdx.x == 0) {
           tl_record(p.sync, epoch + it, tc.phase, m, 0);
           if (scan) s_after_scan(s_st, s_tot, s_tot, p.trace);

@@ -41,6 +41,8 @@ last = 0
 for k in range(1, len(tl)):
     ph, el, comp, t = (int(v) for v in tl[k][:4])
     t_all, t_rel, t_arr1, t_wake1, last_cta, t_last = (int(v) for v in tl[k][4:10])
+    t_start, t_cons, t_red, t_prod, t_lastw, t_pre = (int(v) for v in tl[k][10:16])
+    m_start, m_load, m_shfl, m_fold = (int(v) for v in tl[k][16:20])
     if t == 0 or t < prev:
         break
     dt = (t - prev) / 1e3
@@ -55,7 +57,19 @@ for k in range(1, len(tl)):
                  "reduced": round((t - t_all) / 1e3, 2) if t_all else None,
                  "released": round((t_rel - t) / 1e3, 2) if t_rel else None,
                  "last_cta": last_cta,
-                 "last_arrived": round((t_last - prev_rel) / 1e3, 2) if t_last else None})
+                 "last_arrived": round((t_last - prev_rel) / 1e3, 2) if t_last else None,
+                 # CTA 1 (TMA kernels): pass start / consumers done / reduced / producer done
+                 "c1_start": round((t_start - prev_rel) / 1e3, 2) if t_start and prev_rel else None,
+                 "c1_cons": round((t_cons - prev_rel) / 1e3, 2) if t_cons and prev_rel else None,
+                 "c1_red": round((t_red - prev_rel) / 1e3, 2) if t_red and prev_rel else None,
+                 "c1_prod": round((t_prod - prev_rel) / 1e3, 2) if t_prod and prev_rel else None,
+                 "c1_lastwarp": round((t_lastw - prev_rel) / 1e3, 2) if t_lastw and prev_rel else None,
+                 "c1_last_tid": t_lastw & 511,
+                 "m_start": round((m_start - t_all) / 1e3, 2) if m_start and t_all else None,
+                 "m_load": round((m_load - t_all) / 1e3, 2) if m_load and t_all else None,
+                 "m_shfl": round((m_shfl - t_all) / 1e3, 2) if m_shfl and t_all else None,
+                 "m_fold": round((m_fold - t_all) / 1e3, 2) if m_fold and t_all else None,
+                 "c1_pre": round((t_pre - prev_rel) / 1e3, 2) if t_pre and prev_rel else None})
     prev_rel = t_rel
     prev = t
     last = t
