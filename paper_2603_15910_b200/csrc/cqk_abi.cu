@@ -111,8 +111,8 @@ struct cqk_handle {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int trace_len = 0;
   int grid_limit = 0;                 // 0: full device (virtual ranks share a GPU)
-  unsigned* err_host = nullptr;       // pinned: barrier-timeout flag readback
-  void* host_state = nullptr;         // pinned: solver state in / out (no pageable copies)
+  void* host_state = nullptr;         // pinned + mapped: the kernels' final state (and Alg2Out)
+  void* host_state_dev = nullptr;     // ... its device alias
   // multi-GPU communicator (one rank per GPU; mailboxes in device memory)
   int rank = 0, world = 1;
   double* mbox = nullptr;             // this rank's mailbox
@@ -192,8 +192,9 @@ int cqk_create(cqk_handle** out, int device) {
   e = e ? e : cudaMalloc(&h->out, sizeof(double) * kMaxK);
   e = e ? e : cudaMalloc(&h->wcnt, sizeof(int32_t) * kConsW * (h->sm_count + 8));
   e = e ? e : cudaMalloc(&h->hist, sizeof(int32_t) * kHistB * (h->sm_count + 8));
-  e = e ? e : cudaMallocHost(&h->err_host, 64);
-  e = e ? e : cudaMallocHost(&h->host_state, st_bytes);
+  e = e ? e : cudaMemset(h->hist, 0, sizeof(int32_t) * kHistB * (h->sm_count + 8));
+  e = e ? e : cudaHostAlloc(&h->host_state, st_bytes, cudaHostAllocMapped | cudaHostAllocPortable);
+  e = e ? e : cudaHostGetDevicePointer(&h->host_state_dev, h->host_state, 0);
   e = e ? e : set_prefetch();
   e = e ? e : cudaEventCreate(&h->ev0);
   e = e ? e : cudaEventCreate(&h->ev1);
@@ -235,7 +236,6 @@ int cqk_destroy(cqk_handle* h) {
     if (h->ring[k]) cudaFreeHost(h->ring[k]);
     if (h->ring_ev[k]) cudaEventDestroy(h->ring_ev[k]);
   }
-  if (h->err_host) cudaFreeHost(h->err_host);
   if (h->host_state) cudaFreeHost(h->host_state);
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
@@ -427,17 +427,16 @@ int finish_sync(cqk_handle* h) {
   return 0;
 }
 
-// The barrier-timeout flag travels back with the state (async, on the solve
-// stream: no legacy-stream or device-wide synchronisation, so several handles
-// can run concurrent persistent kernels, e.g. virtual ranks on one GPU).
-int check_timeout(cqk_handle* h) {
-  if (*h->err_host) {
-    *h->err_host = 0;
-    cudaMemsetAsync(h->sync, 0, 64, h->stream);
-    cudaStreamSynchronize(h->stream);
-    return set_err(CQK_E_TIMEOUT, "persistent kernel barrier timed out");
-  }
-  return 0;
+// The barrier-timeout flag travels back inside the published state (no copy
+// on the solve stream, no legacy-stream or device-wide synchronisation, so
+// several handles can run concurrent persistent kernels, e.g. virtual ranks on
+// one GPU).  A state still RUNNING was never published: the grid aborted.
+int check_timeout(cqk_handle* h, int32_t status, int32_t err) {
+  if (status != ST_RUNNING && !err) return 0;
+  cudaMemsetAsync(h->sync, 0, 64, h->stream);
+  cudaMemsetAsync(h->hist, 0, sizeof(int32_t) * kHistB, h->stream);  // may hold a partial scan
+  cudaStreamSynchronize(h->stream);
+  return set_err(CQK_E_TIMEOUT, "persistent kernel barrier timed out");
 }
 
 int map_status(int32_t st) {
@@ -656,10 +655,11 @@ static int solve_impl(cqk_handle* h, int mem, const double* d, const double* a, 
   // scratch: n per array (warp segments) or whole tile slots (TMA engine)
   const size_t per = ((size_t)(tma ? tma_scratch_elems(n) : n) * sizeof(double) + 255) / 256 * 256;
   if (fixing) CUDA_TRY(h->scratch.ensure(per * 5));
-  std::memcpy(h->host_state, &s, sizeof s);  // pinned staging: fully asynchronous
-  CUDA_TRY(cudaMemcpyAsync(h->state, h->host_state, sizeof s, cudaMemcpyHostToDevice, h->stream));
+  std::memcpy(h->host_state, &s, sizeof s);  // status RUNNING until the master publishes
   CqkParams<double> p;
   std::memset(&p, 0, sizeof p);
+  p.init = s;
+  p.out = (CqkState*)h->host_state_dev;
   p.d = dv[0]; p.a = dv[1]; p.b = dv[2]; p.l = dv[3]; p.u = dv[4]; p.xbar = xbar ? dv[5] : nullptr;
   if (fixing) {
     char* sb = (char*)h->scratch.p;
@@ -693,9 +693,6 @@ static int solve_impl(cqk_handle* h, int mem, const double* d, const double* a, 
   CUDA_TRY(cudaLaunchCooperativeKernel(fn, grid, tma ? kTmaThreads : kThreads, args,
                                        tma ? kSmemC : 0, h->stream));
   CUDA_TRY(cudaEventRecord(h->ev1, h->stream));
-  CUDA_TRY(cudaMemcpyAsync(h->host_state, h->state, sizeof s, cudaMemcpyDeviceToHost, h->stream));
-  CUDA_TRY(cudaMemcpyAsync(h->err_host, h->sync + 2, sizeof(unsigned), cudaMemcpyDeviceToHost,
-                           h->stream));
   if (mem == CQK_MEM_HOST && x && xo)
   {
     int rc_ = d2h(h, x, xo, sizeof(double) * n);
@@ -704,7 +701,7 @@ static int solve_impl(cqk_handle* h, int mem, const double* d, const double* a, 
   int rc = finish_sync(h);
   if (rc) return rc;
   std::memcpy(&s, h->host_state, sizeof s);
-  rc = check_timeout(h);
+  rc = check_timeout(h, s.status, s.err);
   if (rc) return rc;
   float ms = 0.f;
   cudaEventElapsedTime(&ms, h->ev0, h->ev1);
@@ -742,10 +739,11 @@ int launch_spx(cqk_handle* h, SpxState& s, const double* yv, int64_t n, double* 
   if (s.fixing)
     CUDA_TRY(h->scratch.ensure(((size_t)(tma ? tma_scratch_elems_y(n) : n) * sizeof(double) + 255) /
                                256 * 256));
-  std::memcpy(h->host_state, &s, sizeof s);  // pinned staging: fully asynchronous
-  CUDA_TRY(cudaMemcpyAsync(h->state, h->host_state, sizeof s, cudaMemcpyHostToDevice, h->stream));
+  std::memcpy(h->host_state, &s, sizeof s);  // status RUNNING until the master publishes
   SpxParams<double> p;
   std::memset(&p, 0, sizeof p);
+  p.init = s;
+  p.out = (SpxState*)h->host_state_dev;
   p.y = yv;
   p.sy = s.fixing ? (double*)h->scratch.p : nullptr;
   p.x = xo;
@@ -761,10 +759,7 @@ int launch_spx(cqk_handle* h, SpxState& s, const double* yv, int64_t n, double* 
   {
     const char* te = getenv("CQK_TAIL");
     p.wcnt = (tma && !sharded && !(te && te[0] == '0')) ? h->wcnt : nullptr;
-    if (tma && !sharded && s.hist_ok) {
-      p.hist = h->hist;
-      CUDA_TRY(cudaMemsetAsync(h->hist, 0, sizeof(int32_t) * kHistB, h->stream));
-    }
+    if (tma && !sharded && s.hist_ok) p.hist = h->hist;  // zero: the kernel clears it after use
   }
   void* args[] = {&p};
   int grid;
@@ -778,9 +773,6 @@ int launch_spx(cqk_handle* h, SpxState& s, const double* yv, int64_t n, double* 
   }
   CUDA_TRY(cudaLaunchCooperativeKernel(fn, grid, tma ? kTmaThreads : kThreads, args,
                                        tma ? kSmemC : 0, h->stream));
-  CUDA_TRY(cudaMemcpyAsync(h->host_state, h->state, sizeof s, cudaMemcpyDeviceToHost, h->stream));
-  CUDA_TRY(cudaMemcpyAsync(h->err_host, h->sync + 2, sizeof(unsigned), cudaMemcpyDeviceToHost,
-                           h->stream));
   return 0;
 }
 
@@ -997,7 +989,7 @@ int spx_common(cqk_handle* h, int mem, const double* y, int64_t n, int64_t n_tot
   int rc = finish_sync(h);
   if (rc) return rc;
   if (!(alg2 && s.iterations < 0)) std::memcpy(&s, h->host_state, sizeof s);
-  rc = check_timeout(h);
+  rc = check_timeout(h, s.status, s.err);
   if (rc) return rc;
   float ms = 0.f;
   cudaEventElapsedTime(&ms, h->ev0, h->ev1);

@@ -81,6 +81,15 @@ DEVI void load_l2(S* dst, const S* src) {
   for (int i = 0; i < (int)(sizeof(S) / 8); ++i) d[i] = __ldcg(s + i);
 }
 
+// The master's final state goes straight to mapped (pinned) host memory: the
+// host reads it after the stream synchronises -- no device-to-host copy is
+// queued behind the kernel.  The grid's barrier-timeout flag rides along.
+template <typename S>
+DEVI void publish_state(S* out, S& st, const GridSync& sy) {
+  st.err = *(volatile int*)sy.error;
+  *out = st;
+}
+
 // ------------------------------------------------------------ barrier
 // Fixed-master grid step: CTA 0 owns the solver state in shared memory for
 // the whole kernel.  Every CTA publishes partials[blockIdx.x][0..K) and
@@ -419,16 +428,16 @@ __global__ void __launch_bounds__(kThreads, 1) cqk_solve_kernel(CqkParams<T> p) 
     s_gen0 = ld_acquire(p.sync.gen);
     s_abort = 0;
     if (master) {
-      s_st = *p.st;  // host-initialised before the launch
+      s_st = p.init;  // host-initialised, passed by value
       s_cmd = s_st.cmd;
       tl_record(p.sync, 0, -1, p.n, 0);
     } else {
-      load_l2(&s_cmd, &p.st->cmd);
+      s_cmd = p.init.cmd;
     }
   }
   __syncthreads();
   const int has_xbar = p.xbar != nullptr;
-  const int check = p.st->check;  // immutable during the solve
+  const int check = p.init.check;  // immutable during the solve
   for (unsigned epoch = 1;; ++epoch) {
     const Cmd c = s_cmd;
     if (c.phase == PH_DONE || s_abort) break;
@@ -528,7 +537,7 @@ __global__ void __launch_bounds__(kThreads, 1) cqk_solve_kernel(CqkParams<T> p) 
     if (threadIdx.x == 0) {
       if (is_master) {
         const int ph = s_st.cmd.phase;
-        if (ph == PH_FINAL || ph == PH_DONE) *p.st = s_st;  // results for the host
+        if (ph == PH_FINAL || ph == PH_DONE) publish_state(p.out, s_st, p.sync);  // results for the host
         s_cmd = s_st.cmd;
         master_release(p.sync, s_gen0 + epoch, s_st.cmd, &p.st->cmd);
         tl_mark(p.sync, epoch, 5);
@@ -553,6 +562,7 @@ struct SpxState {
   int64_t local_active, fixed_local;  // this rank's share (multi-GPU)
   int64_t iterations, phi_evals, max_iter, elems_scan, elems_written;
   int32_t fixing, status, l1, lam0_given, trace_len, trace_cap, start, hist_ok;
+  int32_t err, pad_;  // err: barrier-timeout flag at the final write
   double compact_ratio;
   double lam_hist;  // start "auto": histogram upper bound of the root after the first scan (or NaN)
 };
@@ -569,7 +579,9 @@ struct SpxParams {
   GridSync sync;
   Exchange ex;
   int32_t* wcnt;  // [grid][consumer warps] scratch counts: enables the TMA kernel's tail mode
-  int32_t* hist;  // [kHistB] bucket counts of the first scan (start "auto"), zeroed by the host
+  int32_t* hist;  // [kHistB] bucket counts of the first scan (start "auto"); zero between solves
+  SpxState* out;  // mapped host memory: the final state for the host
+  SpxState init;  // the host-initialised state, by value (no H2D copy)
 };
 
 DEVI void s_finish(SpxState& s, double lam) {
@@ -799,15 +811,15 @@ __global__ void __launch_bounds__(kThreads, 1) spx_solve_kernel(SpxParams<T> p) 
     s_gen0 = ld_acquire(p.sync.gen);
     s_abort = 0;
     if (master) {
-      s_st = *p.st;
+      s_st = p.init;
       s_cmd = s_st.cmd;
       tl_record(p.sync, 0, -1, p.n, 0);
     } else {
-      load_l2(&s_cmd, &p.st->cmd);
+      s_cmd = p.init.cmd;
     }
   }
   __syncthreads();
-  const bool fix = p.st->fixing != 0;
+  const bool fix = p.init.fixing != 0;
   for (unsigned epoch = 1;; ++epoch) {
     const Cmd c = s_cmd;
     if (c.phase == PH_DONE || s_abort) break;
@@ -855,7 +867,7 @@ __global__ void __launch_bounds__(kThreads, 1) spx_solve_kernel(SpxParams<T> p) 
         else if (mode == 1) s_after_scan(s_st, glob, loc, p.trace);
         else s_after_snap(s_st, glob);
         const int ph = s_st.cmd.phase;
-        if (ph == PH_FINAL || ph == PH_DONE || ph == PH_COPY) *p.st = s_st;
+        if (ph == PH_FINAL || ph == PH_DONE || ph == PH_COPY) publish_state(p.out, s_st, p.sync);
         s_cmd = s_st.cmd;
         master_release(p.sync, s_gen0 + epoch, s_st.cmd, &p.st->cmd);
         tl_mark(p.sync, epoch, 5);

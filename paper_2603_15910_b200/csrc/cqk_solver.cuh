@@ -79,7 +79,7 @@ struct CqkState {
   int64_t domain_index;
   double vidx[10];  // first offending index per validate() check (pass 0 / first scan)
   int32_t has_plo, has_phi, fixing, variant, status, has_xbar, check, domain_field;
-  int32_t trace_len, trace_cap, lam0_given, pad;
+  int32_t trace_len, trace_cap, lam0_given, err;  // err: barrier-timeout flag at the final write
 };
 
 template <typename T>
@@ -91,10 +91,12 @@ struct CqkParams {
   int64_t n;                  // elements of this rank's shard
   int64_t offset;             // global index of the shard's first element
   double r;
-  CqkState* st;
+  CqkState* st;               // device: the master's command broadcast (st->cmd)
   double* partials;           // [gridDim.x][kMaxK]
   GridSync sync;
   Exchange ex;                // cross-GPU partial exchange (world 1: none)
+  CqkState* out;              // mapped host memory: the final state for the host
+  CqkState init;              // the host-initialised state, by value (no H2D copy)
 };
 
 // ------------------------------------------------------------ master logic

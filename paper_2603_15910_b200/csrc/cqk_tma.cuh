@@ -631,11 +631,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
     s_probe_last = 0;
     s_probe_pre = 0;
     if (master) {
-      s_st = *p.st;  // host-initialised before the launch
+      s_st = p.init;  // host-initialised, passed by value
       s_cmd = s_st.cmd;
       tl_record(p.sync, 0, -1, p.n, 0);
     } else {
-      load_l2(&s_cmd, &p.st->cmd);
+      s_cmd = p.init.cmd;
     }
   }
   __syncthreads();
@@ -646,7 +646,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
   const Src src_l0x{{p.d, p.a, p.b, p.l, p.u, p.xbar}};
   const bool prod_lane = producer && lane == 0;
   const int has_xbar = p.xbar != nullptr;
-  const int check = p.st->check;  // immutable during the solve
+  const int check = p.init.check;  // immutable during the solve
   bool in_scratch = false;
   int64_t m_w = -1;  // this warp's scratch element count (consumers, once in scratch)
   // The producer lane issues the first tiles of the most likely next pass (a
@@ -809,7 +809,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
     if (threadIdx.x == 0) {
       if (is_master) {
         const int ph = s_st.cmd.phase;
-        if (ph == PH_FINAL || ph == PH_DONE) *p.st = s_st;  // results for the host
+        if (ph == PH_FINAL || ph == PH_DONE) publish_state(p.out, s_st, p.sync);  // results for the host
         s_cmd = s_st.cmd;
         master_release(p.sync, s_gen0 + epoch, s_st.cmd, &p.st->cmd);
         tl_mark(p.sync, epoch, 5);

@@ -276,16 +276,16 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
     s_spec = s_spec_scr = 0;
     s_tail = 0;
     if (master) {
-      s_st = *p.st;
+      s_st = p.init;
       s_cmd = s_st.cmd;
       tl_record(p.sync, 0, -1, p.n, 0);
     } else {
-      load_l2(&s_cmd, &p.st->cmd);
+      s_cmd = p.init.cmd;
     }
   }
   for (int k = threadIdx.x; k < kHistB; k += blockDim.x) s_hist[k] = 0;
   __syncthreads();
-  const bool fix = p.st->fixing != 0;
+  const bool fix = p.init.fixing != 0;
   const int64_t ntiles = (p.n + kTileY - 1) / kTileY;
   const TileWalk orig{p.n, ntiles, -1};
   bool in_scratch = false;
@@ -308,6 +308,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
     }
     const TileWalk work{p.n, ntiles, in_scratch ? s_nslots : -1};
     if (c.phase == PH_FINAL || c.phase == PH_COPY) {
+      if (blockIdx.x <= 1 && threadIdx.x == 0) tl_mark(p.sync, epoch, 10 + 2 * blockIdx.x);
       const bool reuse = spec > 0 && !s_spec_scr;
       if (p.x) {
         const bool copy = c.phase == PH_COPY;
@@ -323,6 +324,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
         }
       } else if (!producer) {
         drain<kStagesY>(pp, spec);
+      }
+      if (blockIdx.x <= 1) {  // uniform per CTA
+        __syncthreads();
+        if (threadIdx.x == 0) tl_mark(p.sync, epoch, 11 + 2 * blockIdx.x);
       }
       break;
     }
@@ -346,7 +351,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
       } else if (!producer) {
         const bool hist = c.hist && p.hist;
         const int64_t mm = t_spx<L1, 1>(p, c, fix, work, m_w, compact, pp, acc,
-                                        hist ? s_hist : nullptr, (double)kHistB / p.st->r);
+                                        hist ? s_hist : nullptr, (double)kHistB / p.init.r);
         if (compact) {
           m_w = mm;
           if (lane == 0) {
@@ -385,7 +390,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
       }
     }
     const bool is_master = grid_step<3>(p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch);
-    if (is_master && mode == 1 && c.hist && p.hist) hist_bound(p, c.lam, s_st.r, s_hist, s_st);
+    if (is_master && mode == 1 && c.hist && p.hist) {
+      hist_bound(p, c.lam, s_st.r, s_hist, s_st);
+      // every CTA's adds preceded its arrival: leave the histogram zero for the next solve
+      for (int k = threadIdx.x; k < kHistB; k += blockDim.x) p.hist[k] = 0;
+    }
     if (threadIdx.x == 0) {
       if (is_master) {
         tl_record(p.sync, epoch, c.phase, mode == 0 ? p.n : s_st.phys_count, s_st.cmd.compact);
@@ -400,7 +409,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
         s_tail = p.wcnt && p.ex.world <= 1 && (ph == PH_SCAN || ph == PH_SNAP) &&
                  s_st.phys_count <= kTailY && (in_scratch || p.n <= kTailY);
         if (!s_tail) {
-          if (ph == PH_FINAL || ph == PH_DONE || ph == PH_COPY) *p.st = s_st;
+          if (ph == PH_FINAL || ph == PH_DONE || ph == PH_COPY) publish_state(p.out, s_st, p.sync);
           s_cmd = s_st.cmd;
           master_release(p.sync, s_gen0 + epoch, s_st.cmd, &p.st->cmd);
           tl_mark(p.sync, epoch, 5);
@@ -453,7 +462,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
       }
       if (threadIdx.x == 0) {
         const int ph = s_st.cmd.phase;
-        if (ph == PH_FINAL || ph == PH_DONE || ph == PH_COPY) *p.st = s_st;
+        if (ph == PH_FINAL || ph == PH_DONE || ph == PH_COPY) publish_state(p.out, s_st, p.sync);
         s_cmd = s_st.cmd;
         s_spec = 0;
         s_tail = 0;

@@ -73,6 +73,17 @@ for k in range(1, len(tl)):
     prev_rel = t_rel
     prev = t
     last = t
+# the final pass's row (the epoch after the last decision): CTA 0 / CTA 1 start, end
+if kind not in ("weak", "corr", "unc", "jac"):
+    rel = int(max(tl[1:, 5]))  # the last release
+    fr = [r_ for r_ in tl[1:] if r_[11]]
+    if fr:
+        fr = fr[-1]
+        print(json.dumps({"final_row": {"m_start": round((int(fr[10]) - rel) / 1e3, 2),
+                                        "m_end": round((int(fr[11]) - rel) / 1e3, 2),
+                                        "c1_start": round((int(fr[12]) - rel) / 1e3, 2) if fr[12] else None,
+                                        "c1_end": round((int(fr[13]) - rel) / 1e3, 2) if fr[13] else None,
+                                        "kernel_end_after_release_us": None}}))
 tot_ms = out.stats["device_ms"]
 final_us = tot_ms * 1e3 - (last - t0) / 1e3
 rows.append({"phase": "final(+launch)", "elems": n, "us": round(final_us, 1),
