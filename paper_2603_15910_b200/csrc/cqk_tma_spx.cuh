@@ -42,7 +42,17 @@ static_assert((kHistB & (kHistB - 1)) == 0, "power of two");
 constexpr int kTailY = 16384;  // elements (128 KB of the stage memory)
 static_assert(kTailY * sizeof(double) <= kSmemC, "tail set must fit the stage memory");
 
-// Gather the working set into V[0, m) (master CTA, all threads).
+// Gather the working set into V[0, m) (master CTA, all threads).  The
+// (CTA, warp) pairs' counts are scanned into exclusive offsets in shared
+// memory behind V; then every thread copies elements e = tid, tid + nt, ...,
+// finding its pair by binary search -- kGatherBatch searches in lockstep, then
+// their loads together (a per-pair loop serialised one L2 round trip per
+// element; serial searches cost ~2 us more).
+constexpr int kGatherBatch = 8;
+constexpr int kMaxGridY = 256;  // tail mode needs gridDim.x <= this (one CTA per SM)
+constexpr int kGatherPer = (kMaxGridY * kConsW + kTmaThreads - 1) / kTmaThreads;  // pairs per thread
+static_assert(kTailY * sizeof(double) + 4 * (kMaxGridY * kConsW + 1) <= kSmemC,
+              "tail set + pair offsets must fit the stage memory");
 template <bool L1>
 DEVI int tail_gather(const SpxParams<double>& p, bool in_scratch, double* V, int* s_scan) {
   const int nt = blockDim.x, tid = threadIdx.x;
@@ -51,12 +61,17 @@ DEVI int tail_gather(const SpxParams<double>& p, bool in_scratch, double* V, int
     for (int i = tid; i < m; i += nt) V[i] = spx_wv<L1>(p.y[i]);
     return m;
   }
+  int* off = reinterpret_cast<int*>(V + kTailY);  // [pairs + 1] exclusive offsets
   // pairs k = c * kConsW + w, a contiguous block of them per thread, in order
   const int pairs = (int)gridDim.x * kConsW;
   const int per = (pairs + nt - 1) / nt;
-  const int k0 = tid * per, k1 = min(k0 + per, pairs);
-  int mine = 0;
-  for (int k = k0; k < k1; ++k) mine += __ldcg(p.wcnt + k);
+  const int k0 = min(tid * per, pairs), k1 = min(k0 + per, pairs);
+  int cnt[kGatherPer], mine = 0;  // per <= kGatherPer: gridDim.x <= kMaxGridY
+#pragma unroll
+  for (int j = 0; j < kGatherPer; ++j) {
+    cnt[j] = k0 + j < k1 ? __ldcg(p.wcnt + k0 + j) : 0;
+    mine += cnt[j];
+  }
   // block exclusive scan of `mine` (warp inclusive scans + warp totals)
   const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
   int incl = mine;
@@ -73,15 +88,45 @@ DEVI int tail_gather(const SpxParams<double>& p, bool in_scratch, double* V, int
     wpre += w < warp ? v : 0;
     total += v;
   }
-  int off = wpre + incl - mine;
+  int o = wpre + incl - mine;
+#pragma unroll
+  for (int j = 0; j < kGatherPer; ++j) {
+    if (k0 + j < k1) off[k0 + j] = o;
+    o += cnt[j];
+  }
+  if (tid == 0) off[pairs] = total;
+  __syncthreads();
   const int64_t g = gridDim.x;
-  for (int k = k0; k < k1; ++k) {
-    const int c = k / kConsW, w = k % kConsW, cnt = __ldcg(p.wcnt + k);
-    for (int i = 0; i < cnt; ++i) {
-      const int64_t q = i / kSegY;
-      V[off + i] = __ldcg(p.sy + ((int64_t)c + q * g) * kTileY + kSegY * w + (i % kSegY));
+  // the kGatherBatch searches advance in lockstep (independent shared loads
+  // per step) and then their global loads issue together
+  const int steps = 32 - __clz(pairs);  // ceil(log2(pairs + 1))
+  for (int e0 = tid; e0 < total; e0 += kGatherBatch * nt) {
+    int lo[kGatherBatch], hi[kGatherBatch], e[kGatherBatch];
+#pragma unroll
+    for (int b = 0; b < kGatherBatch; ++b) {
+      e[b] = min(e0 + b * nt, total - 1);
+      lo[b] = 0;  // largest k with off[k] <= e: off[lo] <= e < off[hi]
+      hi[b] = pairs;
     }
-    off += cnt;
+    for (int st = 0; st < steps; ++st) {
+#pragma unroll
+      for (int b = 0; b < kGatherBatch; ++b) {
+        const int mid = (lo[b] + hi[b]) >> 1;
+        if (hi[b] - lo[b] > 1) {
+          if (off[mid] <= e[b]) lo[b] = mid;
+          else hi[b] = mid;
+        }
+      }
+    }
+    double v[kGatherBatch];
+#pragma unroll
+    for (int b = 0; b < kGatherBatch; ++b) {
+      const int i = e[b] - off[lo[b]], c = lo[b] / kConsW, w = lo[b] % kConsW;
+      v[b] = __ldcg(p.sy + ((int64_t)c + (int64_t)(i / kSegY) * g) * kTileY + kSegY * w + (i % kSegY));
+    }
+#pragma unroll
+    for (int b = 0; b < kGatherBatch; ++b)
+      if (e0 + b * nt < total) V[e0 + b * nt] = v[b];
   }
   __syncthreads();
   return total;
@@ -406,7 +451,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
         else if (mode == 1) s_after_scan(s_st, glob, loc, p.trace);
         else s_after_snap(s_st, glob);
         const int ph = s_st.cmd.phase;
-        s_tail = p.wcnt && p.ex.world <= 1 && (ph == PH_SCAN || ph == PH_SNAP) &&
+        s_tail = p.wcnt && p.ex.world <= 1 && gridDim.x <= kMaxGridY && (ph == PH_SCAN || ph == PH_SNAP) &&
                  s_st.phys_count <= kTailY && (in_scratch || p.n <= kTailY);
         if (!s_tail) {
           if (ph == PH_FINAL || ph == PH_DONE || ph == PH_COPY) publish_state(p.out, s_st, p.sync);
@@ -423,8 +468,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
     if (master && s_tail) {  // uniform in the master CTA; the other CTAs wait for the release
       if (!producer) drain<kStagesY>(pp, s_spec);  // the stage memory becomes the tail set
       __syncthreads();
+      if (threadIdx.x == 0) tl_mark(p.sync, epoch, 14);
       double* V = reinterpret_cast<double*>(s_dyn);
       const int m = tail_gather<L1>(p, in_scratch, V, s_scan);
+      if (threadIdx.x == 0) tl_mark(p.sync, epoch, 15);
       for (unsigned it = 1;; ++it) {
         const Cmd tc = s_st.cmd;
         if (tc.phase != PH_SCAN && tc.phase != PH_SNAP) break;

@@ -79,6 +79,11 @@ if kind not in ("weak", "corr", "unc", "jac"):
     fr = [r_ for r_ in tl[1:] if r_[11]]
     if fr:
         fr = fr[-1]
+        for k_, r_ in enumerate(tl[1:], 1):
+            if r_[15]:
+                print(json.dumps({"tail_entry_row": k_, "decided_to_drained_us": round((int(r_[14]) - int(r_[3])) / 1e3, 2),
+                                  "gather_us": round((int(r_[15]) - int(r_[14])) / 1e3, 2),
+                                  "first_iter_us": round((int(tl[k_ + 1][3]) - int(r_[15])) / 1e3, 2)}))
         print(json.dumps({"final_row": {"m_start": round((int(fr[10]) - rel) / 1e3, 2),
                                         "m_end": round((int(fr[11]) - rel) / 1e3, 2),
                                         "c1_start": round((int(fr[12]) - rel) / 1e3, 2) if fr[12] else None,
