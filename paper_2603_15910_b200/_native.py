@@ -219,6 +219,14 @@ class Handle:
         """Bind to a cudaStream_t; 0 (torch's default stream) maps to
         cudaStreamLegacy so work stays ordered with the caller's stream."""
         self.lib.cqk_set_stream(self.ptr, _P(stream_ptr if stream_ptr else 1))
+        self._stream = stream_ptr
+
+    def use_current_stream(self):
+        """Bind to torch's current stream on this handle's device (the C call
+        only when it changed)."""
+        s = _current_raw_stream(self.device)
+        if s != getattr(self, "_stream", None):
+            self.set_stream(s)
 
     def info(self):
         sm, ctas, thr = _I32(), _I32(), _I32()
@@ -244,6 +252,15 @@ class Handle:
             pass
 
 
+def _current_raw_stream(device):
+    import torch
+
+    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+    if raw is not None:
+        return int(raw(device))
+    return torch.cuda.current_stream(device).cuda_stream
+
+
 def handle(device=None):
     """Thread-local handle for `device` (default: torch's current device)."""
     import torch
@@ -261,18 +278,32 @@ def handle(device=None):
     return h
 
 
+_OPTS_CACHE = {}
+_START = {"formula": 0, "tight": 1, "alg2": 2, "auto": 4}
+
+
 def make_options(opts=None, variant=VARIANT_SOLVE, check=True, lambda0=None,
-                 compact_ratio=None, trace=False, fixing=None, start="auto"):
-    o = Options()
+                 compact_ratio=None, trace=False, fixing=None, start="auto", tau=None):
+    """The C options struct (tau: the tolerance the solve uses).  Structs are
+    cached by value and shared: callers must not mutate the result."""
     fix = getattr(opts, "variable_fixing", True) if fixing is None else fixing
+    max_it = int(getattr(opts, "max_iterations", 100))
+    ts = tau if tau is not None else getattr(opts, "tolerance_scale", None)
+    key = (bool(fix), max_it, ts, variant, bool(check), lambda0, compact_ratio, bool(trace), start)
+    o = _OPTS_CACHE.get(key)
+    if o is not None:
+        return o
+    o = Options()
     o.variable_fixing = 1 if fix else 0
-    o.max_iterations = int(getattr(opts, "max_iterations", 100))
-    ts = getattr(opts, "tolerance_scale", None)
+    o.max_iterations = max_it
     o.tolerance_scale = float(ts) if ts is not None else math.nan
     o.variant = variant
     o.check = 1 if check else 0
     o.lambda0 = math.nan if lambda0 is None else float(lambda0)
     o.compact_ratio = math.nan if compact_ratio is None else float(compact_ratio)
     o.record_trace = 1 if trace else 0
-    o.simplex_start = {"formula": 0, "tight": 1, "alg2": 2, "auto": 4}[start]
+    o.simplex_start = _START[start]
+    if len(_OPTS_CACHE) > 1024:
+        _OPTS_CACHE.clear()
+    _OPTS_CACHE[key] = o
     return o

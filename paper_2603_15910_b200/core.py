@@ -198,7 +198,7 @@ class Marshal:
         import torch
 
         h = N.handle(self.device)
-        h.set_stream(torch.cuda.current_stream(h.device).cuda_stream)
+        h.use_current_stream()
         return h
 
     def empty(self, n):

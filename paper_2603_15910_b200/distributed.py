@@ -126,12 +126,11 @@ class ShardedCQK:
         if opts is None:
             opts = SolverOptions()
         h = self.handle
-        h.set_stream(torch.cuda.current_stream(self.device).cuda_stream)
+        h.use_current_stream()
         x = self.x if want_x else None
         o = N.make_options(opts, variant=_VARIANTS[variant], check=check,
                            compact_ratio=getattr(opts, "compact_ratio", None),
-                           fixing=False if variant == "jacobi" else None)
-        o.tolerance_scale = opts.tau(np.float64)
+                           fixing=False if variant == "jacobi" else None, tau=opts.tau(np.float64))
         res = N.Result()
         xb = None if xbar is None else xbar.to(torch.float64).contiguous()
         rc = h.lib.cqk_solve_sharded_f64(h.ptr, N.MEM_DEVICE, *_ptrs(self.arrays), self.n_local,
@@ -158,14 +157,13 @@ class ShardedCQK:
             if rc != 0:
                 raise N.NativeError(f"cqk_reserve_host failed ({rc}): {N.last_error()}")
             self._host_reserved = True
-        h.set_stream(torch.cuda.current_stream(self.device).cuda_stream)
+        h.use_current_stream()
         arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in host_arrays]
         if x_out is None:
             x_out = torch.empty(self.n_local, dtype=torch.float64, pin_memory=True).numpy()
         o = N.make_options(opts, variant=_VARIANTS[variant], check=check,
                            compact_ratio=getattr(opts, "compact_ratio", None),
-                           fixing=False if variant == "jacobi" else None)
-        o.tolerance_scale = opts.tau(np.float64)
+                           fixing=False if variant == "jacobi" else None, tau=opts.tau(np.float64))
         res = N.Result()
         rc = h.lib.cqk_solve_sharded_f64(h.ptr, N.MEM_HOST, *[a.ctypes.data for a in arrs],
                                          self.n_local, self.offset, self.n_total, self.r, o, None,
@@ -205,9 +203,9 @@ class ShardedProjection:
         if opts is None:
             opts = SolverOptions()
         h = self.handle
-        h.set_stream(torch.cuda.current_stream(self.y.device).cuda_stream)
-        o = N.make_options(opts, compact_ratio=getattr(opts, "compact_ratio", None), start=start)
-        o.tolerance_scale = opts.tau(np.float64)
+        h.use_current_stream()
+        o = N.make_options(opts, compact_ratio=getattr(opts, "compact_ratio", None), start=start,
+                           tau=opts.tau(np.float64))
         res = N.Result()
         fn = h.lib.l1_project_sharded_f64 if l1 else h.lib.spx_project_sharded_f64
         rc = fn(h.ptr, N.MEM_DEVICE, self.y.data_ptr(), int(self.y.numel()), self.n_total,

@@ -119,7 +119,7 @@ def gen_cqk_device(family, n, seed, device=None):
     if family not in CQK_FAMILIES:
         raise FamilyMismatch(f"not a CQK family: {family!r}")
     h = N.handle(device)
-    h.set_stream(torch.cuda.current_stream(h.device).cuda_stream)
+    h.use_current_stream()
     arrs = [torch.empty(int(n), dtype=torch.float64, device=f"cuda:{h.device}") for _ in range(5)]
     r = ctypes.c_double()
     rc = h.lib.cqk_gen_cqk_device(h.ptr, CQK_FAMILIES.index(family), int(n),
@@ -139,7 +139,7 @@ def gen_cqk_shard_device(family, n, seed, lo, hi, device=None):
     if family not in CQK_FAMILIES:
         raise FamilyMismatch(f"not a CQK family: {family!r}")
     h = N.handle(device)
-    h.set_stream(torch.cuda.current_stream(h.device).cuda_stream)
+    h.use_current_stream()
     arrs = [torch.empty(int(hi) - int(lo), dtype=torch.float64, device=f"cuda:{h.device}")
             for _ in range(5)]
     bl, bu = ctypes.c_double(), ctypes.c_double()
@@ -163,7 +163,7 @@ def gen_simplex_y_device(family, n, seed, device=None):
     h = N.handle(device)
     if family != "simplex-u01":
         return torch.from_numpy(gen_simplex_y(family, n, seed)).to(f"cuda:{h.device}")
-    h.set_stream(torch.cuda.current_stream(h.device).cuda_stream)
+    h.use_current_stream()
     y = torch.empty(int(n), dtype=torch.float64, device=f"cuda:{h.device}")
     rc = h.lib.cqk_gen_simplex_u01_device(h.ptr, int(n), int(seed) & (2**64 - 1), y.data_ptr())
     if rc != 0:

@@ -211,8 +211,8 @@ def run_cqk(inst, opts, variant, xbar=None, check=True, lambda0=None, want_x=Tru
     o = N.make_options(opts, variant=variant, check=check, lambda0=lambda0,
                        compact_ratio=getattr(opts, "compact_ratio", None),
                        trace=trace is not None,
-                       fixing=False if variant == N.VARIANT_JACOBI else None)
-    o.tolerance_scale = opts.tau(inst.dtype)
+                       fixing=False if variant == N.VARIANT_JACOBI else None,
+                       tau=opts.tau(inst.dtype))
     res = N.Result()
     rc = h.lib.cqk_solve_f64(h.ptr, m.mem, *m.ptrs[:5], inst.n, float(inst.r), o, m.ptrs[5], xp,
                              res)

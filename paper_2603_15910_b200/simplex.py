@@ -53,7 +53,7 @@ def _alg2(y, r, idx, xbar, sharpened, workers):
     import torch
 
     if dev:
-        h.set_stream(torch.cuda.current_stream(yv.device).cuda_stream)
+        h.use_current_stream()
         mem = N.MEM_DEVICE
         ix = None if idx is None else torch.as_tensor(idx, device=yv.device).to(torch.int64).contiguous()
         xb = None if xbar is None else xbar.to(torch.float64).contiguous()
@@ -63,7 +63,7 @@ def _alg2(y, r, idx, xbar, sharpened, workers):
         ptr = lambda t: None if t is None else t.data_ptr()  # noqa: E731
         yp = yv.data_ptr()
     else:
-        h.set_stream(torch.cuda.current_stream(h.device).cuda_stream)
+        h.use_current_stream()
         mem = N.MEM_HOST
         ix = None if idx is None else np.ascontiguousarray(idx, dtype=np.int64)
         xb = None if xbar is None else np.ascontiguousarray(xbar, dtype=np.float64)
@@ -149,20 +149,19 @@ def _project(y, r, opts, lambda0, trace, l1, start="auto", xbar=None, sharpened=
     if dev:
         import torch
 
-        h.set_stream(torch.cuda.current_stream(yv.device).cuda_stream)
+        h.use_current_stream()
         x = torch.empty_like(yv)
         yp, xp = yv.data_ptr(), x.data_ptr()
         mem = N.MEM_DEVICE
     else:
         import torch
 
-        h.set_stream(torch.cuda.current_stream(h.device).cuda_stream)
+        h.use_current_stream()
         x = np.empty(n)
         yp, xp = yv.ctypes.data, x.ctypes.data
         mem = N.MEM_HOST
     o = N.make_options(opts, lambda0=lambda0, trace=trace is not None,
-                       compact_ratio=getattr(opts, "compact_ratio", None), start=start)
-    o.tolerance_scale = opts.tau(dt)
+                       compact_ratio=getattr(opts, "compact_ratio", None), start=start, tau=opts.tau(dt))
     res = N.Result()
     if warm:
         xbp = None if xb is None else (xb.data_ptr() if dev else xb.ctypes.data)
@@ -265,7 +264,7 @@ def project_simplex_rows(Y, r, opts=None, lambda0=None, start="tight"):
         Yv = Y.to(torch.float64).contiguous()
         rows, cols = Yv.shape
         h = N.handle(Yv.device.index)
-        h.set_stream(torch.cuda.current_stream(Yv.device).cuda_stream)
+        h.use_current_stream()
         X = torch.empty_like(Yv)
         lam = torch.empty(rows, dtype=torch.float64, device=Yv.device)
         its = torch.empty(rows, dtype=torch.int32, device=Yv.device)
@@ -277,14 +276,13 @@ def project_simplex_rows(Y, r, opts=None, lambda0=None, start="tight"):
         h = N.handle(None)
         import torch
 
-        h.set_stream(torch.cuda.current_stream(h.device).cuda_stream)
+        h.use_current_stream()
         X = np.empty_like(Yv)
         lam = np.empty(rows)
         its = np.empty(rows, np.int32)
         ptrs = (Yv.ctypes.data, X.ctypes.data, lam.ctypes.data, its.ctypes.data)
         mem = N.MEM_HOST
-    o = N.make_options(opts, lambda0=lambda0, start=start)
-    o.tolerance_scale = opts.tau(np.float64)
+    o = N.make_options(opts, lambda0=lambda0, start=start, tau=opts.tau(np.float64))
     res = N.Result()
     rc = h.lib.spx_project_batched_f64(h.ptr, mem, ptrs[0], rows, cols, float(r), o, ptrs[1],
                                        ptrs[2], ptrs[3], res)

@@ -54,4 +54,11 @@ for b in ("bench", "bench_ref"):
     p = os.path.join(src, f"{b}_{rnd}.json")
     if os.path.exists(p):
         shutil.copy(p, os.path.join(dst, f"{rnd}_{b}.json"))
+        continue
+    p = os.path.join(src, f"{b}_{rnd}.log")  # profile_all.sh: the bench's last JSON line
+    if os.path.exists(p):
+        lines = [ln for ln in open(p) if ln.startswith("{")]
+        if lines:
+            with open(os.path.join(dst, f"{rnd}_{b}.json"), "w") as f:
+                f.write(lines[-1])
 print(sorted(os.listdir(dst)))
