@@ -103,7 +103,11 @@ struct cqk_handle {
   void* ring[kRing] = {};
   cudaEvent_t ring_ev[kRing] = {};
   int32_t* wcnt = nullptr;            // per-warp scratch counts (simplex tail mode)
-  int32_t* hist = nullptr;            // first-scan bucket counts (simplex start "auto")
+  int32_t* hist = nullptr;            // first-scan bucket counts (simplex start "auto"), two halves
+  int hist_flip = 0;                  // ... the half the next launch uses (arrives zero)
+  double* ar_rows = nullptr;          // masterless grid step: [2][grid][kMaxK] partial rows
+  unsigned* ar_count = nullptr;       // ... [2] arrival counters, alternating per launch
+  unsigned long long ar_seq = 0;      // masterless launches so far
   double* alg2_vals = nullptr;        // gathered free values of the last Algorithm-2 run
   int64_t* alg2_idx = nullptr;        // ... and their global indices
   int64_t* alg2_jplus = nullptr;
@@ -193,6 +197,9 @@ int cqk_create(cqk_handle** out, int device) {
   e = e ? e : cudaMalloc(&h->wcnt, sizeof(int32_t) * kConsW * (h->sm_count + 8));
   e = e ? e : cudaMalloc(&h->hist, sizeof(int32_t) * kHistB * (h->sm_count + 8));
   e = e ? e : cudaMemset(h->hist, 0, sizeof(int32_t) * kHistB * (h->sm_count + 8));
+  e = e ? e : cudaMalloc(&h->ar_rows, sizeof(double) * 2 * kMaxK * (h->sm_count + 8));
+  e = e ? e : cudaMalloc(&h->ar_count, 64);
+  e = e ? e : cudaMemset(h->ar_count, 0, 64);
   e = e ? e : cudaHostAlloc(&h->host_state, st_bytes, cudaHostAllocMapped | cudaHostAllocPortable);
   e = e ? e : cudaHostGetDevicePointer(&h->host_state_dev, h->host_state, 0);
   e = e ? e : set_prefetch();
@@ -232,6 +239,8 @@ int cqk_destroy(cqk_handle* h) {
   cudaFree(h->out);
   if (h->wcnt) cudaFree(h->wcnt);
   if (h->hist) cudaFree(h->hist);
+  if (h->ar_rows) cudaFree(h->ar_rows);
+  if (h->ar_count) cudaFree(h->ar_count);
   for (int k = 0; k < cqk_handle::kRing; ++k) {
     if (h->ring[k]) cudaFreeHost(h->ring[k]);
     if (h->ring_ev[k]) cudaEventDestroy(h->ring_ev[k]);
@@ -434,9 +443,27 @@ int finish_sync(cqk_handle* h) {
 int check_timeout(cqk_handle* h, int32_t status, int32_t err) {
   if (status != ST_RUNNING && !err) return 0;
   cudaMemsetAsync(h->sync, 0, 64, h->stream);
-  cudaMemsetAsync(h->hist, 0, sizeof(int32_t) * kHistB, h->stream);  // may hold a partial scan
+  cudaMemsetAsync(h->ar_count, 0, 64, h->stream);
+  cudaMemsetAsync(h->hist, 0, sizeof(int32_t) * 2 * kHistB, h->stream);  // may hold a partial scan
   cudaStreamSynchronize(h->stream);
   return set_err(CQK_E_TIMEOUT, "persistent kernel barrier timed out");
+}
+
+bool getenv_flag(const char* name) {
+  const char* e = getenv(name);
+  return e && e[0] && e[0] != '0';
+}
+
+// The masterless grid step for a single-GPU persistent TMA launch of `grid`
+// CTAs (one CTA per SM; the buffers hold sm_count + 8 rows).
+GridAR masterless(cqk_handle* h, int grid, const Exchange& ex) {
+  GridAR ar{nullptr, nullptr, nullptr};
+  if (ex.world > 1 || grid > h->sm_count + 8 || getenv_flag("CQK_MASTER_STEP")) return ar;
+  const int k = (int)(h->ar_seq++ & 1u);
+  ar.rows = h->ar_rows;
+  ar.count = h->ar_count + k;
+  ar.count_next = h->ar_count + (k ^ 1);
+  return ar;
 }
 
 int map_status(int32_t st) {
@@ -684,6 +711,7 @@ static int solve_impl(cqk_handle* h, int mem, const double* d, const double* a, 
   if (tma) {
     grid = limit_grid(h, fixing ? h->grid_tma_fix : h->grid_tma_jac);
     fn = fixing ? (const void*)cqk_tma_kernel<true> : (const void*)cqk_tma_kernel<false>;
+    p.ar = masterless(h, grid, p.ex);
   } else {
     grid = limit_grid(h, fixing ? h->grid_cqk_fix : h->grid_cqk_jac);
     fn = fixing ? (const void*)cqk_solve_kernel<double, true>
@@ -759,7 +787,11 @@ int launch_spx(cqk_handle* h, SpxState& s, const double* yv, int64_t n, double* 
   {
     const char* te = getenv("CQK_TAIL");
     p.wcnt = (tma && !sharded && !(te && te[0] == '0')) ? h->wcnt : nullptr;
-    if (tma && !sharded && s.hist_ok) p.hist = h->hist;  // zero: the kernel clears it after use
+    if (tma && !sharded && s.hist_ok) {  // the halves alternate: this one is zero
+      p.hist = h->hist + h->hist_flip * kHistB;
+      p.hist_next = h->hist + (h->hist_flip ^ 1) * kHistB;
+      h->hist_flip ^= 1;
+    }
   }
   void* args[] = {&p};
   int grid;
@@ -767,6 +799,7 @@ int launch_spx(cqk_handle* h, SpxState& s, const double* yv, int64_t n, double* 
   if (tma) {
     grid = limit_grid(h, l1 ? h->grid_tma_l1 : h->grid_tma_spx);
     fn = l1 ? (const void*)spx_tma_kernel<true> : (const void*)spx_tma_kernel<false>;
+    p.ar = masterless(h, grid, p.ex);
   } else {
     grid = limit_grid(h, l1 ? h->grid_l1 : h->grid_spx);
     fn = l1 ? (const void*)spx_solve_kernel<double, true> : (const void*)spx_solve_kernel<double, false>;

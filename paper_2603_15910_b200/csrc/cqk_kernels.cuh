@@ -175,6 +175,97 @@ DEVI bool grid_step(double* partials, const double* s_cta, const int (&ops)[K],
   return !*(volatile int*)s_abort;
 }
 
+// Single GPU (grid_step_any with GridAR rows): every CTA publishes its
+// partial row and counts its arrival (ar_arrive), waits for the epoch's G
+// arrivals, then combines all rows itself in the same fixed order as
+// grid_step's master -- bit-identical totals -- (ar_combine) and runs the
+// deterministic state machine on its own replica of the state: no release
+// round trip.  ar_combine returns false (s_abort set) on a spin timeout.
+template <int K>
+DEVI void ar_arrive(const GridAR& ar, const double* s_cta, const GridSync& sy, unsigned epoch) {
+  const int G = (int)gridDim.x;
+  if (threadIdx.x < K)
+    ar.rows[(size_t)(epoch & 1u) * G * kMaxK + (int64_t)blockIdx.x * kMaxK + threadIdx.x] = s_cta[threadIdx.x];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ar.count) : "memory");
+    if (blockIdx.x == 1) tl_mark(sy, epoch, 6);
+  }
+}
+
+template <int K>
+DEVI bool ar_combine(const GridAR& ar, const int (&ops)[K], const GridSync& sy,
+                     double (*s_red)[kMaxK], double* s_tot, int* s_abort, unsigned epoch) {
+  const int G = (int)gridDim.x;
+  const double* rows = ar.rows + (size_t)(epoch & 1u) * G * kMaxK;
+  if (threadIdx.x == 0) {
+    const unsigned target = epoch * (unsigned)G;
+    const unsigned long long t0 = globaltimer();
+    unsigned polls = 0;
+    while ((int)(ld_relaxed(ar.count) - target) < 0) {
+      if ((++polls & 255u) == 0 && globaltimer() - t0 > kSpinTimeoutNs) {
+        atomicExch(sy.error, 1);
+        *s_abort = 1;
+        break;
+      }
+    }
+    fence_acquire_gpu();
+    if (blockIdx.x == 0) tl_mark(sy, epoch, 4);
+  }
+  __syncthreads();
+  if (*(volatile int*)s_abort) return false;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double acc[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) acc[k] = ops[k] == OP_SUM ? 0.0 : ops[k] == OP_MIN ? HUGE_VAL : -HUGE_VAL;
+  for (int c = threadIdx.x; c < G; c += blockDim.x) {
+    double v[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) v[k] = __ldcg(rows + (int64_t)c * kMaxK + k);
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      acc[k] = ops[k] == OP_SUM ? acc[k] + v[k] : ops[k] == OP_MIN ? fmin(acc[k], v[k]) : fmax(acc[k], v[k]);
+  }
+  const int nw = min((int)(blockDim.x >> 5), (G + 31) >> 5);
+  if (warp < nw) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const double v = ops[k] == OP_SUM ? warp_sum(acc[k]) : ops[k] == OP_MIN ? warp_min(acc[k])
+                                                                             : warp_max(acc[k]);
+      if (lane == 0) s_red[warp][k] = v;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < K) {
+    const int k = threadIdx.x;
+    double v = s_red[0][k];
+    for (int w = 1; w < nw; ++w) {
+      const double o = s_red[w][k];
+      v = ops[k] == OP_SUM ? v + o : ops[k] == OP_MIN ? fmin(v, o) : fmax(v, o);
+    }
+    s_tot[k] = v;
+  }
+  __syncthreads();
+  return true;
+}
+
+// The grid step of either design; true = this CTA runs the decision (every
+// CTA single-GPU, the master otherwise).
+// `overlap` (the producer lane's next-pass speculation) runs once this CTA
+// has arrived when masterless, before the arrival otherwise.
+template <int K, class F>
+DEVI bool grid_step_any(const GridAR& ar, double* partials, const double* s_cta, const int (&ops)[K],
+                        const GridSync& sy, double (*s_red)[kMaxK], double* s_tot, int* s_abort,
+                        unsigned epoch, F&& overlap) {
+  if (ar.rows) {
+    ar_arrive<K>(ar, s_cta, sy, epoch);
+    overlap();
+    return ar_combine<K>(ar, ops, sy, s_red, s_tot, s_abort, epoch);
+  }
+  overlap();
+  return grid_step<K>(partials, s_cta, ops, sy, s_red, s_tot, s_abort, epoch);
+}
+
 // Master (CTA 0, thread 0): publish the next command and release the grid.
 DEVI void master_release(const GridSync& sy, unsigned target, const Cmd& cmd, Cmd* gcmd) {
   const unsigned long long* s = reinterpret_cast<const unsigned long long*>(&cmd);
@@ -579,9 +670,11 @@ struct SpxParams {
   GridSync sync;
   Exchange ex;
   int32_t* wcnt;  // [grid][consumer warps] scratch counts: enables the TMA kernel's tail mode
-  int32_t* hist;  // [kHistB] bucket counts of the first scan (start "auto"); zero between solves
+  int32_t* hist;       // [kHistB] bucket counts of the first scan (start "auto"); arrives zero
+  int32_t* hist_next;  // the next launch's histogram, cleared by this one
   SpxState* out;  // mapped host memory: the final state for the host
   SpxState init;  // the host-initialised state, by value (no H2D copy)
+  GridAR ar;      // single-GPU masterless grid step (rows null: master + release)
 };
 
 DEVI void s_finish(SpxState& s, double lam) {

@@ -97,6 +97,7 @@ struct CqkParams {
   Exchange ex;                // cross-GPU partial exchange (world 1: none)
   CqkState* out;              // mapped host memory: the final state for the host
   CqkState init;              // the host-initialised state, by value (no H2D copy)
+  GridAR ar;                  // single-GPU masterless grid step (rows null: master + release)
 };
 
 // ------------------------------------------------------------ master logic

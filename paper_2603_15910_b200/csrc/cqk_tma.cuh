@@ -598,7 +598,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
   __shared__ double s_red[kConsW + 1][kMaxK];
   __shared__ double s_tot[kMaxK];
   __shared__ Cmd s_cmd;
-  __shared__ CqkState s_st;  // master (CTA 0) only
+  __shared__ CqkState s_st;  // the decision state (every CTA's replica single-GPU, else CTA 0's)
   __shared__ unsigned s_gen0;
   __shared__ int s_abort;
   __shared__ int s_nslots;   // scratch slots of this CTA (max over its warps)
@@ -630,13 +630,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
     s_spec_scr = 0;
     s_probe_last = 0;
     s_probe_pre = 0;
-    if (master) {
-      s_st = p.init;  // host-initialised, passed by value
-      s_cmd = s_st.cmd;
-      tl_record(p.sync, 0, -1, p.n, 0);
-    } else {
-      s_cmd = p.init.cmd;
-    }
+    s_st = p.init;  // host-initialised, passed by value (every CTA: single-GPU replicas)
+    s_cmd = s_st.cmd;
+    if (master) tl_record(p.sync, 0, -1, p.n, 0);
+    if (master && p.ar.rows) *p.ar.count_next = 0u;  // the previous launch's counter
   }
   __syncthreads();
   const int64_t ntiles = (p.n + kTileC - 1) / kTileC;
@@ -659,6 +656,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
     s_spec_scr = in_scratch;
   };
   const bool probe = blockIdx.x == 1 && p.sync.timeline;  // timeline detail columns 10-15
+  const bool single = p.ar.rows != nullptr;  // masterless grid step: every CTA decides
+  GridSync dsync = p.sync;                   // the decision's timeline rows: CTA 0 only
+  if (!master) dsync.timeline = nullptr;
+  double* const dtrace = master ? p.trace : nullptr;
   for (unsigned epoch = 1;; ++epoch) {
     const Cmd c = s_cmd;
     const int spec = s_spec;
@@ -705,10 +706,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
 #pragma unroll
       for (int k = 0; k < 15; ++k) a15[k] = acc[k];
       block_reduce<15, kConsW>(a15, ops, s_red, s_tot);
-      if (prod_lane) speculate();
-      is_master = grid_step<15>(p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch);
+      is_master = grid_step_any<15>(p.ar, p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch,
+                                   [&] { if (prod_lane) speculate(); });
       if (is_master && threadIdx.x == 0) {
-        tl_record(p.sync, epoch, PH_LAMBDA0, p.n, 0);
+        tl_record(dsync, epoch, PH_LAMBDA0, p.n, 0);
         double glob[15];
         if (exchange_totals(p.ex, epoch, 15, ops, s_tot, glob)) m_after_lambda0(s_st, glob);
         else m_stop(s_st, ST_TIMEOUT);
@@ -722,13 +723,13 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
 #pragma unroll
       for (int k = 0; k < kMaxK; ++k) ops[k] = k < kCheckLuSlot ? OP_SUM : OP_MIN;
       block_reduce<kMaxK, kConsW>(acc, ops, s_red, s_tot);
-      if (prod_lane) speculate();
-      is_master = grid_step<kMaxK>(p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch);
+      is_master = grid_step_any<kMaxK>(p.ar, p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch,
+                                   [&] { if (prod_lane) speculate(); });
       if (is_master && threadIdx.x == 0) {
         double loc[kMaxK], glob[kMaxK];
 #pragma unroll
         for (int k = 0; k < kMaxK; ++k) loc[k] = s_tot[k];
-        tl_record(p.sync, epoch, PH_SCAN, s_st.phys_count, 0);
+        tl_record(dsync, epoch, PH_SCAN, s_st.phys_count, 0);
         if (!exchange_totals(p.ex, epoch, kMaxK, ops, loc, glob)) {
           m_stop(s_st, ST_TIMEOUT);
         } else {
@@ -738,7 +739,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
           s_st.vidx[7] = glob[13];  // l <= u
           s_st.vidx[8] = glob[14];  // l == +inf
           s_st.vidx[9] = glob[15];  // u == -inf
-          if (m_validate(s_st, 3, 10)) m_after_scan(s_st, glob, loc, p.trace);
+          if (m_validate(s_st, 3, 10)) m_after_scan(s_st, glob, loc, dtrace);
         }
       }
     } else if (c.phase == PH_SCAN) {
@@ -772,20 +773,21 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
         s_probe_last = 0;
         s_probe_pre = 0;
       }
-      if (prod_lane) {
-        if (compact) {  // nobody else reads s_nslots before the next epoch
-          s_nslots = s_nsl_new;
-          s_nsl_new = 0;
+      is_master = grid_step_any<K>(p.ar, p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch, [&] {
+        if (prod_lane) {
+          if (compact) {  // nobody else reads s_nslots before the next epoch
+            s_nslots = s_nsl_new;
+            s_nsl_new = 0;
+          }
+          speculate();
         }
-        speculate();
-      }
-      is_master = grid_step<K>(p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch);
+      });
       if (is_master && threadIdx.x == 0) {
         double loc[11], glob[11];
 #pragma unroll
         for (int k = 0; k < 11; ++k) loc[k] = glob[k] = k < K ? s_tot[k] : 0.0;
-        tl_record(p.sync, epoch, PH_SCAN, s_st.phys_count, s_st.cmd.compact);
-        if (exchange_totals(p.ex, epoch, K, ops, loc, glob)) m_after_scan(s_st, glob, loc, p.trace);
+        tl_record(dsync, epoch, PH_SCAN, s_st.phys_count, s_st.cmd.compact);
+        if (exchange_totals(p.ex, epoch, K, ops, loc, glob)) m_after_scan(s_st, glob, loc, dtrace);
         else m_stop(s_st, ST_TIMEOUT);
       }
     } else if (c.phase == PH_BP) {
@@ -795,10 +797,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
       int ops[2] = {c.right ? OP_MIN : OP_MAX, OP_SUM};
       double a2[2] = {acc[0], acc[1]};
       block_reduce<2, kConsW>(a2, ops, s_red, s_tot);
-      if (prod_lane) speculate();
-      is_master = grid_step<2>(p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch);
+      is_master = grid_step_any<2>(p.ar, p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch,
+                                   [&] { if (prod_lane) speculate(); });
       if (is_master && threadIdx.x == 0) {
-        tl_record(p.sync, epoch, PH_BP, s_st.phys_count, 0);
+        tl_record(dsync, epoch, PH_BP, s_st.phys_count, 0);
         double glob[2];
         if (exchange_totals(p.ex, epoch, 2, ops, s_tot, glob)) m_after_bp(s_st, glob);
         else m_stop(s_st, ST_TIMEOUT);
@@ -809,10 +811,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
     if (threadIdx.x == 0) {
       if (is_master) {
         const int ph = s_st.cmd.phase;
-        if (ph == PH_FINAL || ph == PH_DONE) publish_state(p.out, s_st, p.sync);  // results for the host
+        if (master && (ph == PH_FINAL || ph == PH_DONE)) publish_state(p.out, s_st, p.sync);  // for the host
         s_cmd = s_st.cmd;
-        master_release(p.sync, s_gen0 + epoch, s_st.cmd, &p.st->cmd);
-        tl_mark(p.sync, epoch, 5);
+        if (!single) master_release(p.sync, s_gen0 + epoch, s_st.cmd, &p.st->cmd);
+        if (master) tl_mark(p.sync, epoch, 5);
       } else if (!s_abort) {
         if (!wait_release(p.sync, s_gen0 + epoch, &p.st->cmd, &s_cmd)) s_abort = 1;
         if (blockIdx.x == 1) tl_mark(p.sync, epoch, 7);

@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
   __shared__ double s_red[kConsW + 1][kMaxK];
   __shared__ double s_tot[kMaxK];
   __shared__ Cmd s_cmd;
-  __shared__ SpxState s_st;  // master (CTA 0) only
+  __shared__ SpxState s_st;  // the decision state (every CTA's replica single-GPU, else CTA 0's)
   __shared__ unsigned s_gen0;
   __shared__ int s_abort;
   __shared__ int s_nslots, s_nsl_new;
@@ -320,16 +320,21 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
     s_nslots = s_nsl_new = 0;
     s_spec = s_spec_scr = 0;
     s_tail = 0;
-    if (master) {
-      s_st = p.init;
-      s_cmd = s_st.cmd;
-      tl_record(p.sync, 0, -1, p.n, 0);
-    } else {
-      s_cmd = p.init.cmd;
-    }
+    s_st = p.init;  // every CTA: single-GPU replicas of the state machine
+    s_cmd = s_st.cmd;
+    if (master) tl_record(p.sync, 0, -1, p.n, 0);
+    if (master && p.ar.rows) *p.ar.count_next = 0u;  // the previous launch's counter
   }
   for (int k = threadIdx.x; k < kHistB; k += blockDim.x) s_hist[k] = 0;
+  // the histograms alternate between launches: this one arrives zero, the
+  // other (the previous launch's) is cleared here for the next
+  if (master && p.hist_next)
+    for (int k = threadIdx.x; k < kHistB; k += blockDim.x) p.hist_next[k] = 0;
   __syncthreads();
+  const bool single = p.ar.rows != nullptr;  // masterless grid step: every CTA decides
+  GridSync dsync = p.sync;                   // the decision's timeline rows: CTA 0 only
+  if (!master) dsync.timeline = nullptr;
+  double* const dtrace = master ? p.trace : nullptr;
   const bool fix = p.init.fixing != 0;
   const int64_t ntiles = (p.n + kTileY - 1) / kTileY;
   const TileWalk orig{p.n, ntiles, -1};
@@ -417,13 +422,6 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
     }
     double a3[3] = {acc[0], acc[1], acc[2]};
     block_reduce<3, kConsW>(a3, ops, s_red, s_tot);  // (its barrier orders the atomicMax above)
-    if (prod_lane) {
-      if (mode == 1 && fix && c.compact) {  // nobody else reads s_nslots before the next epoch
-        s_nslots = s_nsl_new;
-        s_nsl_new = 0;
-      }
-      speculate();
-    }
     if (mode == 1 && c.hist && p.hist) {
       // this CTA's nonzero counts into the global histogram (integer atomics:
       // order-independent); each CTA starts at its own offset so the 148
@@ -434,30 +432,37 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
         if (s_hist[k]) atomicAdd(&p.hist[k], s_hist[k]);
       }
     }
-    const bool is_master = grid_step<3>(p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch);
-    if (is_master && mode == 1 && c.hist && p.hist) {
-      hist_bound(p, c.lam, s_st.r, s_hist, s_st);
-      // every CTA's adds preceded its arrival: leave the histogram zero for the next solve
-      for (int k = threadIdx.x; k < kHistB; k += blockDim.x) p.hist[k] = 0;
-    }
+    const bool is_master = grid_step_any<3>(p.ar, p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch, [&] {
+      if (prod_lane) {
+        if (mode == 1 && fix && c.compact) {  // nobody else reads s_nslots before the next epoch
+          s_nslots = s_nsl_new;
+          s_nsl_new = 0;
+        }
+        speculate();
+      }
+    });
+    if (is_master && mode == 1 && c.hist && p.hist) hist_bound(p, c.lam, s_st.r, s_hist, s_st);
     if (threadIdx.x == 0) {
       if (is_master) {
-        tl_record(p.sync, epoch, c.phase, mode == 0 ? p.n : s_st.phys_count, s_st.cmd.compact);
+        tl_record(dsync, epoch, c.phase, mode == 0 ? p.n : s_st.phys_count, s_st.cmd.compact);
         double loc[3] = {s_tot[0], s_tot[1], s_tot[2]}, glob[3];
         if (!exchange_totals(p.ex, epoch, 3, ops, loc, glob)) {
           s_st.status = ST_TIMEOUT;
           s_st.cmd.phase = PH_DONE;
         } else if (mode == 0) s_after_init(s_st, glob);
-        else if (mode == 1) s_after_scan(s_st, glob, loc, p.trace);
+        else if (mode == 1) s_after_scan(s_st, glob, loc, dtrace);
         else s_after_snap(s_st, glob);
         const int ph = s_st.cmd.phase;
         s_tail = p.wcnt && p.ex.world <= 1 && gridDim.x <= kMaxGridY && (ph == PH_SCAN || ph == PH_SNAP) &&
                  s_st.phys_count <= kTailY && (in_scratch || p.n <= kTailY);
         if (!s_tail) {
-          if (ph == PH_FINAL || ph == PH_DONE || ph == PH_COPY) publish_state(p.out, s_st, p.sync);
+          if (master && (ph == PH_FINAL || ph == PH_DONE || ph == PH_COPY)) publish_state(p.out, s_st, p.sync);
           s_cmd = s_st.cmd;
-          master_release(p.sync, s_gen0 + epoch, s_st.cmd, &p.st->cmd);
-          tl_mark(p.sync, epoch, 5);
+          if (!single) master_release(p.sync, s_gen0 + epoch, s_st.cmd, &p.st->cmd);
+          if (master) tl_mark(p.sync, epoch, 5);
+        } else if (!master) {  // single-GPU: the master finishes alone, then releases once
+          s_tail = 0;
+          if (!wait_release(p.sync, s_gen0 + 1, &p.st->cmd, &s_cmd)) s_abort = 1;
         }
       } else if (!s_abort) {
         if (!wait_release(p.sync, s_gen0 + epoch, &p.st->cmd, &s_cmd)) s_abort = 1;
@@ -513,7 +518,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
         s_cmd = s_st.cmd;
         s_spec = 0;
         s_tail = 0;
-        master_release(p.sync, s_gen0 + epoch, s_st.cmd, &p.st->cmd);
+        master_release(p.sync, single ? s_gen0 + 1 : s_gen0 + epoch, s_st.cmd, &p.st->cmd);
         tl_mark(p.sync, epoch, 5);
       }
       __syncthreads();
