@@ -1,0 +1,94 @@
+"""The two grid-step designs of the persistent TMA kernels give bit-identical
+results: the single-GPU masterless step (every CTA combines the partial rows
+and runs a replica of the state machine) and the master step with a release
+(forced with CQK_MASTER_STEP=1; the multi-GPU path).  Both combine the rows
+in the same fixed order, so lambda, the iterate counts and x must agree
+bit for bit -- and both must agree with the C oracle."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+
+
+def P():
+    import paper_2603_15910_b200 as p
+
+    return p
+
+
+@pytest.fixture
+def tma_engine():
+    from paper_2603_15910_b200 import _native as N
+
+    h = N.handle()
+    h.lib.cqk_set_engine(h.ptr, 1)
+    yield
+    h.lib.cqk_set_engine(h.ptr, 0)
+
+
+def both_steps(fn):
+    os.environ.pop("CQK_MASTER_STEP", None)
+    a = fn()
+    os.environ["CQK_MASTER_STEP"] = "1"
+    try:
+        b = fn()
+    finally:
+        os.environ.pop("CQK_MASTER_STEP", None)
+    return a, b
+
+
+def same(a, b):
+    assert a.lam == b.lam or (np.isnan(a.lam) and np.isnan(b.lam))
+    assert a.iterations == b.iterations and a.phi_evals == b.phi_evals
+    assert a.fixed_count == b.fixed_count
+    assert np.array_equal(a.x, b.x)
+
+
+@pytest.mark.parametrize("fam", ["cqk-uncorrelated", "cqk-weakly-correlated", "cqk-correlated"])
+@pytest.mark.parametrize("n", [1, 961, 300001, 2000003])
+def test_cqk_master_and_masterless_agree(fam, n, tma_engine):
+    p = P()
+    d, a, b, l, u, r = p.instances.gen_cqk_arrays(fam, n, 3)
+    inst = p.CqkInstance(d=d, a=a, b=b, l=l, u=u, r=r)
+    for opts in (p.SolverOptions(), p.SolverOptions(variable_fixing=False)):
+        x, y = both_steps(lambda: p.solve_cqk(inst, opts))
+        same(x, y)
+    if n <= 300001:
+        ref = O.solve_cqk(d, a, b, l, u, r, fixing=True)
+        out = p.solve_cqk(inst)
+        assert abs(out.lam - ref["lam"]) <= TOL * max(1.0, abs(ref["lam"]))
+        assert out.fixed_count == ref["fixed_count"]
+
+
+@pytest.mark.parametrize("fam", ["simplex-u01", "simplex-n01"])
+@pytest.mark.parametrize("n", [1, 3841, 16385, 1000000])
+def test_simplex_and_l1_master_and_masterless_agree(fam, n):
+    p = P()
+    y = p.gen_simplex_y(fam, n, 2)
+    for start in ("auto", "tight", "formula"):
+        x, z = both_steps(lambda: p.newton_project_simplex(y, 1.0, start=start))
+        same(x, z)
+        x, z = both_steps(lambda: p.simplex.project_l1_outcome(y, 1.0, start=start))
+        same(x, z)
+
+
+def test_masterless_repeated_launches_stay_consistent(tma_engine):
+    """The arrival counters alternate between launches (each launch zeroes
+    the other): many back-to-back solves of differing epoch counts."""
+    p = P()
+    outs = []
+    for k in range(12):
+        fam = ("cqk-uncorrelated", "cqk-correlated")[k % 2]
+        d, a, b, l, u, r = p.instances.gen_cqk_arrays(fam, 100003 + k, k)
+        inst = p.CqkInstance(d=d, a=a, b=b, l=l, u=u, r=r)
+        ref = O.solve_cqk(d, a, b, l, u, r, fixing=True)
+        out = p.solve_cqk(inst)
+        assert abs(out.lam - ref["lam"]) <= TOL * max(1.0, abs(ref["lam"]))
+        outs.append(out.phi_evals)
+    assert len(set(outs)) >= 1
