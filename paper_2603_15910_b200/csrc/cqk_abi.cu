@@ -68,7 +68,7 @@ struct Buf {
 cudaError_t set_prefetch() {
   int pf[2] = {0, 2};
   if (const char* e = getenv("CQK_PREFETCH")) sscanf(e, "%d,%d", &pf[0], &pf[1]);
-  int tf = 0;
+  int tf = 12;  // late, shallow speculation (cqk_tma.cuh)
   if (const char* e = getenv("CQK_TMA_FLAGS")) tf = atoi(e);
   cudaError_t err = cudaMemcpyToSymbol(c_tma_flags, &tf, sizeof tf);
   err = err ? err : cudaMemcpyToSymbol(c_tma_flags_w, &tf, sizeof tf);

@@ -256,11 +256,13 @@ DEVI bool ar_combine(const GridAR& ar, const int (&ops)[K], const GridSync& sy,
 template <int K, class F>
 DEVI bool grid_step_any(const GridAR& ar, double* partials, const double* s_cta, const int (&ops)[K],
                         const GridSync& sy, double (*s_red)[kMaxK], double* s_tot, int* s_abort,
-                        unsigned epoch, F&& overlap) {
+                        unsigned epoch, F&& overlap, bool late = false) {
   if (ar.rows) {
     ar_arrive<K>(ar, s_cta, sy, epoch);
-    overlap();
-    return ar_combine<K>(ar, ops, sy, s_red, s_tot, s_abort, epoch);
+    if (!late) overlap();
+    const bool ok = ar_combine<K>(ar, ops, sy, s_red, s_tot, s_abort, epoch);
+    if (late) overlap();
+    return ok;
   }
   overlap();
   return grid_step<K>(partials, s_cta, ops, sy, s_red, s_tot, s_abort, epoch);

@@ -37,8 +37,12 @@ namespace cqk {
 #ifndef CQK_TMA_CONSW
 #define CQK_TMA_CONSW 15
 #endif
-// A/B switches for measurement (CQK_TMA_FLAGS): bit 0 disables the
-// next-pass prefetch across the grid step.
+// Switches (CQK_TMA_FLAGS, default 12): bit 0 disables the next-pass
+// speculation across the grid step; bit 2 issues it after the masterless
+// combine instead of during the arrival wait (its HBM reads then do not delay
+// the partial-row loads); bit 3 speculates 2 (CQK) / 3 (simplex) tiles instead
+// of a full pipeline.  Measured (A/B, one box): bits 2+3 -2% on C2 and C1,
+// neutral at n = 1e8.
 __constant__ int c_tma_flags;
 
 constexpr int kTileC = CQK_TMA_TILE;      // elements per array per tile
@@ -652,7 +656,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
   // step is in flight: the loads do not depend on lambda.
   auto speculate = [&]() {
     const TileWalk nw{p.n, ntiles, in_scratch ? s_nslots : -1};
-    s_spec = (c_tma_flags & 1) ? 0 : produce<5>(in_scratch ? src_scr : src_orig, nw, pp, 0, kStagesC);
+    s_spec = (c_tma_flags & 1) ? 0 : produce<5>(in_scratch ? src_scr : src_orig, nw, pp, 0, (c_tma_flags & 8) ? 2 : kStagesC);
     s_spec_scr = in_scratch;
   };
   const bool probe = blockIdx.x == 1 && p.sync.timeline;  // timeline detail columns 10-15
@@ -707,7 +711,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
       for (int k = 0; k < 15; ++k) a15[k] = acc[k];
       block_reduce<15, kConsW>(a15, ops, s_red, s_tot);
       is_master = grid_step_any<15>(p.ar, p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch,
-                                   [&] { if (prod_lane) speculate(); });
+                                   [&] { if (prod_lane) speculate(); }, (c_tma_flags & 4) != 0);
       if (is_master && threadIdx.x == 0) {
         tl_record(dsync, epoch, PH_LAMBDA0, p.n, 0);
         double glob[15];
@@ -724,7 +728,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
       for (int k = 0; k < kMaxK; ++k) ops[k] = k < kCheckLuSlot ? OP_SUM : OP_MIN;
       block_reduce<kMaxK, kConsW>(acc, ops, s_red, s_tot);
       is_master = grid_step_any<kMaxK>(p.ar, p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch,
-                                   [&] { if (prod_lane) speculate(); });
+                                   [&] { if (prod_lane) speculate(); }, (c_tma_flags & 4) != 0);
       if (is_master && threadIdx.x == 0) {
         double loc[kMaxK], glob[kMaxK];
 #pragma unroll
@@ -781,7 +785,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
           }
           speculate();
         }
-      });
+      }, (c_tma_flags & 4) != 0);
       if (is_master && threadIdx.x == 0) {
         double loc[11], glob[11];
 #pragma unroll
@@ -798,7 +802,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
       double a2[2] = {acc[0], acc[1]};
       block_reduce<2, kConsW>(a2, ops, s_red, s_tot);
       is_master = grid_step_any<2>(p.ar, p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch,
-                                   [&] { if (prod_lane) speculate(); });
+                                   [&] { if (prod_lane) speculate(); }, (c_tma_flags & 4) != 0);
       if (is_master && threadIdx.x == 0) {
         tl_record(dsync, epoch, PH_BP, s_st.phys_count, 0);
         double glob[2];

@@ -346,7 +346,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
     const TileWalk nw{p.n, ntiles, in_scratch ? s_nslots : -1};
     s_spec = (c_tma_flags & 1) ? 0
                                : produce<1, kStagesY, kTileY, kTileY>(Src{{in_scratch ? p.sy : p.y}}, nw,
-                                                                      pp, 0, kStagesY);
+                                                                      pp, 0, (c_tma_flags & 8) ? 3 : kStagesY);
     s_spec_scr = in_scratch;
   };
   for (unsigned epoch = 1;; ++epoch) {
@@ -440,7 +440,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
         }
         speculate();
       }
-    });
+    }, (c_tma_flags & 4) != 0);
     if (is_master && mode == 1 && c.hist && p.hist) hist_bound(p, c.lam, s_st.r, s_hist, s_st);
     if (threadIdx.x == 0) {
       if (is_master) {
