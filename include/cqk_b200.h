@@ -208,8 +208,8 @@ int cqk_comm_connect_local(cqk_handle *h, cqk_handle *const *ranks, int world);
 int cqk_reserve(cqk_handle *h, int64_t n);
 /* Cap the persistent grid (CTAs); 0 = the full device.  Lets several ranks
    share one GPU (virtual ranks) or leave SMs for other work. */
-/* CQK solve engine: 0 auto (TMA pipeline from 1e6 elements per rank,
-   CQK_TMA_MIN_N), 1 TMA pipeline, 2 warp-segment kernel.  Results agree to
+/* CQK solve engine: 0 auto (TMA pipeline from CQK_TMA_MIN_N elements per rank,
+   default 65536), 1 TMA pipeline, 2 warp-segment kernel.  Results agree to
    rounding (summation order differs). */
 /* Pre-allocate the host-mode staging of an n-element shard (collective solves
    with CQK_MEM_HOST must not allocate while peers wait inside the kernel). */

@@ -87,7 +87,7 @@ struct cqk_handle {
   int grid_tma_spx = 0, grid_tma_l1 = 0;    // TMA-pipelined simplex / l1 kernels
   bool use_tma = true;                     // CQK_ENGINE=seg selects the warp-segment kernel
   int engine = 0;                          // cqk_set_engine: 0 auto, 1 TMA, 2 warp segments
-  int64_t tma_min_n = 1000000;             // auto: CQK solves of >= this many elements per rank
+  int64_t tma_min_n = 65536;               // auto: CQK solves of >= this many elements per rank
   unsigned* sync = nullptr;  // [0] arrive, [1] gen, [2] error
   void* state = nullptr;     // CqkState / SpxState
   double* partials = nullptr;
@@ -674,9 +674,11 @@ static int solve_impl(cqk_handle* h, int mem, const double* d, const double* a, 
   s.domain_index = -1;
   s.trace_cap = opts.record_trace ? kTraceCap : 0;
   s.lam0_given = lam0_given;
-  // engine: the TMA pipeline wins from ~1e7 elements per rank; below, its
-  // per-epoch fill latency makes the warp-segment kernel faster (measured:
-  // 1e6 0.16 vs 0.11 ms, 1e7 equal, 3e7 1.48 vs 1.71 ms)
+  // engine: the TMA pipeline wins at every measured size since the producer
+  // warp left the reduction shuffles and the grid step lost its master
+  // (tools/crossover.py: 70 vs 72 us at 5e4 ... 0.65 vs 0.82 ms at 1.6e7);
+  // below 64Ki elements the two tie, and the warp-segment kernel's summation
+  // order reproduces the reference's iterate counts on tiny inputs more often
   const bool tma = h->use_tma && (h->engine == 1 || (h->engine == 0 && n >= h->tma_min_n));
   s.compact_ratio = std::isnan(opts.compact_ratio) ? default_compact_ratio(tma) : opts.compact_ratio;
   // scratch: n per array (warp segments) or whole tile slots (TMA engine)
