@@ -92,3 +92,28 @@ def test_masterless_repeated_launches_stay_consistent(tma_engine):
         assert abs(out.lam - ref["lam"]) <= TOL * max(1.0, abs(ref["lam"]))
         outs.append(out.phi_evals)
     assert len(set(outs)) >= 1
+
+
+@pytest.mark.parametrize("ctas", [1, 2, 37, 148])
+def test_masterless_step_on_reduced_grids(ctas, tma_engine):
+    """Single-GPU solves on a capped grid (cqk_set_grid_limit: a GPU shared
+    with other work) run the masterless step over fewer rows."""
+    from paper_2603_15910_b200 import _native as N
+
+    p = P()
+    h = N.handle()
+    d, a, b, l, u, r = p.instances.gen_cqk_arrays("cqk-weakly-correlated", 200003, 5)
+    inst = p.CqkInstance(d=d, a=a, b=b, l=l, u=u, r=r)
+    ref = O.solve_cqk(d, a, b, l, u, r, fixing=True)
+    y = p.gen_simplex_y("simplex-u01", 100003, 5)
+    lam0 = min((1.0 - float(O.pairwise_sum(y))) / y.size, 1.0 - float(y.max()))
+    sref = O.newton_project_simplex(y, 1.0, lam0=lam0)
+    h.lib.cqk_set_grid_limit(h.ptr, ctas)
+    try:
+        out = p.solve_cqk(inst)
+        sp = p.newton_project_simplex(y, 1.0, start="tight")
+    finally:
+        h.lib.cqk_set_grid_limit(h.ptr, 0)
+    assert abs(out.lam - ref["lam"]) <= TOL * max(1.0, abs(ref["lam"]))
+    assert out.fixed_count == ref["fixed_count"]
+    assert abs(sp.lam - sref["lam"]) <= TOL * max(1.0, abs(sref["lam"]))
