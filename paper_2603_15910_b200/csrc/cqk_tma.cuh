@@ -44,6 +44,7 @@ namespace cqk {
 // of a full pipeline.  Measured (A/B, one box): bits 2+3 -2% on C2 and C1,
 // neutral at n = 1e8.
 __constant__ int c_tma_flags;
+#define kSpecDepthC ((c_tma_flags & 8) ? 2 : kStagesC)  // next-pass tiles speculated (CQK)
 
 constexpr int kTileC = CQK_TMA_TILE;      // elements per array per tile
 constexpr int kStagesC = CQK_TMA_STAGES;
@@ -215,6 +216,82 @@ DEVI void consume(const TileWalk& tw, TPipe& pp, int64_t m_w, Body&& body) {
     if (lane == 0) mbar_arrive_s(pp.empty + 8 * s);
     ++pp.pc;
     if (++s == ST) { s = 0; ph ^= 1; }
+  }
+}
+
+// The final pass with dynamic tile assignment.  It reduces nothing (x is a
+// per-element map), so tile order is free, and CTAs that stream faster take
+// more tiles: the last CTA of a static final pass finished 40 us (C3) /
+// 35 us (simplex 1e8) after the first.  Static prefix: this CTA's tiles
+// c + qG, q < D -- exactly the tiles the speculation issues -- then tiles
+// G*D + k from a grid-wide counter; a tile index of -1 ends the walk.  The
+// producer publishes each dynamic tile's index in s_tix[stage] before the
+// stage's arrive (release), consumers read it after the wait (acquire).
+template <int NA, int ST, int STRIDE, int TT>
+DEVI void produce_final_dyn(const Src src, int64_t n, TPipe& pp, int skip, int D, unsigned* ctr,
+                            long long* s_tix) {
+  const int64_t G = gridDim.x, ntiles = (n + TT - 1) / TT;
+  int s = pp.pc % ST;
+  unsigned ph = ((pp.pc / ST) & 1) ^ 1;
+  bool first_round = pp.pc < (unsigned)ST;
+  auto issue = [&](int64_t t) {
+    if (!first_round) mbar_wait_s(pp.empty + 8 * s, ph);
+    const unsigned fb = pp.full + 8 * s;
+    s_tix[s] = t;
+    unsigned bytes = 0;
+    if (t >= 0) {
+      const int64_t left = n - t * TT;
+      bytes = ((unsigned)(left < TT ? left : TT) * 8u) & ~15u;
+    }
+    mbar_expect_tx_s(fb, NA * bytes);
+    if (bytes) {
+      const unsigned dst = smem_u32(pp.buf) + (unsigned)(s * STRIDE) * 8u;
+#pragma unroll
+      for (int k = 0; k < NA; ++k) tma_load_1d_s(dst + k * TT * 8u, src.p[k] + t * TT, bytes, fb);
+    }
+    ++pp.pc;
+    if (++s == ST) { s = 0; ph ^= 1; first_round = false; }
+  };
+  for (int q = skip; q < D; ++q) {
+    const int64_t t = (int64_t)blockIdx.x + q * G;
+    if (t >= ntiles) break;
+    issue(t);
+  }
+  for (;;) {
+    const int64_t t = G * D + (int64_t)atomicAdd(ctr, 1u);
+    if (t >= ntiles) break;
+    issue(t);
+  }
+  issue(-1);
+}
+
+template <int ST, int STRIDE, int TT, typename Body>
+DEVI void consume_final_dyn(int64_t n, TPipe& pp, int D, const long long* s_tix, Body&& body) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int kSegT = TT / kConsW;
+  const int64_t G = gridDim.x, ntiles = (n + TT - 1) / TT;
+  int s = pp.pc % ST;
+  unsigned ph = (pp.pc / ST) & 1;
+  bool dyn = false;
+  WTile wt;
+  wt.q = 0;
+  for (int q = 0;; ++q) {
+    if (!dyn && (q >= D || (int64_t)blockIdx.x + q * G >= ntiles)) dyn = true;
+    mbar_wait_s(pp.full + 8 * s, ph);
+    const int64_t t = dyn ? (int64_t)s_tix[s] : (int64_t)blockIdx.x + q * G;
+    if (t >= 0) {
+      wt.sm = pp.buf + (size_t)s * STRIDE + kSegT * warp;
+      wt.gbase = t * TT + kSegT * warp;
+      const int64_t left = n - wt.gbase;
+      wt.wcnt = left <= 0 ? 0 : (left < kSegT ? (int)left : kSegT);
+      wt.patch = (wt.wcnt & 1) && wt.wcnt < kSegT;
+      if (wt.wcnt > 0) body(wt);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive_s(pp.empty + 8 * s);
+    ++pp.pc;
+    if (++s == ST) { s = 0; ph ^= 1; }
+    if (t < 0) break;
   }
 }
 
@@ -580,17 +657,20 @@ DEVI void final_tile(const CqkParams<double>& p, const WTile& wt, double lam, do
 }
 
 template <bool FIX>
-DEVI void t_final(const CqkParams<double>& p, const Cmd& c, const TileWalk& tw, TPipe& pp) {
+DEVI void t_final(const CqkParams<double>& p, const Cmd& c, const TileWalk& tw, TPipe& pp,
+                  int D = -1, const long long* s_tix = nullptr) {
   const double lam = c.lam, fhi = c.fix_hi, flo = c.fix_lo;
   // fixed variables need an explicit test only if lam* left the side of the
   // fixing multiplier (the criterion-2 finish(lam + step) edge)
   const bool chk_lo = FIX && c.lam > c.fix_hi, chk_hi = FIX && c.lam < c.fix_lo;
-  consume(tw, pp, -1, [&](const WTile& wt) {
+  auto body = [&](const WTile& wt) {
     if (wt.wcnt == kSeg)
       CQK_DISPATCH_FIXED(chk_lo, chk_hi, (final_tile<FIX, true, CLO, CHI>(p, wt, lam, fhi, flo)));
     else
       CQK_DISPATCH_FIXED(chk_lo, chk_hi, (final_tile<FIX, false, CLO, CHI>(p, wt, lam, fhi, flo)));
-  });
+  };
+  if (D >= 0) consume_final_dyn<kStagesC, kStageElemsC, kTileC>(p.n, pp, D, s_tix, body);
+  else consume(tw, pp, -1, body);
 }
 
 // ------------------------------------------------------------ the kernel
@@ -611,6 +691,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
   __shared__ int s_spec_scr; // ... and whether they came from scratch
   __shared__ unsigned long long s_probe_last;  // timeline probe: last consumer warp done
   __shared__ unsigned long long s_probe_pre;   // ... last warp (incl. producer) at the reduction
+  __shared__ long long s_tix[kStagesC];        // dynamic final pass: tile index per stage
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool producer = warp == kConsW;
   const bool master = blockIdx.x == 0;
@@ -638,6 +719,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
     s_cmd = s_st.cmd;
     if (master) tl_record(p.sync, 0, -1, p.n, 0);
     if (master && p.ar.rows) *p.ar.count_next = 0u;  // the previous launch's counter
+    if (master && p.ar.tiles) *p.ar.tiles_next = 0u;
   }
   __syncthreads();
   const int64_t ntiles = (p.n + kTileC - 1) / kTileC;
@@ -656,7 +738,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
   // step is in flight: the loads do not depend on lambda.
   auto speculate = [&]() {
     const TileWalk nw{p.n, ntiles, in_scratch ? s_nslots : -1};
-    s_spec = (c_tma_flags & 1) ? 0 : produce<5>(in_scratch ? src_scr : src_orig, nw, pp, 0, (c_tma_flags & 8) ? 2 : kStagesC);
+    s_spec = (c_tma_flags & 1) ? 0 : produce<5>(in_scratch ? src_scr : src_orig, nw, pp, 0, kSpecDepthC);
     s_spec_scr = in_scratch;
   };
   const bool probe = blockIdx.x == 1 && p.sync.timeline;  // timeline detail columns 10-15
@@ -675,16 +757,29 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
     const TileWalk work{p.n, ntiles, in_scratch ? s_nslots : -1};
     const Src wsrc = in_scratch ? src_scr : src_orig;
     if (c.phase == PH_FINAL) {
+      if (blockIdx.x <= 1 && threadIdx.x == 0) tl_mark(p.sync, epoch, 10 + 2 * blockIdx.x);
       const bool reuse = spec > 0 && !s_spec_scr;  // the speculated tiles are the final's
+      const bool dyn = p.ar.tiles != nullptr;        // single GPU: dynamic tile assignment
+      const int D = kSpecDepthC;                     // its static prefix: the speculation's tiles
       if (p.x) {
         if (prod_lane) {
-          produce<5>(src_orig, orig, pp, reuse ? spec : 0);
+          if (dyn) produce_final_dyn<5, kStagesC, kStageElemsC, kTileC>(src_orig, p.n, pp, reuse ? spec : 0, D,
+                                                                        p.ar.tiles, s_tix);
+          else produce<5>(src_orig, orig, pp, reuse ? spec : 0);
         } else if (!producer) {
           if (!reuse) drain(pp, spec);
-          t_final<FIX>(p, c, orig, pp);
+          t_final<FIX>(p, c, orig, pp, dyn ? D : -1, s_tix);
         }
       } else if (!producer) {
         drain(pp, spec);
+      }
+      if (p.sync.timeline) {  // uniform: CTA 0 / 1 end, and the last CTA's end
+        __syncthreads();
+        if (threadIdx.x == 0 && epoch < (unsigned)kTimelineCap) {
+          if (blockIdx.x <= 1) tl_mark(p.sync, epoch, 11 + 2 * blockIdx.x);
+          atomicMax(reinterpret_cast<unsigned long long*>(p.sync.timeline + kTimelineCols * epoch + 15),
+                    globaltimer());
+        }
       }
       break;
     }

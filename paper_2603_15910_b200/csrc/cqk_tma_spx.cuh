@@ -16,6 +16,7 @@ constexpr int kTileY = 256 * kConsW;                              // 3840 elemen
 constexpr int kSegY = kTileY / kConsW;                           // 256 per warp
 constexpr int kEptY = kTileY / kConsT;                           // 8 per lane
 constexpr int kStagesY = (int)(kSmemC / (kTileY * sizeof(double)));  // 6
+#define kSpecDepthY ((c_tma_flags & 8) ? 3 : kStagesY)  // next-pass tiles speculated (simplex)
 static_assert(kStagesY >= 2, "pipeline needs at least two stages");
 
 template <bool L1>
@@ -304,6 +305,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
   __shared__ int s_scan[kConsW + 1];
   __shared__ int s_hist[kHistB];      // start "auto": first-scan bucket counts
   __shared__ double s_lam_hist;
+  __shared__ long long s_tix[kStagesY];  // dynamic final pass: tile index per stage
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool producer = warp == kConsW;
   const bool prod_lane = producer && lane == 0;
@@ -324,6 +326,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
     s_cmd = s_st.cmd;
     if (master) tl_record(p.sync, 0, -1, p.n, 0);
     if (master && p.ar.rows) *p.ar.count_next = 0u;  // the previous launch's counter
+    if (master && p.ar.tiles) *p.ar.tiles_next = 0u;
   }
   for (int k = threadIdx.x; k < kHistB; k += blockDim.x) s_hist[k] = 0;
   // the histograms alternate between launches: this one arrives zero, the
@@ -346,7 +349,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
     const TileWalk nw{p.n, ntiles, in_scratch ? s_nslots : -1};
     s_spec = (c_tma_flags & 1) ? 0
                                : produce<1, kStagesY, kTileY, kTileY>(Src{{in_scratch ? p.sy : p.y}}, nw,
-                                                                      pp, 0, (c_tma_flags & 8) ? 3 : kStagesY);
+                                                                      pp, 0, kSpecDepthY);
     s_spec_scr = in_scratch;
   };
   for (unsigned epoch = 1;; ++epoch) {
@@ -360,24 +363,33 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
     if (c.phase == PH_FINAL || c.phase == PH_COPY) {
       if (blockIdx.x <= 1 && threadIdx.x == 0) tl_mark(p.sync, epoch, 10 + 2 * blockIdx.x);
       const bool reuse = spec > 0 && !s_spec_scr;
+      const bool dyn = p.ar.tiles != nullptr;  // single GPU: dynamic tile assignment (cqk_tma.cuh)
       if (p.x) {
         const bool copy = c.phase == PH_COPY;
         if (prod_lane) {
-          produce<1, kStagesY, kTileY, kTileY>(Src{{p.y}}, orig, pp, reuse ? spec : 0);
+          if (dyn) produce_final_dyn<1, kStagesY, kTileY, kTileY>(Src{{p.y}}, p.n, pp, reuse ? spec : 0,
+                                                                   kSpecDepthY, p.ar.tiles, s_tix);
+          else produce<1, kStagesY, kTileY, kTileY>(Src{{p.y}}, orig, pp, reuse ? spec : 0);
         } else if (!producer) {
           if (!reuse) drain<kStagesY>(pp, spec);
           const double lam = c.lam;
-          consume<kStagesY, kTileY, kTileY>(orig, pp, -1, [&](const WTile& wt) {
+          auto body = [&](const WTile& wt) {
             if (wt.wcnt == kSegY) spx_final_tile<L1, true>(p, wt, copy, lam);
             else spx_final_tile<L1, false>(p, wt, copy, lam);
-          });
+          };
+          if (dyn) consume_final_dyn<kStagesY, kTileY, kTileY>(p.n, pp, kSpecDepthY, s_tix, body);
+          else consume<kStagesY, kTileY, kTileY>(orig, pp, -1, body);
         }
       } else if (!producer) {
         drain<kStagesY>(pp, spec);
       }
-      if (blockIdx.x <= 1) {  // uniform per CTA
+      if (p.sync.timeline) {  // uniform: CTA 0 / 1 end, and the last CTA's end
         __syncthreads();
-        if (threadIdx.x == 0) tl_mark(p.sync, epoch, 11 + 2 * blockIdx.x);
+        if (threadIdx.x == 0 && epoch < (unsigned)kTimelineCap) {
+          if (blockIdx.x <= 1) tl_mark(p.sync, epoch, 11 + 2 * blockIdx.x);
+          atomicMax(reinterpret_cast<unsigned long long*>(p.sync.timeline + kTimelineCols * epoch + 15),
+                    globaltimer());
+        }
       }
       break;
     }

@@ -74,13 +74,13 @@ for k in range(1, len(tl)):
     prev = t
     last = t
 # the final pass's row (the epoch after the last decision): CTA 0 / CTA 1 start, end
-if kind not in ("weak", "corr", "unc", "jac"):
+if True:
     rel = int(max(tl[1:, 5]))  # the last release
     fr = [r_ for r_ in tl[1:] if r_[11]]
     if fr:
         fr = fr[-1]
         for k_, r_ in enumerate(tl[1:], 1):
-            if r_[15]:
+            if kind not in ("weak", "corr", "unc", "jac") and r_[15] and r_[14]:
                 print(json.dumps({"tail_entry_row": k_, "decided_to_drained_us": round((int(r_[14]) - int(r_[3])) / 1e3, 2),
                                   "gather_us": round((int(r_[15]) - int(r_[14])) / 1e3, 2),
                                   "first_iter_us": round((int(tl[k_ + 1][3]) - int(r_[15])) / 1e3, 2)}))
@@ -88,7 +88,7 @@ if kind not in ("weak", "corr", "unc", "jac"):
                                         "m_end": round((int(fr[11]) - rel) / 1e3, 2),
                                         "c1_start": round((int(fr[12]) - rel) / 1e3, 2) if fr[12] else None,
                                         "c1_end": round((int(fr[13]) - rel) / 1e3, 2) if fr[13] else None,
-                                        "kernel_end_after_release_us": None}}))
+                                        "last_cta_end": round((int(fr[15]) - rel) / 1e3, 2) if fr[15] else None}}))
 tot_ms = out.stats["device_ms"]
 final_us = tot_ms * 1e3 - (last - t0) / 1e3
 rows.append({"phase": "final(+launch)", "elems": n, "us": round(final_us, 1),
