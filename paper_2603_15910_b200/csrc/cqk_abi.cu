@@ -457,16 +457,15 @@ bool getenv_flag(const char* name) {
 // The masterless grid step for a single-GPU persistent TMA launch of `grid`
 // CTAs (one CTA per SM; the buffers hold sm_count + 8 rows).
 GridAR masterless(cqk_handle* h, int grid, const Exchange& ex) {
-  GridAR ar{nullptr, nullptr, nullptr, nullptr, nullptr};
+  GridAR ar{nullptr, nullptr, nullptr, nullptr, nullptr, 0};
   if (ex.world > 1 || grid > h->sm_count + 8 || getenv_flag("CQK_MASTER_STEP")) return ar;
   const int k = (int)(h->ar_seq++ & 1u);
   ar.rows = h->ar_rows;
   ar.count = h->ar_count + k;
   ar.count_next = h->ar_count + (k ^ 1);
-  if (!getenv_flag("CQK_STATIC_FINAL")) {
-    ar.tiles = h->ar_count + 2 + k;
-    ar.tiles_next = h->ar_count + 2 + (k ^ 1);
-  }
+  ar.tiles = h->ar_count + 2 + k;
+  ar.tiles_next = h->ar_count + 2 + (k ^ 1);
+  ar.dyn_final = !getenv_flag("CQK_STATIC_FINAL");
   return ar;
 }
 

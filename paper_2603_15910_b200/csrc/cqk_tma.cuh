@@ -759,7 +759,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
     if (c.phase == PH_FINAL) {
       if (blockIdx.x <= 1 && threadIdx.x == 0) tl_mark(p.sync, epoch, 10 + 2 * blockIdx.x);
       const bool reuse = spec > 0 && !s_spec_scr;  // the speculated tiles are the final's
-      const bool dyn = p.ar.tiles != nullptr;        // single GPU: dynamic tile assignment
+      const bool dyn = p.ar.dyn_final != 0;          // single GPU: dynamic tile assignment
       const int D = kSpecDepthC;                     // its static prefix: the speculation's tiles
       if (p.x) {
         if (prod_lane) {

@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
     if (c.phase == PH_FINAL || c.phase == PH_COPY) {
       if (blockIdx.x <= 1 && threadIdx.x == 0) tl_mark(p.sync, epoch, 10 + 2 * blockIdx.x);
       const bool reuse = spec > 0 && !s_spec_scr;
-      const bool dyn = p.ar.tiles != nullptr;  // single GPU: dynamic tile assignment (cqk_tma.cuh)
+      const bool dyn = p.ar.dyn_final != 0;  // single GPU: dynamic tile assignment (cqk_tma.cuh)
       if (p.x) {
         const bool copy = c.phase == PH_COPY;
         if (prod_lane) {

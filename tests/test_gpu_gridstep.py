@@ -117,3 +117,26 @@ def test_masterless_step_on_reduced_grids(ctas, tma_engine):
     assert abs(out.lam - ref["lam"]) <= TOL * max(1.0, abs(ref["lam"]))
     assert out.fixed_count == ref["fixed_count"]
     assert abs(sp.lam - sref["lam"]) <= TOL * max(1.0, abs(sref["lam"]))
+
+
+def _with_env(name, fn):
+    os.environ[name] = "1"
+    try:
+        return fn()
+    finally:
+        os.environ.pop(name, None)
+
+
+@pytest.mark.parametrize("n", [1, 959, 960, 961, 3841, 2000003])
+def test_dynamic_and_static_final_pass_agree(n, tma_engine):
+    """The final pass hands out tiles dynamically on one GPU; x is a
+    per-element map, so it must equal the static walk's bit for bit."""
+    p = P()
+    d, a, b, l, u, r = p.instances.gen_cqk_arrays("cqk-weakly-correlated", n, 9)
+    inst = p.CqkInstance(d=d, a=a, b=b, l=l, u=u, r=r)
+    dyn = p.solve_cqk(inst)
+    sta = _with_env("CQK_STATIC_FINAL", lambda: p.solve_cqk(inst))
+    same(dyn, sta)
+    y = p.gen_simplex_y("simplex-n01", n, 9)
+    for f in (lambda: p.newton_project_simplex(y, 1.0), lambda: p.simplex.project_l1_outcome(y, 1.0)):
+        same(f(), _with_env("CQK_STATIC_FINAL", f))
