@@ -458,7 +458,7 @@ bool getenv_flag(const char* name) {
 // CTAs (one CTA per SM; the buffers hold sm_count + 8 rows).
 GridAR masterless(cqk_handle* h, int grid, const Exchange& ex) {
   GridAR ar{nullptr, nullptr, nullptr, nullptr, nullptr, 0};
-  if (ex.world > 1 || grid > h->sm_count + 8 || getenv_flag("CQK_MASTER_STEP")) return ar;
+  if (grid > h->sm_count + 8 || getenv_flag("CQK_MASTER_STEP")) return ar;
   const int k = (int)(h->ar_seq++ & 1u);
   ar.rows = h->ar_rows;
   ar.count = h->ar_count + k;

@@ -810,7 +810,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
       if (is_master && threadIdx.x == 0) {
         tl_record(dsync, epoch, PH_LAMBDA0, p.n, 0);
         double glob[15];
-        if (exchange_totals(p.ex, epoch, 15, ops, s_tot, glob)) m_after_lambda0(s_st, glob);
+        if (exchange_totals(p.ex, epoch, 15, ops, s_tot, glob, master)) m_after_lambda0(s_st, glob);
         else m_stop(s_st, ST_TIMEOUT);
       }
     } else if (c.phase == PH_SCAN && c.check_lu) {
@@ -829,7 +829,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
 #pragma unroll
         for (int k = 0; k < kMaxK; ++k) loc[k] = s_tot[k];
         tl_record(dsync, epoch, PH_SCAN, s_st.phys_count, 0);
-        if (!exchange_totals(p.ex, epoch, kMaxK, ops, loc, glob)) {
+        if (!exchange_totals(p.ex, epoch, kMaxK, ops, loc, glob, master)) {
           m_stop(s_st, ST_TIMEOUT);
         } else {
           s_st.cmd.check_lu = 0;
@@ -886,7 +886,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
 #pragma unroll
         for (int k = 0; k < 11; ++k) loc[k] = glob[k] = k < K ? s_tot[k] : 0.0;
         tl_record(dsync, epoch, PH_SCAN, s_st.phys_count, s_st.cmd.compact);
-        if (exchange_totals(p.ex, epoch, K, ops, loc, glob)) m_after_scan(s_st, glob, loc, dtrace);
+        if (exchange_totals(p.ex, epoch, K, ops, loc, glob, master)) m_after_scan(s_st, glob, loc, dtrace);
         else m_stop(s_st, ST_TIMEOUT);
       }
     } else if (c.phase == PH_BP) {
@@ -901,7 +901,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
       if (is_master && threadIdx.x == 0) {
         tl_record(dsync, epoch, PH_BP, s_st.phys_count, 0);
         double glob[2];
-        if (exchange_totals(p.ex, epoch, 2, ops, s_tot, glob)) m_after_bp(s_st, glob);
+        if (exchange_totals(p.ex, epoch, 2, ops, s_tot, glob, master)) m_after_bp(s_st, glob);
         else m_stop(s_st, ST_TIMEOUT);
       }
     } else {

@@ -458,7 +458,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
       if (is_master) {
         tl_record(dsync, epoch, c.phase, mode == 0 ? p.n : s_st.phys_count, s_st.cmd.compact);
         double loc[3] = {s_tot[0], s_tot[1], s_tot[2]}, glob[3];
-        if (!exchange_totals(p.ex, epoch, 3, ops, loc, glob)) {
+        if (!exchange_totals(p.ex, epoch, 3, ops, loc, glob, master)) {
           s_st.status = ST_TIMEOUT;
           s_st.cmd.phase = PH_DONE;
         } else if (mode == 0) s_after_init(s_st, glob);
