@@ -140,3 +140,37 @@ def test_dynamic_and_static_final_pass_agree(n, tma_engine):
     y = p.gen_simplex_y("simplex-n01", n, 9)
     for f in (lambda: p.newton_project_simplex(y, 1.0), lambda: p.simplex.project_l1_outcome(y, 1.0)):
         same(f(), _with_env("CQK_STATIC_FINAL", f))
+
+
+def test_counters_survive_interleaved_kernels(tma_engine):
+    """Both persistent TMA kernels share a handle's alternating arrival and
+    final-tile counters; interleave them (and the rows kernel, and static /
+    master-step launches) and check every result."""
+    p = P()
+    y = p.gen_simplex_y("simplex-n01", 300007, 4)
+    lam0 = min((1.0 - float(O.pairwise_sum(y))) / y.size, 1.0 - float(y.max()))
+    sref = O.newton_project_simplex(y, 1.0, lam0=lam0)
+    d, a, b, l, u, r = p.instances.gen_cqk_arrays("cqk-correlated", 300007, 4)
+    inst = p.CqkInstance(d=d, a=a, b=b, l=l, u=u, r=r)
+    ref = O.solve_cqk(d, a, b, l, u, r, fixing=True)
+    Y = p.gen_simplex_y("simplex-n01", 64 * 512, 4).reshape(64, 512)
+    X0 = np.asarray(p.project_simplex_rows(Y, 1.0)[0])
+
+    def check_cqk(out):
+        assert abs(out.lam - ref["lam"]) <= TOL * max(1.0, abs(ref["lam"]))
+        assert out.fixed_count == ref["fixed_count"]
+
+    def check_spx(out):
+        assert abs(out.lam - sref["lam"]) <= TOL * max(1.0, abs(sref["lam"]))
+        assert np.array_equal(out.x, np.maximum(0.0, y + out.lam))
+
+    def check_rows(out):
+        assert np.array_equal(np.asarray(out[0]), X0)
+
+    steps = [(lambda: p.solve_cqk(inst), check_cqk),
+             (lambda: p.newton_project_simplex(y, 1.0, start="tight"), check_spx),
+             (lambda: p.project_simplex_rows(Y, 1.0), check_rows)]
+    for k in range(12):
+        call, check = steps[(k * 5) % 3]
+        env = (None, "CQK_STATIC_FINAL", None, "CQK_MASTER_STEP")[k % 4]
+        check(call() if env is None else _with_env(env, call))
