@@ -175,7 +175,7 @@ class Marshal:
                     continue
                 if not _is_torch(a) or not a.is_cuda:
                     raise ValueError("mixing CUDA tensors with host arrays is not supported")
-                t = a.to(torch.float64).contiguous()
+                t = a if a.dtype == torch.float64 and a.is_contiguous() else a.to(torch.float64).contiguous()
                 dev = t.device if dev is None else dev
                 self.keep.append(t)
                 self.ptrs.append(t.data_ptr())

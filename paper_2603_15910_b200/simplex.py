@@ -49,7 +49,7 @@ def _alg2(y, r, idx, xbar, sharpened, workers):
 
     yv, dt, dev = _prep(y)
     n = int(yv.shape[0])
-    h = N.handle(yv.device.index if dev else None)
+    h = N.handle(yv.get_device() if dev else None)
     import torch
 
     if dev:
@@ -123,6 +123,8 @@ def _prep(y):
         if not y.is_cuda:
             y = y.numpy()
         else:
+            if y.dtype == torch.float64 and y.is_contiguous():  # the common case: no dispatch
+                return y, np.float64, True
             dt = np.float32 if y.dtype == torch.float32 else np.float64
             return y.to(torch.float64).contiguous(), dt, True
     y = np.ascontiguousarray(y)
@@ -145,7 +147,7 @@ def _project(y, r, opts, lambda0, trace, l1, start="auto", xbar=None, sharpened=
         if not bool((xb >= 0).all()) and not l1:
             raise DomainError("xbar", None, "warm-start estimate must be >= 0")
     n = int(yv.shape[0])
-    h = N.handle(yv.device.index if dev else None)
+    h = N.handle(yv.get_device() if dev else None)
     if dev:
         import torch
 
