@@ -187,6 +187,16 @@ int spx_project_batched_f64(cqk_handle *h, int mem, const double *Y, int64_t row
                             int64_t cols, double r, const cqk_options *opts, double *X,
                             double *lam, int32_t *iters, cqk_result *res);
 
+/* Batched rows split across GPUs (replicas, no communication):
+   host Y / X (row-major), rows cut into nh contiguous blocks (block q = rows
+   [rows*q/nh, rows*(q+1)/nh)), block q solved by handle hs[q] -- one host
+   thread per handle, all devices concurrently.  Per-row results are those of
+   spx_project_batched_f64 on the same row.  res: summed byte counters,
+   device_ms = the slowest block. */
+int spx_project_batched_multi_f64(cqk_handle *const *hs, int nh, const double *Y, int64_t rows,
+                                  int64_t cols, double r, const cqk_options *opts, double *X,
+                                  double *lam, int32_t *iters, cqk_result *res);
+
 /* Multi-GPU (one process / handle per GPU, n sharded contiguously) -------------
    Replaces the reference's chunked fork-join (parallel.py:174-327, chunks =
    _chunk_ranges parallel.py:82-85, fixed-order _tree_sum parallel.py:62-72)
@@ -249,6 +259,13 @@ int cqk_gen_cqk_device_range(cqk_handle *h, int family, int64_t n, uint64_t seed
 int cqk_gen_simplex_u01_device(cqk_handle *h, int64_t n, uint64_t seed, double *y);
 
 /* Diagnostics ------------------------------------------------------------------ */
+/* Read-only HBM streaming ceiling: `narr` (1..5) device arrays of n doubles
+   streamed by a bulk-copy pipeline (one CTA per SM) `reps` times after one
+   warm-up; best GB/s (and ms).  The roofline's second denominator (SURVEY
+   8(d): the phi passes are reads, MEASURED_PEAKS.json's peak is a copy).
+   `arrays` is a host array of device pointers. */
+int cqk_read_peak_f64(cqk_handle *h, const double *const *arrays, int narr, int64_t n, int reps,
+                      double *gbs_best, double *ms_best);
 /* Bitwise check of the solver's shared-reciprocal division against the IEEE
    library division on `count` random operand pairs (mode 0: exponents in
    [-500, 500]; 1: solver-like ranges; 2: quotients at rounding boundaries). */

@@ -41,8 +41,9 @@ class Result(ctypes.Structure):
 
 def build(force=False):
     """Compile the oracle with its Makefile (gcc, OpenMP)."""
-    if force or not os.path.exists(LIB_PATH) or (
-        os.path.getmtime(LIB_PATH) < os.path.getmtime(os.path.join(_HERE, "cqk_oracle.c"))
+    srcs = ("cqk_oracle.c", "cqk_gen.c", "cqk_oracle.h")
+    if force or not os.path.exists(LIB_PATH) or any(
+        os.path.getmtime(LIB_PATH) < os.path.getmtime(os.path.join(_HERE, f)) for f in srcs
     ):
         subprocess.check_call(["make", "-s", "-C", _HERE])
     return LIB_PATH
@@ -85,6 +86,10 @@ def lib():
         L.orc_newton_simplex_from.argtypes = [_D, i64, dbl, i32, i64, dbl, dbl, _I64, i64, _D, R]
         L.orc_exact_simplex_lambda.argtypes = [_D, i64, dbl]
         L.orc_exact_simplex_lambda.restype = dbl
+        L.orc_project_simplex_rows.argtypes = [_D, i64, i64, dbl, i32, _D, _D, _I64]
+        L.orc_project_simplex_rows.restype = i64
+        L.orc_gen_cqk.argtypes = [i32, i64, ctypes.c_uint64] + [_D] * 6
+        L.orc_gen_simplex_y.argtypes = [i32, i64, ctypes.c_uint64, _D]
         _lib = L
     return _lib
 
@@ -285,3 +290,40 @@ def newton_simplex_from(y, r, lam0, free, fixing=True, max_iter=100, tau=TAU64, 
                                        float(tau), float(lam0), _p(f, _I64), f.size, _p(x),
                                        ctypes.byref(res))
     return _finish(st, res, x)
+
+
+def project_simplex_rows(Y, r, threads=1, want_x=True):
+    """newton_project_simplex per row (OpenMP over rows) -> (X, lam, iterations, failed)."""
+    Y = np.ascontiguousarray(Y, dtype=np.float64)
+    rows, cols = Y.shape
+    X = np.empty_like(Y) if want_x else None
+    lam = np.empty(rows)
+    its = np.empty(rows, np.int64)
+    bad = lib().orc_project_simplex_rows(_p(Y), rows, cols, float(r), int(threads), _p(X), _p(lam),
+                                         _p(its, _I64))
+    return X, lam, its, int(bad)
+
+
+CQK_FAMILIES = ("cqk-uncorrelated", "cqk-weakly-correlated", "cqk-correlated")
+SIMPLEX_FAMILIES = ("simplex-u01", "simplex-n01", "simplex-n0m3")
+
+
+def gen_cqk(family, n, seed):
+    """instances.py:43-70 (cqk_gen.c): (d, a, b, l, u, r), r from pairwise dots."""
+    arrs = [np.empty(int(n)) for _ in range(5)]
+    r = ctypes.c_double()
+    rc = lib().orc_gen_cqk(CQK_FAMILIES.index(family), int(n), int(seed) & (2**64 - 1),
+                           *[_p(v) for v in arrs], ctypes.byref(r))
+    if rc != 0:
+        raise ValueError(f"orc_gen_cqk failed ({rc})")
+    return (*arrs, r.value)
+
+
+def gen_simplex_y(family, n, seed):
+    """instances.py:73-86 (cqk_gen.c)."""
+    y = np.empty(int(n))
+    rc = lib().orc_gen_simplex_y(SIMPLEX_FAMILIES.index(family), int(n), int(seed) & (2**64 - 1),
+                                 _p(y))
+    if rc != 0:
+        raise ValueError(f"orc_gen_simplex_y failed ({rc})")
+    return y

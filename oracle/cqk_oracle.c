@@ -960,3 +960,22 @@ double orc_exact_simplex_lambda(const double *y, int64_t n, double r) {
   free(ys); free(cs);
   return lam;
 }
+
+/* Batched rows (C5; no reference function): newton_project_simplex(Y[i], r)
+ * (simplex.py:218-308, default Algorithm-2 start) per row, rows spread over
+ * `threads` OpenMP threads.  Returns the number of rows that did not solve. */
+int64_t orc_project_simplex_rows(const double *Y, int64_t rows, int64_t cols, double r,
+                                 int threads, double *X, double *lam, int64_t *iters) {
+  int64_t bad = 0;
+  const double tau = pow(2.220446049250313e-16, 0.75); /* newton.py:64-67 */
+#pragma omp parallel for schedule(dynamic, 64) num_threads(threads > 0 ? threads : 1) reduction(+ : bad)
+  for (int64_t i = 0; i < rows; ++i) {
+    orc_result res;
+    const int st = orc_newton_project_simplex(Y + i * cols, cols, r, 1, 100, tau, NULL, 0, NAN,
+                                              X ? X + i * cols : NULL, NULL, 0, &res);
+    if (lam) lam[i] = res.lam;
+    if (iters) iters[i] = res.iterations;
+    bad += st != ORC_SOLVED;
+  }
+  return bad;
+}

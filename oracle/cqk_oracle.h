@@ -136,6 +136,16 @@ int orc_project_l1(const double *y, int64_t n, double r, int fixing,
 /* oracle.py:88-97 oracle_simplex: lam of the sort-based exact projection */
 double orc_exact_simplex_lambda(const double *y, int64_t n, double r);
 
+/* C5 batched rows: orc_newton_project_simplex per row, OpenMP over rows;
+   returns the count of rows that did not solve */
+int64_t orc_project_simplex_rows(const double *Y, int64_t rows, int64_t cols, double r,
+                                 int threads, double *X, double *lam, int64_t *iters);
+
+/* cqk_gen.c: instances.py:43-86 generators, sequential (r from pairwise dots) */
+int orc_gen_cqk(int family, int64_t n, uint64_t seed, double *d, double *a, double *b,
+                double *l, double *u, double *r);
+int orc_gen_simplex_y(int family, int64_t n, uint64_t seed, double *y);
+
 #ifdef __cplusplus
 }
 #endif

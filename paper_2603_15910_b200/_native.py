@@ -89,7 +89,8 @@ EXPORTS = (
     "cqk_comm_ipc_handle_size", "cqk_comm_create", "cqk_comm_connect", "cqk_comm_connect_local",
     "cqk_set_grid_limit", "cqk_set_engine", "cqk_reserve", "cqk_reserve_host", "cqk_solve_sharded_f64", "spx_project_sharded_f64",
     "l1_project_sharded_f64", "spx_init_alg2_f64", "cqk_gen_cqk_device",
-    "cqk_gen_cqk_device_range", "cqk_gen_simplex_u01_device",
+    "cqk_gen_cqk_device_range", "cqk_gen_simplex_u01_device", "spx_project_batched_multi_f64",
+    "cqk_read_peak_f64",
 )
 
 _lib = None
@@ -155,6 +156,10 @@ def _declare(L):
                                            ctypes.POINTER(_D)]
     L.spx_project_batched_f64.argtypes = [_P, ctypes.c_int, _P, _I64, _I64, _D, _OPT, _P, _P,
                                           _P, _RES]
+    L.spx_project_batched_multi_f64.argtypes = [_P, ctypes.c_int, _P, _I64, _I64, _D, _OPT, _P,
+                                                _P, _P, _RES]
+    L.cqk_read_peak_f64.argtypes = [_P, _P, ctypes.c_int, _I64, ctypes.c_int, ctypes.POINTER(_D),
+                                    ctypes.POINTER(_D)]
 
 
 def load_library(path=None):
@@ -244,6 +249,19 @@ class Handle:
         got = self.lib.cqk_get_timeline(self.ptr, out.ctypes.data, int(rows))
         return out[: max(got, 0)]
 
+    def read_peak(self, tensors, reps=5):
+        """Read-only streaming ceiling (GB/s, ms) over equal-length fp64 CUDA
+        tensors on this handle's device (cqk_read_peak_f64)."""
+        n = int(tensors[0].numel())
+        arr = (_P * len(tensors))(*[t.data_ptr() for t in tensors])
+        gbs, ms = _D(), _D()
+        self.use_current_stream()
+        rc = self.lib.cqk_read_peak_f64(self.ptr, arr, len(tensors), n, int(reps), ctypes.byref(gbs),
+                                        ctypes.byref(ms))
+        if rc != 0:
+            raise NativeError(f"cqk_read_peak_f64 failed ({rc}): {last_error()}")
+        return gbs.value, ms.value
+
     def __del__(self):
         try:
             if getattr(self, "ptr", None):
@@ -276,6 +294,20 @@ def handle(device=None):
     if h is None:
         h = cache[device] = Handle(device)
     return h
+
+
+def handle_set(devices):
+    """One distinct handle per list entry (a device may appear several
+    times), cached per thread -- for calls that drive several handles at once
+    (spx_project_batched_multi_f64)."""
+    key = tuple(devices)
+    cache = getattr(_tls, "sets", None)
+    if cache is None:
+        cache = _tls.sets = {}
+    hs = cache.get(key)
+    if hs is None:
+        hs = cache[key] = [Handle(d) for d in devices]
+    return hs
 
 
 _OPTS_CACHE = {}

@@ -15,12 +15,14 @@
 #include <limits>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/cqk_b200.h"
 #include "cqk_kernels.cuh"
 #include "cqk_tma.cuh"
 #include "cqk_tma_spx.cuh"
+#include "cqk_diag.cuh"
 
 using namespace cqk;
 
@@ -117,6 +119,8 @@ struct cqk_handle {
   int grid_limit = 0;                 // 0: full device (virtual ranks share a GPU)
   void* host_state = nullptr;         // pinned + mapped: the kernels' final state (and Alg2Out)
   void* host_state_dev = nullptr;     // ... its device alias
+  volatile int* host_err = nullptr;   // mapped word after the state: any CTA's spin timeout
+  int* host_err_dev = nullptr;        // ... its device alias
   // multi-GPU communicator (one rank per GPU; mailboxes in device memory)
   int rank = 0, world = 1;
   double* mbox = nullptr;             // this rank's mailbox
@@ -200,8 +204,14 @@ int cqk_create(cqk_handle** out, int device) {
   e = e ? e : cudaMalloc(&h->ar_rows, sizeof(double) * 2 * kMaxK * (h->sm_count + 8));
   e = e ? e : cudaMalloc(&h->ar_count, 64);
   e = e ? e : cudaMemset(h->ar_count, 0, 64);
-  e = e ? e : cudaHostAlloc(&h->host_state, st_bytes, cudaHostAllocMapped | cudaHostAllocPortable);
+  const size_t st_pad = (st_bytes + 63) / 64 * 64;
+  e = e ? e : cudaHostAlloc(&h->host_state, st_pad + 64, cudaHostAllocMapped | cudaHostAllocPortable);
   e = e ? e : cudaHostGetDevicePointer(&h->host_state_dev, h->host_state, 0);
+  if (e == cudaSuccess) {
+    h->host_err = (volatile int*)((char*)h->host_state + st_pad);
+    h->host_err_dev = (int*)((char*)h->host_state_dev + st_pad);
+    *h->host_err = 0;
+  }
   e = e ? e : set_prefetch();
   e = e ? e : cudaEventCreate(&h->ev0);
   e = e ? e : cudaEventCreate(&h->ev1);
@@ -441,7 +451,9 @@ int finish_sync(cqk_handle* h) {
 // several handles can run concurrent persistent kernels, e.g. virtual ranks on
 // one GPU).  A state still RUNNING was never published: the grid aborted.
 int check_timeout(cqk_handle* h, int32_t status, int32_t err) {
-  if (status != ST_RUNNING && !err) return 0;
+  const bool any_cta = *h->host_err != 0;  // a CTA that timed out alone (its rows unwritten)
+  *h->host_err = 0;
+  if (status != ST_RUNNING && !err && !any_cta) return 0;
   cudaMemsetAsync(h->sync, 0, 64, h->stream);
   cudaMemsetAsync(h->ar_count, 0, 64, h->stream);
   cudaMemsetAsync(h->hist, 0, sizeof(int32_t) * 2 * kHistB, h->stream);  // may hold a partial scan
@@ -551,10 +563,10 @@ extern "C" int cqk_comm_create(cqk_handle* h, int rank, int world, void* ipc_han
   if (!h || world < 1 || world > kMaxRanks || rank < 0 || rank >= world)
     return set_err(CQK_E_ARG, "need 0 <= rank < world <= 8");
   CUDA_TRY(cudaSetDevice(h->device));
-  if (!h->mbox) {
-    CUDA_TRY(cudaMalloc(&h->mbox, sizeof(double) * kMboxDoubles));
-    CUDA_TRY(cudaMemset(h->mbox, 0, sizeof(double) * kMboxDoubles));
-  }
+  if (!h->mbox) CUDA_TRY(cudaMalloc(&h->mbox, sizeof(double) * kMboxDoubles));
+  // a fresh group restarts its solve sequence at 1: no flag of an earlier
+  // group (e.g. one abandoned after a timeout) may survive to match it
+  CUDA_TRY(cudaMemset(h->mbox, 0, sizeof(double) * kMboxDoubles));
   h->rank = rank;
   h->world = world;
   h->seq = 0;
@@ -588,10 +600,25 @@ extern "C" int cqk_comm_connect(cqk_handle* h, const void* handles) {
 
 extern "C" int cqk_comm_connect_local(cqk_handle* h, cqk_handle* const* ranks, int world) {
   if (!h || !ranks || world != h->world) return set_err(CQK_E_ARG, "bad local rank table");
-  for (int q = 0; q < world; ++q) {
+  for (int q = 0; q < world; ++q)
     if (!ranks[q] || !ranks[q]->mbox) return set_err(CQK_E_ARG, "peer without mailbox");
-    h->peers[q] = ranks[q]->mbox;
+  // this rank's kernel stores into every peer's mailbox: a peer on another
+  // device must be reachable (NVLink P2P) and mapped into this device's
+  // address space before any solve
+  CUDA_TRY(cudaSetDevice(h->device));
+  for (int q = 0; q < world; ++q) {
+    const int pd = ranks[q]->device;
+    if (pd == h->device) continue;
+    int can = 0;
+    CUDA_TRY(cudaDeviceCanAccessPeer(&can, h->device, pd));
+    if (!can)
+      return set_err(CQK_E_ARG, "device " + std::to_string(h->device) + " cannot access device " +
+                                    std::to_string(pd) + " (no P2P): local groups need peer access");
+    cudaError_t e = cudaDeviceEnablePeerAccess(pd, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+    else if (e != cudaSuccess) return set_err(CQK_E_CUDA, std::string("cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(e));
   }
+  for (int q = 0; q < world; ++q) h->peers[q] = ranks[q]->mbox;
   return 0;
 }
 
@@ -710,6 +737,7 @@ static int solve_impl(cqk_handle* h, int mem, const double* d, const double* a, 
   p.sync.gen = h->sync + 1;
   p.sync.error = (int*)(h->sync + 2);
   p.sync.timeline = h->timeline;
+  p.sync.herr = h->host_err_dev;
   void* args[] = {&p};
   int grid;
   const void* fn;
@@ -789,6 +817,7 @@ int launch_spx(cqk_handle* h, SpxState& s, const double* yv, int64_t n, double* 
   p.sync.gen = h->sync + 1;
   p.sync.error = (int*)(h->sync + 2);
   p.sync.timeline = h->timeline;
+  p.sync.herr = h->host_err_dev;
   {
     const char* te = getenv("CQK_TAIL");
     p.wcnt = (tma && !sharded && !(te && te[0] == '0')) ? h->wcnt : nullptr;
@@ -1239,6 +1268,53 @@ extern "C" int spx_project_batched_f64(cqk_handle* h, int mem, const double* Y, 
   return 0;
 }
 
+// C5 across GPUs ("batched rows: replicas only"): contiguous
+// row blocks, one per handle, solved concurrently -- one host thread per
+// handle drives its own device, stream, staging ring and kernel; no
+// communication.  Each block is an ordinary spx_project_batched_f64 call, so
+// a row's result does not depend on the split.
+extern "C" int spx_project_batched_multi_f64(cqk_handle* const* hs, int nh, const double* Y,
+                                             int64_t rows, int64_t cols, double r,
+                                             const cqk_options* opts, double* X, double* lam,
+                                             int32_t* iters, cqk_result* res) {
+  if (!hs || nh < 1 || !Y || !X || !res) return set_err(CQK_E_ARG, "null argument");
+  for (int q = 0; q < nh; ++q)
+    if (!hs[q]) return set_err(CQK_E_ARG, "null handle in the device list");
+  std::memset(res, 0, sizeof *res);
+  res->domain_index = -1;
+  if (rows < 1) return set_err(CQK_E_ARG, "rows >= 1 required");
+  std::vector<cqk_result> part((size_t)nh);
+  std::vector<int> rc((size_t)nh, 0);
+  std::vector<std::string> err((size_t)nh);
+  std::vector<std::thread> th;
+  for (int q = 0; q < nh; ++q) {
+    const int64_t lo = rows * q / nh, hi = rows * (q + 1) / nh;
+    if (hi == lo) continue;
+    th.emplace_back([&, q, lo, hi] {
+      rc[q] = spx_project_batched_f64(hs[q], CQK_MEM_HOST, Y + lo * cols, hi - lo, cols, r, opts,
+                                      X + lo * cols, lam ? lam + lo : nullptr,
+                                      iters ? iters + lo : nullptr, &part[q]);
+      if (rc[q] != 0) err[q] = g_err;  // thread_local: carry it to the caller's thread
+    });
+  }
+  for (auto& t : th) t.join();
+  for (int q = 0; q < nh; ++q) {
+    if (rc[q] != 0) {
+      *res = part[q];
+      return set_err(rc[q], "device list entry " + std::to_string(q) + ": " + err[q]);
+    }
+  }
+  res->status = CQK_SOLVED;
+  for (int q = 0; q < nh; ++q) {
+    res->elems_read += part[q].elems_read;
+    res->elems_written += part[q].elems_written;
+    res->bytes_model += part[q].bytes_model;
+    res->device_ms = std::max(res->device_ms, part[q].device_ms);  // concurrent: the slowest
+    res->launches += part[q].launches;
+  }
+  return 0;
+}
+
 // ------------------------------------------------------------ components
 extern "C" int cqk_phi_f64(cqk_handle* h, int mem, const double* d, const double* a,
                            const double* b, const double* l, const double* u, int64_t n,
@@ -1425,6 +1501,40 @@ extern "C" int cqk_selftest_division(cqk_handle* h, uint64_t seed, int64_t count
   if (e != cudaSuccess) return set_err(CQK_E_CUDA, cudaGetErrorString(e));
   *mismatches = m;
   if (example2) { example2[0] = ex[0]; example2[1] = ex[1]; }
+  return 0;
+}
+
+// ------------------------------------------------------------ read-only peak
+extern "C" int cqk_read_peak_f64(cqk_handle* h, const double* const* arrays, int narr, int64_t n,
+                                 int reps, double* gbs_best, double* ms_best) {
+  if (!h || !arrays || narr < 1 || narr > kPeakMaxArr || n < kPeakTile || reps < 1 || !gbs_best)
+    return set_err(CQK_E_ARG, "read peak: 1..5 device arrays of >= 2048 doubles");
+  CUDA_TRY(cudaSetDevice(h->device));
+  PeakArgs a;
+  std::memset(&a, 0, sizeof a);
+  for (int k = 0; k < narr; ++k) {
+    if (!arrays[k] || !aligned16(arrays[k])) return set_err(CQK_E_ARG, "read peak: bad array");
+    a.arr[k] = arrays[k];
+  }
+  a.narr = narr;
+  a.n = n;
+  a.sink = h->out;
+  const size_t smem = read_peak_smem();
+  CUDA_TRY(cudaFuncSetAttribute(read_peak_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  float best = 1e30f;
+  for (int r = 0; r <= reps; ++r) {  // the first launch warms up
+    CUDA_TRY(cudaEventRecord(h->ev0, h->stream));
+    read_peak_kernel<<<h->sm_count, kPeakThreads, smem, h->stream>>>(a);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaEventRecord(h->ev1, h->stream));
+    CUDA_TRY(cudaEventSynchronize(h->ev1));
+    float ms = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+    if (r > 0 && ms < best) best = ms;
+  }
+  const double bytes = (double)narr * (double)(n / kPeakTile * kPeakTile) * 8.0;
+  *gbs_best = bytes / (best * 1e-3) / 1e9;
+  if (ms_best) *ms_best = best;
   return 0;
 }
 

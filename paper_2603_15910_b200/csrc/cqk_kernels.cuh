@@ -123,7 +123,7 @@ DEVI bool grid_step(double* partials, const double* s_cta, const int (&ops)[K],
     unsigned polls = 0;
     while (ld_relaxed(sy.arrive) < gridDim.x) {  // relaxed polls, one acquire fence
       if ((++polls & 255u) == 0 && globaltimer() - t0 > kSpinTimeoutNs) {
-        atomicExch(sy.error, 1);
+        raise_timeout(sy);
         *s_abort = 1;
         break;
       }
@@ -204,7 +204,7 @@ DEVI bool ar_combine(const GridAR& ar, const int (&ops)[K], const GridSync& sy,
     unsigned polls = 0;
     while ((int)(ld_relaxed(ar.count) - target) < 0) {
       if ((++polls & 255u) == 0 && globaltimer() - t0 > kSpinTimeoutNs) {
-        atomicExch(sy.error, 1);
+        raise_timeout(sy);
         *s_abort = 1;
         break;
       }
@@ -283,7 +283,7 @@ DEVI bool wait_release(const GridSync& sy, unsigned target, const Cmd* gcmd, Cmd
   unsigned polls = 0;
   while ((int)(ld_relaxed(sy.gen) - target) < 0) {
     if ((++polls & 255u) == 0 && globaltimer() - t0 > kSpinTimeoutNs) {
-      atomicExch(sy.error, 1);
+      raise_timeout(sy);
       return false;
     }
   }
@@ -560,8 +560,11 @@ __global__ void __launch_bounds__(kThreads, 1) cqk_solve_kernel(CqkParams<T> p) 
       if (is_master && threadIdx.x == 0) {
         tl_record(p.sync, epoch, PH_LAMBDA0, p.n, 0);
         double glob[15];
-        if (exchange_totals(p.ex, epoch, 15, ops, s_tot, glob)) m_after_lambda0(s_st, glob);
-        else m_stop(s_st, ST_TIMEOUT);
+        if (exchange_totals_1(p.ex, epoch, 15, ops, s_tot, glob)) m_after_lambda0(s_st, glob);
+        else {
+          m_stop(s_st, ST_TIMEOUT);
+          raise_timeout(p.sync);
+        }
       }
     } else if (c.phase == PH_SCAN && c.check_lu) {
       // first scan (original arrays, never compacting) with validate()'s l / u checks
@@ -578,8 +581,9 @@ __global__ void __launch_bounds__(kThreads, 1) cqk_solve_kernel(CqkParams<T> p) 
 #pragma unroll
         for (int k = 0; k < kMaxK; ++k) loc[k] = s_tot[k];
         tl_record(p.sync, epoch, PH_SCAN, s_st.phys_count, 0);
-        if (!exchange_totals(p.ex, epoch, kMaxK, ops, loc, glob)) {
+        if (!exchange_totals_1(p.ex, epoch, kMaxK, ops, loc, glob)) {
           m_stop(s_st, ST_TIMEOUT);
+          raise_timeout(p.sync);
         } else {
           s_st.cmd.check_lu = 0;
           s_st.vidx[3] = glob[11];  // l NaN
@@ -607,8 +611,11 @@ __global__ void __launch_bounds__(kThreads, 1) cqk_solve_kernel(CqkParams<T> p) 
 #pragma unroll
         for (int k = 0; k < 11; ++k) loc[k] = glob[k] = k < K ? s_tot[k] : 0.0;
         tl_record(p.sync, epoch, PH_SCAN, s_st.phys_count, s_st.cmd.compact);
-        if (exchange_totals(p.ex, epoch, K, ops, loc, glob)) m_after_scan(s_st, glob, loc, p.trace);
-        else m_stop(s_st, ST_TIMEOUT);
+        if (exchange_totals_1(p.ex, epoch, K, ops, loc, glob)) m_after_scan(s_st, glob, loc, p.trace);
+        else {
+          m_stop(s_st, ST_TIMEOUT);
+          raise_timeout(p.sync);
+        }
       }
     } else if (c.phase == PH_BP) {
       acc[0] = c.right ? HUGE_VAL : -HUGE_VAL;
@@ -621,8 +628,11 @@ __global__ void __launch_bounds__(kThreads, 1) cqk_solve_kernel(CqkParams<T> p) 
       if (is_master && threadIdx.x == 0) {
         tl_record(p.sync, epoch, PH_BP, s_st.phys_count, 0);
         double glob[2];
-        if (exchange_totals(p.ex, epoch, 2, ops, s_tot, glob)) m_after_bp(s_st, glob);
-        else m_stop(s_st, ST_TIMEOUT);
+        if (exchange_totals_1(p.ex, epoch, 2, ops, s_tot, glob)) m_after_bp(s_st, glob);
+        else {
+          m_stop(s_st, ST_TIMEOUT);
+          raise_timeout(p.sync);
+        }
       }
     } else {
       break;
@@ -955,7 +965,8 @@ __global__ void __launch_bounds__(kThreads, 1) spx_solve_kernel(SpxParams<T> p) 
       if (is_master) {
         tl_record(p.sync, epoch, c.phase, mode == 0 ? p.n : s_st.phys_count, s_st.cmd.compact);
         double loc[3] = {s_tot[0], s_tot[1], s_tot[2]}, glob[3];
-        if (!exchange_totals(p.ex, epoch, 3, ops, loc, glob)) {
+        if (!exchange_totals_1(p.ex, epoch, 3, ops, loc, glob)) {
+          raise_timeout(p.sync);
           s_st.status = ST_TIMEOUT;
           s_st.cmd.phase = PH_DONE;
         } else if (mode == 0) s_after_init(s_st, glob);

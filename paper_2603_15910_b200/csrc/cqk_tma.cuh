@@ -807,11 +807,17 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
       block_reduce<15, kConsW>(a15, ops, s_red, s_tot);
       is_master = grid_step_any<15>(p.ar, p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch,
                                    [&] { if (prod_lane) speculate(); }, (c_tma_flags & 4) != 0);
-      if (is_master && threadIdx.x == 0) {
-        tl_record(dsync, epoch, PH_LAMBDA0, p.n, 0);
+      if (is_master && warp == 0) {
+        if (lane == 0) tl_record(dsync, epoch, PH_LAMBDA0, p.n, 0);
         double glob[15];
-        if (exchange_totals(p.ex, epoch, 15, ops, s_tot, glob, master)) m_after_lambda0(s_st, glob);
-        else m_stop(s_st, ST_TIMEOUT);
+        const bool ok = exchange_totals<15>(p.ex, epoch, ops, s_tot, glob, master);
+        if (lane == 0) {
+          if (ok) m_after_lambda0(s_st, glob);
+          else {
+            m_stop(s_st, ST_TIMEOUT);
+            raise_timeout(p.sync);
+          }
+        }
       }
     } else if (c.phase == PH_SCAN && c.check_lu) {
 #pragma unroll
@@ -824,13 +830,16 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
       block_reduce<kMaxK, kConsW>(acc, ops, s_red, s_tot);
       is_master = grid_step_any<kMaxK>(p.ar, p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch,
                                    [&] { if (prod_lane) speculate(); }, (c_tma_flags & 4) != 0);
-      if (is_master && threadIdx.x == 0) {
+      if (is_master && warp == 0) {
         double loc[kMaxK], glob[kMaxK];
 #pragma unroll
         for (int k = 0; k < kMaxK; ++k) loc[k] = s_tot[k];
-        tl_record(dsync, epoch, PH_SCAN, s_st.phys_count, 0);
-        if (!exchange_totals(p.ex, epoch, kMaxK, ops, loc, glob, master)) {
+        if (lane == 0) tl_record(dsync, epoch, PH_SCAN, s_st.phys_count, 0);
+        const bool ok = exchange_totals<kMaxK>(p.ex, epoch, ops, s_tot, glob, master);
+        if (lane != 0) {
+        } else if (!ok) {
           m_stop(s_st, ST_TIMEOUT);
+          raise_timeout(p.sync);
         } else {
           s_st.cmd.check_lu = 0;
           s_st.vidx[3] = glob[11];  // l NaN
@@ -881,13 +890,19 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
           speculate();
         }
       }, (c_tma_flags & 4) != 0);
-      if (is_master && threadIdx.x == 0) {
+      if (is_master && warp == 0) {
         double loc[11], glob[11];
 #pragma unroll
         for (int k = 0; k < 11; ++k) loc[k] = glob[k] = k < K ? s_tot[k] : 0.0;
-        tl_record(dsync, epoch, PH_SCAN, s_st.phys_count, s_st.cmd.compact);
-        if (exchange_totals(p.ex, epoch, K, ops, loc, glob, master)) m_after_scan(s_st, glob, loc, dtrace);
-        else m_stop(s_st, ST_TIMEOUT);
+        if (lane == 0) tl_record(dsync, epoch, PH_SCAN, s_st.phys_count, s_st.cmd.compact);
+        const bool ok = exchange_totals<K>(p.ex, epoch, ops, s_tot, glob, master);
+        if (lane == 0) {
+          if (ok) m_after_scan(s_st, glob, loc, dtrace);
+          else {
+            m_stop(s_st, ST_TIMEOUT);
+            raise_timeout(p.sync);
+          }
+        }
       }
     } else if (c.phase == PH_BP) {
       acc[0] = c.right ? HUGE_VAL : -HUGE_VAL;
@@ -898,11 +913,17 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
       block_reduce<2, kConsW>(a2, ops, s_red, s_tot);
       is_master = grid_step_any<2>(p.ar, p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch,
                                    [&] { if (prod_lane) speculate(); }, (c_tma_flags & 4) != 0);
-      if (is_master && threadIdx.x == 0) {
-        tl_record(dsync, epoch, PH_BP, s_st.phys_count, 0);
+      if (is_master && warp == 0) {
+        if (lane == 0) tl_record(dsync, epoch, PH_BP, s_st.phys_count, 0);
         double glob[2];
-        if (exchange_totals(p.ex, epoch, 2, ops, s_tot, glob, master)) m_after_bp(s_st, glob);
-        else m_stop(s_st, ST_TIMEOUT);
+        const bool ok = exchange_totals<2>(p.ex, epoch, ops, s_tot, glob, master);
+        if (lane == 0) {
+          if (ok) m_after_bp(s_st, glob);
+          else {
+            m_stop(s_st, ST_TIMEOUT);
+            raise_timeout(p.sync);
+          }
+        }
       }
     } else {
       break;

@@ -454,11 +454,17 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
       }
     }, (c_tma_flags & 4) != 0);
     if (is_master && mode == 1 && c.hist && p.hist) hist_bound(p, c.lam, s_st.r, s_hist, s_st);
+    double glob[3];
+    bool xok = true;
+    if (is_master && warp == 0) {  // the whole warp: the exchange is warp-level
+      if (lane == 0) tl_record(dsync, epoch, c.phase, mode == 0 ? p.n : s_st.phys_count, s_st.cmd.compact);
+      xok = exchange_totals<3>(p.ex, epoch, ops, s_tot, glob, master);
+    }
     if (threadIdx.x == 0) {
       if (is_master) {
-        tl_record(dsync, epoch, c.phase, mode == 0 ? p.n : s_st.phys_count, s_st.cmd.compact);
-        double loc[3] = {s_tot[0], s_tot[1], s_tot[2]}, glob[3];
-        if (!exchange_totals(p.ex, epoch, 3, ops, loc, glob, master)) {
+        double loc[3] = {s_tot[0], s_tot[1], s_tot[2]};
+        if (!xok) {
+          raise_timeout(p.sync);
           s_st.status = ST_TIMEOUT;
           s_st.cmd.phase = PH_DONE;
         } else if (mode == 0) s_after_init(s_st, glob);

@@ -219,6 +219,34 @@ class ShardedProjection:
                             stats=res.stats())
 
 
+    def solve_host(self, y_host, r, l1=False, opts=None, start="tight", x_out=None):
+        """Collective projection of this rank's shard given in HOST memory
+        (numpy, ideally page-locked): H2D, the persistent kernel, D2H of x."""
+        if not r > 0:
+            raise DomainError("r", None, "radius / level r must be positive")
+        if opts is None:
+            opts = SolverOptions()
+        h = self.handle
+        if not getattr(self, "_host_reserved", False):
+            rc = h.lib.cqk_reserve_host(h.ptr, int(self.y.numel()))
+            if rc != 0:
+                raise N.NativeError(f"cqk_reserve_host failed ({rc}): {N.last_error()}")
+            self._host_reserved = True
+        h.use_current_stream()
+        yv = np.ascontiguousarray(y_host, dtype=np.float64)
+        if x_out is None:
+            x_out = np.empty_like(yv)
+        o = N.make_options(opts, compact_ratio=getattr(opts, "compact_ratio", None), start=start,
+                           tau=opts.tau(np.float64))
+        res = N.Result()
+        fn = h.lib.l1_project_sharded_f64 if l1 else h.lib.spx_project_sharded_f64
+        rc = fn(h.ptr, N.MEM_HOST, yv.ctypes.data, int(yv.size), self.n_total, float(r), o,
+                x_out.ctypes.data, res)
+        if rc != 0:
+            raise N.NativeError(f"sharded projection failed ({rc}): {N.last_error()}")
+        return x_out, res.stats()
+
+
 def sharded_projection(comm, y_local, n_total, r, l1=False, opts=None):
     """One-shot collective projection (allocates; prefer ShardedProjection)."""
     return ShardedProjection(comm, y_local, n_total).solve(r, l1=l1, opts=opts)

@@ -251,8 +251,13 @@ def project_l1_outcome(y, r, opts=None, start="auto"):
                         fixed_count=int(res.fixed_count), stats=res.stats())
 
 
-def project_simplex_rows(Y, r, opts=None, lambda0=None, start="tight"):
+def project_simplex_rows(Y, r, opts=None, lambda0=None, start="tight", devices=None):
     """Row-wise newton_project_simplex(Y[i], r) for a 2-d array (B200 extension, K8).
+
+    devices (host Y only): a list of CUDA device ordinals; the rows are cut
+    into len(devices) contiguous blocks solved concurrently, one per device,
+    with no communication (spx_project_batched_multi_f64).  A
+    row's result does not depend on the split.
 
     Returns (X, lam[rows], iterations[rows], stats)."""
     if not r > 0:
@@ -260,6 +265,8 @@ def project_simplex_rows(Y, r, opts=None, lambda0=None, start="tight"):
     if opts is None:
         opts = SolverOptions()
     dev = _is_torch(Y) and Y.is_cuda
+    if devices is not None and dev:
+        raise ValueError("devices= splits a host array; for CUDA tensors call once per device")
     if dev:
         import torch
 
@@ -275,10 +282,6 @@ def project_simplex_rows(Y, r, opts=None, lambda0=None, start="tight"):
     else:
         Yv = np.ascontiguousarray(Y, dtype=np.float64)
         rows, cols = Yv.shape
-        h = N.handle(None)
-        import torch
-
-        h.use_current_stream()
         X = np.empty_like(Yv)
         lam = np.empty(rows)
         its = np.empty(rows, np.int32)
@@ -286,8 +289,18 @@ def project_simplex_rows(Y, r, opts=None, lambda0=None, start="tight"):
         mem = N.MEM_HOST
     o = N.make_options(opts, lambda0=lambda0, start=start, tau=opts.tau(np.float64))
     res = N.Result()
-    rc = h.lib.spx_project_batched_f64(h.ptr, mem, ptrs[0], rows, cols, float(r), o, ptrs[1],
-                                       ptrs[2], ptrs[3], res)
+    if devices is not None:
+        import ctypes
+
+        hs = N.handle_set([int(d) for d in devices])
+        arr = (ctypes.c_void_p * len(hs))(*[h.ptr.value for h in hs])
+        rc = hs[0].lib.spx_project_batched_multi_f64(arr, len(hs), ptrs[0], rows, cols, float(r), o,
+                                                     ptrs[1], ptrs[2], ptrs[3], res)
+    else:
+        h = N.handle(None) if not dev else h
+        h.use_current_stream()
+        rc = h.lib.spx_project_batched_f64(h.ptr, mem, ptrs[0], rows, cols, float(r), o, ptrs[1],
+                                           ptrs[2], ptrs[3], res)
     if rc != 0:
         raise N.NativeError(f"batched projection failed ({rc}): {N.last_error()}")
     return X, lam, its, res.stats()

@@ -19,7 +19,7 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, per_gpu=False):
     import torch
     import torch.distributed as dist
 
@@ -34,10 +34,13 @@ def _worker(rank, world, port, q):
         n = 200_003
         d, a, b, l, u, r = P.instances.gen_cqk_arrays("cqk-weakly-correlated", n, 11)
         lo, hi = D.shard_bounds(n, world, rank)
-        h = N.Handle(0)
-        h.lib.cqk_set_grid_limit(h.ptr, 16)
+        dev = rank if per_gpu else 0  # one process per visible GPU, or all on cuda:0
+        torch.cuda.set_device(dev)
+        h = N.Handle(dev)
+        if not per_gpu:
+            h.lib.cqk_set_grid_limit(h.ptr, 16)
         comm = D.Communicator(h, rank, world)  # IPC handles over gloo
-        sh = [torch.from_numpy(v[lo:hi].copy()).cuda() for v in (d, a, b, l, u)]
+        sh = [torch.from_numpy(v[lo:hi].copy()).cuda(dev) for v in (d, a, b, l, u)]
         solver = D.ShardedCQK(sh, r, n_total=n, offset=lo, comm=comm)
         out = solver.solve()
         # the same collective solve from host memory (H2D / D2H in the library)
@@ -51,14 +54,14 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_ipc_two_processes():
+def _run(world, per_gpu):
     import oracle as O
     import paper_2603_15910_b200 as P
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, per_gpu)) for r in range(world)]
     for p in procs:
         p.start()
     res = sorted([q.get(timeout=300) for _ in procs], key=lambda t: t[0])
@@ -68,8 +71,23 @@ def test_ipc_two_processes():
     n = 200_003
     d, a, b, l, u, r = P.instances.gen_cqk_arrays("cqk-weakly-correlated", n, 11)
     ref = O.solve_cqk(d, a, b, l, u, r)
-    assert res[0][1] == res[1][1]
+    assert len({t[1] for t in res}) == 1  # the identical decision on every rank
     assert abs(res[0][1] - ref["lam"]) <= 1e-12 * max(1.0, abs(ref["lam"]))
     assert res[0][2] == ref["iterations"] and res[0][3] == ref["fixed_count"]
-    x = np.concatenate([res[0][5], res[1][5]])
+    x = np.concatenate([t[5] for t in res])
     assert np.abs(x - ref["x"]).max() <= 1e-12 * 25
+
+
+def test_ipc_two_processes():
+    _run(2, per_gpu=False)
+
+
+def test_ipc_one_process_per_gpu():
+    """The deployment shape: one process per visible GPU, mailboxes mapped
+    over CUDA IPC with peer access (NVLink) -- skipped on a one-GPU box."""
+    import torch
+
+    ngpu = torch.cuda.device_count()
+    if ngpu < 2:
+        pytest.skip("needs >= 2 visible GPUs")
+    _run(min(ngpu, 8), per_gpu=True)

@@ -130,3 +130,47 @@ def test_generated_instances(generated):
         assert o["lam"] == rec["lam"] and o["iterations"] == rec["iterations"]
         o2 = O.newton_project_simplex(y, 1.0, lam0=rec["formula_lam0"])
         assert o2["lam"] == rec["formula_lam"] and o2["iterations"] == rec["formula_iterations"]
+
+
+def test_oracle_generator_matches_reference_and_product():
+    """oracle/cqk_gen.c (the reference arm's input generator, no product
+    library) reproduces the reference's arrays bit for bit (hashes recorded
+    by the real reference) and the product generator's arrays AND r, so both
+    benchmark arms solve one identical instance."""
+    import json
+    import os
+
+    import oracle as O
+    import paper_2603_15910_b200 as P
+    from tests_util import sha
+
+    with open(os.path.join(os.path.dirname(__file__), "golden", "generated.json")) as f:
+        gen = json.load(f)
+    for rec in gen["cqk"]:
+        if rec["n"] <= 10**6:
+            d, a, b, l, u, r = O.gen_cqk(rec["family"], rec["n"], rec["seed"])
+            assert sha(d, a, b, l, u) == rec["sha"]
+            assert abs(r - rec["r"]) <= 1e-14 * abs(rec["r"])  # the reference's r is a BLAS ddot
+    for rec in gen["simplex"]:
+        if rec["n"] <= 10**6:
+            assert sha(O.gen_simplex_y(rec["family"], rec["n"], rec["seed"])) == rec["sha"]
+    for fam in O.CQK_FAMILIES:
+        for n in (1, 7, 131073, 400_001):
+            A = O.gen_cqk(fam, n, 5)
+            B = P.instances.gen_cqk_arrays(fam, n, 5)
+            assert all(np.array_equal(x, y) for x, y in zip(A[:5], B[:5]))
+            assert A[5] == B[5]
+    for fam in O.SIMPLEX_FAMILIES:
+        assert np.array_equal(O.gen_simplex_y(fam, 300_001, 2), P.gen_simplex_y(fam, 300_001, 2))
+
+
+def test_oracle_rows_match_per_row_solves():
+    import oracle as O
+
+    Y = O.gen_simplex_y("simplex-n01", 64 * 512, 9).reshape(64, 512)
+    X, lam, its, bad = O.project_simplex_rows(Y, 1.0, threads=4)
+    assert bad == 0
+    for i in (0, 17, 63):
+        ref = O.newton_project_simplex(Y[i], 1.0)
+        assert lam[i] == ref["lam"] and its[i] == ref["iterations"]
+        assert np.array_equal(X[i], ref["x"])

@@ -33,15 +33,15 @@ for tag, rep in (("solve", "prof_solve"), ("spx", "prof_spx"), ("rows", "prof_ro
     rd, wr = gb(k["dram__bytes_read.sum"]), gb(k["dram__bytes_write.sum"])
     s["dram_bytes_per_launch"] = rd + wr
     s["source_report"] = os.path.basename(path)
+    kind = {"solve": "solve", "spx": "simplex", "rows": "rows"}[tag]
+    st = os.path.join(src, f"profile_{kind}_stats.json")
+    if os.path.exists(st):
+        rec = json.load(open(st))
+        s["algorithmic_bytes_per_launch"] = rec["stats"]["bytes_model"]
+        s["workload"] = {k: rec[k] for k in ("kind", "family", "n")}
+        s["dram_over_algorithmic"] = (rd + wr) / rec["stats"]["bytes_model"]
     with open(os.path.join(dst, f"{rnd}_ncu_{tag}.json"), "w") as f:
         json.dump(s, f, indent=1)
-    if tag == "solve":
-        with open(os.path.join(dst, "ncu_solve_kernel.json"), "w") as f:
-            json.dump({"round": rnd, "kernel": k["kernel"],
-                       "dram_bytes_per_launch": rd + wr,
-                       "gpu_time_ms_cold": k["gpu__time_duration.sum"],
-                       "workload": "C3 cqk-weakly-correlated n=1e8 solve_cqk (tools/profile_solve.py)"},
-                      f, indent=1)
 launch = os.path.join(src, f"launches_{rnd}.csv")
 if os.path.exists(launch):
     rows = [r for r in csv.reader(open(launch)) if len(r) > 10 and r[0] != "ID"]

@@ -28,4 +28,10 @@ else:
 for _ in range(args.reps):
     out = f()
 torch.cuda.synchronize()
-print("done", getattr(out, "stats", None) if not isinstance(out, tuple) else out[3])
+stats = getattr(out, "stats", None) if not isinstance(out, tuple) else out[3]
+print("done", stats)
+os.makedirs("gpurun_out", exist_ok=True)
+import json  # noqa: E402
+
+with open(f"gpurun_out/profile_{args.kind}_stats.json", "w") as f:
+    json.dump({"kind": args.kind, "family": args.family, "n": args.n, "stats": stats}, f)
