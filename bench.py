@@ -177,7 +177,9 @@ def dist_init(args):
         import torch.distributed as dist
 
         torch.cuda.set_device(local)
-        backend = os.environ.get("CQK_BENCH_BACKEND", "nccl")
+        # NCCL refuses two ranks on one device: the one-GPU smoke test uses gloo
+        shared = os.environ.get("CQK_BENCH_DEVICE") is not None
+        backend = os.environ.get("CQK_BENCH_BACKEND", "gloo" if shared else "nccl")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
@@ -733,7 +735,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=6)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
-    ap.add_argument("--n", "--size", dest="n", type=int, default=None,
+    ap.add_argument("--size", dest="n", type=int, default=None,
                     help="override n (C3/C4) or rows (C5) -- a smaller workload than the named config")
     ap.add_argument("--variant", default="solve", choices=["solve", "jacobi"])
     ap.add_argument("--e2e-steps", type=int, default=5)

@@ -327,3 +327,44 @@ def gen_simplex_y(family, n, seed):
     if rc != 0:
         raise ValueError(f"orc_gen_simplex_y failed ({rc})")
     return y
+
+
+def exact_lambda(d, a, b, l, u, r):
+    """Exact root of phi(lam) = r by bisection over the sorted breakpoints and
+    one interpolation on the bracketing affine piece (the method of the
+    reference's oracle.py:23-85, restated) -> (status, lam or None).  Plain
+    numpy, O(n log n): a check for small and medium n."""
+    d, a, b, l, u = (np.asarray(v, dtype=np.float64) for v in (d, a, b, l, u))
+    r = float(r)
+
+    def phi(lam):
+        return float(b @ np.clip((b * lam + a) / d, l, u))
+
+    fl, fu = np.isfinite(l), np.isfinite(u)
+    bps = np.unique(np.concatenate([(d[fl] * l[fl] - a[fl]) / b[fl], (d[fu] * u[fu] - a[fu]) / b[fu]]))
+    w = b * b / d
+    if bps.size == 0:
+        return SOLVED, (r - float(b @ (a / d))) / float(w.sum())
+    top, bot = phi(bps[-1]), phi(bps[0])
+    if r > top:
+        s = float(w[u == np.inf].sum())
+        return (INFEASIBLE, None) if s == 0.0 else (SOLVED, bps[-1] + (r - top) / s)
+    if r < bot:
+        s = float(w[l == -np.inf].sum())
+        return (INFEASIBLE, None) if s == 0.0 else (SOLVED, bps[0] - (bot - r) / s)
+    lo, hi = 0, bps.size - 1  # phi(bps[hi]) >= r > phi(bps[lo - 1])
+    if bot >= r:
+        hi = 0
+    while hi - lo > 1:
+        mid = (lo + hi) // 2
+        if phi(bps[mid]) >= r:
+            hi = mid
+        else:
+            lo = mid
+    vh = phi(bps[hi])
+    if vh == r:  # on a plateau: its left end
+        while hi > 0 and phi(bps[hi - 1]) == r:
+            hi -= 1
+        return SOLVED, float(bps[hi])
+    vl = phi(bps[hi - 1])
+    return SOLVED, float(bps[hi - 1] + (r - vl) * (bps[hi] - bps[hi - 1]) / (vh - vl))

@@ -13,7 +13,8 @@
 namespace cqk {
 
 constexpr int kPeakTile = 2048;   // doubles per array per tile (16 KB)
-constexpr int kPeakStages = 2;    // 5 arrays x 2 stages x 16 KB = 160 KB in flight
+constexpr int kPeakStages = 10;   // stages of one array; narr arrays use 10 / narr stages:
+                                  // 160 KB in flight per SM whatever the array count
 constexpr int kPeakThreads = 544; // 16 consumer warps + the producer warp
 constexpr int kPeakMaxArr = 5;
 
@@ -43,14 +44,15 @@ __global__ void __launch_bounds__(kPeakThreads, 1) read_peak_kernel(PeakArgs a) 
   }
   __syncthreads();
   const long long ntiles = a.n / kPeakTile;
+  const int S = kPeakStages / a.narr;  // stages in flight (each holds narr tiles)
   double acc = 0;
   if (warp == nw) {
     if (lane == 0) {
       int j = 0;
       for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++j) {
-        const int s = j % kPeakStages;
-        if (j >= kPeakStages) {
-          const unsigned ph = ((j / kPeakStages) - 1) & 1;
+        const int s = j % S;
+        if (j >= S) {
+          const unsigned ph = ((j / S) - 1) & 1;
           asm volatile(
               "{\n.reg .pred p;\nPW1_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
               "@!p bra PW1_%=;\n}" ::"r"(peak_su32(&empty[s])), "r"(ph) : "memory");
@@ -60,7 +62,7 @@ __global__ void __launch_bounds__(kPeakThreads, 1) read_peak_kernel(PeakArgs a) 
         for (int k = 0; k < a.narr; ++k)
           asm volatile(
               "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                  peak_su32(buf + ((size_t)s * kPeakMaxArr + k) * kPeakTile)),
+                  peak_su32(buf + ((size_t)s * a.narr + k) * kPeakTile)),
               "l"(a.arr[k] + t * kPeakTile), "r"(kPeakTile * 8), "r"(peak_su32(&full[s]))
               : "memory");
       }
@@ -68,13 +70,13 @@ __global__ void __launch_bounds__(kPeakThreads, 1) read_peak_kernel(PeakArgs a) 
   } else {
     int j = 0;
     for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++j) {
-      const int s = j % kPeakStages;
-      const unsigned ph = (j / kPeakStages) & 1;
+      const int s = j % S;
+      const unsigned ph = (j / S) & 1;
       asm volatile(
           "{\n.reg .pred p;\nPW2_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
           "@!p bra PW2_%=;\n}" ::"r"(peak_su32(&full[s])), "r"(ph) : "memory");
       for (int k = 0; k < a.narr; ++k) {
-        const double2* q = reinterpret_cast<const double2*>(buf + ((size_t)s * kPeakMaxArr + k) * kPeakTile);
+        const double2* q = reinterpret_cast<const double2*>(buf + ((size_t)s * a.narr + k) * kPeakTile);
         for (int i = warp * 32 + lane; i < kPeakTile / 2; i += nw * 32) {
           const double2 v = q[i];
           acc += v.x + v.y;
@@ -88,6 +90,6 @@ __global__ void __launch_bounds__(kPeakThreads, 1) read_peak_kernel(PeakArgs a) 
   if (acc == 1.2345) a.sink[0] = acc;  // keeps the loads live
 }
 
-inline size_t read_peak_smem() { return (size_t)kPeakMaxArr * kPeakTile * kPeakStages * sizeof(double); }
+inline size_t read_peak_smem() { return (size_t)kPeakTile * kPeakStages * sizeof(double); }
 
 }  // namespace cqk

@@ -15,7 +15,7 @@ from . import _native as N
 from .core import CqkInstance
 
 __all__ = ["CQK_FAMILIES", "SIMPLEX_FAMILIES", "FamilyMismatch", "gen_cqk", "gen_simplex_y",
-           "gen_cqk_device", "gen_simplex_y_device", "Xoshiro256pp"]
+           "gen_blobs", "gen_sparse_ls", "gen_cqk_device", "gen_simplex_y_device", "Xoshiro256pp"]
 
 CQK_FAMILIES = ("cqk-uncorrelated", "cqk-weakly-correlated", "cqk-correlated")
 SIMPLEX_FAMILIES = ("simplex-u01", "simplex-n01", "simplex-n0m3")
@@ -108,6 +108,47 @@ class Xoshiro256pp:
     def integers(self, upper, size):
         u = self.uniform01(size)
         return np.minimum((u * upper).astype(np.int64), upper - 1)
+
+
+def gen_blobs(n, dim, separation, seed):
+    """Two Gaussian blobs labelled +1 (even i) / -1 (odd i) for the SVM-dual
+    SPG demo (instances.py:89-101): n*dim normals in point-major order, then
+    the class mean +-separation/2 added to coordinate 0."""
+    g = Xoshiro256pp(seed)
+    pts = g.normal(int(n) * int(dim)).reshape(int(n), int(dim))
+    labels = np.where(np.arange(int(n)) % 2 == 0, 1.0, -1.0)
+    pts[:, 0] += 0.5 * separation * labels
+    return pts, labels
+
+
+def gen_sparse_ls(m, n, density, sparsity_k, seed):
+    """Sparse least squares (A CSR, b = A x_true, x_true) for the basis-pursuit
+    SPG demo (instances.py:103-131).  Stream order: m*n uniforms (entry kept
+    below `density`), one normal per kept entry in row-major order, support
+    indices drawn one at a time (a repeat is redrawn), then sparsity_k
+    normals for the support values."""
+    import scipy.sparse as sp
+
+    from .core import DomainError
+
+    if not 0 < density <= 1:
+        raise DomainError("density", None, "density must be in (0, 1]")
+    if sparsity_k > n:
+        raise DomainError("sparsity_k", None, "sparsity_k must be <= n")
+    g = Xoshiro256pp(seed)
+    keep = g.uniform01(int(m) * int(n)) < density
+    rows, cols = np.nonzero(keep.reshape(int(m), int(n)))
+    A = sp.csr_matrix((g.normal(rows.shape[0]), (rows, cols)), shape=(int(m), int(n)))
+    support, seen = [], set()
+    while len(support) < sparsity_k:
+        c = int(g.integers(int(n), 1)[0])
+        if c not in seen:
+            seen.add(c)
+            support.append(c)
+    x_true = np.zeros(int(n))
+    if sparsity_k:
+        x_true[np.array(support)] = g.normal(int(sparsity_k))
+    return A, A @ x_true, x_true
 
 
 def gen_cqk_device(family, n, seed, device=None):

@@ -28,6 +28,23 @@ def resolve_workers(workers=None):
     return 1
 
 
+def _tree_sum(values):
+    """The determinism contract of the reference's chunk reductions
+    (parallel.py:62-72): adjacent pairs summed level by level, an odd tail
+    carried up unchanged.  The device reductions across CTAs and ranks use
+    fixed orders of the same kind, so reruns are bit-identical; this host
+    form serves callers that combine per-device partials themselves."""
+    level = list(values)
+    if not level:
+        raise ValueError("_tree_sum of nothing")
+    while len(level) > 1:
+        paired = [level[k] + level[k + 1] for k in range(0, len(level) - 1, 2)]
+        if len(level) & 1:
+            paired.append(level[-1])
+        level = paired
+    return level[0]
+
+
 def par_solve_cqk(inst, opts=None, workers=None, xbar=None, check=True,
                   merge_threshold=MERGE_THRESHOLD):
     """Chunked fork-join variant of solve_cqk; same outcome contract (parallel.py:174-327)."""

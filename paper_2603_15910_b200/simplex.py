@@ -137,14 +137,18 @@ def _project(y, r, opts, lambda0, trace, l1, start="auto", xbar=None, sharpened=
     if opts is None:
         opts = SolverOptions()
     yv, dt, dev = _prep(y)
-    # warm start (simplex.py:65-109): Algorithm 2 seeded by xbar's support
-    warm = lambda0 is None and (xbar is not None or (start == "alg2" and sharpened))
+    # warm start (simplex.py:65-109): Algorithm 2 seeded by xbar's support.
+    # A sharpened simplex projection always takes this route: the reference
+    # applies the participation test min(y, y + lam) > 0 through
+    # simplex_init_lambda (simplex.py:243-245), which changes the answer when
+    # lam* > 0.  (For l1, |y| >= 0 and lam* < 0 make the test moot.)
+    warm = lambda0 is None and (xbar is not None or (sharpened and (not l1 or start == "alg2")))
     xb = None
     if warm and xbar is not None:
         xb, _, xdev = _prep(xbar)
         if xdev != dev or int(xb.shape[0]) != int(yv.shape[0]):
             raise DomainError("xbar", None, "xbar must match y in length and placement")
-        if not bool((xb >= 0).all()) and not l1:
+        if not bool((xb >= 0).all()):  # simplex.py:139-140 (project_l1 passes xbar as is)
             raise DomainError("xbar", None, "warm-start estimate must be >= 0")
     n = int(yv.shape[0])
     h = N.handle(yv.get_device() if dev else None)
@@ -229,7 +233,16 @@ def project_l1(y, r, opts=None, output="dense", xbar=None, start="auto"):
     """Project y onto the l1 ball of radius r (simplex.py:311-333)."""
     if not r > 0:
         raise DomainError("r", None, "l1 radius r must be positive")
-    x, res = _project(y, r, opts, None, None, l1=True, start=start, xbar=xbar, sharpened=True)
+    try:
+        x, res = _project(y, r, opts, None, None, l1=True, start=start, xbar=xbar, sharpened=True)
+    except DomainError as e:
+        # the reference tests the ball before it looks at xbar
+        # (simplex.py:324-327): a point inside is returned even then
+        if e.field != "xbar":
+            raise
+        x, res = _project(y, r, opts, None, None, l1=True, start=start)
+        if int(res.iterations) >= 0:
+            raise
     if output == "sparse":
         dev = _is_torch(x)
         if dev:

@@ -174,3 +174,64 @@ def test_oracle_rows_match_per_row_solves():
         ref = O.newton_project_simplex(Y[i], 1.0)
         assert lam[i] == ref["lam"] and its[i] == ref["iterations"]
         assert np.array_equal(X[i], ref["x"])
+
+
+def test_par_drivers_pinned_to_reference():
+    """The oracle's par_solve_cqk / par_simplex_init -- the CPU path the
+    benchmark's reference arm times -- against the real reference's parallel
+    drivers (tests/golden/make_par_golden.py; workers 1, 2, 3, 5, 8; random,
+    generated and degenerate plateau / pinned instances): identical status,
+    iteration, evaluation and fixing counts; lambda bit-identical where the
+    reference's per-chunk lambda0 dot products happen to round like the
+    oracle's pairwise sums, else within 1e-12; Algorithm-2 chunks bit-exact."""
+    import hashlib
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from degenerate_cases import CASES
+
+    z = np.load(os.path.join(G, "par.npz"))
+
+    def arrays(k):
+        p = f"c{k}_"
+        kind, r = str(z[p + "kind"][0]), float(z[p + "r"][0])
+        if kind == "random":
+            return [z[p + nm] for nm in ("d", "a", "b", "l", "u")], r
+        if kind == "gen":
+            fam, n, seed = z[p + "gen"]
+            return list(O.gen_cqk(str(fam), int(n), int(seed))[:5]), r
+        return list(CASES[str(z[p + "degen"][0])]()[:5]), r
+
+    exact = 0
+    for k in range(int(z["n_cqk"][0])):
+        arrs, r = arrays(k)
+        for w in z["workers"]:
+            for fix in (True, False):
+                tag = f"c{k}_w{w}_{'fix' if fix else 'nofix'}"
+                ref = z[tag + "_out"]
+                o = O.par_solve_cqk(*arrs, r, workers=int(w), fixing=fix)
+                assert o["status"] == {0: O.SOLVED, 1: O.INFEASIBLE}[int(ref[0])], tag
+                assert (o["iterations"], o["phi_evals"], o["fixed_count"]) == tuple(int(v) for v in ref[2:]), tag
+                if o["status"] != O.SOLVED:
+                    continue
+                assert abs(o["lam"] - ref[1]) <= 1e-12 * max(1.0, abs(ref[1])), tag
+                exact += o["lam"] == ref[1]
+                if tag + "_x" in z:
+                    assert np.abs(o["x"] - z[tag + "_x"]).max() <= 1e-12 * max(1.0, np.abs(z[tag + "_x"]).max())
+                elif o["lam"] == ref[1]:
+                    assert hashlib.sha256(o["x"].tobytes()).digest() == z[tag + "_xsha"].tobytes(), tag
+    assert exact >= 300
+    for k in range(int(z["n_spx"][0])):
+        p = f"s{k}_"
+        r = float(z[p + "r"][0])
+        if p + "y" in z:
+            y = z[p + "y"]
+        else:
+            fam, n, seed = z[p + "gen"]
+            y = O.gen_simplex_y(str(fam), int(n), int(seed))
+        for w in z["workers"]:
+            lam, free, fixed, sj = O.par_simplex_init(y, r, workers=int(w))
+            rl, rs = z[f"{p}w{w}_lam"]
+            assert lam == rl and sj == rs, (k, w)
+            assert np.array_equal(free, z[f"{p}w{w}_free"]), (k, w)
+            assert int(fixed.sum()) == int(z[f"{p}w{w}_nfixed"][0])
