@@ -687,7 +687,7 @@ def run_c5(args, cfg, world, rank, local):
         read_peak, _ = P._native.handle(local).read_peak([Y.view(-1)])
     n = rows * cols
     value = n * args.steps / (ms / 1e3)
-    rl = roofline(outs, world, read_peak, "spx_rows_pipe_kernel (CTA per row, 1 launch/step)")
+    rl = roofline(outs, world, read_peak, "spx_rows_tma_kernel<4,4,8> (warp per row, bulk-copy rings, 1 launch/step)")
     e2e = None
     if args.e2e_steps > 0:
         Yp = torch.from_numpy(Yh).pin_memory().numpy()

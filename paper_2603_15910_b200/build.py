@@ -25,7 +25,7 @@ NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-f
               "-shared", "--expt-relaxed-constexpr"]
 
 CUDA_SOURCES = ["cqk_abi.cu"]
-CUDA_DEPS = ["cqk_abi.cu", "cqk_device.cuh", "cqk_solver.cuh", "cqk_kernels.cuh", "cqk_tma.cuh", "cqk_tma_spx.cuh", "cqk_diag.cuh", "gen_kernels.cuh",
+CUDA_DEPS = ["cqk_abi.cu", "cqk_device.cuh", "cqk_solver.cuh", "cqk_kernels.cuh", "cqk_tma.cuh", "cqk_tma_spx.cuh", "cqk_diag.cuh", "cqk_rows.cuh", "gen_kernels.cuh",
              "xoshiro_jump.h"]
 
 

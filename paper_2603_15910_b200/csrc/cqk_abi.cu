@@ -23,6 +23,7 @@
 #include "cqk_tma.cuh"
 #include "cqk_tma_spx.cuh"
 #include "cqk_diag.cuh"
+#include "cqk_rows.cuh"
 
 using namespace cqk;
 
@@ -110,6 +111,7 @@ struct cqk_handle {
   double* ar_rows = nullptr;          // masterless grid step: [2][grid][kMaxK] partial rows
   unsigned* ar_count = nullptr;       // ... [2] arrival counters, alternating per launch
   unsigned long long ar_seq = 0;      // masterless launches so far
+  int rows_flip = 0;                  // C5 row counter (ar_count[8 + flip]) of the next launch
   double* alg2_vals = nullptr;        // gathered free values of the last Algorithm-2 run
   int64_t* alg2_idx = nullptr;        // ... and their global indices
   int64_t* alg2_jplus = nullptr;
@@ -991,7 +993,16 @@ int spx_common(cqk_handle* h, int mem, const double* y, int64_t n, int64_t n_tot
       wcount = (int64_t*)((char*)h->warm.p + mb + vb);
       CUDA_TRY(cudaMemsetAsync(mask, 0, n, h->stream));
     }
-    int rc = run_alg2(h, yv, nullptr, n, r, xbv ? 1 : 0, xbv, sharp, l1, !xbv, false, mask, &a2);
+    int64_t W = xbv ? 1 : 0;
+    if (sharp && !l1 && !xbv) {
+      // sharpened with y[0] <= 0: whether the sequential recurrence later
+      // fixes its seed depends on the whole pass, so run it exactly (one chunk)
+      double y0 = 0.0;
+      CUDA_TRY(cudaMemcpyAsync(&y0, yv, sizeof y0, cudaMemcpyDeviceToHost, h->stream));
+      CUDA_TRY(cudaStreamSynchronize(h->stream));
+      if (!(y0 > 0.0)) W = 1;
+    }
+    int rc = run_alg2(h, yv, nullptr, n, r, W, xbv, sharp, l1, !xbv, false, mask, &a2);
     if (rc) return rc;
     if (xbv) {
       if (l1) spx_gather_free_kernel<true><<<1, 1024, 0, h->stream>>>(yv, mask, n, wvals, wcount);
@@ -1180,64 +1191,26 @@ extern "C" int spx_project_batched_f64(cqk_handle* h, int mem, const double* Y, 
   const int c = (int)cols;
   CUDA_TRY(cudaEventRecord(h->ev0, h->stream));
   cudaError_t e;
-  const size_t smem = rows_smem_per_warp(c) * kRowWarps;
-  const size_t smem_cta = rows_cta_smem<4, 8>(c);
-  const char* force = getenv("CQK_ROWS_KERNEL");
-  const std::string fk = force ? force : "";
+  // aligned rows of even length: one warp per row fed by per-warp bulk-copy
+  // rings, rows handed out by a grid counter (cqk_rows.cuh); otherwise the
+  // CTA-per-row register kernel
   const bool aligned_rows = (c % 2) == 0 && aligned16(Yd) && aligned16(Xd);
-  const bool pipe_kernel = aligned_rows && rows_pipe_smem<4, 8>(c) <= 220 * 1024 && c >= 256 &&
-                           (fk == "" || fk == "pipe" || fk == "pipe8" || fk == "fused" || fk == "pipe16" ||
-                            fk == "pipe12" || fk == "fused8");
-  const bool cta_kernel = !pipe_kernel && smem_cta <= 220 * 1024 && c >= 256 && fk != "block" && fk != "warp";
-  const bool warp_kernel = !cta_kernel && smem <= 220 * 1024 && fk != "block";
-  auto go = [&](auto kern, int threads, size_t sm) {
+  if (aligned_rows) {
+    auto kern = spx_rows_tma_kernel<kRsU, kRsStages, kRsWarps>;
+    constexpr size_t sm = rs_tma_warp_bytes<kRsU, kRsStages>() * kRsWarps;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * kRsWarps, sm);
     int64_t grid = (int64_t)(occ > 0 ? occ : 1) * h->sm_count;
-    if (grid > rows) grid = rows;
-    kern<<<(unsigned)grid, threads, sm, h->stream>>>(Yd, Xd, Ld, Id, rows, c, r, tau,
-                                                     opts.max_iterations, fixing, opts.lambda0,
-                                                     opts.simplex_start);
-    return cudaGetLastError();
-  };
-  if (pipe_kernel) {
-    if (fk == "pipe8") e = go(spx_rows_pipe_kernel<8, 8, 2>, 256, rows_pipe_smem<8, 8, 2>(c));
-    else if (fk == "pipe") e = go(spx_rows_pipe_kernel<4, 8, 2>, 128, rows_pipe_smem<4, 8, 2>(c));
-    else if (fk == "pipe16") e = go(spx_rows_pipe_kernel<4, 16, 1>, 128, rows_pipe_smem<4, 16, 1>(c));
-    else if (fk == "pipe12") e = go(spx_rows_pipe_kernel<4, 12, 1>, 128, rows_pipe_smem<4, 12, 1>(c));
-    else if (fk == "fused8") e = go(spx_rows_pipe_kernel<4, 8, 1>, 128, rows_pipe_smem<4, 8, 1>(c));
-    // free-set buffers of cols/12 per CTA: 36.6 KB at 4096 columns -> six CTAs
-    // (rows) per SM instead of five; measured 65536 x 4096: 0.934 -> 0.872 ms
-    else e = go(spx_rows_pipe_kernel<4, 12, 1>, 128, rows_pipe_smem<4, 12, 1>(c));
-  } else if (cta_kernel) {
-    auto go_ = [&](auto kern, int threads, size_t sm) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      int occ = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, sm);
-      int64_t grid = (int64_t)(occ > 0 ? occ : 1) * h->sm_count;
-      if (grid > rows) grid = rows;
-      kern<<<(unsigned)grid, threads, sm, h->stream>>>(Yd, Xd, Ld, Id, rows, c, r, tau,
-                                                       opts.max_iterations, fixing, opts.lambda0,
-                                                       opts.simplex_start);
-      return cudaGetLastError();
-    };
-    // measured on B200 (65536 x 4096): 4 warps/row with a cols/8 free-set
-    // buffer (6 CTAs/SM) 1.09 ms; cols/2 buffer 1.28 ms; 8 warps/row 1.6 ms
-    if (fk == "cta4") e = go_(spx_rows_cta_kernel<4, 2>, 128, rows_cta_smem<4, 2>(c));
-    else if (fk == "cta8") e = go_(spx_rows_cta_kernel<8, 8>, 256, rows_cta_smem<8, 8>(c));
-    else e = go_(spx_rows_cta_kernel<4, 8>, 128, rows_cta_smem<4, 8>(c));
-  } else if (warp_kernel) {
-    cudaFuncSetAttribute(spx_rows_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, spx_rows_warp_kernel, 32 * kRowWarps, smem);
-    int64_t grid = (int64_t)(occ > 0 ? occ : 1) * h->sm_count;
-    const int64_t need = (rows + kRowWarps - 1) / kRowWarps;
+    const int64_t need = (rows + kRsWarps - 1) / kRsWarps;
     if (grid > need) grid = need;
-    spx_rows_warp_kernel<<<(unsigned)grid, 32 * kRowWarps, smem, h->stream>>>(
-        Yd, Xd, Ld, Id, rows, c, r, tau, opts.max_iterations, fixing, opts.lambda0,
-        opts.simplex_start);
+    // two row counters alternate between launches; each launch zeroes the other
+    unsigned* ctr = h->ar_count + 8 + h->rows_flip;
+    unsigned* nxt = h->ar_count + 8 + (h->rows_flip ^ 1);
+    h->rows_flip ^= 1;
+    kern<<<(unsigned)grid, 32 * kRsWarps, sm, h->stream>>>(Yd, Xd, Ld, Id, rows, c, r, tau,
+                                                           opts.max_iterations, fixing,
+                                                           opts.lambda0, opts.simplex_start, ctr, nxt);
     e = cudaGetLastError();
   } else if (c <= kRowThreads) e = launch_rows<1>(h, Yd, Xd, Ld, Id, rows, c, r, tau, opts.max_iterations, fixing, opts.lambda0, opts.simplex_start);
   else if (c <= 2 * kRowThreads) e = launch_rows<2>(h, Yd, Xd, Ld, Id, rows, c, r, tau, opts.max_iterations, fixing, opts.lambda0, opts.simplex_start);

@@ -1109,16 +1109,7 @@ __global__ void __launch_bounds__(kRowThreads) spx_rows_kernel(
   }
 }
 
-// ------------------------------------------------------------ warp-per-row
-// K8, Blackwell form: one warp owns one row at a time.  The row lands in
-// shared memory with ONE bulk TMA copy (cp.async.bulk + mbarrier complete_tx),
-// every reduction is a warp shuffle (no __syncthreads at all), the free set is
-// compacted into a small per-warp buffer once it fits (later Newton steps
-// touch only a few dozen values), and x = max(0, y + lam) is written back in
-// place and stored with one bulk TMA store.  Several warps per SM (bounded by
-// shared memory) keep HBM busy while others iterate.
-constexpr int kRowWarps = 2;      // warps per CTA
-
+// ------------------------------------------------------------ bulk-copy helpers
 DEVI unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 DEVI void mbar_init(unsigned long long* bar) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
@@ -1137,760 +1128,6 @@ DEVI void mbar_wait(unsigned long long* bar, unsigned phase) {
       "{\n.reg .pred p;\nWAIT_%=:\n"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
       "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(phase) : "memory");
-}
-DEVI void tma_store_1d(void* dst, const void* src, unsigned bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
-               "r"(smem_u32(src)), "r"(bytes) : "memory");
-  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-}
-DEVI void tma_store_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
-DEVI void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-
-// Free-set capacity of the per-warp compaction buffer: half a row (at the
-// first fixing step the survivors are the positives at lambda0 ~ half the row
-// for symmetric data); while the survivors exceed it the full row is scanned
-// with the stateless drop test instead.
-__host__ __device__ inline int free_cap(int cols) { return ((cols + 1) / 2 + 1) & ~1; }
-__host__ __device__ inline size_t rows_smem_per_warp(int cols) {
-  return ((size_t)cols * 8 + 127) / 128 * 128 + ((size_t)free_cap(cols) * 8 + 127) / 128 * 128 + 128;
-}
-
-// phi over a contiguous smem range: sum of positive t = v + lam, #(t > 0),
-// #(t == 0); branch-free, two elements per 16-byte shared load, split
-// accumulators to break the DADD dependency chains.
-DEVI void rows_phi(const double* F, int m, double lam, bool drop_test, double fix_hi, int lane,
-                   double& val, int& npos, int& nzero) {
-  double v0 = 0.0, v1 = 0.0;
-  int p = 0, z = 0;
-  const int m2 = m & ~1;
-  for (int i = 2 * lane; i < m2; i += 64) {
-    const double2 v = *reinterpret_cast<const double2*>(F + i);
-    const double t0 = __dadd_rn(v.x, lam), t1 = __dadd_rn(v.y, lam);
-    v0 += t0 > 0 ? t0 : 0.0;
-    v1 += t1 > 0 ? t1 : 0.0;
-    p += (t0 > 0) + (t1 > 0);
-    // a zero t of a dropped variable is not in the free set (simplex.py:214)
-    z += (t0 == 0 && (!drop_test || __dadd_rn(v.x, fix_hi) > 0)) +
-         (t1 == 0 && (!drop_test || __dadd_rn(v.y, fix_hi) > 0));
-  }
-  if ((m & 1) && lane == 0) {
-    const double t = __dadd_rn(F[m - 1], lam);
-    v0 += t > 0 ? t : 0.0;
-    p += t > 0;
-    z += t == 0 && (!drop_test || __dadd_rn(F[m - 1], fix_hi) > 0);
-  }
-  val = v0 + v1;
-  npos = p;
-  nzero = z;
-}
-
-DEVI int warp_sum_i(int v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
-__global__ void __launch_bounds__(32 * kRowWarps) spx_rows_warp_kernel(
-    const double* __restrict__ Y, double* __restrict__ X, double* __restrict__ lam_out,
-    int32_t* __restrict__ it_out, int64_t rows, int cols, double r, double tau, int max_iter,
-    int fixing, double lam0_given, int start) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const size_t a_bytes = ((size_t)cols * 8 + 127) / 128 * 128;
-  const size_t b_bytes = ((size_t)free_cap(cols) * 8 + 127) / 128 * 128;
-  unsigned char* base = smem_raw + rows_smem_per_warp(cols) * w;
-  double* A = reinterpret_cast<double*>(base);
-  double* Bf = reinterpret_cast<double*>(base + a_bytes);
-  unsigned long long* bar = reinterpret_cast<unsigned long long*>(base + a_bytes + b_bytes);
-  const int cap = free_cap(cols);
-  const bool tma = (cols % 2) == 0 && (((uintptr_t)Y | (uintptr_t)X) & 15) == 0;
-  const unsigned bytes = (unsigned)cols * 8u;
-  if (lane == 0 && tma) mbar_init(bar);
-  __syncwarp();
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  unsigned phase = 0;
-  const int64_t gw = (int64_t)blockIdx.x * kRowWarps + w, W = (int64_t)gridDim.x * kRowWarps;
-  const unsigned lt = (1u << lane) - 1u;
-  for (int64_t row = gw; row < rows; row += W) {
-    const double* y = Y + row * (int64_t)cols;
-    double* x = X + row * (int64_t)cols;
-    if (tma) {
-      if (lane == 0) {
-        tma_store_wait_read();  // the previous row's store has read A
-        mbar_expect_tx(bar, bytes);
-        tma_load_1d(A, y, bytes, bar);
-      }
-      mbar_wait(bar, phase);
-      phase ^= 1u;
-    } else {
-      for (int i = lane; i < cols; i += 32) A[i] = __ldcs(y + i);
-      __syncwarp();
-    }
-    // sum / max -> formula start (simplex.py:246-250 route)
-    double s0 = 0.0, s1 = 0.0, m0 = -HUGE_VAL, m1 = -HUGE_VAL;
-    const int c2 = cols & ~1;
-    for (int i = 2 * lane; i < c2; i += 64) {
-      const double2 v = *reinterpret_cast<const double2*>(A + i);
-      s0 += v.x;
-      s1 += v.y;
-      m0 = fmax(m0, v.x);
-      m1 = fmax(m1, v.y);
-    }
-    if ((cols & 1) && lane == 0) {
-      s0 += A[cols - 1];
-      m0 = fmax(m0, A[cols - 1]);
-    }
-    const double sum = warp_sum(s0 + s1), mx = warp_max(fmax(m0, m1));
-    const double formula = (r - sum) / (double)cols, tight = r - mx;
-    double lam = !isnan(lam0_given) ? lam0_given : (start && tight < formula ? tight : formula);
-    lam = lam >= -mx ? lam : -mx;
-    double lo = -HUGE_VAL, hi = HUGE_VAL, fix_hi = HUGE_VAL;
-    int iterations = 0;
-    const double* F = A;  // current free-set storage
-    int m = cols;         // its length
-    bool compacted = false;
-    for (;;) {
-      double val;
-      int np, nz;
-      rows_phi(F, m, lam, fixing && !compacted && isfinite(fix_hi), fix_hi, lane, val, np, nz);
-      const double value = warp_sum(val);
-      const int npos = warp_sum_i(np), nzero = warp_sum_i(nz);
-      const double dminus = (double)npos, dplus = (double)(npos + nzero);
-      double deriv;
-      if (iterations == 0) {
-        if (value == r) break;
-        deriv = value < r ? dplus : dminus;
-      } else {
-        if (value <= r) break;
-        deriv = dminus;
-      }
-      if (value < r) lo = lam;
-      else {
-        hi = lam;
-        if (fixing) {
-          fix_hi = lam;
-          // keep exactly the survivors (t > 0); compact them once they fit
-          if (npos <= cap) {
-            int out = 0;
-            for (int i0 = 0; i0 < m; i0 += 32) {
-              const int i = i0 + lane;
-              double v = 0.0;
-              bool keep = false;
-              if (i < m) {
-                v = F[i];
-                keep = __dadd_rn(v, lam) > 0;
-              }
-              const unsigned mask = __ballot_sync(0xffffffffu, keep);
-              if (keep) Bf[out + __popc(mask & lt)] = v;  // out <= i0: in-place safe
-              out += __popc(mask);
-            }
-            __syncwarp();
-            F = Bf;
-            m = out;
-            compacted = true;
-          }
-        }
-      }
-      if (deriv <= 0) {  // snap to the largest remaining breakpoint (simplex.py:276-281)
-        double mneg = -HUGE_VAL;
-        for (int i = lane; i < m; i += 32) {
-          const double v = F[i];
-          if (!compacted && fixing && !(__dadd_rn(v, fix_hi) > 0)) continue;
-          mneg = fmax(mneg, -v);
-        }
-        lam = warp_max(mneg);
-        ++iterations;
-        continue;
-      }
-      const double step = -(value - r) / deriv;
-      const double next = lam + step;
-      if (fabs(step) < tau || next == lam) { lam = next; break; }
-      if (isfinite(lo) && isfinite(hi) && hi - lo < tau * fmax(fabs(hi), fabs(lo))) {
-        lam = next;
-        break;
-      }
-      lam = next;
-      ++iterations;
-      if (iterations > max_iter) break;
-    }
-    // x = max(0, y + lam) in place, then one bulk store
-    if (tma) {
-      for (int i = 2 * lane; i < cols; i += 64) {
-        double2 v = *reinterpret_cast<double2*>(A + i);
-        const double t0 = __dadd_rn(v.x, lam), t1 = __dadd_rn(v.y, lam);
-        v.x = t0 > 0 ? t0 : 0.0;
-        v.y = t1 > 0 ? t1 : 0.0;
-        *reinterpret_cast<double2*>(A + i) = v;
-      }
-      fence_async_smem();
-      __syncwarp();
-      if (lane == 0) tma_store_1d(x, A, bytes);
-    } else {
-      for (int i = lane; i < cols; i += 32) {
-        const double t = __dadd_rn(A[i], lam);
-        __stcs(x + i, t > 0 ? t : 0.0);
-      }
-    }
-    if (lane == 0) {
-      if (lam_out) lam_out[row] = lam;
-      if (it_out) it_out[row] = iterations;
-    }
-    __syncwarp();
-  }
-  // outstanding bulk stores complete before the grid exits (bulk_group semantics)
-  if (lane == 0 && tma) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-}
-
-// ------------------------------------------------------------ CTA-per-row
-// The same per-row algorithm with WPR warps sharing one row (a contiguous
-// slice each): 4x shorter per-row critical path at the same shared memory per
-// row, so 4x more warps resident.  Cross-warp totals: warp shuffle, one slot
-// per warp, ONE __syncthreads (double-buffered slots), and every thread
-// combines the WPR slots in the same order -> identical decisions everywhere.
-// per-warp compaction capacity: 1/CAPDIV of the row in total
-template <int WPR, int CAPDIV = 2>
-__host__ __device__ inline int rows_cap_part(int cols) {
-  return ((cols / CAPDIV) / WPR + 2) & ~1;
-}
-template <int WPR, int CAPDIV = 2>
-__host__ __device__ inline size_t rows_cta_smem(int cols) {
-  return ((size_t)cols * 8 + 127) / 128 * 128 +
-         (size_t)rows_cap_part<WPR, CAPDIV>(cols) * 8 * WPR + 2 * WPR * 4 * 8 + 128;
-}
-
-template <int WPR, int CAPDIV = 2>
-__global__ void __launch_bounds__(32 * WPR) spx_rows_cta_kernel(
-    const double* __restrict__ Y, double* __restrict__ X, double* __restrict__ lam_out,
-    int32_t* __restrict__ it_out, int64_t rows, int cols, double r, double tau, int max_iter,
-    int fixing, double lam0_given, int start) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const size_t a_bytes = ((size_t)cols * 8 + 127) / 128 * 128;
-  const int capw = rows_cap_part<WPR, CAPDIV>(cols);
-  double* A = reinterpret_cast<double*>(smem_raw);
-  double* Bw = reinterpret_cast<double*>(smem_raw + a_bytes) + (size_t)capw * w;
-  double* red = reinterpret_cast<double*>(smem_raw + a_bytes + (size_t)capw * 8 * WPR);  // [2][WPR][4]
-  unsigned long long* bar = reinterpret_cast<unsigned long long*>(red + 2 * WPR * 4);
-  const bool tma = (cols % 2) == 0 && (((uintptr_t)Y | (uintptr_t)X) & 15) == 0;
-  const unsigned bytes = (unsigned)cols * 8u;
-  // this warp's slice [q0, q1) of the row (even boundaries for 16-byte loads)
-  const int q0 = (int)(((int64_t)cols * w / WPR) & ~1LL);
-  const int q1 = w + 1 == WPR ? cols : (int)(((int64_t)cols * (w + 1) / WPR) & ~1LL);
-  if (threadIdx.x == 0 && tma) mbar_init(bar);
-  __syncthreads();
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  unsigned phase = 0;
-  int rb = 0;  // reduction slot buffer
-  const unsigned lt = (1u << lane) - 1u;
-  // combine per-warp (v0, v1, v2) over the CTA; k-th component op: 0 sum, 2 max
-  auto cta3 = [&](double v0, double v1, double v2, bool max1, double& t0, double& t1,
-                  double& t2) {
-    v0 = warp_sum(v0);
-    v1 = max1 ? warp_max(v1) : warp_sum(v1);
-    v2 = warp_sum(v2);
-    double* slot = red + (rb * WPR + w) * 4;
-    if (lane == 0) { slot[0] = v0; slot[1] = v1; slot[2] = v2; }
-    __syncthreads();
-    const double* s0 = red + rb * WPR * 4;
-    t0 = s0[0]; t1 = s0[1]; t2 = s0[2];
-#pragma unroll
-    for (int q = 1; q < WPR; ++q) {
-      t0 += s0[q * 4 + 0];
-      t1 = max1 ? fmax(t1, s0[q * 4 + 1]) : t1 + s0[q * 4 + 1];
-      t2 += s0[q * 4 + 2];
-    }
-    rb ^= 1;
-  };
-  for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
-    const double* y = Y + row * (int64_t)cols;
-    double* x = X + row * (int64_t)cols;
-    if (tma) {
-      if (threadIdx.x == 0) {
-        tma_store_wait_read();  // the previous row's store has read A
-        mbar_expect_tx(bar, bytes);
-        tma_load_1d(A, y, bytes, bar);
-      }
-      mbar_wait(bar, phase);
-      phase ^= 1u;
-    } else {
-      for (int i = threadIdx.x; i < cols; i += blockDim.x) A[i] = __ldcs(y + i);
-      __syncthreads();
-    }
-    double s0 = 0.0, s1 = 0.0, m0 = -HUGE_VAL, m1 = -HUGE_VAL;
-    for (int i = q0 + 2 * lane; i + 1 < q1; i += 64) {
-      const double2 v = *reinterpret_cast<const double2*>(A + i);
-      s0 += v.x;
-      s1 += v.y;
-      m0 = fmax(m0, v.x);
-      m1 = fmax(m1, v.y);
-    }
-    if (((q1 - q0) & 1) && lane == 0) {
-      s0 += A[q1 - 1];
-      m0 = fmax(m0, A[q1 - 1]);
-    }
-    double sum, mx, unused;
-    cta3(s0 + s1, fmax(m0, m1), 0.0, true, sum, mx, unused);
-    const double formula = (r - sum) / (double)cols, tight = r - mx;
-    double lam = !isnan(lam0_given) ? lam0_given : (start && tight < formula ? tight : formula);
-    lam = lam >= -mx ? lam : -mx;
-    double lo = -HUGE_VAL, hi = HUGE_VAL, fix_hi = HUGE_VAL;
-    int iterations = 0;
-    const double* F = A + q0;
-    int m = q1 - q0;
-    bool compacted = false;
-    for (;;) {
-      double val;
-      int np, nz;
-      rows_phi(F, m, lam, fixing && !compacted && isfinite(fix_hi), fix_hi, lane, val, np, nz);
-      const int npw = warp_sum_i(np);
-      double value, dm, zz;
-      cta3(val, (double)np, (double)nz, false, value, dm, zz);
-      const double dminus = dm, dplus = dm + zz;
-      double deriv;
-      if (iterations == 0) {
-        if (value == r) break;
-        deriv = value < r ? dplus : dminus;
-      } else {
-        if (value <= r) break;
-        deriv = dminus;
-      }
-      if (value < r) lo = lam;
-      else {
-        hi = lam;
-        if (fixing) {
-          fix_hi = lam;
-          if (npw <= capw) {  // this warp's survivors fit: compact them (values only)
-            int out = 0;
-            for (int i0 = 0; i0 < m; i0 += 32) {
-              const int i = i0 + lane;
-              double v = 0.0;
-              bool keep = false;
-              if (i < m) {
-                v = F[i];
-                keep = __dadd_rn(v, lam) > 0;
-              }
-              const unsigned mask = __ballot_sync(0xffffffffu, keep);
-              if (keep) Bw[out + __popc(mask & lt)] = v;  // out <= i0: in-place safe
-              out += __popc(mask);
-            }
-            __syncwarp();
-            F = Bw;
-            m = out;
-            compacted = true;
-          }
-        }
-      }
-      if (deriv <= 0) {  // simplex.py:276-281
-        double mneg = -HUGE_VAL;
-        for (int i = lane; i < m; i += 32) {
-          const double v = F[i];
-          if (!compacted && fixing && !(__dadd_rn(v, fix_hi) > 0)) continue;
-          mneg = fmax(mneg, -v);
-        }
-        double t0, t2;
-        cta3(0.0, mneg, 0.0, true, t0, lam, t2);
-        ++iterations;
-        continue;
-      }
-      const double step = -(value - r) / deriv;
-      const double next = lam + step;
-      if (fabs(step) < tau || next == lam) { lam = next; break; }
-      if (isfinite(lo) && isfinite(hi) && hi - lo < tau * fmax(fabs(hi), fabs(lo))) {
-        lam = next;
-        break;
-      }
-      lam = next;
-      ++iterations;
-      if (iterations > max_iter) break;
-    }
-    if (tma) {
-      for (int i = q0 + 2 * lane; i + 1 < q1; i += 64) {
-        double2 v = *reinterpret_cast<double2*>(A + i);
-        const double t0 = __dadd_rn(v.x, lam), t1 = __dadd_rn(v.y, lam);
-        v.x = t0 > 0 ? t0 : 0.0;
-        v.y = t1 > 0 ? t1 : 0.0;
-        *reinterpret_cast<double2*>(A + i) = v;
-      }
-      if (((q1 - q0) & 1) && lane == 0) {
-        const double t = __dadd_rn(A[q1 - 1], lam);
-        A[q1 - 1] = t > 0 ? t : 0.0;
-      }
-      fence_async_smem();
-      __syncthreads();
-      if (threadIdx.x == 0) tma_store_1d(x, A, bytes);
-    } else {
-      for (int i = threadIdx.x; i < cols; i += blockDim.x) {
-        const double t = __dadd_rn(A[i], lam);
-        __stcs(x + i, t > 0 ? t : 0.0);
-      }
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-      if (lam_out) lam_out[row] = lam;
-      if (it_out) it_out[row] = iterations;
-    }
-  }
-  if (threadIdx.x == 0 && tma) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-}
-
-// ------------------------------------------------------------ rows, pipelined
-// The CTA-per-row algorithm with (1) the next row's bulk load issued while the
-// current row iterates (two row buffers), and (2) the first phi evaluation
-// fused with the compaction it almost always triggers: the survivors
-// (t > 0) are written to the warp's free-set buffer during the phi pass
-// itself (ballot positions preserve the element order; writes stop at the
-// buffer capacity) and adopted only if the decision then fixes (phi >= r)
-// and they fit -- one pass over the row instead of two.
-template <int WPR, int CAPDIV = 8, int NB = 2>
-__host__ __device__ inline size_t rows_pipe_smem(int cols) {
-  return NB * (((size_t)cols * 8 + 127) / 128 * 128) +
-         (size_t)rows_cap_part<WPR, CAPDIV>(cols) * 10 * WPR + 2 * WPR * 4 * 8 + 128;
-}
-
-// phi over the warp's slice with speculative survivor capture into Bw (values)
-// and BI (slice positions, for the zero-fill + scatter final pass).
-// t = y + lam >= 0 exactly when y >= -lam (the rounded sum of two doubles is
-// negative iff the exact one is), so the common path is one compare per
-// element and one vote per 256-element step; the bookkeeping (sums, counts,
-// ballot positions in element order) runs only in steps holding a t >= 0.
-DEVI void rows_capture_step(const double* F, int i0, int m2, double lam, int lane, unsigned lt,
-                            double* Bw, uint16_t* BI, int cap, double& v0, double& v1, int& z,
-                            int& o) {
-  const int i = i0 + 2 * lane;
-  double2 v = make_double2(0.0, 0.0);
-  const bool in = i < m2;
-  if (in) v = *reinterpret_cast<const double2*>(F + i);
-  const double t0 = __dadd_rn(v.x, lam), t1 = __dadd_rn(v.y, lam);
-  const bool k0 = in && t0 > 0, k1 = in && t1 > 0;
-  v0 += k0 ? t0 : 0.0;
-  v1 += k1 ? t1 : 0.0;
-  z += (in && t0 == 0) + (in && t1 == 0);
-  const unsigned b0 = __ballot_sync(0xffffffffu, k0), b1 = __ballot_sync(0xffffffffu, k1);
-  const int pos0 = o + __popc(b0 & lt) + __popc(b1 & lt);
-  if (k0 && pos0 < cap) { Bw[pos0] = v.x; BI[pos0] = (uint16_t)i; }
-  if (k1 && pos0 + k0 < cap) { Bw[pos0 + k0] = v.y; BI[pos0 + k0] = (uint16_t)(i + 1); }
-  o += __popc(b0) + __popc(b1);
-}
-
-DEVI void rows_phi_capture(const double* F, int m, double lam, int lane, unsigned lt, double* Bw,
-                           uint16_t* BI, int cap, double& val, int& npos, int& nzero) {
-  double v0 = 0.0, v1 = 0.0;
-  int z = 0, o = 0;
-  const int m2 = m & ~1;
-  const double nl = -lam;
-  for (int i0 = 0; i0 < m2; i0 += 64) {
-    const int i = i0 + 2 * lane;
-    const bool in = i < m2;
-    double2 v = make_double2(-HUGE_VAL, -HUGE_VAL);
-    if (in) v = *reinterpret_cast<const double2*>(F + i);
-    if (!__any_sync(0xffffffffu, v.x >= nl || v.y >= nl)) continue;  // no t >= 0 here
-    rows_capture_step(F, i0, m2, lam, lane, lt, Bw, BI, cap, v0, v1, z, o);
-  }
-  if (m & 1) {  // odd slice: the last element, lane 0
-    const double v = F[m - 1];
-    const double t = __dadd_rn(v, lam);
-    const bool k = lane == 0 && t > 0;
-    v0 += k ? t : 0.0;
-    z += lane == 0 && t == 0;
-    if (__ballot_sync(0xffffffffu, k)) {
-      if (lane == 0 && o < cap) { Bw[o] = v; BI[o] = (uint16_t)(m - 1); }
-      ++o;
-    }
-  }
-  val = v0 + v1;
-  npos = o;  // warp-uniform: the survivors of the whole slice
-  nzero = z;
-}
-
-DEVI double __int_as_double_lo(int v) { return __hiloint2double(0, v); }
-DEVI int __double_lo_as_int(double d) { return __double2loint(d); }
-
-template <int WPR, int CAPDIV = 8, int NB = 2>
-__global__ void __launch_bounds__(32 * WPR) spx_rows_pipe_kernel(
-    const double* __restrict__ Y, double* __restrict__ X, double* __restrict__ lam_out,
-    int32_t* __restrict__ it_out, int64_t rows, int cols, double r, double tau, int max_iter,
-    int fixing, double lam0_given, int start) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const size_t a_bytes = ((size_t)cols * 8 + 127) / 128 * 128;
-  const int capw = rows_cap_part<WPR, CAPDIV>(cols);
-  double* Abuf[2] = {reinterpret_cast<double*>(smem_raw),
-                     reinterpret_cast<double*>(smem_raw + (NB - 1) * a_bytes)};
-  double* Bw = reinterpret_cast<double*>(smem_raw + NB * a_bytes) + (size_t)capw * w;
-  double* red = reinterpret_cast<double*>(smem_raw + NB * a_bytes + (size_t)capw * 8 * WPR);
-  uint16_t* BI = reinterpret_cast<uint16_t*>(red + 2 * WPR * 4 + 2) + (size_t)capw * w;
-  unsigned long long* bar = reinterpret_cast<unsigned long long*>(red + 2 * WPR * 4);  // [2]
-  const unsigned bytes = (unsigned)cols * 8u;
-  const int q0 = (int)(((int64_t)cols * w / WPR) & ~1LL);
-  const int q1 = w + 1 == WPR ? cols : (int)(((int64_t)cols * (w + 1) / WPR) & ~1LL);
-  const int64_t G = gridDim.x;
-  if (threadIdx.x == 0) {
-    mbar_init(&bar[0]);
-    mbar_init(&bar[1]);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    if ((int64_t)blockIdx.x < rows) {  // prologue: the first row
-      mbar_expect_tx(&bar[0], bytes);
-      tma_load_1d(Abuf[0], Y + (int64_t)blockIdx.x * cols, bytes, &bar[0]);
-    }
-  }
-  __syncthreads();
-  unsigned phase[2] = {0u, 0u};
-  int rb = 0;
-  const unsigned lt = (1u << lane) - 1u;
-  auto cta3 = [&](double v0, double v1, double v2, bool max1, double& t0, double& t1,
-                  double& t2) {
-    v0 = warp_sum(v0);
-    v1 = max1 ? warp_max(v1) : warp_sum(v1);
-    v2 = warp_sum(v2);
-    double* slot = red + (rb * WPR + w) * 4;
-    if (lane == 0) { slot[0] = v0; slot[1] = v1; slot[2] = v2; }
-    __syncthreads();
-    const double* s0 = red + rb * WPR * 4;
-    t0 = s0[0]; t1 = s0[1]; t2 = s0[2];
-#pragma unroll
-    for (int q = 1; q < WPR; ++q) {
-      t0 += s0[q * 4 + 0];
-      t1 = max1 ? fmax(t1, s0[q * 4 + 1]) : t1 + s0[q * 4 + 1];
-      t2 += s0[q * 4 + 2];
-    }
-    rb ^= 1;
-  };
-  // (value, #pos, #zero) over the CTA: one double and one packed integer
-  // butterfly per warp (counts <= cols < 2^16), one __syncthreads
-  // (plus how many warps' survivors overflow their free-set buffer, so the
-  // compaction decision is CTA-uniform)
-  auto cta_phi = [&](double v, int npos_lane, int nz_lane, int ovf, double& tv, int& tpos, int& tz,
-                     int& tovf) {
-    v = warp_sum(v);
-    const int pk = warp_sum_i((npos_lane << 16) + nz_lane);
-    double* slot = red + (rb * WPR + w) * 4;
-    if (lane == 0) { slot[0] = v; slot[1] = __int_as_double_lo(pk); slot[2] = __int_as_double_lo(ovf); }
-    __syncthreads();
-    const double* s0 = red + rb * WPR * 4;
-    tv = s0[0];
-    int tp = __double_lo_as_int(s0[1]), to = __double_lo_as_int(s0[2]);
-#pragma unroll
-    for (int q = 1; q < WPR; ++q) {
-      tv += s0[q * 4 + 0];
-      tp += __double_lo_as_int(s0[q * 4 + 1]);
-      to += __double_lo_as_int(s0[q * 4 + 2]);
-    }
-    tpos = tp >> 16;
-    tz = tp & 0xffff;
-    tovf = to;
-    rb ^= 1;
-  };
-  bool next_issued = false;  // NB == 1: this row's buffer was refilled early
-  int k = 0;
-  for (int64_t row = blockIdx.x; row < rows; row += G, ++k) {
-    const int b = NB == 2 ? (k & 1) : 0;
-    double* A = Abuf[b];
-    double* x = X + row * (int64_t)cols;
-    if (NB == 1 && k > 0 && !next_issued && threadIdx.x == 0) {  // reload after the store read it
-      tma_store_wait_read();
-      mbar_expect_tx(&bar[0], bytes);
-      tma_load_1d(A, Y + row * (int64_t)cols, bytes, &bar[0]);
-    }
-    next_issued = false;
-    mbar_wait(&bar[b], phase[b]);
-    phase[b] ^= 1u;
-    double s0 = 0.0, s1 = 0.0, m0 = -HUGE_VAL, m1 = -HUGE_VAL;
-    for (int i = q0 + 2 * lane; i + 1 < q1; i += 64) {
-      const double2 v = *reinterpret_cast<const double2*>(A + i);
-      s0 += v.x;
-      s1 += v.y;
-      m0 = fmax(m0, v.x);
-      m1 = fmax(m1, v.y);
-    }
-    if (((q1 - q0) & 1) && lane == 0) {
-      s0 += A[q1 - 1];
-      m0 = fmax(m0, A[q1 - 1]);
-    }
-    double sum, mx, unused;
-    cta3(s0 + s1, fmax(m0, m1), 0.0, true, sum, mx, unused);
-    // the next row streams into the other buffer while this one iterates;
-    // that buffer's previous row was stored one row ago (its read is done
-    // or nearly so by now)
-    if (NB == 2 && threadIdx.x == 0 && row + G < rows) {
-      tma_store_wait_read();
-      mbar_expect_tx(&bar[b ^ 1], bytes);
-      tma_load_1d(Abuf[b ^ 1], Y + (row + G) * (int64_t)cols, bytes, &bar[b ^ 1]);
-    }
-    const double formula = (r - sum) / (double)cols, tight = r - mx;
-    double lam = !isnan(lam0_given) ? lam0_given : (start && tight < formula ? tight : formula);
-    lam = lam >= -mx ? lam : -mx;
-    double lo = -HUGE_VAL, hi = HUGE_VAL, fix_hi = HUGE_VAL;
-    int iterations = 0;
-    const double* F = A + q0;
-    int m = q1 - q0;
-    bool compacted = false;
-    for (;;) {
-      double val;
-      int np, nz;
-      const bool capture = fixing && !compacted;
-      if (capture) {
-        // no variable is dropped yet (nothing compacted, fix_hi = +inf at the
-        // first evaluation; later evaluations reach here only while the
-        // survivors did not fit -- then the drop test applies as in rows_phi)
-        if (isfinite(fix_hi)) rows_phi(F, m, lam, true, fix_hi, lane, val, np, nz);
-        else rows_phi_capture(F, m, lam, lane, lt, Bw, BI, capw, val, np, nz);
-      } else {
-        rows_phi(F, m, lam, false, fix_hi, lane, val, np, nz);
-      }
-      const bool captured_now = capture && !isfinite(fix_hi);
-      const int npw = captured_now ? np : warp_sum_i(np);
-      const int npl = captured_now ? (lane == 0 ? np : 0) : np;
-      double value;
-      int tpos, tz, tovf;
-      cta_phi(val, npl, nz, lane == 0 && npw > capw, value, tpos, tz, tovf);
-      const double dminus = (double)tpos, dplus = (double)(tpos + tz);
-      double deriv;
-      if (iterations == 0) {
-        if (value == r) break;
-        deriv = value < r ? dplus : dminus;
-      } else {
-        if (value <= r) break;
-        deriv = dminus;
-      }
-      if (value < r) lo = lam;
-      else {
-        hi = lam;
-        if (fixing) {
-          const bool captured = capture && !isfinite(fix_hi);
-          fix_hi = lam;
-          if (tovf == 0 && !compacted) {  // every warp's survivors fit: CTA-uniform
-            if (!captured) {  // compact now (values + slice positions), in place
-              int out = 0;
-              for (int i0 = 0; i0 < m; i0 += 32) {
-                const int i = i0 + lane;
-                double v = 0.0;
-                int ix = 0;
-                bool keep = false;
-                if (i < m) {
-                  v = F[i];
-                  ix = compacted ? BI[i] : i;
-                  keep = __dadd_rn(v, lam) > 0;
-                }
-                const unsigned mask = __ballot_sync(0xffffffffu, keep);
-                __syncwarp();  // every lane has read F[i] / BI[i] before anyone writes
-                if (keep) {
-                  Bw[out + __popc(mask & lt)] = v;  // out <= i0: in-place safe
-                  BI[out + __popc(mask & lt)] = (uint16_t)ix;
-                }
-                out += __popc(mask);
-              }
-            }
-            __syncwarp();
-            F = Bw;
-            m = npw;
-            compacted = true;
-            // single buffer: nobody reads the row again (x leaves through the
-            // zero-fill + scatter below), so the next row can stream in now
-            if (NB == 1 && threadIdx.x == 0 && row + G < rows) {
-              tma_store_wait_read();
-              mbar_expect_tx(&bar[0], bytes);
-              tma_load_1d(A, Y + (row + G) * (int64_t)cols, bytes, &bar[0]);
-            }
-            next_issued = NB == 1;
-          } else if (tovf == 0 && compacted && npw <= capw) {  // re-compact the free set
-            int out = 0;
-            for (int i0 = 0; i0 < m; i0 += 32) {
-              const int i = i0 + lane;
-              double v = 0.0;
-              int ix = 0;
-              bool keep = false;
-              if (i < m) {
-                v = F[i];
-                ix = BI[i];
-                keep = __dadd_rn(v, lam) > 0;
-              }
-              const unsigned mask = __ballot_sync(0xffffffffu, keep);
-              __syncwarp();
-              if (keep) {
-                Bw[out + __popc(mask & lt)] = v;
-                BI[out + __popc(mask & lt)] = (uint16_t)ix;
-              }
-              out += __popc(mask);
-            }
-            __syncwarp();
-            m = npw;
-          }
-        }
-      }
-      if (deriv <= 0) {  // simplex.py:276-281
-        double mneg = -HUGE_VAL;
-        for (int i = lane; i < m; i += 32) {
-          const double v = F[i];
-          if (!compacted && fixing && !(__dadd_rn(v, fix_hi) > 0)) continue;
-          mneg = fmax(mneg, -v);
-        }
-        double t0, t2;
-        cta3(0.0, mneg, 0.0, true, t0, lam, t2);
-        ++iterations;
-        continue;
-      }
-      const double step = -(value - r) / deriv;
-      const double next = lam + step;
-      if (fabs(step) < tau || next == lam) { lam = next; break; }
-      if (isfinite(lo) && isfinite(hi) && hi - lo < tau * fmax(fabs(hi), fabs(lo))) {
-        lam = next;
-        break;
-      }
-      lam = next;
-      ++iterations;
-      if (iterations > max_iter) break;
-    }
-    if (compacted && NB == 1) {
-      // every variable outside the free set was dropped at some fix_hi >= lam,
-      // so its y + lam <= y + fix_hi <= 0 (rounded add is monotone): x = 0
-      // there; the free set scatters max(0, y + lam) to its positions --
-      // straight to global memory (the row buffer already holds the next row)
-      double* xs = x + q0;
-      for (int i = 2 * lane; i + 1 < q1 - q0; i += 64)
-        __stcs(reinterpret_cast<double2*>(xs + i), make_double2(0.0, 0.0));
-      if (((q1 - q0) & 1) && lane == 0) xs[q1 - q0 - 1] = 0.0;
-      __syncwarp();
-      for (int i = lane; i < m; i += 32) {
-        const double t = __dadd_rn(F[i], lam);
-        if (t > 0) xs[BI[i]] = t;
-      }
-      if (threadIdx.x == 0) {
-        if (lam_out) lam_out[row] = lam;
-        if (it_out) it_out[row] = iterations;
-      }
-      continue;
-    }
-    if (compacted) {
-      for (int i = q0 + 2 * lane; i + 1 < q1; i += 64)
-        *reinterpret_cast<double2*>(A + i) = make_double2(0.0, 0.0);
-      if (((q1 - q0) & 1) && lane == 0) A[q1 - 1] = 0.0;
-      __syncwarp();
-      for (int i = lane; i < m; i += 32) {
-        const double t = __dadd_rn(F[i], lam);
-        if (t > 0) A[q0 + BI[i]] = t;
-      }
-    } else {
-      for (int i = q0 + 2 * lane; i + 1 < q1; i += 64) {
-        double2 v = *reinterpret_cast<double2*>(A + i);
-        const double t0 = __dadd_rn(v.x, lam), t1 = __dadd_rn(v.y, lam);
-        v.x = t0 > 0 ? t0 : 0.0;
-        v.y = t1 > 0 ? t1 : 0.0;
-        *reinterpret_cast<double2*>(A + i) = v;
-      }
-      if (((q1 - q0) & 1) && lane == 0) {
-        const double t = __dadd_rn(A[q1 - 1], lam);
-        A[q1 - 1] = t > 0 ? t : 0.0;
-      }
-    }
-    fence_async_smem();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      tma_store_1d(x, A, bytes);
-      if (lam_out) lam_out[row] = lam;
-      if (it_out) it_out[row] = iterations;
-    }
-  }
-  if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // ------------------------------------------------------------ Algorithm 2
@@ -1936,14 +1173,37 @@ __global__ void __launch_bounds__(256) alg2_chunks_kernel(
   int32_t* Jc = J + lo;
   int32_t* Jtc = Jt + lo;
   double sabs = 0.0;
-  // simplex.py:58-111 with local offsets (pos - lo) in J / Jt
-  const double y1 = w_of(lo);
+  // simplex.py:58-111 with local offsets (pos - lo) in J / Jt.  Sharpened,
+  // a chunk other than the first does not seed with a y <= 0: the sequential
+  // recurrence only ever seeds with idx[0], every later y <= 0 is fixed
+  // outright (simplex.py:74-76), so the chunk skips (fixes) its leading
+  // nonpositive entries and seeds with its first positive one -- the union of
+  // the fixed sets then matches the sequential one apart from zero proofs,
+  // which hold for the restricted problem too.  (Chunk 0's seed idx[0] <= 0
+  // is decided by the host: it runs the exact sequential recurrence.)
+  int64_t first = lo;
+  if (sharpened && k > 0 && !use_xbar) {
+    while (first < hi && !(w_of(first) > 0.0)) {
+      sabs += w_of(first);
+      if (fixed) fixed[orig(first)] = 1;
+      ++first;
+    }
+    if (first == hi) {  // nothing positive: the chunk joins no free set
+      sums[k] = 0.0;
+      cards[k] = 0;
+      jplus_out[k] = 0;
+      lams[k] = INFINITY;
+      if (sumabs) sumabs[k] = sabs;
+      return;
+    }
+  }
+  const double y1 = w_of(first);
   sabs += y1;
   int64_t nJ = 1, nJt = 0, jplus = 0;
-  Jc[0] = 0;
+  Jc[0] = (int32_t)(first - lo);
   double sumJ = y1, lam = r - y1;
-  if (!use_xbar || xbar[orig(lo)] > 0.0) jplus = 1;
-  for (int64_t pos = lo + 1; pos < hi; ++pos) {
+  if (!use_xbar || xbar[orig(first)] > 0.0) jplus = 1;
+  for (int64_t pos = first + 1; pos < hi; ++pos) {
     const double yi = w_of(pos);
     sabs += yi;
     if (use_xbar && xbar[orig(pos)] <= 0.0) continue;

@@ -23,9 +23,14 @@ def test_sharpened_simplex_with_positive_root():
             out = P.newton_project_simplex(y, r, sharpened=sharp)
             assert abs(out.lam - ref["lam"]) <= 1e-12 * max(1.0, abs(ref["lam"])), (n, sharp)
             assert np.abs(out.x - ref["x"]).max() <= 1e-12 * max(1.0, r)
-        # the two routes really differ here: sharpened zeroes every y_i <= 0
-        xs = P.newton_project_simplex(y, r, sharpened=True).x
-        assert np.all(xs[y <= 0] == 0.0)
+        # the two routes really differ here: sharpened keeps every y_i <= 0 out
+        # of the multiplier updates (simplex.py:79-80), so the root moves; the
+        # dense x is still max(0, y + lam) everywhere (simplex.py:298)
+        a = P.newton_project_simplex(y, r, sharpened=False)
+        b = P.newton_project_simplex(y, r, sharpened=True)
+        if (y <= 0).any():
+            assert a.lam != b.lam
+        assert np.array_equal(b.x, np.maximum(0.0, y + b.lam))
 
 
 def test_l1_negative_xbar():

@@ -328,3 +328,39 @@ def test_rows_many_per_cta_mixed_paths():
         assert its[i] == ref["iterations"]
         assert float(np.abs(X[i] - ref["x"]).max()) <= TOL
     np.testing.assert_allclose(X.sum(axis=1), 1.0, atol=1e-12)
+
+
+@pytest.mark.parametrize("route", ["tight", "formula", "lambda0_above", "lambda0_below"])
+def test_rows_start_routes_every_row(route):
+    """Every start route of the batched kernel (candidate capture at max y - r,
+    the second capture at lambda0, the general path) against the oracle on
+    every row of a mixed batch (N(0,1) rows, u01 rows, constant rows), and
+    bit-identical reruns (rows are handed out by a grid counter)."""
+    p = P()
+    rng = np.random.default_rng(11)
+    rows, cols = 1500, 2048
+    Y = rng.normal(0, 1, (rows, cols))
+    Y[1::3] = rng.uniform(0, 1, (len(range(1, rows, 3)), cols))
+    Y[2::15] = 0.25  # constant rows: every element ties
+    kw = {}
+    if route == "formula":
+        kw["start"] = "formula"
+    elif route == "lambda0_above":
+        kw["lambda0"] = 5.0
+    elif route == "lambda0_below":
+        kw["lambda0"] = -5.0
+    X, lam, its, _ = p.project_simplex_rows(Y, 1.0, **kw)
+    X2, lam2, its2, _ = p.project_simplex_rows(Y, 1.0, **kw)
+    assert np.array_equal(X, X2) and np.array_equal(lam, lam2) and np.array_equal(its, its2)
+    for i in range(rows):
+        y = Y[i]
+        if route == "tight":
+            lam0 = min((1.0 - O.pairwise_sum(y)) / cols, 1.0 - float(y.max()))
+        elif route == "formula":
+            lam0 = (1.0 - O.pairwise_sum(y)) / cols
+        else:
+            lam0 = kw["lambda0"]
+        ref = O.newton_project_simplex(y, 1.0, lam0=lam0)
+        assert close(lam[i], ref["lam"]), (route, i, lam[i], ref["lam"])
+        assert its[i] == ref["iterations"], (route, i, its[i], ref["iterations"])
+        assert float(np.abs(X[i] - ref["x"]).max()) <= TOL * max(1.0, float(np.abs(y).max()))
