@@ -225,6 +225,14 @@ int cqk_reserve(cqk_handle *h, int64_t n);
    with CQK_MEM_HOST must not allocate while peers wait inside the kernel). */
 int cqk_reserve_host(cqk_handle *h, int64_t n);
 int cqk_set_engine(cqk_handle *h, int mode);
+/* Fused start of the TMA CQK solve (no explicit lambda0, no xbar): a sample
+   pass estimates lambda0, then ONE pass computes lambda0 (core.py:237-257) and
+   validate() and classifies every element against [est(1 - w), est(1 + w)];
+   the first phi scan then reads only the elements it could not classify.
+   Used from min_n elements per rank (default 4e6, CQK_FUSED_MIN_N); w =
+   half_width (default 2e-3).  Results agree with the unfused solve to
+   rounding (lambda0's terms share the division's reciprocal). */
+int cqk_set_fused(cqk_handle *h, int64_t min_n, double half_width);
 int cqk_set_grid_limit(cqk_handle *h, int max_ctas);
 /* Sharded solve_cqk / jacobi_solve / par_solve_cqk: this rank's shard
    [offset, offset + n_local) of an n_total-element instance.  All ranks call

@@ -87,7 +87,7 @@ EXPORTS = (
     "spx_project_f64", "l1_project_f64", "spx_project_warm_f64", "l1_project_warm_f64",
     "spx_project_batched_f64", "cqk_selftest_division",
     "cqk_comm_ipc_handle_size", "cqk_comm_create", "cqk_comm_connect", "cqk_comm_connect_local",
-    "cqk_set_grid_limit", "cqk_set_engine", "cqk_reserve", "cqk_reserve_host", "cqk_solve_sharded_f64", "spx_project_sharded_f64",
+    "cqk_set_grid_limit", "cqk_set_engine", "cqk_set_fused", "cqk_reserve", "cqk_reserve_host", "cqk_solve_sharded_f64", "spx_project_sharded_f64",
     "l1_project_sharded_f64", "spx_init_alg2_f64", "cqk_gen_cqk_device",
     "cqk_gen_cqk_device_range", "cqk_gen_simplex_u01_device", "spx_project_batched_multi_f64",
     "cqk_read_peak_f64",
@@ -139,6 +139,7 @@ def _declare(L):
     L.cqk_comm_connect_local.argtypes = [_P, _P, ctypes.c_int]
     L.cqk_set_grid_limit.argtypes = [_P, ctypes.c_int]
     L.cqk_set_engine.argtypes = [_P, ctypes.c_int]
+    L.cqk_set_fused.argtypes = [_P, _I64, _D]
     L.cqk_reserve_host.argtypes = [_P, _I64]
     L.cqk_reserve.argtypes = [_P, _I64]
     L.cqk_solve_sharded_f64.argtypes = [_P, ctypes.c_int, *arr5, _I64, _I64, _I64, _D, _OPT, _P,
@@ -225,6 +226,11 @@ class Handle:
         cudaStreamLegacy so work stays ordered with the caller's stream."""
         self.lib.cqk_set_stream(self.ptr, _P(stream_ptr if stream_ptr else 1))
         self._stream = stream_ptr
+
+    def set_fused(self, min_n=4_000_000, half_width=2e-3):
+        """Fused start of the CQK solve from `min_n` elements per rank (cqk_b200.h)."""
+        if self.lib.cqk_set_fused(self.ptr, int(min_n), float(half_width)) != 0:
+            raise NativeError(last_error())
 
     def use_current_stream(self):
         """Bind to torch's current stream on this handle's device (the C call

@@ -91,6 +91,8 @@ struct cqk_handle {
   bool use_tma = true;                     // CQK_ENGINE=seg selects the warp-segment kernel
   int engine = 0;                          // cqk_set_engine: 0 auto, 1 TMA, 2 warp segments
   int64_t tma_min_n = 65536;               // auto: CQK solves of >= this many elements per rank
+  int64_t fused_min_n = 4000000;           // fused start (sample + fused first pass) from this size
+  double fused_width = 2e-3;               // ... its classification interval, relative half-width
   unsigned* sync = nullptr;  // [0] arrive, [1] gen, [2] error
   void* state = nullptr;     // CqkState / SpxState
   double* partials = nullptr;
@@ -225,6 +227,7 @@ int cqk_create(cqk_handle** out, int device) {
   h->stream = h->own;
   if (const char* gl = getenv("CQK_GRID_LIMIT")) h->grid_limit = atoi(gl);  // shared-GPU runs
   if (const char* mn = getenv("CQK_TMA_MIN_N")) h->tma_min_n = atoll(mn);
+  if (const char* fm = getenv("CQK_FUSED_MIN_N")) h->fused_min_n = atoll(fm);
   *out = h;
   return 0;
 }
@@ -555,6 +558,13 @@ extern "C" int cqk_set_engine(cqk_handle* h, int mode) {
   return 0;
 }
 
+extern "C" int cqk_set_fused(cqk_handle* h, int64_t min_n, double half_width) {
+  if (!h || !(half_width >= 0.0)) return set_err(CQK_E_ARG, "fused start: half_width >= 0");
+  h->fused_min_n = min_n;
+  h->fused_width = half_width;
+  return 0;
+}
+
 extern "C" int cqk_set_grid_limit(cqk_handle* h, int max_ctas) {
   if (!h) return set_err(CQK_E_ARG, "null handle");
   h->grid_limit = max_ctas;
@@ -713,9 +723,18 @@ static int solve_impl(cqk_handle* h, int mem, const double* d, const double* a, 
   // order reproduces the reference's iterate counts on tiny inputs more often
   const bool tma = h->use_tma && (h->engine == 1 || (h->engine == 0 && n >= h->tma_min_n));
   s.compact_ratio = std::isnan(opts.compact_ratio) ? default_compact_ratio(tma) : opts.compact_ratio;
+  // fused start (cqk_tma.cuh): lambda0 and the first scan share one pass
+  // (a per-rank size every rank derives alike: the phases must match across ranks)
+  const int64_t per_rank = sharded ? n_total / std::max(h->world, 1) : n;
+  const bool fused = tma && !lam0_given && !xbar && per_rank >= h->fused_min_n;
+  if (fused) {
+    s.fused = 1;
+    s.fused_width = h->fused_width;
+    s.cmd.phase = PH_SAMPLE;
+  }
   // scratch: n per array (warp segments) or whole tile slots (TMA engine)
   const size_t per = ((size_t)(tma ? tma_scratch_elems(n) : n) * sizeof(double) + 255) / 256 * 256;
-  if (fixing) CUDA_TRY(h->scratch.ensure(per * 5));
+  if (fixing || fused) CUDA_TRY(h->scratch.ensure(per * 5));
   std::memcpy(h->host_state, &s, sizeof s);  // status RUNNING until the master publishes
   CqkParams<double> p;
   std::memset(&p, 0, sizeof p);
@@ -723,6 +742,11 @@ static int solve_impl(cqk_handle* h, int mem, const double* d, const double* a, 
   p.out = (CqkState*)h->host_state_dev;
   p.d = dv[0]; p.a = dv[1]; p.b = dv[2]; p.l = dv[3]; p.u = dv[4]; p.xbar = xbar ? dv[5] : nullptr;
   if (fixing) {
+    char* sb = (char*)h->scratch.p;
+    p.sd = (double*)(sb); p.sa = (double*)(sb + per); p.sb = (double*)(sb + 2 * per);
+    p.sl = (double*)(sb + 3 * per); p.su = (double*)(sb + 4 * per);
+  }
+  if (fused && !fixing) {  // the side list needs the scratch arrays
     char* sb = (char*)h->scratch.p;
     p.sd = (double*)(sb); p.sa = (double*)(sb + per); p.sb = (double*)(sb + 2 * per);
     p.sl = (double*)(sb + 3 * per); p.su = (double*)(sb + 4 * per);
@@ -779,7 +803,8 @@ static int solve_impl(cqk_handle* h, int mem, const double* d, const double* a, 
   res->fixed_count = s.fixed_count;
   res->bracket_lo = s.lo;
   res->bracket_hi = s.hi;
-  const int64_t pass0 = (opts.check || !lam0_given) ? n : 0;
+  // fused start: no pass 0; the sample reads 24 B per sampled element
+  const int64_t pass0 = s.fused ? s.elems_sample : ((opts.check || !lam0_given) ? n : 0);
   const int64_t bytes0 = xbar ? 48 : 24;  // l, u are validated on the first scan
   const int64_t fin = (s.status == ST_SOLVED && xo) ? n : 0;
   res->elems_read = pass0 + s.elems_scan + s.elems_bp + fin;

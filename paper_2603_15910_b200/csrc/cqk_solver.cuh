@@ -35,6 +35,8 @@ enum Phase : int32_t {
   PH_DONE = 4,
   PH_COPY = 5,   // simplex/l1: x = y (inside the l1 ball)
   PH_SNAP = 6,   // simplex: max(-y[free]) snap (simplex.py:276-281)
+  PH_SAMPLE = 7, // fused start: lambda0 estimated from sample tiles
+  PH_FUSED = 8,  // fused start: lambda0 sums + validate + the first scan's aggregates
 };
 
 enum Status : int32_t {
@@ -62,7 +64,7 @@ struct Cmd {
   int32_t live_lo;  // a lower-fixed element may still be physically present
   int32_t live_hi;  // ... an upper-fixed one
   int32_t hist;     // simplex: this scan also histograms t > 0 (start "auto")
-  int32_t pad_;
+  int32_t side;     // this scan runs over the fused pass's side list (plus its aggregates)
 };
 
 // Master-side solver state (SolveState, newton.py:70-90, plus counters).
@@ -80,6 +82,15 @@ struct CqkState {
   double vidx[10];  // first offending index per validate() check (pass 0 / first scan)
   int32_t has_plo, has_phi, fixing, variant, status, has_xbar, check, domain_field;
   int32_t trace_len, trace_cap, lam0_given, err;  // err: barrier-timeout flag at the final write
+  // fused start (PH_SAMPLE -> PH_FUSED -> side scan): the first scan's
+  // contributions of every element whose status is fixed on the interval
+  // [cmd.lam - cmd.edge, cmd.lam + cmd.edge] around the estimated lambda0
+  int32_t fused, pad2_;
+  double fused_width;       // relative half-width of the classification interval
+  double agg[11];           // scan slots 0..10 of those elements at lambda0 (all ranks)
+  double agg_lo_loc, agg_hi_loc;  // their lower / upper at-bound counts on this rank
+  int64_t side_local;       // elements in this rank's side list
+  int64_t elems_sample;     // sample elements read (24 B each)
 };
 
 template <typename T>
@@ -164,7 +175,12 @@ DEVI void m_secant_or_fail(CqkState& s) {
 // ranks; loc: the same vector of this rank alone (local bookkeeping only).
 DEVI void m_after_scan(CqkState& s, const double* tot, const double* loc, double* trace) {
   s.phi_evals += 1;
-  s.elems_scan += s.phys_count;
+  if (s.cmd.side) {  // the fused pass read every element; this scan only the side list
+    s.elems_scan += s.side_local;
+    s.cmd.side = 0;
+  } else {
+    s.elems_scan += s.phys_count;
+  }
   if (s.cmd.compact) {
     s.elems_written += s.pending_phys;
     s.fixed_removed += s.phys_count - s.pending_phys;
@@ -295,6 +311,73 @@ DEVI void m_after_lambda0(CqkState& s, const double* tot) {
     s.cmd.lam = lam;
   }
   s.cmd.phase = PH_SCAN;
+}
+
+// Fused start.  The sample pass: tot 0 sum b a/d, 1 sum b^2/d, 2 elements
+// over the sample tiles -> the estimated lambda0 and the half-width of the
+// interval the fused pass classifies against.
+DEVI void m_after_sample(CqkState& s, const double* tot, double local_count) {
+  s.elems_sample += (int64_t)local_count;
+  const double scale = (double)s.n / fmax(tot[2], 1.0);
+  const double est = (s.r_orig - tot[0] * scale) / (tot[1] * scale);
+  s.cmd.lam = est;
+  // relative half-width (default 2e-3; sampled estimates land within ~5e-4 of
+  // lambda0 on the generator families)
+  s.cmd.edge = isfinite(est) ? s.fused_width * fabs(est) : 0.0;
+  s.cmd.phase = PH_FUSED;
+}
+
+// The fused pass: tot 0 s_all, 1 q_all (the lambda0 sums, same per-element
+// terms and order as pass 0), 2 the first failing validate() check as
+// class * 2^40 + index (min), 3..5 lower at-bound (sum bl, sum |bl|, count),
+// 6..8 upper at-bound, 9 / 10 interior with t >= 0 (sum b^2/d, sum b a/d),
+// 11 / 12 interior with t <= 0 (unused: such elements go to the side list),
+// 13 side-list elements.  loc: this rank's
+// vector.
+constexpr int kFusedK = 14;
+constexpr double kVKey = 1099511627776.0;  // 2^40
+DEVI void m_after_fused(CqkState& s, const double* tot, const double* loc) {
+  s.elems_scan += s.phys_count;  // 40 B per element: d, a, b, l, u
+  s.side_local = (int64_t)loc[13];
+  s.elems_written += s.side_local;  // the side list (40 B per element)
+  if (s.check) {
+    for (int c = 0; c < 10; ++c) s.vidx[c] = (double)s.n;
+    if (tot[2] < HUGE_VAL) {
+      const double c = floor(tot[2] / kVKey);
+      s.vidx[(int)c] = tot[2] - c * kVKey;
+    }
+    if (!m_validate(s, 0, 10)) return;
+  }
+  const double lam = (s.r_orig - tot[0]) / tot[1];  // m_after_lambda0's formula
+  s.lam0 = lam;
+  const double ia = s.cmd.lam - s.cmd.edge, ib = s.cmd.lam + s.cmd.edge;
+  s.cmd.lam = lam;
+  s.cmd.phase = PH_SCAN;
+  s.cmd.check_lu = 0;
+  s.cmd.edge = 0.0;
+  if (ia <= lam && lam <= ib) {  // the classification holds at lambda0: scan the side list only
+    const double pos = lam * tot[9] + tot[10], neg = lam * tot[11] + tot[12];
+    s.agg[0] = tot[3] + tot[6] + pos + neg;
+    s.agg[1] = tot[4] + tot[7] + pos - neg;
+    s.agg[2] = tot[9] + tot[11];
+    s.agg[3] = s.agg[4] = 0.0;  // no exact tie outside the side list
+    for (int k = 0; k < 3; ++k) {
+      s.agg[5 + k] = tot[3 + k];
+      s.agg[8 + k] = tot[6 + k];
+    }
+    s.agg_lo_loc = loc[5];
+    s.agg_hi_loc = loc[8];
+    s.cmd.side = 1;
+  } else {
+    s.cmd.side = 0;  // a full first scan (the side list is dropped)
+  }
+}
+
+// the side scan's totals plus the aggregates (glob: all ranks, loc: this rank)
+DEVI void m_add_aggregates(const CqkState& s, double* glob, double* loc) {
+  for (int k = 0; k < 11; ++k) glob[k] += s.agg[k];
+  loc[7] += s.agg_lo_loc;
+  loc[10] += s.agg_hi_loc;
 }
 
 // ------------------------------------------------------------ element ops

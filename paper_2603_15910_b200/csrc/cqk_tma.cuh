@@ -673,6 +673,232 @@ DEVI void t_final(const CqkParams<double>& p, const Cmd& c, const TileWalk& tw, 
   else consume(tw, pp, -1, body);
 }
 
+// ------------------------------------------------------------ fused start
+// The first two passes of solve_cqk -- lambda0 sums (core.py:237-257, 24 B
+// per element) then the first phi scan at lambda0 (40 B) -- become one 40 B
+// pass: a sample pass (kSampleTiles tiles per CTA, spread over its walk)
+// estimates lambda0; the fused pass computes the exact lambda0 sums (the same
+// per-element terms in the same order as pass 0, so lambda0 is bit-identical)
+// and classifies every element against the interval I = [est - h, est + h]:
+// below (t(I) < l), above (t(I) > u) or strictly interior with a fixed sign
+// of t -- their scan contributions at any lambda0 in I are known in closed
+// form (b*l, b*u, lambda0 * sum b^2/d + sum b*a/d) -- or ambiguous, appended
+// to a side list in scratch (per-warp sub-segments, as compaction does).
+// When lambda0 lands in I the first scan reads only the side list and adds
+// the aggregates; otherwise it is an ordinary full scan.  Exact ties t == l /
+// t == u can only occur in the side list, so the one-sided slopes are exact.
+constexpr int kSampleTiles = 4;
+
+// this CTA's q-th sample tile (orig walk ordinal), -1 past the end
+DEVI int64_t sample_tile(int64_t ntiles, int k) {
+  const int64_t G = gridDim.x, c = blockIdx.x;
+  const int64_t Q = c < ntiles ? (ntiles - c + G - 1) / G : 0;  // tiles of this CTA
+  if (Q <= 0) return -1;
+  const int64_t q = Q >= kSampleTiles ? (int64_t)k * Q / kSampleTiles : k;
+  return q < Q ? c + q * G : -1;
+}
+
+DEVI void produce_sample(const Src src, int64_t n, int64_t ntiles, TPipe& pp) {
+  for (int k = 0; k < kSampleTiles; ++k) {
+    const int64_t t = sample_tile(ntiles, k);
+    if (t < 0) break;
+    const int s = pp.pc % kStages3;
+    const unsigned ph = ((pp.pc / kStages3) & 1) ^ 1;
+    if (pp.pc >= (unsigned)kStages3) mbar_wait_s(pp.empty + 8 * s, ph);
+    const int64_t left = n - t * kTileC;
+    const unsigned bytes = ((unsigned)(left < kTileC ? left : kTileC) * 8u) & ~15u;
+    const unsigned fb = pp.full + 8 * s;
+    mbar_expect_tx_s(fb, 3 * bytes);
+    if (bytes) {
+      const unsigned dst = smem_u32(pp.buf) + (unsigned)(s * kStride3) * 8u;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) tma_load_1d_s(dst + a * kTileC * 8u, src.p[a] + t * kTileC, bytes, fb);
+    }
+    ++pp.pc;
+  }
+}
+
+// acc 0 sum b a/d, 1 sum b^2/d, 2 elements (t_lambda0's per-element terms)
+DEVI void t_sample(const CqkParams<double>& p, int64_t ntiles, TPipe& pp, double (&acc)[kMaxK]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int k = 0; k < kSampleTiles; ++k) {
+    const int64_t t = sample_tile(ntiles, k);
+    if (t < 0) break;
+    const int s = pp.pc % kStages3;
+    WTile wt;
+    wt.sm = pp.buf + (size_t)s * kStride3 + kSeg * warp;
+    wt.gbase = t * kTileC + kSeg * warp;
+    const int64_t left = p.n - wt.gbase;
+    wt.wcnt = left <= 0 ? 0 : (left < kSeg ? (int)left : kSeg);
+    wt.patch = (wt.wcnt & 1) && wt.wcnt < kSeg;
+    wt.q = k;
+    mbar_wait_s(pp.full + 8 * s, (pp.pc / kStages3) & 1);
+    if (wt.wcnt > 0) {
+      double D[kEptC], A[kEptC], B[kEptC];
+      tile_load(wt, 0, p.d, D, 1.0);
+      tile_load(wt, 1, p.a, A);
+      tile_load(wt, 2, p.b, B, 1.0);
+#pragma unroll
+      for (int j = 0; j < kEptC; ++j) {
+        if (e_loc(lane, j) >= wt.wcnt) continue;
+        const double y = rcp_nr(D[j]);
+        acc[0] += mul_rn(B[j], A[j] * y);
+        acc[1] += mul_rn(B[j], B[j] * y);
+        acc[2] += 1.0;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive_s(pp.empty + 8 * s);
+    ++pp.pc;
+  }
+}
+
+// Append the elements with keep[j] of this warp's tile (values from the held
+// stage) to the warp's scratch sub-segments: slot q_out at offset off_out.
+DEVI void append_tile(const CqkParams<double>& p, const WTile& wt, const Src& src,
+                      const bool (&keep)[kEptC], int64_t& q_out, int& off_out, int64_t& out_m) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned ltm = (1u << lane) - 1u;
+  const int64_t g = gridDim.x;
+  const int64_t b0 = ((int64_t)blockIdx.x + q_out * g) * kTileC + kSeg * warp;
+  const int64_t b1 = b0 + g * kTileC;
+  double D[kEptC], A[kEptC], B[kEptC], L[kEptC], U[kEptC];
+  if (wt.wcnt == kSeg) {
+    tile_load<true>(wt, 0, src.p[0], D);
+    tile_load<true>(wt, 1, src.p[1], A);
+    tile_load<true>(wt, 2, src.p[2], B);
+    tile_load<true>(wt, 3, src.p[3], L);
+    tile_load<true>(wt, 4, src.p[4], U);
+  } else {
+    tile_load(wt, 0, src.p[0], D);
+    tile_load(wt, 1, src.p[1], A);
+    tile_load(wt, 2, src.p[2], B);
+    tile_load(wt, 3, src.p[3], L);
+    tile_load(wt, 4, src.p[4], U);
+  }
+  int r = off_out;
+#pragma unroll
+  for (int j = 0; j < kEptC; ++j) {
+    const unsigned bal = __ballot_sync(0xffffffffu, keep[j]);
+    if (keep[j]) {
+      const int o = r + __popc(bal & ltm);
+      const int64_t pos = o < kSeg ? b0 + o : b1 + (o - kSeg);
+      p.sd[pos] = D[j]; p.sa[pos] = A[j]; p.sb[pos] = B[j]; p.sl[pos] = L[j]; p.su[pos] = U[j];
+    }
+    r += __popc(bal);
+  }
+  out_m += r - off_out;
+  off_out = r;
+  if (off_out >= kSeg) { off_out -= kSeg; ++q_out; }
+}
+
+constexpr double kBracketEps = 16.0 * 2.220446049250313e-16;
+
+template <bool CHECK, bool FULL>
+DEVI void fused_tile(const CqkParams<double>& p, const WTile& wt, const Src& src, double lam_hat,
+                     double h2, double (&acc)[kMaxK], int& nlo, int& nhi, int& nside,
+                     bool (&side)[kEptC], bool& anyside_out) {
+  const int lane = threadIdx.x & 31;
+  double D[kEptC], A[kEptC], B[kEptC], L[kEptC], U[kEptC];
+  tile_load<FULL>(wt, 0, src.p[0], D, 1.0);
+  tile_load<FULL>(wt, 1, src.p[1], A);
+  tile_load<FULL>(wt, 2, src.p[2], B, 1.0);
+  tile_load<FULL>(wt, 3, src.p[3], L);
+  tile_load<FULL>(wt, 4, src.p[4], U);
+    if (CHECK) {  // all ten validate() checks; the first failing one as class * 2^40 + index
+      // the common case in predicate logic (no short-circuit branches): 0 < d, b < inf,
+      // |a| < inf, l <= u (false for NaN), l < +inf, u > -inf
+      bool bad = false;
+#pragma unroll
+      for (int j = 0; j < kEptC; ++j) {
+        const bool good = (D[j] > 0.0) & (D[j] < HUGE_VAL) & (fabs(A[j]) < HUGE_VAL) & (B[j] > 0.0) &
+                          (B[j] < HUGE_VAL) & (L[j] <= U[j]) & (L[j] < HUGE_VAL) & (U[j] > -HUGE_VAL);
+        bad |= (FULL || e_loc(lane, j) < wt.wcnt) & !good;
+      }
+      if (__any_sync(0xffffffffu, bad)) {
+#pragma unroll
+        for (int j = 0; j < kEptC; ++j) {
+          const int e = e_loc(lane, j);
+          if (e >= wt.wcnt) continue;
+          const double gi = (double)(p.offset + wt.gbase + e);
+          const double d = D[j], a = A[j], b = B[j], l = L[j], u = U[j];
+          int cls = -1;  // validate()'s order (core.py:135-165); 5 is r (host-side)
+          if (!isfinite(d)) cls = 0;
+          else if (!isfinite(a)) cls = 1;
+          else if (!isfinite(b)) cls = 2;
+          else if (isnan(l)) cls = 3;
+          else if (isnan(u)) cls = 4;
+          else if (!(d > 0.0)) cls = 6;
+          else if (!(b > 0.0)) cls = 7;
+          else if (!(l <= u)) cls = 8;
+          else if (l == HUGE_VAL) cls = 9;
+          else if (u == -HUGE_VAL) cls = 10;
+          if (cls >= 0) acc[2] = fmin(acc[2], (double)(cls > 5 ? cls - 1 : cls) * kVKey + gi);
+        }
+      }
+    }
+    // A conservative bracket of the rounded t(lambda) over I: tm = lam^ b/d
+    // + a/d (one reciprocal), widened by the interval (hw) and by 16 eps of
+    // the magnitudes involved -- far above the few-ulp error of the bracket
+    // and of t's own roundings (b*lam, + a, / d).  Misjudging an element only
+    // costs a side-list slot, so only the certain verdicts must be certain.
+    bool anyside = false;
+#pragma unroll
+    for (int j = 0; j < kEptC; ++j) {
+      const bool valid = FULL || e_loc(lane, j) < wt.wcnt;
+      const double yd = rcp_div(D[j]);
+      const double by = B[j] * yd, ay = A[j] * yd;  // b/d, a/d
+      const double qj = B[j] * by, sj = B[j] * ay;  // the lambda0 terms b^2/d, b a/d
+      const double pm = lam_hat * by;
+      const double tm = pm + ay;
+      const double w2 = h2 * by + kBracketEps * (fabs(pm) + fabs(ay));
+      const double tlo = tm - w2, thi = tm + w2;
+      const double l = L[j], u = U[j];
+      const bool rng = exp_ok(D[j]);  // the reciprocal is accurate here
+      const bool below = rng & (thi < l), above = rng & (tlo > u);
+      const bool inner = rng & (tlo > l) & (thi < u) & (tlo >= 0.0);  // interior, t >= 0
+      const double bl = mul_rn(B[j], l), bu = mul_rn(B[j], u);
+      const bool vb = valid & below, va = valid & above, vp = valid & inner;
+      acc[0] += valid ? sj : 0.0;
+      acc[1] += valid ? qj : 0.0;
+      acc[3] += vb ? bl : 0.0;
+      acc[4] += vb ? fabs(bl) : 0.0;
+      acc[6] += va ? bu : 0.0;
+      acc[7] += va ? fabs(bu) : 0.0;
+      acc[9] += vp ? qj : 0.0;
+      acc[10] += vp ? sj : 0.0;
+      nlo += vb;
+      nhi += va;
+      side[j] = valid & !below & !above & !inner;
+      nside += side[j];
+      anyside |= side[j];
+    }
+    anyside_out = anyside;
+}
+
+// The fused pass (slots: m_after_fused).  Returns this warp's side-list count.
+template <bool CHECK>
+DEVI int64_t t_fused(const CqkParams<double>& p, const Cmd& c, const TileWalk& tw,
+                     const Src src, TPipe& pp, double (&acc)[kMaxK]) {
+  // I = [lam^ - h, lam^ + h] as the host-side check sees it; h2 also covers
+  // the rounding of the interval ends
+  const double lam_hat = c.lam, h2 = c.edge + kBracketEps * fabs(c.lam);
+  int64_t out_m = 0, q_out = 0;
+  int off_out = 0;
+  int nlo = 0, nhi = 0, nside = 0;
+  consume(tw, pp, -1, [&](const WTile& wt) {
+    bool side[kEptC], anyside;
+    if (wt.wcnt == kSeg) fused_tile<CHECK, true>(p, wt, src, lam_hat, h2, acc, nlo, nhi, nside, side, anyside);
+    else fused_tile<CHECK, false>(p, wt, src, lam_hat, h2, acc, nlo, nhi, nside, side, anyside);
+    if (__any_sync(0xffffffffu, anyside)) append_tile(p, wt, src, side, q_out, off_out, out_m);
+  });
+  acc[5] += (double)nlo;
+  acc[8] += (double)nhi;
+  acc[13] += (double)nside;
+  fence_proxy_async_global();  // generic stores -> the side scan's bulk loads
+  return out_m;
+}
+
 // ------------------------------------------------------------ the kernel
 template <bool FIX>
 __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<double> p) {
@@ -731,6 +957,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
   const int has_xbar = p.xbar != nullptr;
   const int check = p.init.check;  // immutable during the solve
   bool in_scratch = false;
+  bool side_pending = false;  // the fused pass left a side list in scratch
   int64_t m_w = -1;  // this warp's scratch element count (consumers, once in scratch)
   // The producer lane issues the first tiles of the most likely next pass (a
   // phi scan / breakpoint pass over the current working set -- or, before
@@ -748,11 +975,22 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
   double* const dtrace = master ? p.trace : nullptr;
   for (unsigned epoch = 1;; ++epoch) {
     const Cmd c = s_cmd;
-    const int spec = s_spec;
+    int spec = s_spec;
     if (probe && threadIdx.x == 0) tl_mark(p.sync, epoch, 10);
     if (c.phase == PH_DONE || s_abort) {
       if (!producer) drain(pp, spec);  // never leave bulk copies in flight
       break;
+    }
+    if (side_pending && c.phase != PH_FUSED) {
+      // after the fused pass the producer speculated the side list; a full
+      // first scan (lambda0 outside the interval) or a stop drops it
+      side_pending = false;
+      if (!(c.phase == PH_SCAN && c.side)) {
+        if (!producer && spec > 0) drain(pp, spec);
+        spec = 0;
+        in_scratch = false;
+        m_w = -1;
+      }
     }
     const TileWalk work{p.n, ntiles, in_scratch ? s_nslots : -1};
     const Src wsrc = in_scratch ? src_scr : src_orig;
@@ -819,6 +1057,63 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
           }
         }
       }
+    } else if (c.phase == PH_SAMPLE) {
+      if (prod_lane) produce_sample(src_l0x, p.n, ntiles, pp3);
+      else if (!producer) t_sample(p, ntiles, pp3, acc);
+      const int ops[3] = {OP_SUM, OP_SUM, OP_SUM};
+      double a3[3] = {acc[0], acc[1], acc[2]};
+      block_reduce<3, kConsW>(a3, ops, s_red, s_tot);
+      is_master = grid_step_any<3>(p.ar, p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch,
+                                   [&] { if (prod_lane) speculate(); }, (c_tma_flags & 4) != 0);
+      if (is_master && warp == 0) {
+        if (lane == 0) tl_record(dsync, epoch, PH_SAMPLE, p.n, 0);
+        double glob[3];
+        const bool ok = exchange_totals<3>(p.ex, epoch, ops, s_tot, glob, master);
+        if (lane == 0) {
+          if (ok) m_after_sample(s_st, glob, s_tot[2]);
+          else {
+            m_stop(s_st, ST_TIMEOUT);
+            raise_timeout(p.sync);
+          }
+        }
+      }
+    } else if (c.phase == PH_FUSED) {
+      acc[2] = HUGE_VAL;  // the first failing validate() check (min)
+      if (prod_lane) produce<5>(src_orig, orig, pp, spec);
+      else if (!producer) {
+        const int64_t mm = check ? t_fused<true>(p, c, orig, src_orig, pp, acc)
+                                 : t_fused<false>(p, c, orig, src_orig, pp, acc);
+        m_w = mm;
+        if (lane == 0) atomicMax(&s_nsl_new, (int)((mm + kSeg - 1) / kSeg));
+      }
+      in_scratch = true;  // speculate the side list: the likely next walk
+      side_pending = true;
+      int ops[kFusedK];
+      double aK[kFusedK];
+#pragma unroll
+      for (int k = 0; k < kFusedK; ++k) { ops[k] = k == 2 ? OP_MIN : OP_SUM; aK[k] = acc[k]; }
+      block_reduce<kFusedK, kConsW>(aK, ops, s_red, s_tot);
+      is_master = grid_step_any<kFusedK>(p.ar, p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch, [&] {
+        if (prod_lane) {
+          s_nslots = s_nsl_new;
+          s_nsl_new = 0;
+          speculate();
+        }
+      }, (c_tma_flags & 4) != 0);
+      if (is_master && warp == 0) {
+        double loc[kFusedK], glob[kFusedK];
+#pragma unroll
+        for (int k = 0; k < kFusedK; ++k) loc[k] = s_tot[k];
+        if (lane == 0) tl_record(dsync, epoch, PH_FUSED, p.n, 0);
+        const bool ok = exchange_totals<kFusedK>(p.ex, epoch, ops, loc, glob, master);
+        if (lane == 0) {
+          if (ok) m_after_fused(s_st, glob, loc);
+          else {
+            m_stop(s_st, ST_TIMEOUT);
+            raise_timeout(p.sync);
+          }
+        }
+      }
     } else if (c.phase == PH_SCAN && c.check_lu) {
 #pragma unroll
       for (int k = kCheckLuSlot; k < kMaxK; ++k) acc[k] = HUGE_VAL;
@@ -865,6 +1160,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
         }
       }
       if (compact) in_scratch = true;
+      if (c.side) {  // the side list is consumed; the working set is the original arrays
+        in_scratch = false;
+        m_w = -1;
+      }
       constexpr int K = FIX ? 11 : 5;
       int ops[K];
       double aK[K];
@@ -897,6 +1196,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
         if (lane == 0) tl_record(dsync, epoch, PH_SCAN, s_st.phys_count, s_st.cmd.compact);
         const bool ok = exchange_totals<K>(p.ex, epoch, ops, s_tot, glob, master);
         if (lane == 0) {
+          if (ok && c.side) m_add_aggregates(s_st, glob, loc);
           if (ok) m_after_scan(s_st, glob, loc, dtrace);
           else {
             m_stop(s_st, ST_TIMEOUT);

@@ -18,6 +18,9 @@ d, a, b, l, u, r = P.instances.gen_cqk_arrays("cqk-uncorrelated", n, 7)
 if prior:
     print("single", P.solve_cqk(P.CqkInstance(d=d, a=a, b=b, l=l, u=u, r=r)).lam)
 comms = D.local_group([0, 0], grid_limit=grid)
+fused_min = int(float(os.environ.get("DIAG_FUSED_MIN", "1e18")))
+for c in comms:
+    c.handle.set_fused(fused_min, 2e-3)
 solvers = []
 for q in range(2):
     lo, hi = D.shard_bounds(n, 2, q)
@@ -41,5 +44,5 @@ th = [threading.Thread(target=work, args=(q,)) for q in range(2)]
 [t.join() for t in th]
 print("grid", grid, "n", n, "prior", prior, res)
 for q in range(2):
-    tl = solvers[q].handle.timeline(8)
-    print("rank", q, "start", tl[0, 3], [tuple(int(v) for v in row) for row in tl[1:4]])
+    tl = solvers[q].handle.timeline(12)
+    print("rank", q, "start", tl[0, 3], [tuple(int(v) for v in row[:4]) for row in tl[1:10]])

@@ -38,7 +38,8 @@ def cqk(fam, n, jac=False, ratio=None):
     st = out.stats
     return {"ms": ms, "kernel_ms": st["device_ms"], "GBps": st["bytes_model"] / st["device_ms"] / 1e6,
             "frac": st["bytes_model"] / st["device_ms"] / 1e6 / PEAK, "evals": out.phi_evals,
-            "elem_per_s": n / ms * 1e3, "bytes_per_elem": st["bytes_model"] / n}
+            "elem_per_s": n / ms * 1e3, "bytes_per_elem": st["bytes_model"] / n,
+            "lam": out.lam, "iterations": out.iterations, "fixed": out.fixed_count}
 
 
 res = {}
@@ -53,6 +54,10 @@ for w in which:
         res[w] = cqk("cqk-correlated", 10**8)
     elif w == "unc7":
         res[w] = cqk("cqk-uncorrelated", 10**7)
+    elif w == "weak7":
+        res[w] = cqk("cqk-weakly-correlated", 10**7)
+    elif w == "unc8":
+        res[w] = cqk("cqk-uncorrelated", 10**8)
     elif w == "jac":
         res[w] = cqk("cqk-weakly-correlated", 10**8, jac=True)
     elif w.split("_")[0] in ("spx", "l1") and not w.startswith("spx1e6"):
