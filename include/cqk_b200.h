@@ -147,6 +147,22 @@ int cqk_solve_f64(cqk_handle *h, int mem, const double *d, const double *a,
                   double r, const cqk_options *opts, const double *xbar, double *x,
                   cqk_result *res);
 
+/* float32 instances (core.py:55-64 keeps float32 arrays float32): the element
+   math in float -- t = (b * float(lam) + a) / d, x = clip(t, l, u), b x
+   (core.py:195-200) -- with fp64 accumulation of the sums, on the
+   warp-segment kernel; the fp32 tau eps32^(3/4) unless opts set one
+   (newton.py:64-67).  Same contract as cqk_solve_f64 otherwise. */
+int cqk_solve_f32(cqk_handle *h, int mem, const float *d, const float *a, const float *b,
+                  const float *l, const float *u, int64_t n, double r, const cqk_options *opts,
+                  const float *xbar, float *x, cqk_result *res);
+/* float32 simplex / l1: v = y + float(lam) in float (simplex.py:207-215), x =
+   max(0, y + float(lam)) in float (simplex.py:303, 333); the formula / tight
+   starts (simplex_start 2 = alg2 runs as tight). */
+int spx_project_f32(cqk_handle *h, int mem, const float *y, int64_t n, double r,
+                    const cqk_options *opts, float *x, cqk_result *res);
+int l1_project_f32(cqk_handle *h, int mem, const float *y, int64_t n, double r,
+                   const cqk_options *opts, float *x, cqk_result *res);
+
 /* Simplex / l1 ---------------------------------------------------------------- */
 /* newton_project_simplex(y, r, opts, lambda0)  simplex.py:218-308.  The device
    initializer is lambda0 = min((r - sum y)/n, r - max y) (opts->simplex_start
@@ -233,6 +249,21 @@ int cqk_set_engine(cqk_handle *h, int mode);
    half_width (default 2e-3).  Results agree with the unfused solve to
    rounding (lambda0's terms share the division's reciprocal). */
 int cqk_set_fused(cqk_handle *h, int64_t min_n, double half_width);
+/* Direction guess of the fused start (fixing solves, default 1 = auto,
+   CQK_FUSED_GUESS): a second sample pass estimates the sign of
+   phi(lambda0) - r, i.e. which bound the first Newton iteration fixes
+   (newton.py:165-206); the fused pass then also writes every element that
+   fixing would not drop, and when the side scan confirms the direction those
+   survivors become the working set (the first full re-read is avoided).
+   0 off, 2 / 3 force +1 / -1 (tests: a wrong guess is simply not adopted).
+   Results agree with mode 0 to rounding (summation order differs). */
+int cqk_set_fused_guess(cqk_handle *h, int mode);
+/* A/B switches of the persistent kernels (defaults 0 = the measured best;
+   the environment variables of the same names set them at cqk_create):
+   bit 0 CQK_MASTER_STEP (master + release grid step instead of masterless),
+   bit 1 CQK_STATIC_FINAL (static final-pass tiles), bit 2 CQK_TAIL=0 (no
+   single-CTA simplex tail).  Results are bit-identical either way. */
+int cqk_set_switches(cqk_handle *h, int flags);
 int cqk_set_grid_limit(cqk_handle *h, int max_ctas);
 /* Sharded solve_cqk / jacobi_solve / par_solve_cqk: this rank's shard
    [offset, offset + n_local) of an n_total-element instance.  All ranks call
@@ -250,6 +281,30 @@ int spx_project_sharded_f64(cqk_handle *h, int mem, const double *y, int64_t n_l
 int l1_project_sharded_f64(cqk_handle *h, int mem, const double *y, int64_t n_local,
                            int64_t n_total, double r, const cqk_options *opts, double *x,
                            cqk_result *res);
+
+/* Device groups: one process, several GPUs ------------------------------------
+   The GPU analogue of the reference's worker pool (workers= / CQK_WORKERS,
+   parallel.py:52-59): a group holds one handle and rank per listed device
+   (mailboxes connected, peer access enabled; a device listed k times hosts k
+   ranks on 1/k of its SMs), and its solves take HOST arrays, cut n into
+   contiguous shards (_chunk_ranges, parallel.py:82-85) and run every rank's
+   sharded solve concurrently, one host thread per rank (each rank stages its
+   own shard over its own PCIe link).  The outcome is that of the sharded
+   entry points; counters are summed over ranks, device_ms is the slowest
+   rank.  Python: CQK_DEVICES="0,1,..." routes host-array solve_cqk /
+   jacobi_solve / par_solve_cqk / newton_project_simplex / project_l1 calls
+   here. */
+typedef struct cqk_group cqk_group;
+int cqk_group_create(cqk_group **out, const int *devices, int ndev);
+int cqk_group_destroy(cqk_group *g);
+int cqk_group_size(const cqk_group *g);
+int cqk_solve_group_f64(cqk_group *g, const double *d, const double *a, const double *b,
+                        const double *l, const double *u, int64_t n, double r,
+                        const cqk_options *opts, const double *xbar, double *x, cqk_result *res);
+int spx_project_group_f64(cqk_group *g, const double *y, int64_t n, double r,
+                          const cqk_options *opts, double *x, cqk_result *res);
+int l1_project_group_f64(cqk_group *g, const double *y, int64_t n, double r,
+                         const cqk_options *opts, double *x, cqk_result *res);
 
 /* On-device instances --------------------------------------
    gen_cqk(family, n, seed) (instances.py:43-70) straight into device arrays,

@@ -87,10 +87,12 @@ EXPORTS = (
     "spx_project_f64", "l1_project_f64", "spx_project_warm_f64", "l1_project_warm_f64",
     "spx_project_batched_f64", "cqk_selftest_division",
     "cqk_comm_ipc_handle_size", "cqk_comm_create", "cqk_comm_connect", "cqk_comm_connect_local",
-    "cqk_set_grid_limit", "cqk_set_engine", "cqk_set_fused", "cqk_reserve", "cqk_reserve_host", "cqk_solve_sharded_f64", "spx_project_sharded_f64",
+    "cqk_set_grid_limit", "cqk_set_engine", "cqk_set_fused", "cqk_set_fused_guess", "cqk_set_switches", "cqk_reserve", "cqk_reserve_host", "cqk_solve_sharded_f64", "spx_project_sharded_f64",
     "l1_project_sharded_f64", "spx_init_alg2_f64", "cqk_gen_cqk_device",
     "cqk_gen_cqk_device_range", "cqk_gen_simplex_u01_device", "spx_project_batched_multi_f64",
-    "cqk_read_peak_f64",
+    "cqk_read_peak_f64", "cqk_group_create", "cqk_group_destroy", "cqk_group_size",
+    "cqk_solve_group_f64", "spx_project_group_f64", "l1_project_group_f64",
+    "cqk_solve_f32", "spx_project_f32", "l1_project_f32",
 )
 
 _lib = None
@@ -140,6 +142,8 @@ def _declare(L):
     L.cqk_set_grid_limit.argtypes = [_P, ctypes.c_int]
     L.cqk_set_engine.argtypes = [_P, ctypes.c_int]
     L.cqk_set_fused.argtypes = [_P, _I64, _D]
+    L.cqk_set_fused_guess.argtypes = [_P, ctypes.c_int]
+    L.cqk_set_switches.argtypes = [_P, ctypes.c_int]
     L.cqk_reserve_host.argtypes = [_P, _I64]
     L.cqk_reserve.argtypes = [_P, _I64]
     L.cqk_solve_sharded_f64.argtypes = [_P, ctypes.c_int, *arr5, _I64, _I64, _I64, _D, _OPT, _P,
@@ -159,6 +163,15 @@ def _declare(L):
                                           _P, _RES]
     L.spx_project_batched_multi_f64.argtypes = [_P, ctypes.c_int, _P, _I64, _I64, _D, _OPT, _P,
                                                 _P, _P, _RES]
+    L.cqk_solve_f32.argtypes = [_P, ctypes.c_int, *arr5, _I64, _D, _OPT, _P, _P, _RES]
+    L.spx_project_f32.argtypes = [_P, ctypes.c_int, _P, _I64, _D, _OPT, _P, _RES]
+    L.l1_project_f32.argtypes = [_P, ctypes.c_int, _P, _I64, _D, _OPT, _P, _RES]
+    L.cqk_group_create.argtypes = [ctypes.POINTER(_P), _P, ctypes.c_int]
+    L.cqk_group_destroy.argtypes = [_P]
+    L.cqk_group_size.argtypes = [_P]
+    L.cqk_solve_group_f64.argtypes = [_P, *arr5, _I64, _D, _OPT, _P, _P, _RES]
+    L.spx_project_group_f64.argtypes = [_P, _P, _I64, _D, _OPT, _P, _RES]
+    L.l1_project_group_f64.argtypes = [_P, _P, _I64, _D, _OPT, _P, _RES]
     L.cqk_read_peak_f64.argtypes = [_P, _P, ctypes.c_int, _I64, ctypes.c_int, ctypes.POINTER(_D),
                                     ctypes.POINTER(_D)]
 
@@ -227,9 +240,18 @@ class Handle:
         self.lib.cqk_set_stream(self.ptr, _P(stream_ptr if stream_ptr else 1))
         self._stream = stream_ptr
 
-    def set_fused(self, min_n=4_000_000, half_width=2e-3):
-        """Fused start of the CQK solve from `min_n` elements per rank (cqk_b200.h)."""
+    def set_fused(self, min_n=4_000_000, half_width=2e-3, guess=1):
+        """Fused start of the CQK solve from `min_n` elements per rank, with
+        the direction guess mode `guess` (cqk_b200.h)."""
         if self.lib.cqk_set_fused(self.ptr, int(min_n), float(half_width)) != 0:
+            raise NativeError(last_error())
+        if self.lib.cqk_set_fused_guess(self.ptr, int(guess)) != 0:
+            raise NativeError(last_error())
+
+    def set_switches(self, master_step=False, static_final=False, tail=True):
+        """A/B switches of the persistent kernels (cqk_set_switches)."""
+        flags = (1 if master_step else 0) | (2 if static_final else 0) | (0 if tail else 4)
+        if self.lib.cqk_set_switches(self.ptr, flags) != 0:
             raise NativeError(last_error())
 
     def use_current_stream(self):
@@ -314,6 +336,62 @@ def handle_set(devices):
     if hs is None:
         hs = cache[key] = [Handle(d) for d in devices]
     return hs
+
+
+class Group:
+    """A same-process device group (cqk_group, include/cqk_b200.h): one rank
+    per listed device, solves over host arrays sharded across them."""
+
+    def __init__(self, devices):
+        import torch
+
+        if not torch.cuda.is_available():
+            raise NativeUnavailable("no CUDA device visible (the solver has no CPU fallback)")
+        self.lib = load_library()
+        self.devices = tuple(int(d) for d in devices)
+        arr = (ctypes.c_int * len(self.devices))(*self.devices)
+        g = _P()
+        rc = self.lib.cqk_group_create(ctypes.byref(g), arr, len(self.devices))
+        if rc != 0:
+            raise NativeError(f"cqk_group_create failed ({rc}): {last_error()}")
+        self.ptr = g
+        self.lock = threading.Lock()  # a group is not re-entrant
+
+    def __del__(self):
+        try:
+            if getattr(self, "ptr", None):
+                self.lib.cqk_group_destroy(self.ptr)
+        except Exception:
+            pass
+
+
+_groups = {}
+_glock = threading.Lock()
+
+
+def parse_devices(spec):
+    """CQK_DEVICES syntax: comma-separated CUDA ordinals ("0,1,2,3"; a device
+    may repeat to host several ranks)."""
+    out = [int(t) for t in str(spec).replace(" ", "").split(",") if t != ""]
+    if any(d < 0 for d in out):
+        raise ValueError(f"bad device list {spec!r}")
+    return out
+
+
+def env_group():
+    """The process-wide group of CQK_DEVICES when it lists >= 2 entries, else
+    None (the GPU analogue of CQK_WORKERS, parallel.py:52-59)."""
+    spec = os.environ.get("CQK_DEVICES")
+    if not spec:
+        return None
+    devs = tuple(parse_devices(spec))
+    if len(devs) < 2:
+        return None
+    with _glock:
+        g = _groups.get(devs)
+        if g is None:
+            g = _groups[devs] = Group(devs)
+    return g
 
 
 _OPTS_CACHE = {}

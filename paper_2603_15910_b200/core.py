@@ -157,14 +157,16 @@ class Breakpoints:
 # ------------------------------------------------------------- marshalling
 class Marshal:
     """Pointers for the C-ABI: numpy -> host mode (fp64 staging), CUDA torch
-    tensors -> device mode (zero-copy).  fp32 instances are solved in fp64
-    arithmetic and cast back (the reference computes in fp32); tolerances use
-    the instance dtype."""
+    tensors -> device mode (zero-copy).  float64 by default; f32=True keeps
+    float32 instances float32 for the *_f32 entry points (the reference
+    computes float32 instances in float32, core.py:55-64, 195-200)."""
 
-    def __init__(self, *arrays):
+    def __init__(self, *arrays, f32=False):
+        """f32: keep float32 arrays float32 (the *_f32 entry points)."""
         self.torch = any(_is_torch(a) for a in arrays if a is not None)
         self.keep = []
         self.ptrs = []
+        self.f32 = f32
         if self.torch:
             import torch
 
@@ -175,7 +177,8 @@ class Marshal:
                     continue
                 if not _is_torch(a) or not a.is_cuda:
                     raise ValueError("mixing CUDA tensors with host arrays is not supported")
-                t = a if a.dtype == torch.float64 and a.is_contiguous() else a.to(torch.float64).contiguous()
+                want = torch.float32 if f32 else torch.float64
+                t = a if a.dtype == want and a.is_contiguous() else a.to(want).contiguous()
                 dev = t.device if dev is None else dev
                 self.keep.append(t)
                 self.ptrs.append(t.data_ptr())
@@ -186,7 +189,7 @@ class Marshal:
                 if a is None:
                     self.ptrs.append(None)
                     continue
-                v = np.ascontiguousarray(a, dtype=np.float64)
+                v = np.ascontiguousarray(a, dtype=np.float32 if f32 else np.float64)
                 self.keep.append(v)
                 self.ptrs.append(v.ctypes.data)
             self.device = None
@@ -204,12 +207,13 @@ class Marshal:
     def empty(self, n):
         import torch
 
+        tdt = torch.float32 if self.f32 else torch.float64
         if self.torch:
-            t = torch.empty(n, dtype=torch.float64, device=f"cuda:{self.device}")
+            t = torch.empty(n, dtype=tdt, device=f"cuda:{self.device}")
             return t, t.data_ptr()
         # host results land in page-locked memory (torch's caching host
         # allocator), so the device-to-host copy of x runs at full DMA rate
-        v = torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
+        v = torch.empty(n, dtype=tdt, pin_memory=True).numpy()
         return v, v.ctypes.data
 
     def index(self, idx, n):

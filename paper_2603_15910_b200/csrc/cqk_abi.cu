@@ -16,6 +16,7 @@
 #include <mutex>
 #include <string>
 #include <thread>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/cqk_b200.h"
@@ -86,11 +87,14 @@ struct cqk_handle {
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
   int grid_cqk_fix = 0, grid_cqk_jac = 0, grid_spx = 0, grid_l1 = 0;
+  int grid_cqk_fix32 = 0, grid_cqk_jac32 = 0, grid_spx32 = 0, grid_l1_32 = 0;  // float instances
   int grid_tma_fix = 0, grid_tma_jac = 0;  // TMA-pipelined CQK kernels (0: unavailable)
   int grid_tma_spx = 0, grid_tma_l1 = 0;    // TMA-pipelined simplex / l1 kernels
   bool use_tma = true;                     // CQK_ENGINE=seg selects the warp-segment kernel
   int engine = 0;                          // cqk_set_engine: 0 auto, 1 TMA, 2 warp segments
   int64_t tma_min_n = 65536;               // auto: CQK solves of >= this many elements per rank
+  int fused_guess = 1;                     // fused start: direction guess + survivor list (CQK_FUSED_GUESS)
+  static constexpr int64_t kGuessMinN = 8000000;  // ... from this many elements per rank
   int64_t fused_min_n = 4000000;           // fused start (sample + fused first pass) from this size
   double fused_width = 2e-3;               // ... its classification interval, relative half-width
   unsigned* sync = nullptr;  // [0] arrive, [1] gen, [2] error
@@ -121,6 +125,11 @@ struct cqk_handle {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int trace_len = 0;
   int grid_limit = 0;                 // 0: full device (virtual ranks share a GPU)
+  // A/B switches, read once at cqk_create (environment)
+  bool master_step = false;           // CQK_MASTER_STEP: master + release grid step
+  bool static_final = false;          // CQK_STATIC_FINAL: static final-pass tiles
+  bool tail_mode = true;              // CQK_TAIL=0: no single-CTA simplex tail
+  int64_t alg2_chunk = 256;           // CQK_ALG2_CHUNK: device Algorithm-2 chunk length
   void* host_state = nullptr;         // pinned + mapped: the kernels' final state (and Alg2Out)
   void* host_state_dev = nullptr;     // ... its device alias
   volatile int* host_err = nullptr;   // mapped word after the state: any CTA's spin timeout
@@ -164,6 +173,10 @@ int cqk_create(cqk_handle** out, int device) {
   h->grid_cqk_jac = occ((const void*)cqk_solve_kernel<double, false>);
   h->grid_spx = occ((const void*)spx_solve_kernel<double, false>);
   h->grid_l1 = occ((const void*)spx_solve_kernel<double, true>);
+  h->grid_cqk_fix32 = occ((const void*)cqk_solve_kernel<float, true>);
+  h->grid_cqk_jac32 = occ((const void*)cqk_solve_kernel<float, false>);
+  h->grid_spx32 = occ((const void*)spx_solve_kernel<float, false>);
+  h->grid_l1_32 = occ((const void*)spx_solve_kernel<float, true>);
   {
     auto occ_tma = [&](const void* fn) {
       if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemC) !=
@@ -186,6 +199,8 @@ int cqk_create(cqk_handle** out, int device) {
   gmax = gmax > h->grid_cqk_jac ? gmax : h->grid_cqk_jac;
   gmax = gmax > h->grid_spx ? gmax : h->grid_spx;
   gmax = gmax > h->grid_l1 ? gmax : h->grid_l1;
+  for (int g32 : {h->grid_cqk_fix32, h->grid_cqk_jac32, h->grid_spx32, h->grid_l1_32})
+    gmax = gmax > g32 ? gmax : g32;
   if (gmax == 0) {
     delete h;
     return set_err(CQK_E_CUDA, "persistent kernels do not fit on an SM");
@@ -228,6 +243,15 @@ int cqk_create(cqk_handle** out, int device) {
   if (const char* gl = getenv("CQK_GRID_LIMIT")) h->grid_limit = atoi(gl);  // shared-GPU runs
   if (const char* mn = getenv("CQK_TMA_MIN_N")) h->tma_min_n = atoll(mn);
   if (const char* fm = getenv("CQK_FUSED_MIN_N")) h->fused_min_n = atoll(fm);
+  if (const char* fg = getenv("CQK_FUSED_GUESS")) h->fused_guess = atoi(fg);
+  auto flag = [](const char* name) {
+    const char* e = getenv(name);
+    return e && e[0] && e[0] != '0';
+  };
+  h->master_step = flag("CQK_MASTER_STEP");
+  h->static_final = flag("CQK_STATIC_FINAL");
+  if (const char* te = getenv("CQK_TAIL")) h->tail_mode = te[0] != '0';
+  if (const char* e = getenv("CQK_ALG2_CHUNK")) h->alg2_chunk = atoll(e) > 0 ? atoll(e) : 256;
   *out = h;
   return 0;
 }
@@ -433,12 +457,16 @@ int stage_inputs(cqk_handle* h, int mem, int64_t n, const T* const* in, int coun
 // families (n = 1e8): with the TMA engine 0.5 streams 2-5% fewer bytes and is
 // fastest (weak 3.99 -> 3.88 ms, corr 4.26 -> 3.88 ms); the warp-segment
 // engine (small n) keeps 0.25.
-double default_compact_ratio(bool tma = false) {
+// After a fused start with the direction guess the working set is already
+// the guessed survivors, and 0.4 compacts them once more (tools/policy_ab.py,
+// 36 instances 5e6..1e8: 0.4 the best mean, 0.5 leaves C3 weak seed 1
+// uncompacted at 3.36 ms against 3.23).
+double default_compact_ratio(bool tma = false, bool guessed = false) {
   static double v = [] {
     const char* e = getenv("CQK_COMPACT_RATIO");
     return e ? atof(e) : -1.0;
   }();
-  return v >= 0 ? v : (tma ? 0.5 : 0.25);
+  return v >= 0 ? v : (tma ? (guessed ? 0.4 : 0.5) : 0.25);
 }
 
 bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
@@ -466,23 +494,18 @@ int check_timeout(cqk_handle* h, int32_t status, int32_t err) {
   return set_err(CQK_E_TIMEOUT, "persistent kernel barrier timed out");
 }
 
-bool getenv_flag(const char* name) {
-  const char* e = getenv(name);
-  return e && e[0] && e[0] != '0';
-}
-
 // The masterless grid step for a single-GPU persistent TMA launch of `grid`
 // CTAs (one CTA per SM; the buffers hold sm_count + 8 rows).
 GridAR masterless(cqk_handle* h, int grid, const Exchange& ex) {
   GridAR ar{nullptr, nullptr, nullptr, nullptr, nullptr, 0};
-  if (grid > h->sm_count + 8 || getenv_flag("CQK_MASTER_STEP")) return ar;
+  if (grid > h->sm_count + 8 || h->master_step) return ar;
   const int k = (int)(h->ar_seq++ & 1u);
   ar.rows = h->ar_rows;
   ar.count = h->ar_count + k;
   ar.count_next = h->ar_count + (k ^ 1);
   ar.tiles = h->ar_count + 2 + k;
   ar.tiles_next = h->ar_count + 2 + (k ^ 1);
-  ar.dyn_final = !getenv_flag("CQK_STATIC_FINAL");
+  ar.dyn_final = !h->static_final;
   return ar;
 }
 
@@ -537,7 +560,7 @@ extern "C" int cqk_reserve(cqk_handle* h, int64_t n) {
   if (!h || n < 0) return set_err(CQK_E_ARG, "bad reserve");
   CUDA_TRY(cudaSetDevice(h->device));
   const size_t per = ((size_t)tma_scratch_elems(n) * sizeof(double) + 255) / 256 * 256;
-  CUDA_TRY(h->scratch.ensure(per * 5));
+  CUDA_TRY(h->scratch.ensure(per * 10));  // compaction + side-list scratch (fused start)
   CUDA_TRY(cudaDeviceSynchronize());
   return 0;
 }
@@ -562,6 +585,20 @@ extern "C" int cqk_set_fused(cqk_handle* h, int64_t min_n, double half_width) {
   if (!h || !(half_width >= 0.0)) return set_err(CQK_E_ARG, "fused start: half_width >= 0");
   h->fused_min_n = min_n;
   h->fused_width = half_width;
+  return 0;
+}
+
+extern "C" int cqk_set_fused_guess(cqk_handle* h, int mode) {
+  if (!h || mode < 0 || mode > 3) return set_err(CQK_E_ARG, "fused guess: mode 0..3");
+  h->fused_guess = mode;
+  return 0;
+}
+
+extern "C" int cqk_set_switches(cqk_handle* h, int flags) {
+  if (!h) return set_err(CQK_E_ARG, "null handle");
+  h->master_step = (flags & 1) != 0;
+  h->static_final = (flags & 2) != 0;
+  h->tail_mode = (flags & 4) == 0;
   return 0;
 }
 
@@ -635,10 +672,11 @@ extern "C" int cqk_comm_connect_local(cqk_handle* h, cqk_handle* const* ranks, i
 }
 
 // ------------------------------------------------------------ CQK solve
-static int solve_impl(cqk_handle* h, int mem, const double* d, const double* a, const double* b,
-                      const double* l, const double* u, int64_t n, int64_t offset,
-                      int64_t n_total, double r, const cqk_options* opts_in, const double* xbar,
-                      double* x, cqk_result* res, bool sharded);
+template <typename T>
+static int solve_impl(cqk_handle* h, int mem, const T* d, const T* a, const T* b, const T* l,
+                      const T* u, int64_t n, int64_t offset, int64_t n_total, double r,
+                      const cqk_options* opts_in, const T* xbar, T* x, cqk_result* res,
+                      bool sharded);
 
 extern "C" int cqk_solve_f64(cqk_handle* h, int mem, const double* d, const double* a,
                              const double* b, const double* l, const double* u, int64_t n,
@@ -656,10 +694,23 @@ extern "C" int cqk_solve_sharded_f64(cqk_handle* h, int mem, const double* d, co
   return solve_impl(h, mem, d, a, b, l, u, n_local, offset, n_total, r, opts, xbar, x, res, true);
 }
 
-static int solve_impl(cqk_handle* h, int mem, const double* d, const double* a, const double* b,
-                      const double* l, const double* u, int64_t n, int64_t offset,
-                      int64_t n_total, double r, const cqk_options* opts_in, const double* xbar,
-                      double* x, cqk_result* res, bool sharded) {
+extern "C" int cqk_solve_f32(cqk_handle* h, int mem, const float* d, const float* a,
+                             const float* b, const float* l, const float* u, int64_t n, double r,
+                             const cqk_options* opts_in, const float* xbar, float* x,
+                             cqk_result* res) {
+  return solve_impl<float>(h, mem, d, a, b, l, u, n, 0, n, r, opts_in, xbar, x, res, false);
+}
+
+// T = double: the TMA engine (n >= tma_min_n) or the warp-segment kernel;
+// T = float: the warp-segment kernel with the element math in float (the
+// reference computes t, x, b x of a float32 instance in float32, core.py:195-200)
+// and fp64 accumulation.
+template <typename T>
+static int solve_impl(cqk_handle* h, int mem, const T* d, const T* a, const T* b, const T* l,
+                      const T* u, int64_t n, int64_t offset, int64_t n_total, double r,
+                      const cqk_options* opts_in, const T* xbar, T* x, cqk_result* res,
+                      bool sharded) {
+  constexpr bool F64 = std::is_same<T, double>::value;
   if (!h || !d || !a || !b || !l || !u || !res) return set_err(CQK_E_ARG, "null argument");
   std::memset(res, 0, sizeof *res);
   res->domain_index = -1;
@@ -676,12 +727,12 @@ static int solve_impl(cqk_handle* h, int mem, const double* d, const double* a, 
   }
   const bool jacobi = opts.variant == CQK_VARIANT_JACOBI;
   const bool fixing = !jacobi && opts.variable_fixing;
-  const double* dv[6];
-  double* xo = x;
-  double* xdev = nullptr;
+  const T* dv[6];
+  T* xo = x;
+  T* xdev = nullptr;
   {
-    const double* in[6] = {d, a, b, l, u, xbar};
-    int rc = stage_inputs<double>(h, mem, n, in, 6, dv, (mem == CQK_MEM_HOST && x) ? 1 : 0, &xdev);
+    const T* in[6] = {d, a, b, l, u, xbar};
+    int rc = stage_inputs<T>(h, mem, n, in, 6, dv, (mem == CQK_MEM_HOST && x) ? 1 : 0, &xdev);
     if (rc) return rc;
     if (mem == CQK_MEM_HOST) xo = x ? xdev : nullptr;
   }
@@ -701,7 +752,7 @@ static int solve_impl(cqk_handle* h, int mem, const double* d, const double* a, 
   s.hi = INFINITY;
   s.r_res = r;
   s.r_orig = r;
-  s.tau = tau_of(&opts, false);
+  s.tau = tau_of(&opts, !F64);
   s.lam0 = s.cmd.lam;
   s.fhi_phys = INFINITY;  // the original arrays: nothing removed yet
   s.flo_phys = -INFINITY;
@@ -721,35 +772,44 @@ static int solve_impl(cqk_handle* h, int mem, const double* d, const double* a, 
   // (tools/crossover.py: 70 vs 72 us at 5e4 ... 0.65 vs 0.82 ms at 1.6e7);
   // below 64Ki elements the two tie, and the warp-segment kernel's summation
   // order reproduces the reference's iterate counts on tiny inputs more often
-  const bool tma = h->use_tma && (h->engine == 1 || (h->engine == 0 && n >= h->tma_min_n));
-  s.compact_ratio = std::isnan(opts.compact_ratio) ? default_compact_ratio(tma) : opts.compact_ratio;
+  const bool tma = F64 && h->use_tma && (h->engine == 1 || (h->engine == 0 && n >= h->tma_min_n));
   // fused start (cqk_tma.cuh): lambda0 and the first scan share one pass
   // (a per-rank size every rank derives alike: the phases must match across ranks)
   const int64_t per_rank = sharded ? n_total / std::max(h->world, 1) : n;
   const bool fused = tma && !lam0_given && !xbar && per_rank >= h->fused_min_n;
+  // the direction guess's extra sample epoch (~12 us) pays from ~1e7 elements
+  // per rank (tools/policy_ab.py: 1e7 -1.7% mean, 1e8 -4.2%; 5e6 +1.5%);
+  // the forced modes (tests) apply at any size
+  const int guess = !(fused && fixing) ? 0
+                    : (h->fused_guess >= 2 || per_rank >= cqk_handle::kGuessMinN) ? h->fused_guess : 0;
+  s.compact_ratio = std::isnan(opts.compact_ratio) ? default_compact_ratio(tma, guess != 0)
+                                                   : opts.compact_ratio;
   if (fused) {
     s.fused = 1;
+    s.fused_guess = guess;
     s.fused_width = h->fused_width;
     s.cmd.phase = PH_SAMPLE;
   }
   // scratch: n per array (warp segments) or whole tile slots (TMA engine)
-  const size_t per = ((size_t)(tma ? tma_scratch_elems(n) : n) * sizeof(double) + 255) / 256 * 256;
-  if (fixing || fused) CUDA_TRY(h->scratch.ensure(per * 5));
+  const size_t per = ((size_t)(tma ? tma_scratch_elems(n) : n) * sizeof(T) + 255) / 256 * 256;
+  // fused start: the side list gets its own five arrays behind the compaction
+  // scratch (the fused pass also writes its guessed survivors into the latter)
+  if (fixing || fused) CUDA_TRY(h->scratch.ensure(per * (fused ? 10 : 5)));
   std::memcpy(h->host_state, &s, sizeof s);  // status RUNNING until the master publishes
-  CqkParams<double> p;
+  CqkParams<T> p;
   std::memset(&p, 0, sizeof p);
   p.init = s;
   p.out = (CqkState*)h->host_state_dev;
   p.d = dv[0]; p.a = dv[1]; p.b = dv[2]; p.l = dv[3]; p.u = dv[4]; p.xbar = xbar ? dv[5] : nullptr;
   if (fixing) {
     char* sb = (char*)h->scratch.p;
-    p.sd = (double*)(sb); p.sa = (double*)(sb + per); p.sb = (double*)(sb + 2 * per);
-    p.sl = (double*)(sb + 3 * per); p.su = (double*)(sb + 4 * per);
+    p.sd = (T*)(sb); p.sa = (T*)(sb + per); p.sb = (T*)(sb + 2 * per);
+    p.sl = (T*)(sb + 3 * per); p.su = (T*)(sb + 4 * per);
   }
-  if (fused && !fixing) {  // the side list needs the scratch arrays
-    char* sb = (char*)h->scratch.p;
-    p.sd = (double*)(sb); p.sa = (double*)(sb + per); p.sb = (double*)(sb + 2 * per);
-    p.sl = (double*)(sb + 3 * per); p.su = (double*)(sb + 4 * per);
+  if (fused) {
+    char* sb = (char*)h->scratch.p + 5 * per;
+    p.vd = (T*)(sb); p.va = (T*)(sb + per); p.vb = (T*)(sb + 2 * per);
+    p.vl = (T*)(sb + 3 * per); p.vu = (T*)(sb + 4 * per);
   }
   p.x = xo;
   p.trace = h->trace;
@@ -767,14 +827,19 @@ static int solve_impl(cqk_handle* h, int mem, const double* d, const double* a, 
   void* args[] = {&p};
   int grid;
   const void* fn;
-  if (tma) {
-    grid = limit_grid(h, fixing ? h->grid_tma_fix : h->grid_tma_jac);
-    fn = fixing ? (const void*)cqk_tma_kernel<true> : (const void*)cqk_tma_kernel<false>;
-    p.ar = masterless(h, grid, p.ex);
+  if constexpr (F64) {
+    if (tma) {
+      grid = limit_grid(h, fixing ? h->grid_tma_fix : h->grid_tma_jac);
+      fn = fixing ? (const void*)cqk_tma_kernel<true> : (const void*)cqk_tma_kernel<false>;
+      p.ar = masterless(h, grid, p.ex);
+    } else {
+      grid = limit_grid(h, fixing ? h->grid_cqk_fix : h->grid_cqk_jac);
+      fn = fixing ? (const void*)cqk_solve_kernel<double, true>
+                  : (const void*)cqk_solve_kernel<double, false>;
+    }
   } else {
-    grid = limit_grid(h, fixing ? h->grid_cqk_fix : h->grid_cqk_jac);
-    fn = fixing ? (const void*)cqk_solve_kernel<double, true>
-                : (const void*)cqk_solve_kernel<double, false>;
+    grid = limit_grid(h, fixing ? h->grid_cqk_fix32 : h->grid_cqk_jac32);
+    fn = fixing ? (const void*)cqk_solve_kernel<float, true> : (const void*)cqk_solve_kernel<float, false>;
   }
   CUDA_TRY(cudaEventRecord(h->ev0, h->stream));
   CUDA_TRY(cudaLaunchCooperativeKernel(fn, grid, tma ? kTmaThreads : kThreads, args,
@@ -782,7 +847,7 @@ static int solve_impl(cqk_handle* h, int mem, const double* d, const double* a, 
   CUDA_TRY(cudaEventRecord(h->ev1, h->stream));
   if (mem == CQK_MEM_HOST && x && xo)
   {
-    int rc_ = d2h(h, x, xo, sizeof(double) * n);
+    int rc_ = d2h(h, x, xo, sizeof(T) * n);
     if (rc_) return rc_;
   }
   int rc = finish_sync(h);
@@ -805,11 +870,12 @@ static int solve_impl(cqk_handle* h, int mem, const double* d, const double* a, 
   res->bracket_hi = s.hi;
   // fused start: no pass 0; the sample reads 24 B per sampled element
   const int64_t pass0 = s.fused ? s.elems_sample : ((opts.check || !lam0_given) ? n : 0);
-  const int64_t bytes0 = xbar ? 48 : 24;  // l, u are validated on the first scan
+  constexpr int64_t E = sizeof(T);         // bytes per array element
+  const int64_t bytes0 = xbar ? 6 * E : 3 * E;  // l, u are validated on the first scan
   const int64_t fin = (s.status == ST_SOLVED && xo) ? n : 0;
   res->elems_read = pass0 + s.elems_scan + s.elems_bp + fin;
   res->elems_written = s.elems_written + fin;
-  res->bytes_model = pass0 * bytes0 + 40 * (s.elems_scan + s.elems_bp + s.elems_written) + 48 * fin;
+  res->bytes_model = pass0 * bytes0 + 5 * E * (s.elems_scan + s.elems_bp + s.elems_written) + 6 * E * fin;
   res->device_ms = ms;
   res->launches = 1;
   res->trace_len = s.trace_len;
@@ -821,19 +887,20 @@ namespace {
 
 // Enqueue one persistent simplex / l1 solve (state H2D, launch, state and
 // timeout flag D2H) on the handle's stream; the caller synchronises.
-int launch_spx(cqk_handle* h, SpxState& s, const double* yv, int64_t n, double* xo, bool l1,
-               bool sharded) {
-  const bool tma = h->use_tma;
+template <typename T>
+int launch_spx(cqk_handle* h, SpxState& s, const T* yv, int64_t n, T* xo, bool l1, bool sharded) {
+  constexpr bool F64 = std::is_same<T, double>::value;
+  const bool tma = F64 && h->use_tma;
   if (s.fixing)
-    CUDA_TRY(h->scratch.ensure(((size_t)(tma ? tma_scratch_elems_y(n) : n) * sizeof(double) + 255) /
+    CUDA_TRY(h->scratch.ensure(((size_t)(tma ? tma_scratch_elems_y(n) : n) * sizeof(T) + 255) /
                                256 * 256));
   std::memcpy(h->host_state, &s, sizeof s);  // status RUNNING until the master publishes
-  SpxParams<double> p;
+  SpxParams<T> p;
   std::memset(&p, 0, sizeof p);
   p.init = s;
   p.out = (SpxState*)h->host_state_dev;
   p.y = yv;
-  p.sy = s.fixing ? (double*)h->scratch.p : nullptr;
+  p.sy = s.fixing ? (T*)h->scratch.p : nullptr;
   p.x = xo;
   p.trace = h->trace;
   p.n = n;
@@ -846,8 +913,7 @@ int launch_spx(cqk_handle* h, SpxState& s, const double* yv, int64_t n, double* 
   p.sync.timeline = h->timeline;
   p.sync.herr = h->host_err_dev;
   {
-    const char* te = getenv("CQK_TAIL");
-    p.wcnt = (tma && !sharded && !(te && te[0] == '0')) ? h->wcnt : nullptr;
+    p.wcnt = (tma && !sharded && h->tail_mode) ? h->wcnt : nullptr;
     if (tma && !sharded && s.hist_ok) {  // the halves alternate: this one is zero
       p.hist = h->hist + h->hist_flip * kHistB;
       p.hist_next = h->hist + (h->hist_flip ^ 1) * kHistB;
@@ -857,13 +923,18 @@ int launch_spx(cqk_handle* h, SpxState& s, const double* yv, int64_t n, double* 
   void* args[] = {&p};
   int grid;
   const void* fn;
-  if (tma) {
-    grid = limit_grid(h, l1 ? h->grid_tma_l1 : h->grid_tma_spx);
-    fn = l1 ? (const void*)spx_tma_kernel<true> : (const void*)spx_tma_kernel<false>;
-    p.ar = masterless(h, grid, p.ex);
+  if constexpr (F64) {
+    if (tma) {
+      grid = limit_grid(h, l1 ? h->grid_tma_l1 : h->grid_tma_spx);
+      fn = l1 ? (const void*)spx_tma_kernel<true> : (const void*)spx_tma_kernel<false>;
+      p.ar = masterless(h, grid, p.ex);
+    } else {
+      grid = limit_grid(h, l1 ? h->grid_l1 : h->grid_spx);
+      fn = l1 ? (const void*)spx_solve_kernel<double, true> : (const void*)spx_solve_kernel<double, false>;
+    }
   } else {
-    grid = limit_grid(h, l1 ? h->grid_l1 : h->grid_spx);
-    fn = l1 ? (const void*)spx_solve_kernel<double, true> : (const void*)spx_solve_kernel<double, false>;
+    grid = limit_grid(h, l1 ? h->grid_l1_32 : h->grid_spx32);
+    fn = l1 ? (const void*)spx_solve_kernel<float, true> : (const void*)spx_solve_kernel<float, false>;
   }
   CUDA_TRY(cudaLaunchCooperativeKernel(fn, grid, tma ? kTmaThreads : kThreads, args,
                                        tma ? kSmemC : 0, h->stream));
@@ -878,9 +949,7 @@ int run_alg2(cqk_handle* h, const double* yv, const int64_t* idx, int64_t p, dou
              uint8_t* fixed_dev, Alg2Out* out) {
   if (W < 1) {  // auto: chunks of >= 256 elements (a chunk must be long enough
                 // for its multiplier to prove zeros), at most one per GPU thread
-    int64_t chunk = 256;
-    if (const char* e = getenv("CQK_ALG2_CHUNK")) chunk = atoll(e) > 0 ? atoll(e) : 256;
-    W = p / chunk;
+    W = p / h->alg2_chunk;
     if (W > (int64_t)h->sm_count * 1024) W = (int64_t)h->sm_count * 1024;
     if (W < 1) W = 1;
   }
@@ -935,9 +1004,13 @@ int run_alg2(cqk_handle* h, const double* yv, const int64_t* idx, int64_t p, dou
   return 0;
 }
 
-int spx_common(cqk_handle* h, int mem, const double* y, int64_t n, int64_t n_total, double r,
-               const cqk_options* opts_in, double* x, cqk_result* res, bool l1, bool sharded,
-               const double* xbar = nullptr, int sharpened = -1) {
+// T = float: the warp-segment kernel with y + lam in float (simplex.py:207-215)
+// and the formula / tight starts (the device Algorithm 2 is fp64-only).
+template <typename T>
+int spx_common(cqk_handle* h, int mem, const T* y, int64_t n, int64_t n_total, double r,
+               const cqk_options* opts_in, T* x, cqk_result* res, bool l1, bool sharded,
+               const T* xbar = nullptr, int sharpened = -1) {
+  constexpr bool F64 = std::is_same<T, double>::value;
   if (!h || !y || !res) return set_err(CQK_E_ARG, "null argument");
   std::memset(res, 0, sizeof *res);
   res->domain_index = -1;
@@ -950,14 +1023,14 @@ int spx_common(cqk_handle* h, int mem, const double* y, int64_t n, int64_t n_tot
     return CQK_E_DOMAIN;
   }
   if (n_total < 1 || (!sharded && n < 1)) return set_err(CQK_E_ARG, "n must be >= 1");
-  const double* yv;
-  const double* xbv = nullptr;
-  double* xdev = nullptr;
-  double* xo = x;
+  const T* yv;
+  const T* xbv = nullptr;
+  T* xdev = nullptr;
+  T* xo = x;
   {
-    const double* in[2] = {y, xbar};
-    const double* dv[2] = {nullptr, nullptr};
-    int rc = stage_inputs<double>(h, mem, n, in, 2, dv, (mem == CQK_MEM_HOST && x) ? 1 : 0, &xdev);
+    const T* in[2] = {y, xbar};
+    const T* dv[2] = {nullptr, nullptr};
+    int rc = stage_inputs<T>(h, mem, n, in, 2, dv, (mem == CQK_MEM_HOST && x) ? 1 : 0, &xdev);
     if (rc) return rc;
     yv = dv[0];
     xbv = xbar ? dv[1] : nullptr;
@@ -967,7 +1040,7 @@ int spx_common(cqk_handle* h, int mem, const double* y, int64_t n, int64_t n_tot
     return set_err(CQK_E_ARG, "device arrays must be 16-byte aligned");
   const bool fixing = opts.variable_fixing != 0;
   // the Algorithm-2 route: start "alg2", or a warm start (xbar, simplex.py:65-109)
-  const bool alg2 = (opts.simplex_start == 2 || xbv) && !sharded && std::isnan(opts.lambda0);
+  const bool alg2 = F64 && (opts.simplex_start == 2 || xbv) && !sharded && std::isnan(opts.lambda0);
   SpxState s;
   std::memset(&s, 0, sizeof s);
   s.cmd.fix_hi = INFINITY;
@@ -976,7 +1049,7 @@ int spx_common(cqk_handle* h, int mem, const double* y, int64_t n, int64_t n_tot
   s.lo = -INFINITY;
   s.hi = INFINITY;
   s.r = r;
-  s.tau = tau_of(&opts, false);
+  s.tau = tau_of(&opts, !F64);
   s.n = n_total;
   s.active = n_total;
   s.local_active = n;
@@ -989,16 +1062,19 @@ int spx_common(cqk_handle* h, int mem, const double* y, int64_t n, int64_t n_tot
   s.lam0_value = opts.lambda0;
   s.trace_cap = opts.record_trace ? kTraceCap : 0;
   s.compact_ratio = std::isnan(opts.compact_ratio) ? default_compact_ratio() : opts.compact_ratio;
-  s.start = opts.simplex_start;
+  s.start = (!F64 && opts.simplex_start == 2) ? 1 : opts.simplex_start;  // float: alg2 -> tight
   // start "auto": the histogram scan costs ~10% of one pass and saves grid
   // epochs; it pays while epochs dominate (measured: u01 1e6 139 -> 81 us; at
   // 1e9 the tail mode already makes the late epochs cheap and it costs 2%)
-  s.hist_ok = !sharded && n <= 30000000;
+  s.hist_ok = F64 && h->use_tma && !sharded && n <= 30000000;
   s.lam_hist = NAN;
   int launches = 1;
   int64_t extra_read = 0;
   CUDA_TRY(cudaEventRecord(h->ev0, h->stream));
-  if (alg2) {
+  if constexpr (!F64) {
+    int rc = launch_spx<T>(h, s, yv, n, xo, l1, sharded);
+    if (rc) return rc;
+  } else if (alg2) {
     // simplex.py:243-245 with the chunked initializer: Algorithm 4 then runs
     // on the gathered free set (values only) and x is one dense pass.
     Alg2Out a2;
@@ -1069,7 +1145,7 @@ int spx_common(cqk_handle* h, int mem, const double* y, int64_t n, int64_t n_tot
       s.fixed_count = n - m;  // proven zero by the initializer (simplex.py:251)
       s.fixed_local = n - m;
       s.fixed_removed = n - m;
-      rc = launch_spx(h, s, h->alg2_vals, m, nullptr, false, false);
+      rc = launch_spx<double>(h, s, h->alg2_vals, m, nullptr, false, false);
       if (rc) return rc;
       if (xo) {
         CUDA_TRY(cudaStreamSynchronize(h->stream));
@@ -1086,7 +1162,7 @@ int spx_common(cqk_handle* h, int mem, const double* y, int64_t n, int64_t n_tot
   CUDA_TRY(cudaEventRecord(h->ev1, h->stream));
   if (mem == CQK_MEM_HOST && x && xo)
   {
-    int rc_ = d2h(h, x, xo, sizeof(double) * n);
+    int rc_ = d2h(h, x, xo, sizeof(T) * n);
     if (rc_) return rc_;
   }
   int rc = finish_sync(h);
@@ -1109,7 +1185,7 @@ int spx_common(cqk_handle* h, int mem, const double* y, int64_t n, int64_t n_tot
   const int64_t pass0 = alg2 ? extra_read : n;
   res->elems_read = pass0 + s.elems_scan + fin;
   res->elems_written = s.elems_written + fin;
-  res->bytes_model = 8 * (pass0 + s.elems_scan + s.elems_written) + 16 * fin;
+  res->bytes_model = (int64_t)sizeof(T) * (pass0 + s.elems_scan + s.elems_written + 2 * fin);
   res->device_ms = ms;
   res->launches = launches;
   res->trace_len = s.trace_len;
@@ -1121,6 +1197,16 @@ int spx_common(cqk_handle* h, int mem, const double* y, int64_t n, int64_t n_tot
 extern "C" int spx_project_f64(cqk_handle* h, int mem, const double* y, int64_t n, double r,
                                const cqk_options* opts, double* x, cqk_result* res) {
   return spx_common(h, mem, y, n, n, r, opts, x, res, false, false);
+}
+
+extern "C" int spx_project_f32(cqk_handle* h, int mem, const float* y, int64_t n, double r,
+                               const cqk_options* opts, float* x, cqk_result* res) {
+  return spx_common<float>(h, mem, y, n, n, r, opts, x, res, false, false);
+}
+
+extern "C" int l1_project_f32(cqk_handle* h, int mem, const float* y, int64_t n, double r,
+                              const cqk_options* opts, float* x, cqk_result* res) {
+  return spx_common<float>(h, mem, y, n, n, r, opts, x, res, true, false);
 }
 
 extern "C" int spx_project_sharded_f64(cqk_handle* h, int mem, const double* y, int64_t n_local,
@@ -1311,6 +1397,149 @@ extern "C" int spx_project_batched_multi_f64(cqk_handle* const* hs, int nh, cons
     res->launches += part[q].launches;
   }
   return 0;
+}
+
+// ------------------------------------------------------------ device groups
+// One process driving several GPUs (the GPU analogue of the reference's
+// worker pool, parallel.py:52-59): one handle and one rank per listed device,
+// mailboxes wired with cqk_comm_connect_local (peer access enabled), n cut
+// into contiguous shards (_chunk_ranges, parallel.py:82-85), one host thread
+// per rank calling the sharded entry point, so every rank's persistent kernel
+// is in flight at once.  A device listed k times hosts k ranks on 1/k of its
+// SMs each (a one-GPU stand-in for k GPUs).
+struct cqk_group {
+  std::vector<cqk_handle*> h;
+  int64_t reserved = -1;  // the largest shard the scratch and staging hold
+};
+
+extern "C" int cqk_group_create(cqk_group** out, const int* devices, int ndev) {
+  if (!out || !devices || ndev < 1 || ndev > kMaxRanks)
+    return set_err(CQK_E_ARG, "need 1..8 devices");
+  auto* g = new cqk_group;
+  auto fail = [&](int rc) {
+    for (auto* x : g->h) cqk_destroy(x);
+    delete g;
+    return rc;
+  };
+  for (int q = 0; q < ndev; ++q) {
+    cqk_handle* x = nullptr;
+    if (int rc = cqk_create(&x, devices[q])) return fail(rc);
+    g->h.push_back(x);
+  }
+  for (int q = 0; q < ndev; ++q) {
+    int mult = 0;
+    for (int k = 0; k < ndev; ++k) mult += devices[k] == devices[q];
+    if (mult > 1) g->h[q]->grid_limit = g->h[q]->sm_count / mult;
+    if (int rc = cqk_comm_create(g->h[q], q, ndev, nullptr)) return fail(rc);
+  }
+  for (int q = 0; q < ndev; ++q)
+    if (int rc = cqk_comm_connect_local(g->h[q], g->h.data(), ndev)) return fail(rc);
+  *out = g;
+  return 0;
+}
+
+extern "C" int cqk_group_destroy(cqk_group* g) {
+  if (!g) return 0;
+  for (auto* x : g->h) cqk_destroy(x);
+  delete g;
+  return 0;
+}
+
+extern "C" int cqk_group_size(const cqk_group* g) { return g ? (int)g->h.size() : 0; }
+
+namespace {
+
+// Allocate every rank's scratch and host staging for shards of up to
+// n / W + 1 elements before any kernel starts: an allocation while a peer's
+// kernel waits in the exchange could synchronise a shared device.
+int group_reserve(cqk_group* g, int64_t n) {
+  const int64_t W = (int64_t)g->h.size();
+  const int64_t per = n / W + 1;
+  if (per <= g->reserved) return 0;
+  for (auto* x : g->h) {
+    if (int rc = cqk_reserve(x, per)) return rc;
+    if (int rc = cqk_reserve_host(x, per)) return rc;
+  }
+  g->reserved = per;
+  return 0;
+}
+
+// Run f(q, lo, hi, &res_q) on one thread per rank; combine the outcomes
+// (identical on every rank except the per-rank byte counters).
+template <class F>
+int group_run(cqk_group* g, int64_t n, cqk_result* res, F&& f) {
+  const int W = (int)g->h.size();
+  std::vector<cqk_result> part((size_t)W);
+  std::vector<int> rc((size_t)W, 0);
+  std::vector<std::string> err((size_t)W);
+  std::vector<std::thread> th;
+  for (int q = 0; q < W; ++q) {
+    const int64_t lo = n * q / W, hi = n * (q + 1) / W;
+    th.emplace_back([&, q, lo, hi] {
+      rc[q] = f(q, lo, hi, &part[q]);
+      if (rc[q] < 0) err[q] = g_err;  // thread_local: carry it to the caller's thread
+    });
+  }
+  for (auto& t : th) t.join();
+  *res = part[0];
+  for (int q = 0; q < W; ++q)
+    if (rc[q] < 0 && rc[q] != CQK_E_DOMAIN && rc[q] != CQK_E_MAXITER && rc[q] != CQK_E_CONTRACT)
+      return set_err(rc[q], "group rank " + std::to_string(q) + ": " + err[q]);
+  for (int q = 1; q < W; ++q) {
+    const cqk_result& o = part[q];
+    if (o.status != res->status || o.iterations != res->iterations ||
+        !(o.lam == res->lam || (std::isnan(o.lam) && std::isnan(res->lam))))
+      return set_err(CQK_E_CUDA, "group ranks disagree on the outcome (rank " + std::to_string(q) + ")");
+    if (o.domain_index >= 0 && (res->domain_index < 0 || o.domain_index < res->domain_index)) {
+      res->domain_field = o.domain_field;
+      res->domain_index = o.domain_index;
+    }
+    res->elems_read += o.elems_read;
+    res->elems_written += o.elems_written;
+    res->bytes_model += o.bytes_model;
+    res->device_ms = std::max(res->device_ms, o.device_ms);  // concurrent: the slowest
+    res->launches += o.launches;
+  }
+  return rc[0];
+}
+
+}  // namespace
+
+extern "C" int cqk_solve_group_f64(cqk_group* g, const double* d, const double* a,
+                                   const double* b, const double* l, const double* u, int64_t n,
+                                   double r, const cqk_options* opts, const double* xbar,
+                                   double* x, cqk_result* res) {
+  if (!g || !d || !a || !b || !l || !u || !res) return set_err(CQK_E_ARG, "null argument");
+  const int W = (int)g->h.size();
+  if (n < W) return cqk_solve_f64(g->h[0], CQK_MEM_HOST, d, a, b, l, u, n, r, opts, xbar, x, res);
+  if (int rc = group_reserve(g, n)) return rc;
+  return group_run(g, n, res, [&](int q, int64_t lo, int64_t hi, cqk_result* rq) {
+    return cqk_solve_sharded_f64(g->h[q], CQK_MEM_HOST, d + lo, a + lo, b + lo, l + lo, u + lo,
+                                 hi - lo, lo, n, r, opts, xbar ? xbar + lo : nullptr,
+                                 x ? x + lo : nullptr, rq);
+  });
+}
+
+static int spx_group(cqk_group* g, const double* y, int64_t n, double r, const cqk_options* opts,
+                     double* x, cqk_result* res, bool l1) {
+  if (!g || !y || !res) return set_err(CQK_E_ARG, "null argument");
+  const int W = (int)g->h.size();
+  if (n < W) return spx_common(g->h[0], CQK_MEM_HOST, y, n, n, r, opts, x, res, l1, false);
+  if (int rc = group_reserve(g, n)) return rc;
+  return group_run(g, n, res, [&](int q, int64_t lo, int64_t hi, cqk_result* rq) {
+    return spx_common(g->h[q], CQK_MEM_HOST, y + lo, hi - lo, n, r, opts, x ? x + lo : nullptr, rq,
+                      l1, true);
+  });
+}
+
+extern "C" int spx_project_group_f64(cqk_group* g, const double* y, int64_t n, double r,
+                                     const cqk_options* opts, double* x, cqk_result* res) {
+  return spx_group(g, y, n, r, opts, x, res, false);
+}
+
+extern "C" int l1_project_group_f64(cqk_group* g, const double* y, int64_t n, double r,
+                                    const cqk_options* opts, double* x, cqk_result* res) {
+  return spx_group(g, y, n, r, opts, x, res, true);
 }
 
 // ------------------------------------------------------------ components

@@ -37,6 +37,7 @@ enum Phase : int32_t {
   PH_SNAP = 6,   // simplex: max(-y[free]) snap (simplex.py:276-281)
   PH_SAMPLE = 7, // fused start: lambda0 estimated from sample tiles
   PH_FUSED = 8,  // fused start: lambda0 sums + validate + the first scan's aggregates
+  PH_SAMPLE2 = 9, // fused start: phi at the estimate over the sample tiles (direction guess)
 };
 
 enum Status : int32_t {
@@ -65,6 +66,10 @@ struct Cmd {
   int32_t live_hi;  // ... an upper-fixed one
   int32_t hist;     // simplex: this scan also histograms t > 0 (start "auto")
   int32_t side;     // this scan runs over the fused pass's side list (plus its aggregates)
+  int32_t guess;    // fused start: +1 lower / -1 upper fixing expected at lambda0, 0 unknown;
+                    // the fused pass then also writes the elements that would survive it
+  int32_t adopt;    // the side scan confirmed the guess: those survivors are the working set
+  int32_t pad_[2];
 };
 
 // Master-side solver state (SolveState, newton.py:70-90, plus counters).
@@ -85,18 +90,20 @@ struct CqkState {
   // fused start (PH_SAMPLE -> PH_FUSED -> side scan): the first scan's
   // contributions of every element whose status is fixed on the interval
   // [cmd.lam - cmd.edge, cmd.lam + cmd.edge] around the estimated lambda0
-  int32_t fused, pad2_;
+  int32_t fused, fused_guess;  // fused start; with the direction guess (fixing solves)
   double fused_width;       // relative half-width of the classification interval
   double agg[11];           // scan slots 0..10 of those elements at lambda0 (all ranks)
   double agg_lo_loc, agg_hi_loc;  // their lower / upper at-bound counts on this rank
   int64_t side_local;       // elements in this rank's side list
   int64_t elems_sample;     // sample elements read (24 B each)
+  int64_t surv_local;       // elements the fused pass wrote as the guessed survivors
 };
 
 template <typename T>
 struct CqkParams {
   const T *d, *a, *b, *l, *u, *xbar;
   T *sd, *sa, *sb, *sl, *su;  // compaction scratch (n each) or null
+  T *vd, *va, *vb, *vl, *vu;  // fused start: the side-list scratch (n each) or null
   T* x;                       // output or null
   double* trace;              // 4 doubles per phi evaluation
   int64_t n;                  // elements of this rank's shard
@@ -175,7 +182,9 @@ DEVI void m_secant_or_fail(CqkState& s) {
 // ranks; loc: the same vector of this rank alone (local bookkeeping only).
 DEVI void m_after_scan(CqkState& s, const double* tot, const double* loc, double* trace) {
   s.phi_evals += 1;
-  if (s.cmd.side) {  // the fused pass read every element; this scan only the side list
+  const bool side_scan = s.cmd.side != 0;
+  s.cmd.adopt = 0;
+  if (side_scan) {  // the fused pass read every element; this scan only the side list
     s.elems_scan += s.side_local;
     s.cmd.side = 0;
   } else {
@@ -225,7 +234,18 @@ DEVI void m_after_scan(CqkState& s, const double* tot, const double* loc, double
         else s.cmd.fix_lo = lam;
       }
     }
+    // fused start: the fused pass dropped every element it classified as
+    // fixed in the guessed direction (t < l on the whole interval for +1);
+    // if that is the direction just taken, they are all fixed now and the
+    // rest is the working set.  Fixed-but-present elements (side-list ones
+    // with t == l, ...) stay under the live fixed tests (fhi_phys unchanged).
+    if (side_scan && s.cmd.guess != 0 && dir == s.cmd.guess) {
+      s.fixed_removed += (int64_t)(dir > 0 ? s.agg_lo_loc : s.agg_hi_loc);
+      s.phys_count = s.surv_local;
+      s.cmd.adopt = 1;
+    }
   }
+  s.cmd.guess = 0;
   if (diff < 0) {
     if (dplus > 0) {
       const double step = -diff / dplus;
@@ -324,6 +344,29 @@ DEVI void m_after_sample(CqkState& s, const double* tot, double local_count) {
   // relative half-width (default 2e-3; sampled estimates land within ~5e-4 of
   // lambda0 on the generator families)
   s.cmd.edge = isfinite(est) ? s.fused_width * fabs(est) : 0.0;
+  s.cmd.guess = 0;
+  s.cmd.phase = (s.fixing && s.fused_guess) ? PH_SAMPLE2 : PH_FUSED;
+}
+
+// The second sample pass (fixing only): tot 0 sum b x(est), 1 sum (b x)^2,
+// 2 elements, 3 sum |b x| over the same sample tiles -> the sign of
+// phi(lambda0) - r, i.e. which bound the first iteration will fix
+// (newton.py:165-206), when the sampled estimate is clear of r by six
+// standard errors.  The survivor list pays only if several scans follow
+// it, and a small initial residual means a short solve (C2 families:
+// |phi(lambda0) - r| / sum|b x| of 1e-3 .. 2e-2 took 3-4 phi evaluations,
+// 3e-2 .. 9e-2 took 5-7), so it is written only above kGuessResid.  A wrong
+// or missing guess costs bytes only: the list is then simply not adopted.
+constexpr double kGuessResid = 0.025;
+DEVI void m_after_sample2(CqkState& s, const double* tot, double local_count) {
+  s.elems_scan += (int64_t)local_count;  // 40 B per sampled element
+  const double m = fmax(tot[2], 1.0), N = (double)s.n;
+  const double mean = tot[0] / m;
+  const double var = fmax(tot[1] / m - mean * mean, 0.0);
+  const double diff = N * mean - s.r_orig, se = N * sqrt(var / m), scale = N * tot[3] / m;
+  const bool clear = fabs(diff) > 6.0 * se && fabs(diff) > kGuessResid * scale;
+  s.cmd.guess = clear && isfinite(diff) ? (diff > 0 ? 1 : -1) : 0;
+  if (s.fused_guess >= 2) s.cmd.guess = s.fused_guess == 2 ? 1 : -1;  // forced (tests)
   s.cmd.phase = PH_FUSED;
 }
 
@@ -332,14 +375,15 @@ DEVI void m_after_sample(CqkState& s, const double* tot, double local_count) {
 // class * 2^40 + index (min), 3..5 lower at-bound (sum bl, sum |bl|, count),
 // 6..8 upper at-bound, 9 / 10 interior with t >= 0 (sum b^2/d, sum b a/d),
 // 11 / 12 interior with t <= 0 (unused: such elements go to the side list),
-// 13 side-list elements.  loc: this rank's
-// vector.
-constexpr int kFusedK = 14;
+// 13 side-list elements, 14 guessed survivors written (cmd.guess != 0).
+// loc: this rank's vector.
+constexpr int kFusedK = 15;
 constexpr double kVKey = 1099511627776.0;  // 2^40
 DEVI void m_after_fused(CqkState& s, const double* tot, const double* loc) {
   s.elems_scan += s.phys_count;  // 40 B per element: d, a, b, l, u
   s.side_local = (int64_t)loc[13];
-  s.elems_written += s.side_local;  // the side list (40 B per element)
+  s.surv_local = (int64_t)loc[14];
+  s.elems_written += s.side_local + s.surv_local;  // side list + survivors (40 B per element)
   if (s.check) {
     for (int c = 0; c < 10; ++c) s.vidx[c] = (double)s.n;
     if (tot[2] < HUGE_VAL) {
@@ -370,6 +414,7 @@ DEVI void m_after_fused(CqkState& s, const double* tot, const double* loc) {
     s.cmd.side = 1;
   } else {
     s.cmd.side = 0;  // a full first scan (the side list is dropped)
+    s.cmd.guess = 0;  // and the survivors, classified on the wrong interval
   }
 }
 
@@ -404,7 +449,7 @@ DEVI bool elem_scan(T d, T a, T b, T l, T u, T lam, T fhi, T flo, bool chk_lo, b
   const bool tlo = alo && t == l && l < u;
   const bool thi = ahi && t == u && l < u;
   if (interior || tlo || thi) {
-    const double w = (double)(mul_rn(b, b) * yd);
+    const double w = (double)w_of(b, d, yd);
     if (interior) acc[2] += w;
     else if (tlo) acc[3] += w;
     else acc[4] += w;

@@ -698,21 +698,23 @@ DEVI int64_t sample_tile(int64_t ntiles, int k) {
   return q < Q ? c + q * G : -1;
 }
 
+// NA arrays of this CTA's sample tiles into the ST x STRIDE pipeline
+template <int NA = 3, int ST = kStages3, int STRIDE = kStride3>
 DEVI void produce_sample(const Src src, int64_t n, int64_t ntiles, TPipe& pp) {
   for (int k = 0; k < kSampleTiles; ++k) {
     const int64_t t = sample_tile(ntiles, k);
     if (t < 0) break;
-    const int s = pp.pc % kStages3;
-    const unsigned ph = ((pp.pc / kStages3) & 1) ^ 1;
-    if (pp.pc >= (unsigned)kStages3) mbar_wait_s(pp.empty + 8 * s, ph);
+    const int s = pp.pc % ST;
+    const unsigned ph = ((pp.pc / ST) & 1) ^ 1;
+    if (pp.pc >= (unsigned)ST) mbar_wait_s(pp.empty + 8 * s, ph);
     const int64_t left = n - t * kTileC;
     const unsigned bytes = ((unsigned)(left < kTileC ? left : kTileC) * 8u) & ~15u;
     const unsigned fb = pp.full + 8 * s;
-    mbar_expect_tx_s(fb, 3 * bytes);
+    mbar_expect_tx_s(fb, NA * bytes);
     if (bytes) {
-      const unsigned dst = smem_u32(pp.buf) + (unsigned)(s * kStride3) * 8u;
+      const unsigned dst = smem_u32(pp.buf) + (unsigned)(s * STRIDE) * 8u;
 #pragma unroll
-      for (int a = 0; a < 3; ++a) tma_load_1d_s(dst + a * kTileC * 8u, src.p[a] + t * kTileC, bytes, fb);
+      for (int a = 0; a < NA; ++a) tma_load_1d_s(dst + a * kTileC * 8u, src.p[a] + t * kTileC, bytes, fb);
     }
     ++pp.pc;
   }
@@ -753,9 +755,52 @@ DEVI void t_sample(const CqkParams<double>& p, int64_t ntiles, TPipe& pp, double
   }
 }
 
+// The second sample pass (fixing solves): phi's sum b x at the estimate
+// over the same sample tiles (all five arrays), for the direction guess.
+// acc 0 sum b x, 1 sum (b x)^2, 2 elements, 3 sum |b x|
+DEVI void t_sample2(const CqkParams<double>& p, double lam, int64_t ntiles, TPipe& pp,
+                    double (&acc)[kMaxK]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int k = 0; k < kSampleTiles; ++k) {
+    const int64_t t = sample_tile(ntiles, k);
+    if (t < 0) break;
+    const int s = pp.pc % kStagesC;
+    WTile wt;
+    wt.sm = pp.buf + (size_t)s * kStageElemsC + kSeg * warp;
+    wt.gbase = t * kTileC + kSeg * warp;
+    const int64_t left = p.n - wt.gbase;
+    wt.wcnt = left <= 0 ? 0 : (left < kSeg ? (int)left : kSeg);
+    wt.patch = (wt.wcnt & 1) && wt.wcnt < kSeg;
+    wt.q = k;
+    mbar_wait_s(pp.full + 8 * s, (pp.pc / kStagesC) & 1);
+    if (wt.wcnt > 0) {
+      double D[kEptC], A[kEptC], B[kEptC], L[kEptC], U[kEptC];
+      tile_load(wt, 0, p.d, D, 1.0);
+      tile_load(wt, 1, p.a, A);
+      tile_load(wt, 2, p.b, B, 1.0);
+      tile_load(wt, 3, p.l, L);
+      tile_load(wt, 4, p.u, U);
+#pragma unroll
+      for (int j = 0; j < kEptC; ++j) {
+        if (e_loc(lane, j) >= wt.wcnt) continue;
+        const double x = clip(div_rn(add_rn(mul_rn(B[j], lam), A[j]), D[j]), L[j], U[j]);
+        const double bx = mul_rn(B[j], x);
+        acc[0] += bx;
+        acc[1] += bx * bx;
+        acc[2] += 1.0;
+        acc[3] += fabs(bx);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive_s(pp.empty + 8 * s);
+    ++pp.pc;
+  }
+}
+
 // Append the elements with keep[j] of this warp's tile (values from the held
-// stage) to the warp's scratch sub-segments: slot q_out at offset off_out.
-DEVI void append_tile(const CqkParams<double>& p, const WTile& wt, const Src& src,
+// stage) to the warp's sub-segments of the scratch set dst: slot q_out at
+// offset off_out.
+DEVI void append_tile(double* const (&dst)[5], const WTile& wt, const Src& src,
                       const bool (&keep)[kEptC], int64_t& q_out, int& off_out, int64_t& out_m) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned ltm = (1u << lane) - 1u;
@@ -783,7 +828,7 @@ DEVI void append_tile(const CqkParams<double>& p, const WTile& wt, const Src& sr
     if (keep[j]) {
       const int o = r + __popc(bal & ltm);
       const int64_t pos = o < kSeg ? b0 + o : b1 + (o - kSeg);
-      p.sd[pos] = D[j]; p.sa[pos] = A[j]; p.sb[pos] = B[j]; p.sl[pos] = L[j]; p.su[pos] = U[j];
+      dst[0][pos] = D[j]; dst[1][pos] = A[j]; dst[2][pos] = B[j]; dst[3][pos] = L[j]; dst[4][pos] = U[j];
     }
     r += __popc(bal);
   }
@@ -796,8 +841,8 @@ constexpr double kBracketEps = 16.0 * 2.220446049250313e-16;
 
 template <bool CHECK, bool FULL>
 DEVI void fused_tile(const CqkParams<double>& p, const WTile& wt, const Src& src, double lam_hat,
-                     double h2, double (&acc)[kMaxK], int& nlo, int& nhi, int& nside,
-                     bool (&side)[kEptC], bool& anyside_out) {
+                     double h2, int guess, double (&acc)[kMaxK], int& nlo, int& nhi, int& nside,
+                     bool (&side)[kEptC], bool& anyside_out, bool (&surv)[kEptC]) {
   const int lane = threadIdx.x & 31;
   double D[kEptC], A[kEptC], B[kEptC], L[kEptC], U[kEptC];
   tile_load<FULL>(wt, 0, src.p[0], D, 1.0);
@@ -872,30 +917,43 @@ DEVI void fused_tile(const CqkParams<double>& p, const WTile& wt, const Src& src
       side[j] = valid & !below & !above & !inner;
       nside += side[j];
       anyside |= side[j];
+      surv[j] = valid & !(guess > 0 ? below : above);  // (guess 0: not used)
     }
     anyside_out = anyside;
 }
 
-// The fused pass (slots: m_after_fused).  Returns this warp's side-list count.
+// The fused pass (slots: m_after_fused).  The side list goes to the side
+// scratch set; with a direction guess (fixing solves) every element the
+// guessed fixing would not drop also goes to the compaction scratch -- the
+// working set of the following scans if the side scan confirms the guess.
+// Returns this warp's side-list count; *surv_m its survivor count.
 template <bool CHECK>
 DEVI int64_t t_fused(const CqkParams<double>& p, const Cmd& c, const TileWalk& tw,
-                     const Src src, TPipe& pp, double (&acc)[kMaxK]) {
+                     const Src src, TPipe& pp, double (&acc)[kMaxK], int64_t* surv_m) {
   // I = [lam^ - h, lam^ + h] as the host-side check sees it; h2 also covers
   // the rounding of the interval ends
   const double lam_hat = c.lam, h2 = c.edge + kBracketEps * fabs(c.lam);
-  int64_t out_m = 0, q_out = 0;
-  int off_out = 0;
+  const int guess = c.guess;
+  double* const dside[5] = {p.vd, p.va, p.vb, p.vl, p.vu};
+  double* const dsurv[5] = {p.sd, p.sa, p.sb, p.sl, p.su};
+  int64_t out_m = 0, q_out = 0, sv_m = 0, q_sv = 0;
+  int off_out = 0, off_sv = 0;
   int nlo = 0, nhi = 0, nside = 0;
   consume(tw, pp, -1, [&](const WTile& wt) {
-    bool side[kEptC], anyside;
-    if (wt.wcnt == kSeg) fused_tile<CHECK, true>(p, wt, src, lam_hat, h2, acc, nlo, nhi, nside, side, anyside);
-    else fused_tile<CHECK, false>(p, wt, src, lam_hat, h2, acc, nlo, nhi, nside, side, anyside);
-    if (__any_sync(0xffffffffu, anyside)) append_tile(p, wt, src, side, q_out, off_out, out_m);
+    bool side[kEptC], surv[kEptC], anyside;
+    if (wt.wcnt == kSeg)
+      fused_tile<CHECK, true>(p, wt, src, lam_hat, h2, guess, acc, nlo, nhi, nside, side, anyside, surv);
+    else
+      fused_tile<CHECK, false>(p, wt, src, lam_hat, h2, guess, acc, nlo, nhi, nside, side, anyside, surv);
+    if (__any_sync(0xffffffffu, anyside)) append_tile(dside, wt, src, side, q_out, off_out, out_m);
+    if (guess != 0) append_tile(dsurv, wt, src, surv, q_sv, off_sv, sv_m);
   });
   acc[5] += (double)nlo;
   acc[8] += (double)nhi;
   acc[13] += (double)nside;
-  fence_proxy_async_global();  // generic stores -> the side scan's bulk loads
+  if ((threadIdx.x & 31) == 0) acc[14] += (double)sv_m;  // a warp total: counted once
+  fence_proxy_async_global();  // generic stores -> the next passes' bulk loads
+  *surv_m = sv_m;
   return out_m;
 }
 
@@ -913,8 +971,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
   __shared__ int s_abort;
   __shared__ int s_nslots;   // scratch slots of this CTA (max over its warps)
   __shared__ int s_nsl_new;  // ... being formed by a compacting pass
+  __shared__ int s_nsl_side, s_nsl_side_new;  // side-list slots (fused start)
+  __shared__ int s_nsl_surv;  // the fused pass's guessed survivors (compaction scratch)
   __shared__ int s_spec;     // tiles of the next pass issued across the grid step
-  __shared__ int s_spec_scr; // ... and whether they came from scratch
+  __shared__ int s_spec_scr; // ... and their walk: 0 original arrays, 1 scratch, 2 side list
   __shared__ unsigned long long s_probe_last;  // timeline probe: last consumer warp done
   __shared__ unsigned long long s_probe_pre;   // ... last warp (incl. producer) at the reduction
   __shared__ long long s_tix[kStagesC];        // dynamic final pass: tile index per stage
@@ -937,6 +997,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
     s_abort = 0;
     s_nslots = 0;
     s_nsl_new = 0;
+    s_nsl_side = s_nsl_side_new = s_nsl_surv = 0;
     s_spec = 0;
     s_spec_scr = 0;
     s_probe_last = 0;
@@ -952,21 +1013,25 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
   const TileWalk orig{p.n, ntiles, -1};
   const Src src_orig{{p.d, p.a, p.b, p.l, p.u, nullptr}};
   const Src src_scr{{p.sd, p.sa, p.sb, p.sl, p.su, nullptr}};
+  const Src src_side{{p.vd, p.va, p.vb, p.vl, p.vu, nullptr}};
   const Src src_l0x{{p.d, p.a, p.b, p.l, p.u, p.xbar}};
   const bool prod_lane = producer && lane == 0;
   const int has_xbar = p.xbar != nullptr;
   const int check = p.init.check;  // immutable during the solve
   bool in_scratch = false;
-  bool side_pending = false;  // the fused pass left a side list in scratch
+  bool side_pending = false;  // the fused pass left a side list in the side scratch
+  bool adopt_pending = false; // the side scan may have adopted the guessed survivors
   int64_t m_w = -1;  // this warp's scratch element count (consumers, once in scratch)
+  int64_t m_side = 0, m_surv = 0;  // this warp's side-list / guessed-survivor counts
   // The producer lane issues the first tiles of the most likely next pass (a
   // phi scan / breakpoint pass over the current working set -- or, before
   // any compaction, the final pass over the original arrays) while the grid
   // step is in flight: the loads do not depend on lambda.
-  auto speculate = [&]() {
-    const TileWalk nw{p.n, ntiles, in_scratch ? s_nslots : -1};
-    s_spec = (c_tma_flags & 1) ? 0 : produce<5>(in_scratch ? src_scr : src_orig, nw, pp, 0, kSpecDepthC);
-    s_spec_scr = in_scratch;
+  auto speculate = [&](int kind) {  // 0 original arrays, 1 scratch, 2 side list
+    const TileWalk nw{p.n, ntiles, kind == 0 ? -1 : (kind == 1 ? s_nslots : s_nsl_side)};
+    const Src& sr = kind == 0 ? src_orig : (kind == 1 ? src_scr : src_side);
+    s_spec = (c_tma_flags & 1) ? 0 : produce<5>(sr, nw, pp, 0, kSpecDepthC);
+    s_spec_scr = kind;
   };
   const bool probe = blockIdx.x == 1 && p.sync.timeline;  // timeline detail columns 10-15
   const bool single = p.ar.rows != nullptr;  // masterless grid step: every CTA decides
@@ -981,22 +1046,27 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
       if (!producer) drain(pp, spec);  // never leave bulk copies in flight
       break;
     }
-    if (side_pending && c.phase != PH_FUSED) {
-      // after the fused pass the producer speculated the side list; a full
-      // first scan (lambda0 outside the interval) or a stop drops it
-      side_pending = false;
-      if (!(c.phase == PH_SCAN && c.side)) {
-        if (!producer && spec > 0) drain(pp, spec);
-        spec = 0;
-        in_scratch = false;
-        m_w = -1;
+    const bool side_walk = side_pending && c.phase == PH_SCAN && c.side;
+    if (side_pending && c.phase != PH_FUSED) side_pending = false;
+    if (adopt_pending) {  // the epoch after the side scan: adopt the guessed survivors?
+      adopt_pending = false;
+      if (c.adopt) {
+        in_scratch = true;
+        m_w = m_surv;
       }
     }
-    const TileWalk work{p.n, ntiles, in_scratch ? s_nslots : -1};
-    const Src wsrc = in_scratch ? src_scr : src_orig;
+    // speculated tiles of another walk than this epoch's (a guess the
+    // decision did not take, a side list not scanned) are dropped
+    if (spec > 0 && c.phase != PH_FINAL && s_spec_scr != (side_walk ? 2 : (in_scratch ? 1 : 0))) {
+      if (!producer) drain(pp, spec);
+      spec = 0;
+    }
+    const TileWalk work{p.n, ntiles, side_walk ? s_nsl_side : (in_scratch ? s_nslots : -1)};
+    const Src wsrc = side_walk ? src_side : (in_scratch ? src_scr : src_orig);
+    const int64_t m_walk = side_walk ? m_side : m_w;
     if (c.phase == PH_FINAL) {
       if (blockIdx.x <= 1 && threadIdx.x == 0) tl_mark(p.sync, epoch, 10 + 2 * blockIdx.x);
-      const bool reuse = spec > 0 && !s_spec_scr;  // the speculated tiles are the final's
+      const bool reuse = spec > 0 && s_spec_scr == 0;  // the speculated tiles are the final's
       const bool dyn = p.ar.dyn_final != 0;          // single GPU: dynamic tile assignment
       const int D = kSpecDepthC;                     // its static prefix: the speculation's tiles
       if (p.x) {
@@ -1044,7 +1114,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
       for (int k = 0; k < 15; ++k) a15[k] = acc[k];
       block_reduce<15, kConsW>(a15, ops, s_red, s_tot);
       is_master = grid_step_any<15>(p.ar, p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch,
-                                   [&] { if (prod_lane) speculate(); }, (c_tma_flags & 4) != 0);
+                                   [&] { if (prod_lane) speculate(0); }, (c_tma_flags & 4) != 0);
       if (is_master && warp == 0) {
         if (lane == 0) tl_record(dsync, epoch, PH_LAMBDA0, p.n, 0);
         double glob[15];
@@ -1063,8 +1133,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
       const int ops[3] = {OP_SUM, OP_SUM, OP_SUM};
       double a3[3] = {acc[0], acc[1], acc[2]};
       block_reduce<3, kConsW>(a3, ops, s_red, s_tot);
+      // (fixing solves sample twice: the second sample pass owns the pipeline next)
       is_master = grid_step_any<3>(p.ar, p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch,
-                                   [&] { if (prod_lane) speculate(); }, (c_tma_flags & 4) != 0);
+                                   [&] { if (prod_lane && !(FIX && p.init.fused_guess)) speculate(0); }, (c_tma_flags & 4) != 0);
       if (is_master && warp == 0) {
         if (lane == 0) tl_record(dsync, epoch, PH_SAMPLE, p.n, 0);
         double glob[3];
@@ -1077,17 +1148,41 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
           }
         }
       }
+    } else if (c.phase == PH_SAMPLE2) {
+      if (prod_lane) produce_sample<5, kStagesC, kStageElemsC>(src_orig, p.n, ntiles, pp);
+      else if (!producer) t_sample2(p, c.lam, ntiles, pp, acc);
+      const int ops[4] = {OP_SUM, OP_SUM, OP_SUM, OP_SUM};
+      double a4[4] = {acc[0], acc[1], acc[2], acc[3]};
+      block_reduce<4, kConsW>(a4, ops, s_red, s_tot);
+      is_master = grid_step_any<4>(p.ar, p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch,
+                                   [&] { if (prod_lane) speculate(0); }, (c_tma_flags & 4) != 0);
+      if (is_master && warp == 0) {
+        if (lane == 0) tl_record(dsync, epoch, PH_SAMPLE2, p.n, 0);
+        double glob[4];
+        const bool ok = exchange_totals<4>(p.ex, epoch, ops, s_tot, glob, master);
+        if (lane == 0) {
+          if (ok) m_after_sample2(s_st, glob, s_tot[2]);
+          else {
+            m_stop(s_st, ST_TIMEOUT);
+            raise_timeout(p.sync);
+          }
+        }
+      }
     } else if (c.phase == PH_FUSED) {
       acc[2] = HUGE_VAL;  // the first failing validate() check (min)
       if (prod_lane) produce<5>(src_orig, orig, pp, spec);
       else if (!producer) {
-        const int64_t mm = check ? t_fused<true>(p, c, orig, src_orig, pp, acc)
-                                 : t_fused<false>(p, c, orig, src_orig, pp, acc);
-        m_w = mm;
-        if (lane == 0) atomicMax(&s_nsl_new, (int)((mm + kSeg - 1) / kSeg));
+        int64_t sv = 0;
+        const int64_t mm = check ? t_fused<true>(p, c, orig, src_orig, pp, acc, &sv)
+                                 : t_fused<false>(p, c, orig, src_orig, pp, acc, &sv);
+        m_side = mm;
+        m_surv = sv;
+        if (lane == 0) {
+          atomicMax(&s_nsl_side_new, (int)((mm + kSeg - 1) / kSeg));
+          atomicMax(&s_nsl_new, (int)((sv + kSeg - 1) / kSeg));
+        }
       }
-      in_scratch = true;  // speculate the side list: the likely next walk
-      side_pending = true;
+      side_pending = true;  // speculate the side list: the likely next walk
       int ops[kFusedK];
       double aK[kFusedK];
 #pragma unroll
@@ -1095,9 +1190,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
       block_reduce<kFusedK, kConsW>(aK, ops, s_red, s_tot);
       is_master = grid_step_any<kFusedK>(p.ar, p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch, [&] {
         if (prod_lane) {
-          s_nslots = s_nsl_new;
+          s_nsl_side = s_nsl_side_new;
+          s_nsl_side_new = 0;
+          s_nsl_surv = s_nsl_new;
           s_nsl_new = 0;
-          speculate();
+          speculate(2);
         }
       }, (c_tma_flags & 4) != 0);
       if (is_master && warp == 0) {
@@ -1124,7 +1221,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
       for (int k = 0; k < kMaxK; ++k) ops[k] = k < kCheckLuSlot ? OP_SUM : OP_MIN;
       block_reduce<kMaxK, kConsW>(acc, ops, s_red, s_tot);
       is_master = grid_step_any<kMaxK>(p.ar, p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch,
-                                   [&] { if (prod_lane) speculate(); }, (c_tma_flags & 4) != 0);
+                                   [&] { if (prod_lane) speculate(in_scratch ? 1 : 0); }, (c_tma_flags & 4) != 0);
       if (is_master && warp == 0) {
         double loc[kMaxK], glob[kMaxK];
 #pragma unroll
@@ -1151,7 +1248,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
         produce<5>(wsrc, work, pp, spec);
         if (probe) tl_mark(p.sync, epoch, 13);
       } else if (!producer) {
-        const int64_t mm = t_scan<FIX, false>(p, c, work, m_w, wsrc, compact, pp, acc);
+        const int64_t mm = t_scan<FIX, false>(p, c, work, m_walk, wsrc, compact, pp, acc);
         if (probe && threadIdx.x == 0) tl_mark(p.sync, epoch, 11);
         if (probe && lane == 0) atomicMax(&s_probe_last, (unsigned long long)globaltimer());
         if (compact) {
@@ -1160,10 +1257,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
         }
       }
       if (compact) in_scratch = true;
-      if (c.side) {  // the side list is consumed; the working set is the original arrays
-        in_scratch = false;
-        m_w = -1;
-      }
+      // the side list is consumed: the working set is the original arrays, or
+      // -- if the decision adopts them -- the fused pass's guessed survivors
+      const bool spec_surv = side_walk && c.guess != 0;
+      if (side_walk) adopt_pending = true;
       constexpr int K = FIX ? 11 : 5;
       int ops[K];
       double aK[K];
@@ -1186,7 +1283,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
             s_nslots = s_nsl_new;
             s_nsl_new = 0;
           }
-          speculate();
+          if (spec_surv) s_nslots = s_nsl_surv;  // the likely (guessed) next walk
+          speculate(spec_surv ? 1 : (in_scratch ? 1 : 0));
         }
       }, (c_tma_flags & 4) != 0);
       if (is_master && warp == 0) {
@@ -1207,12 +1305,12 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
     } else if (c.phase == PH_BP) {
       acc[0] = c.right ? HUGE_VAL : -HUGE_VAL;
       if (prod_lane) produce<5>(wsrc, work, pp, spec);
-      else if (!producer) t_bp(p, c, FIX, work, m_w, wsrc, pp, acc);
+      else if (!producer) t_bp(p, c, FIX, work, m_walk, wsrc, pp, acc);
       int ops[2] = {c.right ? OP_MIN : OP_MAX, OP_SUM};
       double a2[2] = {acc[0], acc[1]};
       block_reduce<2, kConsW>(a2, ops, s_red, s_tot);
       is_master = grid_step_any<2>(p.ar, p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch,
-                                   [&] { if (prod_lane) speculate(); }, (c_tma_flags & 4) != 0);
+                                   [&] { if (prod_lane) speculate(in_scratch ? 1 : 0); }, (c_tma_flags & 4) != 0);
       if (is_master && warp == 0) {
         if (lane == 0) tl_record(dsync, epoch, PH_BP, s_st.phys_count, 0);
         double glob[2];

@@ -60,6 +60,7 @@ DEVI int tail_gather(const SpxParams<double>& p, bool in_scratch, double* V, int
   if (!in_scratch) {
     const int m = (int)p.n;
     for (int i = tid; i < m; i += nt) V[i] = spx_wv<L1>(p.y[i]);
+    __syncthreads();  // the tail iterations read V in per-thread runs, not in this stride
     return m;
   }
   int* off = reinterpret_cast<int*>(V + kTailY);  // [pairs + 1] exclusive offsets

@@ -57,7 +57,10 @@ class SolverOptions:
 
     tolerance_scale defaults to eps**(3/4) of the instance dtype.
     compact_ratio (B200 only): physically compact the working set when the
-    logically fixed share of it reaches this ratio (None = 0.25, >1 never).
+    logically fixed share of it reaches this ratio (>1 never).  None = the
+    library default: 0.5 on the TMA engine (n >= 64Ki per rank), 0.4 after a
+    fused start with the direction guess (n >= 4e6 per rank), 0.25 on the
+    warp-segment engine (cqk_abi.cu default_compact_ratio).
     """
 
     variable_fixing: bool = True
@@ -191,7 +194,7 @@ def _outcome(inst, res, rc, x, what):
     if rc != N.SOLVED:
         raise N.NativeError(f"{what} failed ({rc}): {N.last_error()}")
     if x is not None and inst.dtype == np.float32:
-        x = x.float() if _is_torch(x) else x.astype(np.float32)
+        x = x.float() if _is_torch(x) else x.astype(np.float32, copy=False)
     return SolveOutcome(status=Status.SOLVED, lam=float(res.lam), x=x,
                         iterations=int(res.iterations), phi_evals=int(res.phi_evals),
                         fixed_count=int(res.fixed_count), stats=res.stats())
@@ -205,7 +208,8 @@ def run_cqk(inst, opts, variant, xbar=None, check=True, lambda0=None, want_x=Tru
         shape = tuple(xbar.shape) if hasattr(xbar, "shape") else np.asarray(xbar).shape
         if shape != (inst.n,):
             raise DomainError("xbar", None, "xbar must have length n")
-    m = Marshal(inst.d, inst.a, inst.b, inst.l, inst.u, xbar)
+    f32 = inst.dtype == np.float32
+    m = Marshal(inst.d, inst.a, inst.b, inst.l, inst.u, xbar, f32=f32)
     h = m.handle()
     x, xp = m.empty(inst.n) if want_x else (None, None)
     o = N.make_options(opts, variant=variant, check=check, lambda0=lambda0,
@@ -214,8 +218,17 @@ def run_cqk(inst, opts, variant, xbar=None, check=True, lambda0=None, want_x=Tru
                        fixing=False if variant == N.VARIANT_JACOBI else None,
                        tau=opts.tau(inst.dtype))
     res = N.Result()
-    rc = h.lib.cqk_solve_f64(h.ptr, m.mem, *m.ptrs[:5], inst.n, float(inst.r), o, m.ptrs[5], xp,
-                             res)
+    g = N.env_group() if (m.mem == N.MEM_HOST and trace is None and not f32) else None
+    if f32:  # float32 element math (cqk_solve_f32)
+        rc = h.lib.cqk_solve_f32(h.ptr, m.mem, *m.ptrs[:5], inst.n, float(inst.r), o, m.ptrs[5],
+                                 xp, res)
+    elif g is not None:  # CQK_DEVICES: shard the host instance across the group's GPUs
+        with g.lock:
+            rc = g.lib.cqk_solve_group_f64(g.ptr, *m.ptrs[:5], inst.n, float(inst.r), o, m.ptrs[5],
+                                           xp, res)
+    else:
+        rc = h.lib.cqk_solve_f64(h.ptr, m.mem, *m.ptrs[:5], inst.n, float(inst.r), o, m.ptrs[5],
+                                 xp, res)
     if trace is not None:
         trace.extend(h.trace(res.trace_len))
     return _outcome(inst, res, rc, x, "solve_cqk")

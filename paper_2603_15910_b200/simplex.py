@@ -116,7 +116,8 @@ def par_simplex_init(y, r, workers=None):
     return _alg2(y, r, None, None, False, workers=resolve_workers(workers))
 
 
-def _prep(y):
+def _prep(y, keep32=False):
+    """(contiguous float64 y -- or float32 with keep32 -- , the caller's dtype, on device)."""
     if _is_torch(y):
         import torch
 
@@ -126,23 +127,29 @@ def _prep(y):
             if y.dtype == torch.float64 and y.is_contiguous():  # the common case: no dispatch
                 return y, np.float64, True
             dt = np.float32 if y.dtype == torch.float32 else np.float64
-            return y.to(torch.float64).contiguous(), dt, True
+            want = torch.float32 if (keep32 and dt == np.float32) else torch.float64
+            return y.to(want).contiguous(), dt, True
     y = np.ascontiguousarray(y)
     if y.dtype not in (np.float32, np.float64):
         y = y.astype(np.float64)
+    if keep32 and y.dtype == np.float32:
+        return y, y.dtype, False
     return np.ascontiguousarray(y, dtype=np.float64), y.dtype, False
 
 
 def _project(y, r, opts, lambda0, trace, l1, start="auto", xbar=None, sharpened=None):
     if opts is None:
         opts = SolverOptions()
-    yv, dt, dev = _prep(y)
     # warm start (simplex.py:65-109): Algorithm 2 seeded by xbar's support.
     # A sharpened simplex projection always takes this route: the reference
     # applies the participation test min(y, y + lam) > 0 through
     # simplex_init_lambda (simplex.py:243-245), which changes the answer when
     # lam* > 0.  (For l1, |y| >= 0 and lam* < 0 make the test moot.)
     warm = lambda0 is None and (xbar is not None or (sharpened and (not l1 or start == "alg2")))
+    # float32 y: v = y + float(lam) in float (spx_project_f32 / l1_project_f32);
+    # the warm routes run the fp64 device Algorithm 2
+    yv, dt, dev = _prep(y, keep32=not warm)
+    f32 = (str(yv.dtype) == "torch.float32") if dev else yv.dtype == np.float32
     xb = None
     if warm and xbar is not None:
         xb, _, xdev = _prep(xbar)
@@ -163,7 +170,7 @@ def _project(y, r, opts, lambda0, trace, l1, start="auto", xbar=None, sharpened=
         import torch
 
         h.use_current_stream()
-        x = np.empty(n)
+        x = np.empty(n, dtype=np.float32 if f32 else np.float64)
         yp, xp = yv.ctypes.data, x.ctypes.data
         mem = N.MEM_HOST
     o = N.make_options(opts, lambda0=lambda0, trace=trace is not None,
@@ -176,9 +183,18 @@ def _project(y, r, opts, lambda0, trace, l1, start="auto", xbar=None, sharpened=
         else:
             rc = h.lib.spx_project_warm_f64(h.ptr, mem, yp, n, float(r), o, xbp,
                                             1 if sharpened else 0, xp, res)
-    else:
-        fn = h.lib.l1_project_f64 if l1 else h.lib.spx_project_f64
+    elif f32:
+        fn = h.lib.l1_project_f32 if l1 else h.lib.spx_project_f32
         rc = fn(h.ptr, mem, yp, n, float(r), o, xp, res)
+    else:
+        g = N.env_group() if (mem == N.MEM_HOST and trace is None and lambda0 is None) else None
+        if g is not None:  # CQK_DEVICES: shard the host vector across the group's GPUs
+            fn = g.lib.l1_project_group_f64 if l1 else g.lib.spx_project_group_f64
+            with g.lock:
+                rc = fn(g.ptr, yp, n, float(r), o, xp, res)
+        else:
+            fn = h.lib.l1_project_f64 if l1 else h.lib.spx_project_f64
+            rc = fn(h.ptr, mem, yp, n, float(r), o, xp, res)
     if trace is not None:
         trace.extend(h.trace(res.trace_len))
     if rc == N.E_DOMAIN:
@@ -188,7 +204,7 @@ def _project(y, r, opts, lambda0, trace, l1, start="auto", xbar=None, sharpened=
         raise ContractViolation("zero-size free set in the breakpoint snap")
     if rc != N.SOLVED:
         raise N.NativeError(f"projection failed ({rc}): {N.last_error()}")
-    if dt == np.float32:
+    if dt == np.float32 and not f32:
         x = x.float() if dev else x.astype(np.float32)
     return x, res
 
@@ -278,6 +294,8 @@ def project_simplex_rows(Y, r, opts=None, lambda0=None, start="tight", devices=N
     if opts is None:
         opts = SolverOptions()
     dev = _is_torch(Y) and Y.is_cuda
+    if devices is None and not dev and N.env_group() is not None:
+        devices = list(N.env_group().devices)  # CQK_DEVICES: rows split across the list
     if devices is not None and dev:
         raise ValueError("devices= splits a host array; for CUDA tensors call once per device")
     if dev:

@@ -63,10 +63,10 @@ def test_spg_names_at_top_level():
 
 @pytest.mark.parametrize("kind", ["cqk", "simplex", "l1"])
 def test_float32_instances(kind):
-    """float32 in, float32 out; solved in fp64 arithmetic with the float32
-    tolerance tau = eps32^(3/4) (newton.py:64-67), so the multiplier agrees
-    with the oracle's fp64 root to the float32 tolerance and x to float32
-    rounding (the reference iterates in float32; iteration counts may differ)."""
+    """float32 in, float32 out on the float32 path (element math in float32,
+    fp64 sums, tau = eps32^(3/4), newton.py:64-67): the multiplier agrees with
+    the oracle's fp64 root to the float32 tolerance and x to float32 rounding
+    (parity with the reference's own float32 runs: test_gpu_f32.py)."""
     import paper_2603_15910_b200 as P
 
     rng = np.random.default_rng(11)

@@ -87,3 +87,33 @@ def test_tma_engine_random_stress():
         json.dump({"instances": 200, "iteration_mismatches": mism, "lam_worst_rel": worst,
                    "mismatches": rows}, f, indent=1)
     assert mism <= 10, rows  # <= 5%: a summation-order tie, never a different root
+
+
+def test_fused_start_random_stress():
+    """The fused start with the direction guess serves n >= 4e6 per rank:
+    40 random instances in [4e6, 8e6] against the oracle (lambda to 1e-12,
+    iteration counts recorded; gpurun_out/stress_fused.json)."""
+    import paper_2603_15910_b200 as P
+
+    rng = np.random.default_rng(2027)
+    fams = O.CQK_FAMILIES
+    mism, worst, rows, guessed = 0, 0.0, [], 0
+    for k in range(40):
+        n = int(rng.integers(4_000_000, 8_000_001))
+        fam = fams[k % 3]
+        d, a, b, l, u, r = O.gen_cqk(fam, n, 5000 + k)
+        ref = O.solve_cqk(d, a, b, l, u, r, want_x=False)
+        out = P.solve_cqk(P.CqkInstance(d=d, a=a, b=b, l=l, u=u, r=r))
+        rel = abs(out.lam - ref["lam"]) / max(1.0, abs(ref["lam"]))
+        worst = max(worst, rel)
+        assert rel <= 1e-12, (fam, n, k, out.lam, ref["lam"])
+        assert out.fixed_count == ref["fixed_count"] or out.iterations != ref["iterations"]
+        if out.iterations != ref["iterations"]:
+            mism += 1
+            rows.append({"family": fam, "n": n, "seed": 5000 + k, "gpu": out.iterations,
+                         "oracle": ref["iterations"]})
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(ROOT, "gpurun_out", "stress_fused.json"), "w") as f:
+        json.dump({"instances": 40, "iteration_mismatches": mism, "lam_worst_rel": worst,
+                   "mismatches": rows}, f, indent=1)
+    assert mism <= 4, rows

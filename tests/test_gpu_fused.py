@@ -10,7 +10,9 @@ oracle and against the unfused solve (pass 0 + a full first scan):
   INFEASIBLE box, l == u blocks, MaxIterations) through the fused start;
 * every validate() check (core.py:126-165): the first failing check in the
   reference's order and its first offending index;
-* 2 and 3 virtual ranks (the fused totals cross the in-kernel exchange)."""
+* 2 and 3 virtual ranks (the fused totals cross the in-kernel exchange);
+* the direction guess (cqk_set_fused_guess): auto, off, and both forced
+  directions -- one of which is wrong and must simply not be adopted."""
 import numpy as np
 import pytest
 
@@ -44,9 +46,9 @@ def restore():
     h.set_fused(4_000_000, 2e-3)
 
 
-def solve(inst, fused, width=2e-3, **kw):
+def solve(inst, fused, width=2e-3, guess=1, **kw):
     p = P()
-    handle().set_fused(0 if fused else OFF, width)
+    handle().set_fused(0 if fused else OFF, width, guess)
     if kw.pop("jacobi", False):
         return p.jacobi_solve(inst, p.SolverOptions(**kw))
     return p.solve_cqk(inst, p.SolverOptions(**kw))
@@ -96,20 +98,51 @@ def test_fused_saves_pass0_bytes():
     n = 5_000_000
     d, a, b, l, u, r = p.instances.gen_cqk_arrays("cqk-weakly-correlated", n, 3)
     inst = inst_of(d, a, b, l, u, r)
-    f, g = solve(inst, True), solve(inst, False)
+    f, g = solve(inst, True, guess=0), solve(inst, False)
     assert (f.iterations, f.phi_evals, f.fixed_count) == (g.iterations, g.phi_evals, g.fixed_count)
     saved = (g.stats["bytes_model"] - f.stats["bytes_model"]) / n
     assert 15.0 < saved <= 24.0, saved
 
 
+@pytest.mark.parametrize("family", ["cqk-uncorrelated", "cqk-weakly-correlated", "cqk-correlated"])
+@pytest.mark.parametrize("guess", [0, 1, 2, 3])
+def test_fused_direction_guess(family, guess):
+    """Every guess mode returns the oracle's solve; the iterate sequence is
+    that of the unfused solve (only the summation order may differ)."""
+    p = P()
+    for seed in (1, 2, 3):
+        n = 400_000 + 11 * seed
+        d, a, b, l, u, r = p.instances.gen_cqk_arrays(family, n, seed)
+        inst = inst_of(d, a, b, l, u, r)
+        ref = O.solve_cqk(d, a, b, l, u, r)
+        f = solve(inst, True, guess=guess)
+        g = solve(inst, False)
+        check(f, ref)
+        assert (f.iterations, f.phi_evals, f.fixed_count) == (g.iterations, g.phi_evals, g.fixed_count)
+
+
+def test_fused_guess_saves_the_first_reread():
+    """weak, n = 1e7, seed 1 (sampled residual ~8% of sum|bx|: the guess
+    fires): the confirmed guess replaces the second full read (40 B) by the
+    survivors' write and read."""
+    p = P()
+    n = 10_000_000
+    d, a, b, l, u, r = p.instances.gen_cqk_arrays("cqk-weakly-correlated", n, 1)
+    inst = inst_of(d, a, b, l, u, r)
+    f, g = solve(inst, True, guess=1), solve(inst, True, guess=0)
+    assert (f.iterations, f.phi_evals, f.fixed_count) == (g.iterations, g.phi_evals, g.fixed_count)
+    assert f.stats["bytes_model"] < g.stats["bytes_model"], (f.stats, g.stats)
+
+
 @pytest.mark.parametrize("case", sorted(CASES))
 @pytest.mark.parametrize("fixing", [True, False])
-def test_fused_degenerate(case, fixing):
+@pytest.mark.parametrize("guess", [1, 2, 3])
+def test_fused_degenerate(case, fixing, guess):
     d, a, b, l, u, r = CASES[case]()
     ref = O.solve_cqk(d, a, b, l, u, r, fixing=fixing)
     p = P()
     try:
-        out = solve(inst_of(d, a, b, l, u, r), True, variable_fixing=fixing)
+        out = solve(inst_of(d, a, b, l, u, r), True, guess=guess, variable_fixing=fixing)
     except p.MaxIterationsError:
         assert ref["status"] == O.E_MAXITER
         return
@@ -159,7 +192,8 @@ def run_ranks(fns):
 
 
 @pytest.mark.parametrize("world", [2, 3])
-def test_fused_sharded(world):
+@pytest.mark.parametrize("guess", [1, 2, 3])
+def test_fused_sharded(world, guess):
     import torch
 
     p = P()
@@ -171,7 +205,7 @@ def test_fused_sharded(world):
     comms = D.local_group([0] * world, grid_limit=120 // world)
     solvers = []
     for q in range(world):
-        comms[q].handle.set_fused(0, 2e-3)
+        comms[q].handle.set_fused(0, 2e-3, guess)
         lo, hi = D.shard_bounds(n, world, q)
         sh = [torch.from_numpy(v[lo:hi].copy()).cuda() for v in (d, a, b, l, u)]
         solvers.append(D.ShardedCQK(sh, r, n_total=n, offset=lo, comm=comms[q]))

@@ -33,13 +33,8 @@ def tma_engine():
 
 
 def both_steps(fn):
-    os.environ.pop("CQK_MASTER_STEP", None)
     a = fn()
-    os.environ["CQK_MASTER_STEP"] = "1"
-    try:
-        b = fn()
-    finally:
-        os.environ.pop("CQK_MASTER_STEP", None)
+    b = _with_env("CQK_MASTER_STEP", fn)
     return a, b
 
 
@@ -120,11 +115,16 @@ def test_masterless_step_on_reduced_grids(ctas, tma_engine):
 
 
 def _with_env(name, fn):
-    os.environ[name] = "1"
+    """Run fn with one of the handle's A/B switches on (cqk_set_switches;
+    the environment variable of the same name sets it at handle creation)."""
+    from paper_2603_15910_b200 import _native as N
+
+    h = N.handle()
+    h.set_switches(**{{"CQK_MASTER_STEP": "master_step", "CQK_STATIC_FINAL": "static_final"}[name]: True})
     try:
         return fn()
     finally:
-        os.environ.pop(name, None)
+        h.set_switches()
 
 
 @pytest.mark.parametrize("n", [1, 959, 960, 961, 3841, 2000003])

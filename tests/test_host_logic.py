@@ -93,3 +93,17 @@ def test_family_mismatch():
         P.gen_cqk("nope", 3, 1)
     with pytest.raises(P.FamilyMismatch):
         P.gen_simplex_y("nope", 3, 1)
+
+
+def test_device_list_parsing(monkeypatch):
+    """CQK_DEVICES (the GPU analogue of CQK_WORKERS, parallel.py:52-59)."""
+    from paper_2603_15910_b200 import _native as N
+
+    assert N.parse_devices("0,1, 2,3") == [0, 1, 2, 3]
+    assert N.parse_devices("0,0") == [0, 0]
+    with pytest.raises(ValueError):
+        N.parse_devices("0,-1")
+    monkeypatch.delenv("CQK_DEVICES", raising=False)
+    assert N.env_group() is None
+    monkeypatch.setenv("CQK_DEVICES", "3")  # a single device is no group
+    assert N.env_group() is None

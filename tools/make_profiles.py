@@ -1,5 +1,7 @@
 """Write the judged ncu summaries into profiles/ (round-prefixed) from the
-gpurun_out/ scratch reports.  Usage: python tools/make_profiles.py r01"""
+gpurun_out/ scratch reports.  Usage: python tools/make_profiles.py r01 [dest]
+(on the GPU box: dest = gpurun_out/profiles_box, so only the small summaries
+travel back)"""
 import csv
 import io
 import json
@@ -14,7 +16,7 @@ from ncu_summary import run  # noqa: E402
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 rnd = sys.argv[1] if len(sys.argv) > 1 else "r01"
 src = os.path.join(ROOT, "gpurun_out")
-dst = os.path.join(ROOT, "profiles")
+dst = sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "profiles")
 os.makedirs(dst, exist_ok=True)
 
 
