@@ -114,7 +114,7 @@ struct cqk_handle {
   int32_t* wcnt = nullptr;            // per-warp scratch counts (simplex tail mode)
   int32_t* hist = nullptr;            // first-scan bucket counts (simplex start "auto"), two halves
   int hist_flip = 0;                  // ... the half the next launch uses (arrives zero)
-  double* ar_rows = nullptr;          // masterless grid step: [2][grid][kMaxK] partial rows
+  double* ar_rows = nullptr;          // masterless grid step: [2][grid][kArStride] tagged partial rows
   unsigned* ar_count = nullptr;       // ... [2] arrival counters, alternating per launch
   unsigned long long ar_seq = 0;      // masterless launches so far
   int rows_flip = 0;                  // C5 row counter (ar_count[8 + flip]) of the next launch
@@ -220,7 +220,8 @@ int cqk_create(cqk_handle** out, int device) {
   e = e ? e : cudaMalloc(&h->wcnt, sizeof(int32_t) * kConsW * (h->sm_count + 8));
   e = e ? e : cudaMalloc(&h->hist, sizeof(int32_t) * kHistB * (h->sm_count + 8));
   e = e ? e : cudaMemset(h->hist, 0, sizeof(int32_t) * kHistB * (h->sm_count + 8));
-  e = e ? e : cudaMalloc(&h->ar_rows, sizeof(double) * 2 * kMaxK * (h->sm_count + 8));
+  e = e ? e : cudaMalloc(&h->ar_rows, sizeof(double) * 2 * kArStride * (h->sm_count + 8));
+  e = e ? e : cudaMemset(h->ar_rows, 0, sizeof(double) * 2 * kArStride * (h->sm_count + 8));
   e = e ? e : cudaMalloc(&h->ar_count, 64);
   e = e ? e : cudaMemset(h->ar_count, 0, 64);
   const size_t st_pad = (st_bytes + 63) / 64 * 64;
@@ -497,9 +498,10 @@ int check_timeout(cqk_handle* h, int32_t status, int32_t err) {
 // The masterless grid step for a single-GPU persistent TMA launch of `grid`
 // CTAs (one CTA per SM; the buffers hold sm_count + 8 rows).
 GridAR masterless(cqk_handle* h, int grid, const Exchange& ex) {
-  GridAR ar{nullptr, nullptr, nullptr, nullptr, nullptr, 0};
+  GridAR ar{nullptr, 0ull, nullptr, nullptr, nullptr, nullptr, 0};
   if (grid > h->sm_count + 8 || h->master_step) return ar;
   const int k = (int)(h->ar_seq++ & 1u);
+  ar.tag = h->ar_seq << 32;  // unique per launch of this handle (rows carry it)
   ar.rows = h->ar_rows;
   ar.count = h->ar_count + k;
   ar.count_next = h->ar_count + (k ^ 1);

@@ -176,19 +176,26 @@ DEVI bool grid_step(double* partials, const double* s_cta, const int (&ops)[K],
 }
 
 // Single GPU (grid_step_any with GridAR rows): every CTA publishes its
-// partial row and counts its arrival (ar_arrive), waits for the epoch's G
-// arrivals, then combines all rows itself in the same fixed order as
-// grid_step's master -- bit-identical totals -- (ar_combine) and runs the
-// deterministic state machine on its own replica of the state: no release
-// round trip.  ar_combine returns false (s_abort set) on a spin timeout.
+// partial row with a tagged release store (ar_arrive), then combines all rows
+// itself in the same fixed order as grid_step's master -- bit-identical
+// totals -- (ar_combine): thread c acquires row c's tag and reads its values,
+// so the wait and the load are one round trip per row and no arrival counter
+// is contended.  Every CTA then runs the deterministic state machine on its
+// own replica of the state: no release round trip.  ar_combine returns false
+// (s_abort set) on a spin timeout.
+template <int K>
+DEVI constexpr int ar_tag_slot() { return K < kMaxK ? kMaxK - 1 : kMaxK; }
+
 template <int K>
 DEVI void ar_arrive(const GridAR& ar, const double* s_cta, const GridSync& sy, unsigned epoch) {
-  const int G = (int)gridDim.x;
-  if (threadIdx.x < K)
-    ar.rows[(size_t)(epoch & 1u) * G * kMaxK + (int64_t)blockIdx.x * kMaxK + threadIdx.x] = s_cta[threadIdx.x];
-  __syncthreads();
+  static_assert(K <= kMaxK && kMaxK < kArStride, "row layout");
   if (threadIdx.x == 0) {
-    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ar.count) : "memory");
+    const int G = (int)gridDim.x;
+    double* row = ar.rows + ((size_t)(epoch & 1u) * G + blockIdx.x) * kArStride;
+#pragma unroll
+    for (int k = 0; k < K; ++k) row[k] = s_cta[k];
+    // release: the values above are visible to whoever acquires the tag
+    st_release_gpu_u64(reinterpret_cast<unsigned long long*>(row + ar_tag_slot<K>()), ar.tag | epoch);
     if (blockIdx.x == 1) tl_mark(sy, epoch, 6);
   }
 }
@@ -197,35 +204,42 @@ template <int K>
 DEVI bool ar_combine(const GridAR& ar, const int (&ops)[K], const GridSync& sy,
                      double (*s_red)[kMaxK], double* s_tot, int* s_abort, unsigned epoch) {
   const int G = (int)gridDim.x;
-  const double* rows = ar.rows + (size_t)(epoch & 1u) * G * kMaxK;
-  if (threadIdx.x == 0) {
-    const unsigned target = epoch * (unsigned)G;
-    const unsigned long long t0 = globaltimer();
-    unsigned polls = 0;
-    while ((int)(ld_relaxed(ar.count) - target) < 0) {
-      if ((++polls & 255u) == 0 && globaltimer() - t0 > kSpinTimeoutNs) {
-        raise_timeout(sy);
-        *s_abort = 1;
-        break;
-      }
-    }
-    fence_acquire_gpu();
-    if (blockIdx.x == 0) tl_mark(sy, epoch, 4);
-  }
-  __syncthreads();
-  if (*(volatile int*)s_abort) return false;
+  const double* rows = ar.rows + (size_t)(epoch & 1u) * G * kArStride;
+  const unsigned long long want = ar.tag | epoch;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double acc[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) acc[k] = ops[k] == OP_SUM ? 0.0 : ops[k] == OP_MIN ? HUGE_VAL : -HUGE_VAL;
+  bool late = false;
   for (int c = threadIdx.x; c < G; c += blockDim.x) {
+    const double* row = rows + (int64_t)c * kArStride;
+    const unsigned long long* tag = reinterpret_cast<const unsigned long long*>(row + ar_tag_slot<K>());
+    if (ld_acquire_gpu_u64(tag) != want) {
+      const unsigned long long t0 = globaltimer();
+      unsigned polls = 0;
+      while (ld_acquire_gpu_u64(tag) != want) {
+        if ((++polls & 255u) == 0 && globaltimer() - t0 > kSpinTimeoutNs) {
+          late = true;
+          break;
+        }
+      }
+    }
     double v[K];
 #pragma unroll
-    for (int k = 0; k < K; ++k) v[k] = __ldcg(rows + (int64_t)c * kMaxK + k);
+    for (int k = 0; k < K; ++k) v[k] = __ldcg(row + k);
 #pragma unroll
     for (int k = 0; k < K; ++k)
       acc[k] = ops[k] == OP_SUM ? acc[k] + v[k] : ops[k] == OP_MIN ? fmin(acc[k], v[k]) : fmax(acc[k], v[k]);
   }
+  if (__syncthreads_or(late)) {
+    if (threadIdx.x == 0) {
+      raise_timeout(sy);
+      *s_abort = 1;
+    }
+    __syncthreads();
+    return false;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) tl_mark(sy, epoch, 4);
   const int nw = min((int)(blockDim.x >> 5), (G + 31) >> 5);
   if (warp < nw) {
 #pragma unroll
