@@ -250,13 +250,16 @@ int cqk_set_engine(cqk_handle *h, int mode);
    rounding (lambda0's terms share the division's reciprocal). */
 int cqk_set_fused(cqk_handle *h, int64_t min_n, double half_width);
 /* Direction guess of the fused start (fixing solves, default 1 = auto,
-   CQK_FUSED_GUESS): a second sample pass estimates the sign of
-   phi(lambda0) - r, i.e. which bound the first Newton iteration fixes
-   (newton.py:165-206); the fused pass then also writes every element that
-   fixing would not drop, and when the side scan confirms the direction those
-   survivors become the working set (the first full re-read is avoided).
-   0 off, 2 / 3 force +1 / -1 (tests: a wrong guess is simply not adopted).
-   Results agree with mode 0 to rounding (summation order differs). */
+   CQK_FUSED_GUESS; from 8e6 elements per rank): the sample tiles carry all
+   five arrays and stay in shared memory; once the estimate is known each CTA
+   evaluates phi there over its own sample and, when its estimate of
+   phi(lambda0) - r is decisive, guesses which bound the first Newton
+   iteration fixes (newton.py:165-206).  The fused pass then also writes that
+   CTA's elements the fixing would not drop; when the side scan confirms the
+   direction, the CTAs that guessed it adopt those survivors as their working
+   set (the first full re-read is avoided).  0 off, 2 / 3 force +1 / -1 in
+   every CTA (tests: a wrong guess is simply not adopted).  Results agree with
+   mode 0 to rounding (summation order differs). */
 int cqk_set_fused_guess(cqk_handle *h, int mode);
 /* A/B switches of the persistent kernels (defaults 0 = the measured best;
    the environment variables of the same names set them at cqk_create):

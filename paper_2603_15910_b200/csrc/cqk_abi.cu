@@ -458,16 +458,16 @@ int stage_inputs(cqk_handle* h, int mem, int64_t n, const T* const* in, int coun
 // families (n = 1e8): with the TMA engine 0.5 streams 2-5% fewer bytes and is
 // fastest (weak 3.99 -> 3.88 ms, corr 4.26 -> 3.88 ms); the warp-segment
 // engine (small n) keeps 0.25.
-// After a fused start with the direction guess the working set is already
-// the guessed survivors, and 0.4 compacts them once more (tools/policy_ab.py,
+// Once the direction guess's survivors are adopted the working set is
+// already compacted once, and 0.4 compacts it once more (tools/policy_ab.py,
 // 36 instances 5e6..1e8: 0.4 the best mean, 0.5 leaves C3 weak seed 1
-// uncompacted at 3.36 ms against 3.23).
-double default_compact_ratio(bool tma = false, bool guessed = false) {
+// uncompacted at 3.36 ms against 3.23); without adoption 0.5 stays.
+double default_compact_ratio(bool tma = false, bool adopted = false) {
   static double v = [] {
     const char* e = getenv("CQK_COMPACT_RATIO");
     return e ? atof(e) : -1.0;
   }();
-  return v >= 0 ? v : (tma ? (guessed ? 0.4 : 0.5) : 0.25);
+  return v >= 0 ? v : (tma ? (adopted ? 0.4 : 0.5) : 0.25);
 }
 
 bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
@@ -784,8 +784,9 @@ static int solve_impl(cqk_handle* h, int mem, const T* d, const T* a, const T* b
   // the forced modes (tests) apply at any size
   const int guess = !(fused && fixing) ? 0
                     : (h->fused_guess >= 2 || per_rank >= cqk_handle::kGuessMinN) ? h->fused_guess : 0;
-  s.compact_ratio = std::isnan(opts.compact_ratio) ? default_compact_ratio(tma, guess != 0)
-                                                   : opts.compact_ratio;
+  s.compact_ratio = std::isnan(opts.compact_ratio) ? default_compact_ratio(tma) : opts.compact_ratio;
+  s.compact_ratio_adopt =
+      std::isnan(opts.compact_ratio) ? default_compact_ratio(tma, true) : opts.compact_ratio;
   if (fused) {
     s.fused = 1;
     s.fused_guess = guess;

@@ -37,7 +37,7 @@ enum Phase : int32_t {
   PH_SNAP = 6,   // simplex: max(-y[free]) snap (simplex.py:276-281)
   PH_SAMPLE = 7, // fused start: lambda0 estimated from sample tiles
   PH_FUSED = 8,  // fused start: lambda0 sums + validate + the first scan's aggregates
-  PH_SAMPLE2 = 9, // fused start: phi at the estimate over the sample tiles (direction guess)
+  PH_GUESS = 9,  // fused start: phi at the estimate over the kept sample tiles (direction guess)
 };
 
 enum Status : int32_t {
@@ -66,9 +66,10 @@ struct Cmd {
   int32_t live_hi;  // ... an upper-fixed one
   int32_t hist;     // simplex: this scan also histograms t > 0 (start "auto")
   int32_t side;     // this scan runs over the fused pass's side list (plus its aggregates)
-  int32_t guess;    // fused start: +1 lower / -1 upper fixing expected at lambda0, 0 unknown;
-                    // the fused pass then also writes the elements that would survive it
-  int32_t adopt;    // the side scan confirmed the guess: those survivors are the working set
+  int32_t guess;    // fused start: the fixing direction (+1 lower, -1 upper) expected at
+                    // lambda0 -- the fused pass then also writes the elements it would keep
+  int32_t adopt;    // after the side scan: the direction taken at lambda0 when it is the
+                    // guessed one -- the survivors become the working set; 0 none
   int32_t pad_[2];
 };
 
@@ -96,7 +97,10 @@ struct CqkState {
   double agg_lo_loc, agg_hi_loc;  // their lower / upper at-bound counts on this rank
   int64_t side_local;       // elements in this rank's side list
   int64_t elems_sample;     // sample elements read (24 B each)
-  int64_t surv_local;       // elements the fused pass wrote as the guessed survivors
+  int64_t surv_local;       // elements the fused pass wrote as guessed survivors (this rank)
+  double rem_plus, rem_minus;          // elements the +1 / -1 guessing CTAs left out (all ranks)
+  double rem_plus_loc, rem_minus_loc;  // ... of this rank
+  double compact_ratio_adopt;          // compact_ratio once the survivors are adopted
 };
 
 template <typename T>
@@ -234,15 +238,18 @@ DEVI void m_after_scan(CqkState& s, const double* tot, const double* loc, double
         else s.cmd.fix_lo = lam;
       }
     }
-    // fused start: the fused pass dropped every element it classified as
-    // fixed in the guessed direction (t < l on the whole interval for +1);
-    // if that is the direction just taken, they are all fixed now and the
-    // rest is the working set.  Fixed-but-present elements (side-list ones
-    // with t == l, ...) stay under the live fixed tests (fhi_phys unchanged).
-    if (side_scan && s.cmd.guess != 0 && dir == s.cmd.guess) {
-      s.fixed_removed += (int64_t)(dir > 0 ? s.agg_lo_loc : s.agg_hi_loc);
-      s.phys_count = s.surv_local;
-      s.cmd.adopt = 1;
+    // fused start: with the guess g the fused pass left every element it
+    // classified as fixed in that direction (t < l on the whole interval for
+    // +1) out of the survivor lists; if g is the direction just taken, those
+    // are all fixed now and the survivors are the working set.
+    // Fixed-but-present elements (side-list ones with t == l, ...) stay
+    // under the live fixed tests (fhi_phys unchanged).
+    if (side_scan && s.cmd.guess == dir && dir != 0 && (dir > 0 ? s.rem_plus : s.rem_minus) > 0) {
+      const int64_t rem = (int64_t)(dir > 0 ? s.rem_plus_loc : s.rem_minus_loc);
+      s.fixed_removed += rem;
+      s.phys_count -= rem;
+      s.cmd.adopt = dir;
+      s.compact_ratio = s.compact_ratio_adopt;
     }
   }
   s.cmd.guess = 0;
@@ -335,9 +342,13 @@ DEVI void m_after_lambda0(CqkState& s, const double* tot) {
 
 // Fused start.  The sample pass: tot 0 sum b a/d, 1 sum b^2/d, 2 elements
 // over the sample tiles -> the estimated lambda0 and the half-width of the
-// interval the fused pass classifies against.
+// interval the fused pass classifies against.  With the direction guess
+// (fixing solves) the sample tiles carry all five arrays (40 B per sampled
+// element) and stay in shared memory for the guess epoch (m_after_guess).
 DEVI void m_after_sample(CqkState& s, const double* tot, double local_count) {
-  s.elems_sample += (int64_t)local_count;
+  const bool guess = s.fixing && s.fused_guess;
+  if (guess) s.elems_scan += (int64_t)local_count;
+  else s.elems_sample += (int64_t)local_count;
   const double scale = (double)s.n / fmax(tot[2], 1.0);
   const double est = (s.r_orig - tot[0] * scale) / (tot[1] * scale);
   s.cmd.lam = est;
@@ -345,27 +356,28 @@ DEVI void m_after_sample(CqkState& s, const double* tot, double local_count) {
   // lambda0 on the generator families)
   s.cmd.edge = isfinite(est) ? s.fused_width * fabs(est) : 0.0;
   s.cmd.guess = 0;
-  s.cmd.phase = (s.fixing && s.fused_guess) ? PH_SAMPLE2 : PH_FUSED;
+  s.cmd.phase = guess ? PH_GUESS : PH_FUSED;
 }
 
-// The second sample pass (fixing only): tot 0 sum b x(est), 1 sum (b x)^2,
-// 2 elements, 3 sum |b x| over the same sample tiles -> the sign of
+// The guess epoch: tot 0 sum b x, 1 sum (b x)^2, 2 elements, 3 sum |b x| at
+// the estimate over the kept sample tiles (no memory traffic) -> the sign of
 // phi(lambda0) - r, i.e. which bound the first iteration will fix
-// (newton.py:165-206), when the sampled estimate is clear of r by six
-// standard errors.  The survivor list pays only if several scans follow
-// it, and a small initial residual means a short solve (C2 families:
+// (newton.py:165-206), when the sampled estimate is clear of zero by six
+// standard errors.  The survivor list pays only if several scans follow it,
+// and a small initial residual means a short solve (C2 families:
 // |phi(lambda0) - r| / sum|b x| of 1e-3 .. 2e-2 took 3-4 phi evaluations,
-// 3e-2 .. 9e-2 took 5-7), so it is written only above kGuessResid.  A wrong
-// or missing guess costs bytes only: the list is then simply not adopted.
+// 3e-2 .. 9e-2 took 5-7), so the list is written only above kGuessResid.
+// The decision is global: a working set adopted by only some CTAs would leave
+// the others streaming their whole tiles (static tile ownership).  A wrong or
+// missing guess costs bytes only: the list is then simply not adopted.
 constexpr double kGuessResid = 0.025;
-DEVI void m_after_sample2(CqkState& s, const double* tot, double local_count) {
-  s.elems_scan += (int64_t)local_count;  // 40 B per sampled element
+DEVI void m_after_guess(CqkState& s, const double* tot) {
   const double m = fmax(tot[2], 1.0), N = (double)s.n;
   const double mean = tot[0] / m;
   const double var = fmax(tot[1] / m - mean * mean, 0.0);
   const double diff = N * mean - s.r_orig, se = N * sqrt(var / m), scale = N * tot[3] / m;
-  const bool clear = fabs(diff) > 6.0 * se && fabs(diff) > kGuessResid * scale;
-  s.cmd.guess = clear && isfinite(diff) ? (diff > 0 ? 1 : -1) : 0;
+  const bool clear = fabs(diff) > 6.0 * se && fabs(diff) > kGuessResid * scale && isfinite(diff);
+  s.cmd.guess = clear ? (diff > 0 ? 1 : -1) : 0;
   if (s.fused_guess >= 2) s.cmd.guess = s.fused_guess == 2 ? 1 : -1;  // forced (tests)
   s.cmd.phase = PH_FUSED;
 }
@@ -374,9 +386,9 @@ DEVI void m_after_sample2(CqkState& s, const double* tot, double local_count) {
 // terms and order as pass 0), 2 the first failing validate() check as
 // class * 2^40 + index (min), 3..5 lower at-bound (sum bl, sum |bl|, count),
 // 6..8 upper at-bound, 9 / 10 interior with t >= 0 (sum b^2/d, sum b a/d),
-// 11 / 12 interior with t <= 0 (unused: such elements go to the side list),
-// 13 side-list elements, 14 guessed survivors written (cmd.guess != 0).
-// loc: this rank's vector.
+// 11 / 12 elements left out of the survivor lists by the CTAs guessing +1
+// (their below elements) / -1 (above), 13 side-list elements, 14 survivors
+// written.  loc: this rank's vector.
 constexpr int kFusedK = 15;
 constexpr double kVKey = 1099511627776.0;  // 2^40
 DEVI void m_after_fused(CqkState& s, const double* tot, const double* loc) {
@@ -399,11 +411,15 @@ DEVI void m_after_fused(CqkState& s, const double* tot, const double* loc) {
   s.cmd.phase = PH_SCAN;
   s.cmd.check_lu = 0;
   s.cmd.edge = 0.0;
+  s.rem_plus = tot[11];
+  s.rem_minus = tot[12];
+  s.rem_plus_loc = loc[11];
+  s.rem_minus_loc = loc[12];
   if (ia <= lam && lam <= ib) {  // the classification holds at lambda0: scan the side list only
-    const double pos = lam * tot[9] + tot[10], neg = lam * tot[11] + tot[12];
-    s.agg[0] = tot[3] + tot[6] + pos + neg;
-    s.agg[1] = tot[4] + tot[7] + pos - neg;
-    s.agg[2] = tot[9] + tot[11];
+    const double pos = lam * tot[9] + tot[10];
+    s.agg[0] = tot[3] + tot[6] + pos;
+    s.agg[1] = tot[4] + tot[7] + pos;
+    s.agg[2] = tot[9];
     s.agg[3] = s.agg[4] = 0.0;  // no exact tie outside the side list
     for (int k = 0; k < 3; ++k) {
       s.agg[5 + k] = tot[3 + k];

@@ -720,26 +720,30 @@ DEVI void produce_sample(const Src src, int64_t n, int64_t ntiles, TPipe& pp) {
   }
 }
 
-// acc 0 sum b a/d, 1 sum b^2/d, 2 elements (t_lambda0's per-element terms)
+// acc 0 sum b a/d, 1 sum b^2/d, 2 elements (t_lambda0's per-element terms).
+// KEEP (direction guess): the tiles stay in their stages (no release) for the
+// CTA's guess at the start of the fused pass (t_sample_guess).
+template <int ST = kStages3, int STRIDE = kStride3, bool KEEP = false>
 DEVI void t_sample(const CqkParams<double>& p, int64_t ntiles, TPipe& pp, double (&acc)[kMaxK]) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  static_assert(!KEEP || ST >= kSampleTiles, "kept sample tiles must fit the pipeline");
   for (int k = 0; k < kSampleTiles; ++k) {
     const int64_t t = sample_tile(ntiles, k);
     if (t < 0) break;
-    const int s = pp.pc % kStages3;
+    const int s = pp.pc % ST;
     WTile wt;
-    wt.sm = pp.buf + (size_t)s * kStride3 + kSeg * warp;
+    wt.sm = pp.buf + (size_t)s * STRIDE + kSeg * warp;
     wt.gbase = t * kTileC + kSeg * warp;
     const int64_t left = p.n - wt.gbase;
     wt.wcnt = left <= 0 ? 0 : (left < kSeg ? (int)left : kSeg);
     wt.patch = (wt.wcnt & 1) && wt.wcnt < kSeg;
     wt.q = k;
-    mbar_wait_s(pp.full + 8 * s, (pp.pc / kStages3) & 1);
+    mbar_wait_s(pp.full + 8 * s, (pp.pc / ST) & 1);
     if (wt.wcnt > 0) {
       double D[kEptC], A[kEptC], B[kEptC];
-      tile_load(wt, 0, p.d, D, 1.0);
-      tile_load(wt, 1, p.a, A);
-      tile_load(wt, 2, p.b, B, 1.0);
+      tile_load<false, kTileC>(wt, 0, p.d, D, 1.0);
+      tile_load<false, kTileC>(wt, 1, p.a, A);
+      tile_load<false, kTileC>(wt, 2, p.b, B, 1.0);
 #pragma unroll
       for (int j = 0; j < kEptC; ++j) {
         if (e_loc(lane, j) >= wt.wcnt) continue;
@@ -750,21 +754,27 @@ DEVI void t_sample(const CqkParams<double>& p, int64_t ntiles, TPipe& pp, double
       }
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive_s(pp.empty + 8 * s);
+    if (!KEEP && lane == 0) mbar_arrive_s(pp.empty + 8 * s);
     ++pp.pc;
   }
 }
 
-// The second sample pass (fixing solves): phi's sum b x at the estimate
-// over the same sample tiles (all five arrays), for the direction guess.
-// acc 0 sum b x, 1 sum (b x)^2, 2 elements, 3 sum |b x|
-DEVI void t_sample2(const CqkParams<double>& p, double lam, int64_t ntiles, TPipe& pp,
-                    double (&acc)[kMaxK]) {
+
+
+
+
+DEVI int sample_count(int64_t ntiles) {
+  int k = 0;
+  while (k < kSampleTiles && sample_tile(ntiles, k) >= 0) ++k;
+  return k;
+}
+DEVI void t_sample_guess(const CqkParams<double>& p, double lam, int64_t ntiles, const TPipe& pp,
+                         double (&acc)[4]) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int k = 0; k < kSampleTiles; ++k) {
+  const int ns = sample_count(ntiles);
+  for (int k = 0; k < ns; ++k) {
     const int64_t t = sample_tile(ntiles, k);
-    if (t < 0) break;
-    const int s = pp.pc % kStagesC;
+    const int s = (pp.pc - ns + k) % kStagesC;
     WTile wt;
     wt.sm = pp.buf + (size_t)s * kStageElemsC + kSeg * warp;
     wt.gbase = t * kTileC + kSeg * warp;
@@ -772,29 +782,30 @@ DEVI void t_sample2(const CqkParams<double>& p, double lam, int64_t ntiles, TPip
     wt.wcnt = left <= 0 ? 0 : (left < kSeg ? (int)left : kSeg);
     wt.patch = (wt.wcnt & 1) && wt.wcnt < kSeg;
     wt.q = k;
-    mbar_wait_s(pp.full + 8 * s, (pp.pc / kStagesC) & 1);
-    if (wt.wcnt > 0) {
-      double D[kEptC], A[kEptC], B[kEptC], L[kEptC], U[kEptC];
-      tile_load(wt, 0, p.d, D, 1.0);
-      tile_load(wt, 1, p.a, A);
-      tile_load(wt, 2, p.b, B, 1.0);
-      tile_load(wt, 3, p.l, L);
-      tile_load(wt, 4, p.u, U);
+    if (wt.wcnt <= 0) continue;
+    double D[kEptC], A[kEptC], B[kEptC], L[kEptC], U[kEptC];
+    tile_load(wt, 0, p.d, D, 1.0);
+    tile_load(wt, 1, p.a, A);
+    tile_load(wt, 2, p.b, B, 1.0);
+    tile_load(wt, 3, p.l, L);
+    tile_load(wt, 4, p.u, U);
 #pragma unroll
-      for (int j = 0; j < kEptC; ++j) {
-        if (e_loc(lane, j) >= wt.wcnt) continue;
-        const double x = clip(div_rn(add_rn(mul_rn(B[j], lam), A[j]), D[j]), L[j], U[j]);
-        const double bx = mul_rn(B[j], x);
-        acc[0] += bx;
-        acc[1] += bx * bx;
-        acc[2] += 1.0;
-        acc[3] += fabs(bx);
-      }
+    for (int j = 0; j < kEptC; ++j) {
+      if (e_loc(lane, j) >= wt.wcnt) continue;
+      const double x = clip(div_rn(add_rn(mul_rn(B[j], lam), A[j]), D[j]), L[j], U[j]);
+      const double bx = mul_rn(B[j], x);
+      acc[0] += bx;
+      acc[1] += bx * bx;
+      acc[2] += 1.0;
+      acc[3] += fabs(bx);
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive_s(pp.empty + 8 * s);
-    ++pp.pc;
   }
+}
+DEVI void release_sample(int64_t ntiles, const TPipe& pp) {
+  const int ns = sample_count(ntiles);
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0)
+    for (int k = 0; k < ns; ++k) mbar_arrive_s(pp.empty + 8 * ((pp.pc - ns + k) % kStagesC));
 }
 
 // Append the elements with keep[j] of this warp's tile (values from the held
@@ -929,11 +940,10 @@ DEVI void fused_tile(const CqkParams<double>& p, const WTile& wt, const Src& src
 // Returns this warp's side-list count; *surv_m its survivor count.
 template <bool CHECK>
 DEVI int64_t t_fused(const CqkParams<double>& p, const Cmd& c, const TileWalk& tw,
-                     const Src src, TPipe& pp, double (&acc)[kMaxK], int64_t* surv_m) {
+                     const Src src, TPipe& pp, double (&acc)[kMaxK], int guess, int64_t* surv_m) {
   // I = [lam^ - h, lam^ + h] as the host-side check sees it; h2 also covers
   // the rounding of the interval ends
   const double lam_hat = c.lam, h2 = c.edge + kBracketEps * fabs(c.lam);
-  const int guess = c.guess;
   double* const dside[5] = {p.vd, p.va, p.vb, p.vl, p.vu};
   double* const dsurv[5] = {p.sd, p.sa, p.sb, p.sl, p.su};
   int64_t out_m = 0, q_out = 0, sv_m = 0, q_sv = 0;
@@ -950,6 +960,8 @@ DEVI int64_t t_fused(const CqkParams<double>& p, const Cmd& c, const TileWalk& t
   });
   acc[5] += (double)nlo;
   acc[8] += (double)nhi;
+  acc[11] += guess > 0 ? (double)nlo : 0.0;  // left out of this CTA's survivor list
+  acc[12] += guess < 0 ? (double)nhi : 0.0;
   acc[13] += (double)nside;
   if ((threadIdx.x & 31) == 0) acc[14] += (double)sv_m;  // a warp total: counted once
   fence_proxy_async_global();  // generic stores -> the next passes' bulk loads
@@ -1023,6 +1035,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
   bool adopt_pending = false; // the side scan may have adopted the guessed survivors
   int64_t m_w = -1;  // this warp's scratch element count (consumers, once in scratch)
   int64_t m_side = 0, m_surv = 0;  // this warp's side-list / guessed-survivor counts
+  int g_cta = 0;  // the direction guess the fused pass wrote its survivor lists for
+  const bool guess_mode = FIX && p.init.fused_guess != 0;
   // The producer lane issues the first tiles of the most likely next pass (a
   // phi scan / breakpoint pass over the current working set -- or, before
   // any compaction, the final pass over the original arrays) while the grid
@@ -1050,7 +1064,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
     if (side_pending && c.phase != PH_FUSED) side_pending = false;
     if (adopt_pending) {  // the epoch after the side scan: adopt the guessed survivors?
       adopt_pending = false;
-      if (c.adopt) {
+      if (c.adopt != 0 && c.adopt == g_cta) {
         in_scratch = true;
         m_w = m_surv;
       }
@@ -1128,14 +1142,20 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
         }
       }
     } else if (c.phase == PH_SAMPLE) {
-      if (prod_lane) produce_sample(src_l0x, p.n, ntiles, pp3);
-      else if (!producer) t_sample(p, ntiles, pp3, acc);
+      // with the direction guess the sample tiles carry all five arrays and
+      // stay in the main pipeline's stages (no speculation across this step)
+      if (guess_mode) {
+        if (prod_lane) produce_sample<5, kStagesC, kStageElemsC>(src_orig, p.n, ntiles, pp);
+        else if (!producer) t_sample<kStagesC, kStageElemsC, true>(p, ntiles, pp, acc);
+      } else {
+        if (prod_lane) produce_sample(src_l0x, p.n, ntiles, pp3);
+        else if (!producer) t_sample(p, ntiles, pp3, acc);
+      }
       const int ops[3] = {OP_SUM, OP_SUM, OP_SUM};
       double a3[3] = {acc[0], acc[1], acc[2]};
       block_reduce<3, kConsW>(a3, ops, s_red, s_tot);
-      // (fixing solves sample twice: the second sample pass owns the pipeline next)
       is_master = grid_step_any<3>(p.ar, p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch,
-                                   [&] { if (prod_lane && !(FIX && p.init.fused_guess)) speculate(0); }, (c_tma_flags & 4) != 0);
+                                   [&] { if (prod_lane && !guess_mode) speculate(0); }, (c_tma_flags & 4) != 0);
       if (is_master && warp == 0) {
         if (lane == 0) tl_record(dsync, epoch, PH_SAMPLE, p.n, 0);
         double glob[3];
@@ -1148,20 +1168,25 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
           }
         }
       }
-    } else if (c.phase == PH_SAMPLE2) {
-      if (prod_lane) produce_sample<5, kStagesC, kStageElemsC>(src_orig, p.n, ntiles, pp);
-      else if (!producer) t_sample2(p, c.lam, ntiles, pp, acc);
+    } else if (c.phase == PH_GUESS) {
+      // phi at the estimate over the kept sample tiles, then free their
+      // stages: the producer speculates the fused pass's first tiles across
+      // this grid step
+      double a4[4] = {0.0, 0.0, 0.0, 0.0};
+      if (!producer) {
+        t_sample_guess(p, c.lam, ntiles, pp, a4);
+        release_sample(ntiles, pp);
+      }
       const int ops[4] = {OP_SUM, OP_SUM, OP_SUM, OP_SUM};
-      double a4[4] = {acc[0], acc[1], acc[2], acc[3]};
       block_reduce<4, kConsW>(a4, ops, s_red, s_tot);
       is_master = grid_step_any<4>(p.ar, p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch,
                                    [&] { if (prod_lane) speculate(0); }, (c_tma_flags & 4) != 0);
       if (is_master && warp == 0) {
-        if (lane == 0) tl_record(dsync, epoch, PH_SAMPLE2, p.n, 0);
+        if (lane == 0) tl_record(dsync, epoch, PH_GUESS, p.n, 0);
         double glob[4];
         const bool ok = exchange_totals<4>(p.ex, epoch, ops, s_tot, glob, master);
         if (lane == 0) {
-          if (ok) m_after_sample2(s_st, glob, s_tot[2]);
+          if (ok) m_after_guess(s_st, glob);
           else {
             m_stop(s_st, ST_TIMEOUT);
             raise_timeout(p.sync);
@@ -1169,12 +1194,13 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
         }
       }
     } else if (c.phase == PH_FUSED) {
+      g_cta = c.guess;  // the global guess (every CTA alike)
       acc[2] = HUGE_VAL;  // the first failing validate() check (min)
       if (prod_lane) produce<5>(src_orig, orig, pp, spec);
       else if (!producer) {
         int64_t sv = 0;
-        const int64_t mm = check ? t_fused<true>(p, c, orig, src_orig, pp, acc, &sv)
-                                 : t_fused<false>(p, c, orig, src_orig, pp, acc, &sv);
+        const int64_t mm = check ? t_fused<true>(p, c, orig, src_orig, pp, acc, g_cta, &sv)
+                                 : t_fused<false>(p, c, orig, src_orig, pp, acc, g_cta, &sv);
         m_side = mm;
         m_surv = sv;
         if (lane == 0) {

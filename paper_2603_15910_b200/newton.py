@@ -58,8 +58,8 @@ class SolverOptions:
     tolerance_scale defaults to eps**(3/4) of the instance dtype.
     compact_ratio (B200 only): physically compact the working set when the
     logically fixed share of it reaches this ratio (>1 never).  None = the
-    library default: 0.5 on the TMA engine (n >= 64Ki per rank), 0.4 after a
-    fused start with the direction guess (n >= 4e6 per rank), 0.25 on the
+    library default: 0.5 on the TMA engine (n >= 64Ki per rank), 0.4 once a
+    fused start's guessed survivors were adopted (n >= 8e6 per rank), 0.25 on the
     warp-segment engine (cqk_abi.cu default_compact_ratio).
     """
 
