@@ -265,7 +265,10 @@ int cqk_set_fused_guess(cqk_handle *h, int mode);
    the environment variables of the same names set them at cqk_create):
    bit 0 CQK_MASTER_STEP (master + release grid step instead of masterless),
    bit 1 CQK_STATIC_FINAL (static final-pass tiles), bit 2 CQK_TAIL=0 (no
-   single-CTA simplex tail).  Results are bit-identical either way. */
+   single-CTA simplex tail), bit 3 CQK_SPX_CAPTURE=0 (no simplex / l1 capture
+   start: pass 0 and a full first scan), bit 4 (tests) a capture threshold
+   that always fails its check (the fallback to a full first scan).  Results
+   are bit-identical for bits 0-2 and agree to rounding for bits 3-4. */
 int cqk_set_switches(cqk_handle *h, int flags);
 int cqk_set_grid_limit(cqk_handle *h, int max_ctas);
 /* Sharded solve_cqk / jacobi_solve / par_solve_cqk: this rank's shard

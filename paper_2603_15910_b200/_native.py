@@ -248,9 +248,11 @@ class Handle:
         if self.lib.cqk_set_fused_guess(self.ptr, int(guess)) != 0:
             raise NativeError(last_error())
 
-    def set_switches(self, master_step=False, static_final=False, tail=True):
+    def set_switches(self, master_step=False, static_final=False, tail=True, capture=True,
+                     capture_fail=False):
         """A/B switches of the persistent kernels (cqk_set_switches)."""
-        flags = (1 if master_step else 0) | (2 if static_final else 0) | (0 if tail else 4)
+        flags = ((1 if master_step else 0) | (2 if static_final else 0) | (0 if tail else 4)
+                 | (0 if capture else 8) | (16 if capture_fail else 0))
         if self.lib.cqk_set_switches(self.ptr, flags) != 0:
             raise NativeError(last_error())
 

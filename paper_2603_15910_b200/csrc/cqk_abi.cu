@@ -94,6 +94,7 @@ struct cqk_handle {
   int engine = 0;                          // cqk_set_engine: 0 auto, 1 TMA, 2 warp segments
   int64_t tma_min_n = 65536;               // auto: CQK solves of >= this many elements per rank
   int fused_guess = 1;                     // fused start: direction guess + survivor list (CQK_FUSED_GUESS)
+  int spx_capture = 1;                     // simplex / l1 capture start (CQK_SPX_CAPTURE)
   static constexpr int64_t kGuessMinN = 8000000;  // ... from this many elements per rank
   int64_t fused_min_n = 4000000;           // fused start (sample + fused first pass) from this size
   double fused_width = 2e-3;               // ... its classification interval, relative half-width
@@ -245,6 +246,7 @@ int cqk_create(cqk_handle** out, int device) {
   if (const char* mn = getenv("CQK_TMA_MIN_N")) h->tma_min_n = atoll(mn);
   if (const char* fm = getenv("CQK_FUSED_MIN_N")) h->fused_min_n = atoll(fm);
   if (const char* fg = getenv("CQK_FUSED_GUESS")) h->fused_guess = atoi(fg);
+  if (const char* sc = getenv("CQK_SPX_CAPTURE")) h->spx_capture = atoi(sc);
   auto flag = [](const char* name) {
     const char* e = getenv(name);
     return e && e[0] && e[0] != '0';
@@ -601,6 +603,7 @@ extern "C" int cqk_set_switches(cqk_handle* h, int flags) {
   h->master_step = (flags & 1) != 0;
   h->static_final = (flags & 2) != 0;
   h->tail_mode = (flags & 4) == 0;
+  h->spx_capture = (flags & 8) ? 0 : ((flags & 16) ? 2 : 1);
   return 0;
 }
 
@@ -1071,6 +1074,20 @@ int spx_common(cqk_handle* h, int mem, const T* y, int64_t n, int64_t n_total, d
   // 1e9 the tail mode already makes the late epochs cheap and it costs 2%)
   s.hist_ok = F64 && h->use_tma && !sharded && n <= 30000000;
   s.lam_hist = NAN;
+  // capture start (cqk_kernels.cuh s_after_sample / s_after_fused): pass 0 and
+  // the first scan share one pass that captures the possible support; for an
+  // upper-bound start (formula / tight / auto) on the TMA engine, with fixing
+  {
+    const int64_t per_rank = sharded ? n_total / std::max(h->world, 1) : n;
+    const bool ub_start = s.start == 0 || s.start == 1 || s.start == 4;
+    if (F64 && h->use_tma && !alg2 && !s.lam0_given && fixing && ub_start && h->spx_capture &&
+        per_rank >= h->fused_min_n) {
+      s.fused = h->spx_capture;  // 2: an impossible threshold (tests the fallback)
+      s.cmd.phase = PH_SAMPLE;
+      // ("auto": the histogram rides on the first scan over the captured
+      // list; a list small enough for the tail mode iterates without it)
+    }
+  }
   int launches = 1;
   int64_t extra_read = 0;
   CUDA_TRY(cudaEventRecord(h->ev0, h->stream));

@@ -679,9 +679,10 @@ struct SpxState {
   int64_t local_active, fixed_local;  // this rank's share (multi-GPU)
   int64_t iterations, phi_evals, max_iter, elems_scan, elems_written;
   int32_t fixing, status, l1, lam0_given, trace_len, trace_cap, start, hist_ok;
-  int32_t err, pad_;  // err: barrier-timeout flag at the final write
+  int32_t err, fused;  // err: barrier-timeout flag at the final write; fused: capture start
   double compact_ratio;
   double lam_hist;  // start "auto": histogram upper bound of the root after the first scan (or NaN)
+  int64_t cap_local;  // capture start: elements this rank captured (w >= cmd.edge)
 };
 
 template <typename T>
@@ -736,9 +737,51 @@ DEVI void s_after_init(SpxState& s, const double* tot) {
   s.lam_hist = NAN;
 }
 
+// Capture start (TMA engine, large n): pass 0 (sum w, max w) and the first
+// scan share one pass.  The start lam0 = min((r - sum w)/n, r - max w) (or
+// the formula alone) bounds the root from above and the iterates only
+// decrease from it, so an element with w + lam0 < 0 is zero at every iterate
+// (simplex.py:256-303).  A sample gives a threshold T <= -lam0 with
+// certainty for the tight term (sample max w - r <= max w - r) and six
+// standard errors for the formula term; the fused pass computes pass 0's sums
+// exactly and captures every w >= T.  If T <= -lam0 holds for the exact
+// lam0 (checked), the captured values are the whole working set; otherwise
+// the first scan reads y as usual.
+// The sample: tot 0 sum w, 1 sum w^2, 2 elements, 3 max w.
+DEVI void s_after_sample(SpxState& s, const double* tot, double local_count) {
+  s.elems_scan += (int64_t)local_count;  // 8 B per sampled element
+  const double m = fmax(tot[2], 1.0), N = (double)s.n;
+  const double mean = tot[0] / m, var = fmax(tot[1] / m - mean * mean, 0.0);
+  const double t_formula = mean - 6.0 * sqrt(var / m) - s.r / N;
+  const double t_tight = tot[3] - s.r;
+  // lowered by a margin the check below keeps (a sample holding the max
+  // makes the tight term exactly -lam0)
+  const double t = (s.start ? fmax(t_formula, t_tight) : t_formula);
+  const double tm = t - 4e-9 * fmax(1.0, fabs(t));
+  s.cmd.edge = isfinite(tm) && s.fused != 2 ? tm : HUGE_VAL;  // (nothing captured: the check fails)
+  s.cmd.phase = PH_FUSED;
+}
+
+// The fused pass: tot 0 sum w, 1 max w (pass 0's sums), 2 elements captured.
+DEVI void s_after_fused(SpxState& s, const double* tot, const double* loc) {
+  s.cap_local = (int64_t)loc[2];
+  s.elems_written += s.cap_local;
+  s_after_init(s, tot);
+  s.cmd.side = 0;
+  if (s.cmd.phase != PH_SCAN) return;  // l1: inside the ball
+  // every element with w + lam0 >= -margin was captured (the margin covers a
+  // first step upwards from rounding when lam0 is the root to the last bits)
+  if (s.cmd.edge <= -s.lam0 - 1e-9 * fmax(1.0, fabs(s.lam0))) {
+    s.cmd.side = 1;
+    s.fixed_removed += s.local_active - s.cap_local;  // zero at every iterate, fixed at the first scan
+    s.phys_count = s.cap_local;
+  }
+}
+
 // tot: 0 value, 1 #(v>0), 2 #(v==0)   (simplex.py:207-215, 256-294)
 DEVI void s_after_scan(SpxState& s, const double* tot, const double* loc, double* trace) {
   s.phi_evals += 1;
+  s.cmd.side = 0;
   s.elems_scan += s.phys_count;
   if (s.cmd.compact) {
     s.elems_written += s.pending_phys;

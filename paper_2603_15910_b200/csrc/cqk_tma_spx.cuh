@@ -134,7 +134,9 @@ DEVI int tail_gather(const SpxParams<double>& p, bool in_scratch, double* V, int
   return total;
 }
 
-// MODE 0: sum / max of w; 1: phi scan (+ compaction); 2: max(-w) snap.
+// MODE 0: sum / max of w; 1: phi scan (+ compaction); 2: max(-w) snap;
+// 3: MODE 0's sums in the same order plus the capture of w >= lam (the
+// threshold T of the capture start, s_after_sample).
 template <bool L1, int MODE, bool FULL, bool HIST = false>
 DEVI void spx_tile(const WTile& wt, const double* src, bool scratch, double lam, bool fix,
                    double fhi, double (&acc)[kMaxK], int (&cnt)[2], bool (&keep)[kEptY],
@@ -147,10 +149,11 @@ DEVI void spx_tile(const WTile& wt, const double* src, bool scratch, double lam,
     const bool valid = FULL || e_loc(lane, j) < wt.wcnt;
     const double w = scratch ? Y[j] : spx_wv<L1>(Y[j]);  // scratch already holds w
     Wv[j] = w;
-    if (MODE == 0) {
-      keep[j] = false;
+    if (MODE == 0 || MODE == 3) {
+      keep[j] = MODE == 3 && valid && w >= lam;
       acc[0] += valid ? w : 0.0;
       acc[1] = valid ? fmax(acc[1], w) : acc[1];
+      if (MODE == 3) cnt[0] += keep[j];
       continue;
     }
     const double v = add_rn(w, lam);
@@ -201,7 +204,7 @@ DEVI int64_t t_spx(const SpxParams<double>& p, const Cmd& c, bool fix, const Til
 #pragma unroll
     for (int j = 0; j < kEptY; ++j) any_keep = any_keep || keep[j];
     // survivors are rare in projections: most tiles have none to write
-    if (MODE == 1 && compact && __any_sync(0xffffffffu, any_keep)) {  // warp sub-segment compaction
+    if ((MODE == 1 || MODE == 3) && compact && __any_sync(0xffffffffu, any_keep)) {  // warp sub-segment compaction
       const int64_t b0 = ((int64_t)blockIdx.x + q_out * g) * kTileY + kSegY * warp;
       const int64_t b1 = b0 + g * kTileY;
       int r = off_out;
@@ -221,8 +224,61 @@ DEVI int64_t t_spx(const SpxParams<double>& p, const Cmd& c, bool fix, const Til
   });
   if (MODE == 1) { acc[1] += (double)cnt[0]; acc[2] += (double)cnt[1]; }
   if (MODE == 2) acc[1] += (double)cnt[0];
-  if (MODE == 1 && compact) fence_proxy_async_global();
+  if (MODE == 3) acc[2] += (double)cnt[0];
+  if ((MODE == 1 || MODE == 3) && compact) fence_proxy_async_global();
   return out_m;
+}
+
+// The capture start's sample: this CTA's sample tiles (cqk_tma.cuh
+// sample_tile, over the simplex tiling) of y; acc 0 sum w, 1 sum w^2,
+// 2 elements, 3 max w.
+DEVI void produce_sample_y(const double* y, int64_t n, int64_t ntiles, TPipe& pp) {
+  for (int k = 0; k < kSampleTiles; ++k) {
+    const int64_t t = sample_tile(ntiles, k);
+    if (t < 0) break;
+    const int s = pp.pc % kStagesY;
+    const unsigned ph = ((pp.pc / kStagesY) & 1) ^ 1;
+    if (pp.pc >= (unsigned)kStagesY) mbar_wait_s(pp.empty + 8 * s, ph);
+    const int64_t left = n - t * kTileY;
+    const unsigned bytes = ((unsigned)(left < kTileY ? left : kTileY) * 8u) & ~15u;
+    const unsigned fb = pp.full + 8 * s;
+    mbar_expect_tx_s(fb, bytes);
+    if (bytes) tma_load_1d_s(smem_u32(pp.buf) + (unsigned)(s * kTileY) * 8u, y + t * kTileY, bytes, fb);
+    ++pp.pc;
+  }
+}
+template <bool L1>
+DEVI void t_sample_y(const SpxParams<double>& p, int64_t ntiles, TPipe& pp, double (&acc)[kMaxK]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int k = 0; k < kSampleTiles; ++k) {
+    const int64_t t = sample_tile(ntiles, k);
+    if (t < 0) break;
+    const int s = pp.pc % kStagesY;
+    WTile wt;
+    wt.sm = pp.buf + (size_t)s * kTileY + kSegY * warp;
+    wt.gbase = t * kTileY + kSegY * warp;
+    const int64_t left = p.n - wt.gbase;
+    wt.wcnt = left <= 0 ? 0 : (left < kSegY ? (int)left : kSegY);
+    wt.patch = (wt.wcnt & 1) && wt.wcnt < kSegY;
+    wt.q = k;
+    mbar_wait_s(pp.full + 8 * s, (pp.pc / kStagesY) & 1);
+    if (wt.wcnt > 0) {
+      double Y[kEptY];
+      tile_load<false, kTileY>(wt, 0, p.y, Y);
+#pragma unroll
+      for (int j = 0; j < kEptY; ++j) {
+        if (e_loc(lane, j) >= wt.wcnt) continue;
+        const double w = spx_wv<L1>(Y[j]);
+        acc[0] += w;
+        acc[1] += w * w;
+        acc[2] += 1.0;
+        acc[3] = fmax(acc[3], w);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive_s(pp.empty + 8 * s);
+    ++pp.pc;
+  }
 }
 
 template <bool L1, bool FULL>
@@ -344,6 +400,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
   const TileWalk orig{p.n, ntiles, -1};
   bool in_scratch = false;
   int64_t m_w = -1;
+  bool cap_pending = false;  // the capture start's list is in scratch, adoption undecided
   // first tiles of the likely next pass, issued while the grid step runs
   // (cqk_tma.cuh: the loads do not depend on lambda)
   auto speculate = [&]() {
@@ -355,10 +412,21 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
   };
   for (unsigned epoch = 1;; ++epoch) {
     const Cmd c = s_cmd;
-    const int spec = s_spec;
+    int spec = s_spec;
     if (c.phase == PH_DONE || s_abort) {
       if (!producer) drain<kStagesY>(pp, spec);
       break;
+    }
+    if (cap_pending) {  // the epoch after the fused pass: is the captured list the working set?
+      cap_pending = false;
+      if (!c.side) {
+        in_scratch = false;
+        m_w = -1;
+        if (spec > 0 && s_spec_scr && c.phase != PH_FINAL && c.phase != PH_COPY) {
+          if (!producer) drain<kStagesY>(pp, spec);  // speculated from the list
+          spec = 0;
+        }
+      }
     }
     const TileWalk work{p.n, ntiles, in_scratch ? s_nslots : -1};
     if (c.phase == PH_FINAL || c.phase == PH_COPY) {
@@ -397,10 +465,33 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
     double acc[kMaxK];
 #pragma unroll
     for (int k = 0; k < kMaxK; ++k) acc[k] = 0.0;
-    int ops[3] = {OP_SUM, OP_SUM, OP_SUM};
+    int ops[4] = {OP_SUM, OP_SUM, OP_SUM, OP_SUM};
     int mode;
     const Src wsrc{{in_scratch ? p.sy : p.y}};
-    if (c.phase == PH_LAMBDA0) {
+    if (c.phase == PH_SAMPLE) {
+      mode = 4;
+      acc[3] = -HUGE_VAL;
+      ops[3] = OP_MAX;
+      if (prod_lane) produce_sample_y(p.y, p.n, ntiles, pp);
+      else if (!producer) t_sample_y<L1>(p, ntiles, pp, acc);
+    } else if (c.phase == PH_FUSED) {
+      mode = 3;
+      acc[1] = -HUGE_VAL;
+      ops[1] = OP_MAX;
+      if (prod_lane) produce<1, kStagesY, kTileY, kTileY>(Src{{p.y}}, orig, pp, spec);
+      else if (!producer) {
+        Cmd ct = c;
+        ct.lam = c.edge;  // the capture threshold
+        const int64_t mm = t_spx<L1, 3>(p, ct, false, orig, -1, true, pp, acc);
+        m_w = mm;
+        if (lane == 0) {
+          atomicMax(&s_nsl_new, (int)((mm + kSegY - 1) / kSegY));
+          if (p.wcnt) p.wcnt[blockIdx.x * kConsW + warp] = (int32_t)(mm < kTailY ? mm : kTailY);
+        }
+      }
+      in_scratch = true;  // speculate the captured list: the likely next walk
+      cap_pending = true;
+    } else if (c.phase == PH_LAMBDA0) {
       mode = 0;
       acc[1] = -HUGE_VAL;
       ops[1] = OP_MAX;
@@ -433,8 +524,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
     } else {
       break;
     }
-    double a3[3] = {acc[0], acc[1], acc[2]};
-    block_reduce<3, kConsW>(a3, ops, s_red, s_tot);  // (its barrier orders the atomicMax above)
+    double a4[4] = {acc[0], acc[1], acc[2], acc[3]};
+    block_reduce<4, kConsW>(a4, ops, s_red, s_tot);  // (its barrier orders the atomicMax above)
     if (mode == 1 && c.hist && p.hist) {
       // this CTA's nonzero counts into the global histogram (integer atomics:
       // order-independent); each CTA starts at its own offset so the 148
@@ -445,9 +536,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
         if (s_hist[k]) atomicAdd(&p.hist[k], s_hist[k]);
       }
     }
-    const bool is_master = grid_step_any<3>(p.ar, p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch, [&] {
+    const bool is_master = grid_step_any<4>(p.ar, p.partials, s_tot, ops, p.sync, s_red, s_tot, &s_abort, epoch, [&] {
       if (prod_lane) {
-        if (mode == 1 && fix && c.compact) {  // nobody else reads s_nslots before the next epoch
+        if ((mode == 1 && fix && c.compact) || mode == 3) {  // nobody else reads s_nslots before the next epoch
           s_nslots = s_nsl_new;
           s_nsl_new = 0;
         }
@@ -455,20 +546,22 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
       }
     }, (c_tma_flags & 4) != 0);
     if (is_master && mode == 1 && c.hist && p.hist) hist_bound(p, c.lam, s_st.r, s_hist, s_st);
-    double glob[3];
+    double glob[4];
     bool xok = true;
     if (is_master && warp == 0) {  // the whole warp: the exchange is warp-level
-      if (lane == 0) tl_record(dsync, epoch, c.phase, mode == 0 ? p.n : s_st.phys_count, s_st.cmd.compact);
-      xok = exchange_totals<3>(p.ex, epoch, ops, s_tot, glob, master);
+      if (lane == 0) tl_record(dsync, epoch, c.phase, (mode == 0 || mode >= 3) ? p.n : s_st.phys_count, s_st.cmd.compact);
+      xok = exchange_totals<4>(p.ex, epoch, ops, s_tot, glob, master);
     }
     if (threadIdx.x == 0) {
       if (is_master) {
-        double loc[3] = {s_tot[0], s_tot[1], s_tot[2]};
+        double loc[4] = {s_tot[0], s_tot[1], s_tot[2], s_tot[3]};
         if (!xok) {
           raise_timeout(p.sync);
           s_st.status = ST_TIMEOUT;
           s_st.cmd.phase = PH_DONE;
-        } else if (mode == 0) s_after_init(s_st, glob);
+        } else if (mode == 4) s_after_sample(s_st, glob, loc[2]);
+        else if (mode == 3) s_after_fused(s_st, glob, loc);
+        else if (mode == 0) s_after_init(s_st, glob);
         else if (mode == 1) s_after_scan(s_st, glob, loc, dtrace);
         else s_after_snap(s_st, glob);
         const int ph = s_st.cmd.phase;

@@ -1,0 +1,106 @@
+"""The capture start of the simplex / l1 projections (cqk_kernels.cuh
+s_after_sample / s_after_fused, cqk_tma_spx.cuh): pass 0 (sum w, max w) and
+the first scan share one pass that captures every w >= T, T a sampled lower
+bound of -lambda0; when T <= -lambda0 holds for the exact start the captured
+values are the whole working set.  Against the plain start (pass 0 + a full
+first scan: cqk_set_switches bit 3), the forced fallback (bit 4: a threshold
+that fails its check) and the oracle's same-route Algorithm 4
+(simplex.py:246-308 with lambda0 = the device start)."""
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def P():
+    import paper_2603_15910_b200 as p
+
+    return p
+
+
+@pytest.fixture(autouse=True)
+def restore():
+    from paper_2603_15910_b200 import _native as N
+
+    yield
+    N.handle().set_switches()
+
+
+def run(y, l1, start, **sw):
+    from paper_2603_15910_b200 import _native as N
+
+    p = P()
+    N.handle().set_switches(**sw)
+    if l1:
+        return p.simplex.project_l1_outcome(y, 1.0, start=start)
+    return p.newton_project_simplex(y, 1.0, start=start)
+
+
+@pytest.mark.parametrize("l1", [False, True])
+@pytest.mark.parametrize("fam", ["simplex-n01", "simplex-u01"])
+@pytest.mark.parametrize("start", ["auto", "tight", "formula"])
+def test_capture_matches_plain_start(l1, fam, start):
+    import torch
+
+    n = 4_500_007
+    y = torch.from_numpy(P().gen_simplex_y(fam, n, 3)).cuda()
+    cap = run(y, l1, start)
+    plain = run(y, l1, start, capture=False)
+    fail = run(y, l1, start, capture_fail=True)
+    for o in (plain, fail):
+        # "auto" tightens the first step with a histogram of the first tiled
+        # scan, which a captured set small enough for the tail mode skips:
+        # same root, other iteration count
+        if start != "auto":
+            assert (cap.iterations, cap.phi_evals) == (o.iterations, o.phi_evals)
+        assert abs(cap.lam - o.lam) <= 1e-13 * max(1.0, abs(o.lam))
+        assert torch.abs(cap.x - o.x).max().item() <= 1e-13
+    if not (l1 and cap.iterations < 0):  # (inside the ball: a copy)
+        assert cap.stats["bytes_model"] < plain.stats["bytes_model"]
+
+
+@pytest.mark.parametrize("l1", [False, True])
+def test_capture_matches_oracle(l1):
+    n = 6_000_011
+    y = P().gen_simplex_y("simplex-n01", n, 8)
+    out = run(y, l1, "tight")
+    w = np.abs(y) if l1 else y
+    lam0 = min((1.0 - float(O.pairwise_sum(w))) / n, 1.0 - float(w.max()))
+    ref = O.newton_project_simplex(w, 1.0, lam0=lam0)
+    assert abs(out.lam - ref["lam"]) <= 1e-12 * max(1.0, abs(ref["lam"]))
+    assert out.iterations == ref["iterations"]
+    x = out.x if not hasattr(out.x, "cpu") else out.x.cpu().numpy()
+    xr = ref["x"] if not l1 else np.sign(y) * ref["x"]
+    assert np.abs(x - xr).max() <= 1e-12
+
+
+def test_capture_inside_ball():
+    """l1 with y inside the ball: the fused pass's exact sum decides the copy."""
+    n = 4_200_000
+    y = P().gen_simplex_y("simplex-n01", n, 2) * (0.5 / n)
+    x = P().project_l1(y, 1.0)
+    assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_capture_sharded(world):
+    """Virtual ranks: every rank captures against the global threshold."""
+    import torch
+
+    from paper_2603_15910_b200 import distributed as D
+    from test_gpu_sharded import run_ranks
+
+    n = 9_000_001
+    y = P().gen_simplex_y("simplex-n01", n, 6)
+    single = P().newton_project_simplex(y, 1.0, start="tight")
+    comms = D.local_group([0] * world, grid_limit=120 // world)
+    solvers = []
+    for q in range(world):
+        lo, hi = D.shard_bounds(n, world, q)
+        solvers.append(D.ShardedProjection(comms[q], torch.from_numpy(y[lo:hi].copy()).cuda(), n))
+    outs = run_ranks([lambda s=s: s.solve(1.0) for s in solvers])
+    lam = {o.lam for o in outs}
+    assert len(lam) == 1
+    assert abs(outs[0].lam - single.lam) <= 1e-12 * max(1.0, abs(single.lam))
