@@ -897,9 +897,12 @@ template <typename T>
 int launch_spx(cqk_handle* h, SpxState& s, const T* yv, int64_t n, T* xo, bool l1, bool sharded) {
   constexpr bool F64 = std::is_same<T, double>::value;
   const bool tma = F64 && h->use_tma;
-  if (s.fixing)
-    CUDA_TRY(h->scratch.ensure(((size_t)(tma ? tma_scratch_elems_y(n) : n) * sizeof(T) + 255) /
-                               256 * 256));
+  // scratch: working values; with the capture start also the captured
+  // elements' indices and (l1) the sign bits of y
+  const size_t per_y = ((size_t)(tma ? tma_scratch_elems_y(n) : n) * sizeof(T) + 255) / 256 * 256;
+  const size_t per_i = s.fused ? ((size_t)tma_scratch_elems_y(n) * 8 + 255) / 256 * 256 : 0;
+  const size_t per_s = s.fused && l1 ? ((size_t)tma_scratch_elems_y(n) / 8 + 255) / 256 * 256 : 0;
+  if (s.fixing) CUDA_TRY(h->scratch.ensure(per_y + per_i + per_s));
   std::memcpy(h->host_state, &s, sizeof s);  // status RUNNING until the master publishes
   SpxParams<T> p;
   std::memset(&p, 0, sizeof p);
@@ -907,6 +910,8 @@ int launch_spx(cqk_handle* h, SpxState& s, const T* yv, int64_t n, T* xo, bool l
   p.out = (SpxState*)h->host_state_dev;
   p.y = yv;
   p.sy = s.fixing ? (T*)h->scratch.p : nullptr;
+  p.sidx = per_i ? (int64_t*)((char*)h->scratch.p + per_y) : nullptr;
+  p.signs = per_s ? (uint32_t*)((char*)h->scratch.p + per_y + per_i) : nullptr;
   p.x = xo;
   p.trace = h->trace;
   p.n = n;
@@ -1206,6 +1211,14 @@ int spx_common(cqk_handle* h, int mem, const T* y, int64_t n, int64_t n_total, d
   res->elems_read = pass0 + s.elems_scan + fin;
   res->elems_written = s.elems_written + fin;
   res->bytes_model = (int64_t)sizeof(T) * (pass0 + s.elems_scan + s.elems_written + 2 * fin);
+  if (s.sparse_final && fin) {
+    // x is written (8 B) without re-reading y; l1 writes and reads one sign
+    // bit per element; each captured element: its index written by the fused
+    // pass, then index + y read and x written by the scatter
+    res->elems_read = pass0 + s.elems_scan + 2 * s.cap_local;
+    res->bytes_model = (int64_t)sizeof(T) * (pass0 + s.elems_scan + s.elems_written + fin) +
+                       (l1 ? 2 * ((n + 7) / 8) : 0) + 32 * s.cap_local;
+  }
   res->device_ms = ms;
   res->launches = launches;
   res->trace_len = s.trace_len;

@@ -683,12 +683,15 @@ struct SpxState {
   double compact_ratio;
   double lam_hist;  // start "auto": histogram upper bound of the root after the first scan (or NaN)
   int64_t cap_local;  // capture start: elements this rank captured (w >= cmd.edge)
+  int32_t sparse_final, pad2_;  // the captured list was adopted: x = signed zeros + a scatter
 };
 
 template <typename T>
 struct SpxParams {
   const T* y;
   T* sy;  // scratch (working values w)
+  int64_t* sidx;      // capture start: the captured elements' indices (the fused pass's slots)
+  uint32_t* signs;    // capture start, l1: y < 0 bits per (tile, warp, j) of the fused pass
   T* x;
   double* trace;
   int64_t n;  // elements of this rank's shard
@@ -775,6 +778,13 @@ DEVI void s_after_fused(SpxState& s, const double* tot, const double* loc) {
     s.cmd.side = 1;
     s.fixed_removed += s.local_active - s.cap_local;  // zero at every iterate, fixed at the first scan
     s.phys_count = s.cap_local;
+    // every other x is a (signed) zero: the final pass need not re-read y --
+    // worth it while the scatter of the captured x (index, y and x, each a
+    // random sector) stays small against the 8 B per element it saves
+    if (tot[2] * 64.0 <= (double)s.n) {
+      s.sparse_final = 1;
+      s.cmd.sparse = 1;
+    }
   }
 }
 

@@ -70,7 +70,9 @@ struct Cmd {
                     // lambda0 -- the fused pass then also writes the elements it would keep
   int32_t adopt;    // after the side scan: the direction taken at lambda0 when it is the
                     // guessed one -- the survivors become the working set; 0 none
-  int32_t pad_[2];
+  int32_t sparse;   // simplex capture start adopted: the final pass writes signed zeros and
+                    // scatters the captured elements' x (cqk_tma_spx.cuh spx_sparse_final)
+  int32_t pad_;
 };
 
 // Master-side solver state (SolveState, newton.py:70-90, plus counters).

@@ -140,10 +140,21 @@ DEVI int tail_gather(const SpxParams<double>& p, bool in_scratch, double* V, int
 template <bool L1, int MODE, bool FULL, bool HIST = false>
 DEVI void spx_tile(const WTile& wt, const double* src, bool scratch, double lam, bool fix,
                    double fhi, double (&acc)[kMaxK], int (&cnt)[2], bool (&keep)[kEptY],
-                   double (&Wv)[kEptY], int* s_hist, double hscale) {
+                   double (&Wv)[kEptY], int* s_hist, double hscale, uint32_t* signw = nullptr) {
   const int lane = threadIdx.x & 31;
   double Y[kEptY];
   tile_load<FULL, kTileY>(wt, 0, src, Y);
+  if (MODE == 3 && L1 && signw) {  // capture start, l1: the sign bits for the sparse final
+    uint32_t b[kEptY];
+#pragma unroll
+    for (int j = 0; j < kEptY; ++j)
+      b[j] = __ballot_sync(0xffffffffu, (FULL || e_loc(lane, j) < wt.wcnt) && Y[j] < 0.0);
+    static_assert(kEptY == 8, "two 16-byte stores of sign words");
+    if (lane == 0) {
+      reinterpret_cast<uint4*>(signw)[0] = make_uint4(b[0], b[1], b[2], b[3]);
+      reinterpret_cast<uint4*>(signw)[1] = make_uint4(b[4], b[5], b[6], b[7]);
+    }
+  }
 #pragma unroll
   for (int j = 0; j < kEptY; ++j) {
     const bool valid = FULL || e_loc(lane, j) < wt.wcnt;
@@ -189,8 +200,15 @@ DEVI int64_t t_spx(const SpxParams<double>& p, const Cmd& c, bool fix, const Til
   consume<kStagesY, kTileY, kTileY>(tw, pp, m_w, [&](const WTile& wt) {
     bool keep[kEptY];
     double Wv[kEptY];
-    // the histogram (start "auto") rides on one scan per solve: its own instance
-    if (MODE == 1 && s_hist) {
+    if (MODE == 3) {  // the capture start's fused pass (original tiles, static walk)
+      uint32_t* sw = L1 && p.signs
+                         ? p.signs + ((wt.gbase - kSegY * warp) / kTileY * kConsW + warp) * kEptY
+                         : nullptr;
+      if (wt.wcnt == kSegY)
+        spx_tile<L1, MODE, true>(wt, src, scratch, lam, fix, fhi, acc, cnt, keep, Wv, s_hist, hscale, sw);
+      else
+        spx_tile<L1, MODE, false>(wt, src, scratch, lam, fix, fhi, acc, cnt, keep, Wv, s_hist, hscale, sw);
+    } else if (MODE == 1 && s_hist) {
       if (wt.wcnt == kSegY)
         spx_tile<L1, MODE, true, true>(wt, src, scratch, lam, fix, fhi, acc, cnt, keep, Wv, s_hist, hscale);
       else
@@ -213,7 +231,9 @@ DEVI int64_t t_spx(const SpxParams<double>& p, const Cmd& c, bool fix, const Til
         const unsigned bal = __ballot_sync(0xffffffffu, keep[j]);
         if (keep[j]) {
           const int o = r + __popc(bal & ltm);
-          p.sy[o < kSegY ? b0 + o : b1 + (o - kSegY)] = Wv[j];
+          const int64_t pos = o < kSegY ? b0 + o : b1 + (o - kSegY);
+          p.sy[pos] = Wv[j];
+          if (MODE == 3 && p.sidx) p.sidx[pos] = wt.gbase + e_loc(lane, j);  // for the sparse final
         }
         r += __popc(bal);
       }
@@ -304,6 +324,85 @@ DEVI void spx_final_tile(const SpxParams<double>& p, const WTile& wt, bool copy,
     double* xp = p.x + wt.gbase + e;
     if (FULL || e + 1 < wt.wcnt) store_out(reinterpret_cast<double2*>(xp), make_double2(X[2 * u], X[2 * u + 1]));
     else if (e < wt.wcnt) *xp = X[2 * u];
+  }
+}
+
+// The sparse final of the capture start (cmd.sparse): every element the
+// fused pass did not capture has w + lam* < 0, so its x is a zero -- signed
+// like sign(y) * 0 for l1 (the sign bits the fused pass recorded), +0 for
+// the simplex -- and is written without re-reading y (8 B per element
+// instead of 16).  After a grid barrier each warp scatters the x of the
+// elements it captured (their indices sit in the fused pass's slots), with
+// spx_final_tile's formula: x = max(0, w + lam), sign restored for l1.
+template <bool L1>
+DEVI void spx_sparse_final(const SpxParams<double>& p, double lam, int64_t ntiles, int64_t m_cap) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t G = gridDim.x;
+  if (warp < kConsW) {
+    // groups of kGrp tiles: their sign words are loaded together (lane
+    // 8k + j holds word j of the group's k-th tile), then the stores follow,
+    // so the warp does not wait one load latency per tile
+    constexpr int kGrp = 4;
+    static_assert(kGrp * kEptY <= 32, "one sign word per lane");
+    for (int64_t t0 = blockIdx.x; t0 < ntiles; t0 += kGrp * G) {
+      uint32_t mine = 0u;
+      if (L1) {
+        const int k = lane / kEptY, j = lane % kEptY;
+        const int64_t t = t0 + k * G;
+        if (t < ntiles) mine = __ldcg(p.signs + (t * kConsW + warp) * kEptY + j);
+      }
+#pragma unroll
+      for (int k = 0; k < kGrp; ++k) {
+        const int64_t t = t0 + k * G;
+        const int64_t gbase = t * kTileY + kSegY * warp;
+        const int64_t left = p.n - gbase;
+        const int wcnt = t >= ntiles || left <= 0 ? 0 : (left < kSegY ? (int)left : kSegY);
+        uint32_t sg[kEptY];
+#pragma unroll
+        for (int j = 0; j < kEptY; ++j) sg[j] = L1 ? __shfl_sync(0xffffffffu, mine, k * kEptY + j) : 0u;
+        if (wcnt <= 0) continue;
+#pragma unroll
+        for (int u = 0; u < kEptY / 2; ++u) {
+          const int e = 64 * u + 2 * lane;
+          const double x0 = (L1 && ((sg[2 * u] >> lane) & 1u)) ? -0.0 : 0.0;
+          const double x1 = (L1 && ((sg[2 * u + 1] >> lane) & 1u)) ? -0.0 : 0.0;
+          double* xp = p.x + gbase + e;
+          if (e + 1 < wcnt) store_out(reinterpret_cast<double2*>(xp), make_double2(x0, x1));
+          else if (e < wcnt) *xp = x0;
+        }
+      }
+    }
+  }
+  // grid barrier (the launch's final-tile counter, which arrives zero):
+  // every zero is written before any scatter
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(p.ar.tiles, 1u);
+    const unsigned long long t0 = globaltimer();
+    unsigned polls = 0;
+    while (ld_acquire(p.ar.tiles) < (unsigned)G) {
+      if ((++polls & 255u) == 0 && globaltimer() - t0 > kSpinTimeoutNs) {
+        raise_timeout(p.sync);
+        break;
+      }
+    }
+  }
+  __syncthreads();
+  if (warp < kConsW) {
+    for (int64_t i = lane; i < m_cap; i += 32) {
+      const int64_t pos = ((int64_t)blockIdx.x + (i / kSegY) * G) * kTileY + kSegY * warp + (i % kSegY);
+      const int64_t idx = __ldcg(p.sidx + pos);
+      const double yv = p.y[idx];
+      const double v = add_rn(spx_wv<L1>(yv), lam);
+      const double pos_v = v > 0.0 ? v : 0.0;  // np.maximum(0, w + lam)
+      double x = pos_v;
+      if (L1) {
+        const double sgv = yv > 0.0 ? 1.0 : (yv < 0.0 ? -1.0 : 0.0);
+        x = mul_rn(sgv, pos_v);
+      }
+      p.x[idx] = x;
+    }
   }
 }
 
@@ -401,6 +500,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
   bool in_scratch = false;
   int64_t m_w = -1;
   bool cap_pending = false;  // the capture start's list is in scratch, adoption undecided
+  int64_t m_cap = 0;         // this warp's captured elements (the sparse final's scatter)
   // first tiles of the likely next pass, issued while the grid step runs
   // (cqk_tma.cuh: the loads do not depend on lambda)
   auto speculate = [&]() {
@@ -429,6 +529,18 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
       }
     }
     const TileWalk work{p.n, ntiles, in_scratch ? s_nslots : -1};
+    const bool sparse = c.phase == PH_FINAL && c.sparse && p.x && p.sidx && p.ar.tiles;
+    if (sparse) {  // the capture start's final: signed zeros + a scatter, y not re-read
+      if (blockIdx.x <= 1 && threadIdx.x == 0) tl_mark(p.sync, epoch, 10 + 2 * blockIdx.x);
+      if (!producer) drain<kStagesY>(pp, spec);
+      spx_sparse_final<L1>(p, c.lam, ntiles, m_cap);
+      if (p.sync.timeline && threadIdx.x == 0 && epoch < (unsigned)kTimelineCap) {
+        if (blockIdx.x <= 1) tl_mark(p.sync, epoch, 11 + 2 * blockIdx.x);
+        atomicMax(reinterpret_cast<unsigned long long*>(p.sync.timeline + kTimelineCols * epoch + 15),
+                  globaltimer());
+      }
+      break;
+    }
     if (c.phase == PH_FINAL || c.phase == PH_COPY) {
       if (blockIdx.x <= 1 && threadIdx.x == 0) tl_mark(p.sync, epoch, 10 + 2 * blockIdx.x);
       const bool reuse = spec > 0 && !s_spec_scr;
@@ -484,6 +596,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
         ct.lam = c.edge;  // the capture threshold
         const int64_t mm = t_spx<L1, 3>(p, ct, false, orig, -1, true, pp, acc);
         m_w = mm;
+        m_cap = mm;
         if (lane == 0) {
           atomicMax(&s_nsl_new, (int)((mm + kSegY - 1) / kSegY));
           if (p.wcnt) p.wcnt[blockIdx.x * kConsW + warp] = (int32_t)(mm < kTailY ? mm : kTailY);

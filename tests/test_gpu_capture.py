@@ -57,6 +57,9 @@ def test_capture_matches_plain_start(l1, fam, start):
             assert (cap.iterations, cap.phi_evals) == (o.iterations, o.phi_evals)
         assert abs(cap.lam - o.lam) <= 1e-13 * max(1.0, abs(o.lam))
         assert torch.abs(cap.x - o.x).max().item() <= 1e-13
+        # the sparse final's zeros carry sign(y) * 0 like the dense formula
+        zero = (cap.x == 0) & (o.x == 0)
+        assert torch.equal(torch.signbit(cap.x[zero]), torch.signbit(o.x[zero]))
     if not (l1 and cap.iterations < 0):  # (inside the ball: a copy)
         assert cap.stats["bytes_model"] < plain.stats["bytes_model"]
 

@@ -29,6 +29,7 @@ x = out.x
 s_abs = float(x.abs().sum())
 sign_ok = bool(((x == 0) | (torch.sign(x) == torch.sign(yd))).all())
 xr = torch.sign(yd) * torch.clamp(yd.abs() + out.lam, min=0.0)
+bits_ok = bool(torch.equal(x.view(torch.int64), xr.view(torch.int64)))  # signed zeros included
 peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                    "MEASURED_PEAKS.json")))["hbm_gbs"]
 ms = min(ks)
@@ -38,4 +39,5 @@ print(json.dumps({"config": "C4 l1 n01 r=1 single GPU", "n": n, "kernel_ms": ms,
                   "GBps": out.stats["bytes_model"] / ms / 1e6,
                   "frac": out.stats["bytes_model"] / ms / 1e6 / peak,
                   "sum_abs_x_minus_r": s_abs - 1.0, "sign_ok": sign_ok,
-                  "x_formula_maxdiff": float((x - xr).abs().max()), "host_gen_s": tg}))
+                  "x_formula_maxdiff": float((x - xr).abs().max()), "x_formula_bitwise": bits_ok,
+                  "host_gen_s": tg}))
