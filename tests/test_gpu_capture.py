@@ -107,3 +107,15 @@ def test_capture_sharded(world):
     lam = {o.lam for o in outs}
     assert len(lam) == 1
     assert abs(outs[0].lam - single.lam) <= 1e-12 * max(1.0, abs(single.lam))
+    x = np.concatenate([o.x.cpu().numpy() for o in outs])
+    assert np.abs(x - single.x).max() <= 1e-12
+    assert np.array_equal(x, np.maximum(0.0, y + outs[0].lam))  # the sparse final's zeros included
+
+    # l1 across the ranks: signed zeros from each rank's sign bits
+    for q in range(world):
+        solvers[q].y.neg_()  # a sign pattern that differs from y's
+    ys = -y
+    outs = run_ranks([lambda s=s: s.solve(1.0, l1=True) for s in solvers])
+    x = np.concatenate([o.x.cpu().numpy() for o in outs])
+    xr = np.sign(ys) * np.maximum(0.0, np.abs(ys) + outs[0].lam)
+    assert np.array_equal(x, xr) and np.array_equal(np.signbit(x), np.signbit(xr))

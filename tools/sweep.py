@@ -60,6 +60,14 @@ for w in which:
         res[w] = cqk("cqk-uncorrelated", 10**8)
     elif w == "jac":
         res[w] = cqk("cqk-weakly-correlated", 10**8, jac=True)
+    elif w == "weak_f32":  # the float32 path (warp-segment kernel, float element math)
+        d, a, b, l, u, r = P.instances.gen_cqk_arrays("cqk-weakly-correlated", 10**8, 1)
+        inst = P.CqkInstance(*[torch.from_numpy(v.astype(np.float32)).cuda() for v in (d, a, b, l, u)], r=r)
+        ms, out = timeit(lambda: P.solve_cqk(inst))
+        st = out.stats
+        res[w] = {"ms": ms, "kernel_ms": st["device_ms"], "GBps": st["bytes_model"] / st["device_ms"] / 1e6,
+                  "frac": st["bytes_model"] / st["device_ms"] / 1e6 / PEAK, "evals": out.phi_evals,
+                  "elem_per_s": 10**8 / ms * 1e3, "bytes_per_elem": st["bytes_model"] / 10**8}
     elif w.split("_")[0] in ("spx", "l1") and not w.startswith("spx1e6"):
         n = 10**8
         start = w.split("_")[1] if "_" in w else "auto"
