@@ -95,6 +95,7 @@ struct cqk_handle {
   int64_t tma_min_n = 65536;               // auto: CQK solves of >= this many elements per rank
   int fused_guess = 1;                     // fused start: direction guess + survivor list (CQK_FUSED_GUESS)
   int spx_capture = 1;                     // simplex / l1 capture start (CQK_SPX_CAPTURE)
+  int64_t spx_capture_min_n = 4000000;     // ... from this many elements per rank (CQK_SPX_CAPTURE_MIN_N)
   static constexpr int64_t kGuessMinN = 8000000;  // ... from this many elements per rank
   int64_t fused_min_n = 4000000;           // fused start (sample + fused first pass) from this size
   double fused_width = 2e-3;               // ... its classification interval, relative half-width
@@ -247,6 +248,7 @@ int cqk_create(cqk_handle** out, int device) {
   if (const char* fm = getenv("CQK_FUSED_MIN_N")) h->fused_min_n = atoll(fm);
   if (const char* fg = getenv("CQK_FUSED_GUESS")) h->fused_guess = atoi(fg);
   if (const char* sc = getenv("CQK_SPX_CAPTURE")) h->spx_capture = atoi(sc);
+  if (const char* sm = getenv("CQK_SPX_CAPTURE_MIN_N")) h->spx_capture_min_n = atoll(sm);
   auto flag = [](const char* name) {
     const char* e = getenv(name);
     return e && e[0] && e[0] != '0';
@@ -500,13 +502,11 @@ int check_timeout(cqk_handle* h, int32_t status, int32_t err) {
 // The masterless grid step for a single-GPU persistent TMA launch of `grid`
 // CTAs (one CTA per SM; the buffers hold sm_count + 8 rows).
 GridAR masterless(cqk_handle* h, int grid, const Exchange& ex) {
-  GridAR ar{nullptr, 0ull, nullptr, nullptr, nullptr, nullptr, 0};
+  GridAR ar{nullptr, 0ull, nullptr, nullptr, 0};
   if (grid > h->sm_count + 8 || h->master_step) return ar;
   const int k = (int)(h->ar_seq++ & 1u);
   ar.tag = h->ar_seq << 32;  // unique per launch of this handle (rows carry it)
   ar.rows = h->ar_rows;
-  ar.count = h->ar_count + k;
-  ar.count_next = h->ar_count + (k ^ 1);
   ar.tiles = h->ar_count + 2 + k;
   ar.tiles_next = h->ar_count + 2 + (k ^ 1);
   ar.dyn_final = !h->static_final;
@@ -1086,7 +1086,7 @@ int spx_common(cqk_handle* h, int mem, const T* y, int64_t n, int64_t n_total, d
     const int64_t per_rank = sharded ? n_total / std::max(h->world, 1) : n;
     const bool ub_start = s.start == 0 || s.start == 1 || s.start == 4;
     if (F64 && h->use_tma && !alg2 && !s.lam0_given && fixing && ub_start && h->spx_capture &&
-        per_rank >= h->fused_min_n) {
+        per_rank >= h->spx_capture_min_n) {
       s.fused = h->spx_capture;  // 2: an impossible threshold (tests the fallback)
       s.cmd.phase = PH_SAMPLE;
       // ("auto": the histogram rides on the first scan over the captured

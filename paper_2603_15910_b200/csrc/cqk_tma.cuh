@@ -1017,7 +1017,6 @@ __global__ void __launch_bounds__(kTmaThreads, 1) cqk_tma_kernel(CqkParams<doubl
     s_st = p.init;  // host-initialised, passed by value (every CTA: single-GPU replicas)
     s_cmd = s_st.cmd;
     if (master) tl_record(p.sync, 0, -1, p.n, 0);
-    if (master && p.ar.rows) *p.ar.count_next = 0u;  // the previous launch's counter
     if (master && p.ar.tiles) *p.ar.tiles_next = 0u;
   }
   __syncthreads();

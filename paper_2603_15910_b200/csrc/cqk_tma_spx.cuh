@@ -481,7 +481,6 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
     s_st = p.init;  // every CTA: single-GPU replicas of the state machine
     s_cmd = s_st.cmd;
     if (master) tl_record(p.sync, 0, -1, p.n, 0);
-    if (master && p.ar.rows) *p.ar.count_next = 0u;  // the previous launch's counter
     if (master && p.ar.tiles) *p.ar.tiles_next = 0u;
   }
   for (int k = threadIdx.x; k < kHistB; k += blockDim.x) s_hist[k] = 0;

@@ -119,3 +119,58 @@ def test_capture_sharded(world):
     x = np.concatenate([o.x.cpu().numpy() for o in outs])
     xr = np.sign(ys) * np.maximum(0.0, np.abs(ys) + outs[0].lam)
     assert np.array_equal(x, xr) and np.array_equal(np.signbit(x), np.signbit(xr))
+
+
+def _edge_vectors():
+    rng = np.random.default_rng(11)
+    n = 4_000_001  # odd: a partial last tile with an odd element count
+    base = rng.normal(0.0, 1.0, n)
+    ties = np.round(base * 4.0) / 4.0  # many exact ties (also at the threshold)
+    zeros = base.copy()
+    zeros[::7] = 0.0
+    zeros[3::7] = -0.0  # signed zeros in y (l1 sign bits)
+    outlier = base.copy()
+    outlier[n // 2 + 12345] = 40.0  # a max far outside any sample tile (likely)
+    const = np.full(n, 0.3)
+    return {"ties": ties, "zeros": zeros, "outlier": outlier, "const": const}
+
+
+EDGE = _edge_vectors()
+
+
+@pytest.mark.parametrize("name", sorted(EDGE))
+@pytest.mark.parametrize("l1", [False, True])
+@pytest.mark.parametrize("r", [1.0, 1e-6, 1e5])
+def test_capture_edge_inputs(name, l1, r):
+    """Ties, signed zeros, an unsampled outlier, a constant vector, tiny and huge
+    levels: the capture start (and its sparse final, when taken) returns
+    the plain start's projection bit for bit up to the multiplier's last bits."""
+    import torch
+
+    from paper_2603_15910_b200 import _native as N
+
+    p = P()
+    y = torch.from_numpy(EDGE[name]).cuda()
+    outs = []
+    for sw in ({}, {"capture": False}):
+        N.handle().set_switches(**sw)
+        if l1:
+            outs.append(p.simplex.project_l1_outcome(y, r, start="tight"))
+        else:
+            outs.append(p.newton_project_simplex(y, r, start="tight"))
+    cap, plain = outs
+    if l1 and plain.iterations < 0:  # inside the ball: x = y (a copy)
+        assert cap.iterations < 0 and torch.equal(cap.x, y)
+        return
+    assert (cap.iterations, cap.phi_evals) == (plain.iterations, plain.phi_evals)
+    assert abs(cap.lam - plain.lam) <= 1e-13 * max(1.0, abs(plain.lam))
+    assert torch.abs(cap.x - plain.x).max().item() <= 1e-12 * max(1.0, r)
+    zero = (cap.x == 0) & (plain.x == 0)
+    assert torch.equal(torch.signbit(cap.x[zero]), torch.signbit(plain.x[zero]))
+    # against the formula at the capture's own multiplier: bit for bit
+    w = y.abs() if l1 else y
+    xr = torch.clamp(w + cap.lam, min=0.0)
+    if l1:  # np.sign semantics: sign(-0.0) = +0.0 (torch.sign keeps the zero's sign)
+        sg = (y > 0).double() - (y < 0).double()
+        xr = sg * xr
+    assert torch.equal(cap.x.view(torch.int64), xr.view(torch.int64))

@@ -56,6 +56,10 @@ for w in which:
         res[w] = cqk("cqk-uncorrelated", 10**7)
     elif w == "weak7":
         res[w] = cqk("cqk-weakly-correlated", 10**7)
+    elif w == "unc6":
+        res[w] = cqk("cqk-uncorrelated", 10**6)
+    elif w == "weak6":
+        res[w] = cqk("cqk-weakly-correlated", 10**6)
     elif w == "unc8":
         res[w] = cqk("cqk-uncorrelated", 10**8)
     elif w == "jac":
