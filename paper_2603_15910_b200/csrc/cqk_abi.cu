@@ -1079,6 +1079,7 @@ int spx_common(cqk_handle* h, int mem, const T* y, int64_t n, int64_t n_total, d
   // 1e9 the tail mode already makes the late epochs cheap and it costs 2%)
   s.hist_ok = F64 && h->use_tma && !sharded && n <= 30000000;
   s.lam_hist = NAN;
+  s.cap_first = F64 && h->use_tma && h->spx_capture;  // the first scan captures (s_after_init)
   // capture start (cqk_kernels.cuh s_after_sample / s_after_fused): pass 0 and
   // the first scan share one pass that captures the possible support; for an
   // upper-bound start (formula / tight / auto) on the TMA engine, with fixing

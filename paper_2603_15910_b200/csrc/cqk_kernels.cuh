@@ -683,7 +683,8 @@ struct SpxState {
   double compact_ratio;
   double lam_hist;  // start "auto": histogram upper bound of the root after the first scan (or NaN)
   int64_t cap_local;  // capture start: elements this rank captured (w >= cmd.edge)
-  int32_t sparse_final, pad2_;  // the captured list was adopted: x = signed zeros + a scatter
+  int32_t sparse_final;  // the captured list was adopted: x = signed zeros + a scatter
+  int32_t cap_first;     // TMA engine: the first scan may capture (s_after_init)
 };
 
 template <typename T>
@@ -738,6 +739,17 @@ DEVI void s_after_init(SpxState& s, const double* tot) {
   s.cmd.phase = PH_SCAN;
   s.cmd.hist = s.hist_ok && s.start == 4 && !s.lam0_given && s.fixing;
   s.lam_hist = NAN;
+  // First-scan capture (TMA engine): from an upper-bound start the iterates
+  // only decrease, so w + lam0 < 0 means zero at every iterate; the first
+  // scan already keeps only w > -lam0 - margin (the drop rule of the fixed
+  // test with fix_hi = lam0 + margin), i.e. it compacts one scan earlier
+  // than the fixing would.  Its sums are unchanged (dropped elements have
+  // v < 0).  The margin covers a rounding-sized first step upwards.
+  if (s.cap_first && s.fixing && !s.lam0_given) {
+    s.cmd.capture = 1;
+    s.cmd.compact = 1;
+    s.cmd.fix_hi = s.lam0 + 1e-9 * fmax(1.0, fabs(s.lam0));
+  }
 }
 
 // Capture start (TMA engine, large n): pass 0 (sum w, max w) and the first
@@ -772,6 +784,9 @@ DEVI void s_after_fused(SpxState& s, const double* tot, const double* loc) {
   s_after_init(s, tot);
   s.cmd.side = 0;
   if (s.cmd.phase != PH_SCAN) return;  // l1: inside the ball
+  s.cmd.capture = 0;  // (the fused pass captured already; its fallback scans everything)
+  s.cmd.compact = 0;
+  s.cmd.fix_hi = INFINITY;
   // every element with w + lam0 >= -margin was captured (the margin covers a
   // first step upwards from rounding when lam0 is the root to the last bits)
   if (s.cmd.edge <= -s.lam0 - 1e-9 * fmax(1.0, fabs(s.lam0))) {
@@ -794,10 +809,13 @@ DEVI void s_after_scan(SpxState& s, const double* tot, const double* loc, double
   s.cmd.side = 0;
   s.elems_scan += s.phys_count;
   if (s.cmd.compact) {
-    s.elems_written += s.pending_phys;
-    s.fixed_removed += s.phys_count - s.pending_phys;
-    s.phys_count = s.pending_phys;
+    // a capturing scan's survivors are counted by the scan itself (slot 3)
+    const int64_t kept = s.cmd.capture ? (int64_t)loc[3] : s.pending_phys;
+    s.elems_written += kept;
+    s.fixed_removed += s.phys_count - kept;
+    s.phys_count = kept;
     s.cmd.compact = 0;
+    s.cmd.capture = 0;
   }
   const double lam = s.cmd.lam, value = tot[0], dminus = tot[1], dplus = tot[1] + tot[2];
   if (trace && s.trace_len < s.trace_cap) {

@@ -72,7 +72,8 @@ struct Cmd {
                     // guessed one -- the survivors become the working set; 0 none
   int32_t sparse;   // simplex capture start adopted: the final pass writes signed zeros and
                     // scatters the captured elements' x (cqk_tma_spx.cuh spx_sparse_final)
-  int32_t pad_;
+  int32_t capture;  // simplex, first scan from an upper-bound start: keep (compact) only
+                    // w > -fix_hi, the possible support; the kept count comes back in slot 3
 };
 
 // Master-side solver state (SolveState, newton.py:70-90, plus counters).

@@ -243,6 +243,7 @@ DEVI int64_t t_spx(const SpxParams<double>& p, const Cmd& c, bool fix, const Til
     }
   });
   if (MODE == 1) { acc[1] += (double)cnt[0]; acc[2] += (double)cnt[1]; }
+  if (MODE == 1 && compact && lane == 0) acc[3] += (double)out_m;  // survivors written (a warp total)
   if (MODE == 2) acc[1] += (double)cnt[0];
   if (MODE == 3) acc[2] += (double)cnt[0];
   if ((MODE == 1 || MODE == 3) && compact) fence_proxy_async_global();
