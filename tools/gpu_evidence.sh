@@ -1,4 +1,4 @@
-# Round-2 evidence pass: GPU tests, smoke, reference-suite replay, sweep, then the profile/bench pass.
+# Evidence pass (tools/gpu_evidence.sh): GPU tests, smoke, reference-suite replay, sweep, then the profile/bench pass.
 O=gpurun_out; mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > $O/gpu.txt 2>&1
 timeout 1500 python -m pytest tests -m gpu -q -x > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
