@@ -803,6 +803,8 @@ DEVI void s_after_fused(SpxState& s, const double* tot, const double* loc) {
   }
 }
 
+constexpr int64_t kCaptureEveryMax = 1 << 20;  // working sets up to 8 MB capture at every scan
+
 // tot: 0 value, 1 #(v>0), 2 #(v==0)   (simplex.py:207-215, 256-294)
 DEVI void s_after_scan(SpxState& s, const double* tot, const double* loc, double* trace) {
   s.phi_evals += 1;
@@ -862,7 +864,15 @@ DEVI void s_after_scan(SpxState& s, const double* tot, const double* loc, double
   if (s.iterations > s.max_iter) { s_finish(s, next); return; }
   s.cmd.phase = PH_SCAN;
   s.cmd.compact = 0;
-  if (s.fixing) {
+  if (s.cap_first && s.fixing && !s.lam0_given && s.phys_count <= kCaptureEveryMax) {
+    // a small working set captures at every scan: the iterates only decrease
+    // (upper-bound start), so w + next < 0 is zero from here on -- dropped in
+    // the scan at next itself, one scan before the fixing would (the latency
+    // of a grid epoch outweighs rewriting a small set)
+    s.cmd.capture = 1;
+    s.cmd.compact = 1;
+    s.cmd.fix_hi = next + 1e-9 * fmax(1.0, fabs(next));
+  } else if (s.fixing) {
     const int64_t present = s.fixed_local - s.fixed_removed;
     if (present > 0 && (double)present >= s.compact_ratio * (double)s.phys_count) {
       s.cmd.compact = 1;
