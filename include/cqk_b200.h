@@ -36,6 +36,8 @@ enum {
   CQK_E_ARG = -5,
   CQK_E_EMPTY = -6,
   CQK_E_TIMEOUT = -7,
+  CQK_SPARSE_DENSE = 2,     /* spx_project_sparse_f64: take the dense route */
+  CQK_SPARSE_OVERFLOW = 3,  /* ... more than cap nonzero entries (count set) */
 };
 
 /* DomainError.field codes */
@@ -146,6 +148,17 @@ int cqk_solve_f64(cqk_handle *h, int mem, const double *d, const double *a,
                   const double *b, const double *l, const double *u, int64_t n,
                   double r, const cqk_options *opts, const double *xbar, double *x,
                   cqk_result *res);
+
+/* output="sparse" (simplex.py:296-300; project_l1 simplex.py:328-331): the
+   nonzero x as (index, value) pairs in increasing index order, without a
+   dense x -- from the capture start's list (n >= 4e6 per rank, a support of
+   at most n/64).  l1 = 1: project_l1's signed values.  idx_out / val_out hold
+   cap entries (host or device memory per `mem`); *count = the number of
+   nonzeros.  Returns 0, CQK_SPARSE_DENSE (the route does not apply: call the
+   dense entry point), CQK_SPARSE_OVERFLOW (count > cap) or an error. */
+int spx_project_sparse_f64(cqk_handle *h, int mem, const double *y, int64_t n, double r,
+                           const cqk_options *opts, int l1, int64_t *idx_out, double *val_out,
+                           int64_t cap, int64_t *count, cqk_result *res);
 
 /* float32 instances (core.py:55-64 keeps float32 arrays float32): the element
    math in float -- t = (b * float(lam) + a) / d, x = clip(t, l, u), b x

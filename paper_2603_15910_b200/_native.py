@@ -92,8 +92,9 @@ EXPORTS = (
     "cqk_gen_cqk_device_range", "cqk_gen_simplex_u01_device", "spx_project_batched_multi_f64",
     "cqk_read_peak_f64", "cqk_group_create", "cqk_group_destroy", "cqk_group_size",
     "cqk_solve_group_f64", "spx_project_group_f64", "l1_project_group_f64",
-    "cqk_solve_f32", "spx_project_f32", "l1_project_f32",
+    "cqk_solve_f32", "spx_project_f32", "l1_project_f32", "spx_project_sparse_f64",
 )
+SPARSE_DENSE, SPARSE_OVERFLOW = 2, 3
 
 _lib = None
 _gen = None
@@ -163,6 +164,8 @@ def _declare(L):
                                           _P, _RES]
     L.spx_project_batched_multi_f64.argtypes = [_P, ctypes.c_int, _P, _I64, _I64, _D, _OPT, _P,
                                                 _P, _P, _RES]
+    L.spx_project_sparse_f64.argtypes = [_P, ctypes.c_int, _P, _I64, _D, _OPT, ctypes.c_int, _P, _P,
+                                         _I64, ctypes.POINTER(_I64), _RES]
     L.cqk_solve_f32.argtypes = [_P, ctypes.c_int, *arr5, _I64, _D, _OPT, _P, _P, _RES]
     L.spx_project_f32.argtypes = [_P, ctypes.c_int, _P, _I64, _D, _OPT, _P, _RES]
     L.l1_project_f32.argtypes = [_P, ctypes.c_int, _P, _I64, _D, _OPT, _P, _RES]

@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "../../include/cqk_b200.h"
+#include <cub/device/device_radix_sort.cuh>
 #include "cqk_kernels.cuh"
 #include "cqk_tma.cuh"
 #include "cqk_tma_spx.cuh"
@@ -107,6 +108,14 @@ struct cqk_handle {
   double* red = nullptr;     // utility partials
   double* out = nullptr;     // utility outputs (kMaxK doubles)
   Buf scratch, stage, idxbuf, flags, alg2, warm;
+  Buf sparse_buf;                     // output="sparse": (index, value) pairs, counter, sort space
+  struct SparseReq {                  // set by spx/l1_project_sparse_f64 for one call
+    int64_t* idx;
+    double* val;
+    unsigned long long* cnt;
+    int64_t cap;
+  };
+  const SparseReq* sparse_req = nullptr;
   // pageable host inputs / outputs: a ring of pinned chunk buffers filled /
   // drained by OpenMP memcpy while the copy engine moves the previous chunk
   static constexpr int kRing = 4;
@@ -271,6 +280,7 @@ int cqk_destroy(cqk_handle* h) {
   h->flags.release();
   h->alg2.release();
   h->warm.release();
+  h->sparse_buf.release();
   for (int q = 0; q < kMaxRanks; ++q)
     if (h->ipc_opened[q] && h->peers[q]) cudaIpcCloseMemHandle(h->peers[q]);
   if (h->mbox) cudaFree(h->mbox);
@@ -901,7 +911,8 @@ int launch_spx(cqk_handle* h, SpxState& s, const T* yv, int64_t n, T* xo, bool l
   // elements' indices and (l1) the sign bits of y
   const size_t per_y = ((size_t)(tma ? tma_scratch_elems_y(n) : n) * sizeof(T) + 255) / 256 * 256;
   const size_t per_i = s.fused ? ((size_t)tma_scratch_elems_y(n) * 8 + 255) / 256 * 256 : 0;
-  const size_t per_s = s.fused && l1 ? ((size_t)tma_scratch_elems_y(n) / 8 + 255) / 256 * 256 : 0;
+  // (the sign bits serve the dense sparse-final only)
+  const size_t per_s = s.fused && l1 && !h->sparse_req ? ((size_t)tma_scratch_elems_y(n) / 8 + 255) / 256 * 256 : 0;
   if (s.fixing) CUDA_TRY(h->scratch.ensure(per_y + per_i + per_s));
   std::memcpy(h->host_state, &s, sizeof s);  // status RUNNING until the master publishes
   SpxParams<T> p;
@@ -912,6 +923,12 @@ int launch_spx(cqk_handle* h, SpxState& s, const T* yv, int64_t n, T* xo, bool l
   p.sy = s.fixing ? (T*)h->scratch.p : nullptr;
   p.sidx = per_i ? (int64_t*)((char*)h->scratch.p + per_y) : nullptr;
   p.signs = per_s ? (uint32_t*)((char*)h->scratch.p + per_y + per_i) : nullptr;
+  if (h->sparse_req) {
+    p.out_idx = h->sparse_req->idx;
+    p.out_val = h->sparse_req->val;
+    p.out_cnt = h->sparse_req->cnt;
+    p.out_cap = h->sparse_req->cap;
+  }
   p.x = xo;
   p.trace = h->trace;
   p.n = n;
@@ -1279,6 +1296,58 @@ extern "C" int l1_project_warm_f64(cqk_handle* h, int mem, const double* y, int6
 extern "C" int l1_project_f64(cqk_handle* h, int mem, const double* y, int64_t n, double r,
                               const cqk_options* opts, double* x, cqk_result* res) {
   return spx_common(h, mem, y, n, n, r, opts, x, res, true, false);
+}
+
+// ------------------------------------------------------------ sparse output
+// output="sparse" of newton_project_simplex / project_l1 (simplex.py:296-300,
+// 328-331): the capture start's list holds every nonzero x, so the solve
+// writes no dense x -- the kernel appends (index, value) pairs, which are
+// sorted by index here (the reference's order).  Returns CQK_SPARSE_DENSE
+// when the route does not apply (no adopted capture: small n, a large
+// support, l1 inside the ball) and CQK_SPARSE_OVERFLOW (with *count) when
+// more than cap entries are nonzero; the caller then takes the dense route.
+extern "C" int spx_project_sparse_f64(cqk_handle* h, int mem, const double* y, int64_t n, double r,
+                                      const cqk_options* opts, int l1, int64_t* idx_out,
+                                      double* val_out, int64_t cap, int64_t* count,
+                                      cqk_result* res) {
+  if (!h || !y || !idx_out || !val_out || !count || !res || cap < 1)
+    return set_err(CQK_E_ARG, "null argument or cap < 1");
+  CUDA_TRY(cudaSetDevice(h->device));
+  int end_bit = 1;
+  while (end_bit < 63 && ((int64_t)1 << end_bit) < n) ++end_bit;
+  size_t sort_bytes = 0;
+  CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, (const int64_t*)nullptr, (int64_t*)nullptr,
+                                           (const double*)nullptr, (double*)nullptr, (int)cap, 0, end_bit,
+                                           h->stream));
+  const size_t pb = ((size_t)cap * 8 + 255) / 256 * 256;
+  CUDA_TRY(h->sparse_buf.ensure(256 + 4 * pb + sort_bytes));
+  char* b = (char*)h->sparse_buf.p;
+  auto* cnt = (unsigned long long*)b;
+  auto* idx_a = (int64_t*)(b + 256);
+  auto* val_a = (double*)(b + 256 + pb);
+  auto* idx_b = (int64_t*)(b + 256 + 2 * pb);
+  auto* val_b = (double*)(b + 256 + 3 * pb);
+  void* tmp = b + 256 + 4 * pb;
+  CUDA_TRY(cudaMemsetAsync(cnt, 0, 8, h->stream));
+  const cqk_handle::SparseReq req{idx_a, val_a, cnt, cap};
+  h->sparse_req = &req;
+  int rc = spx_common(h, mem, y, n, n, r, opts, (double*)nullptr, res, l1 != 0, false);
+  h->sparse_req = nullptr;
+  if (rc != 0) return rc;
+  if (res->iterations < 0) return CQK_SPARSE_DENSE;  // l1 inside the ball: x = y
+  unsigned long long got = 0;
+  CUDA_TRY(cudaMemcpyAsync(&got, cnt, 8, cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  *count = (int64_t)got;
+  if (got == 0) return CQK_SPARSE_DENSE;  // the kernel took the dense route (r > 0: x != 0)
+  if ((int64_t)got > cap) return CQK_SPARSE_OVERFLOW;
+  CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, sort_bytes, idx_a, idx_b, val_a, val_b, (int)got, 0,
+                                           end_bit, h->stream));
+  const cudaMemcpyKind k = mem == CQK_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  CUDA_TRY(cudaMemcpyAsync(idx_out, idx_b, sizeof(int64_t) * got, k, h->stream));
+  CUDA_TRY(cudaMemcpyAsync(val_out, val_b, sizeof(double) * got, k, h->stream));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return 0;
 }
 
 // ------------------------------------------------------------ batched rows

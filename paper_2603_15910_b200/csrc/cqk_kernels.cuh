@@ -693,6 +693,10 @@ struct SpxParams {
   T* sy;  // scratch (working values w)
   int64_t* sidx;      // capture start: the captured elements' indices (the fused pass's slots)
   uint32_t* signs;    // capture start, l1: y < 0 bits per (tile, warp, j) of the fused pass
+  int64_t* out_idx;   // sparse output (output="sparse"): nonzero x as (index, value), any order,
+  double* out_val;    // ... up to out_cap entries; out_cnt counts all of them
+  unsigned long long* out_cnt;
+  int64_t out_cap;
   T* x;
   double* trace;
   int64_t n;  // elements of this rank's shard

@@ -407,6 +407,31 @@ DEVI void spx_sparse_final(const SpxParams<double>& p, double lam, int64_t ntile
   }
 }
 
+// The sparse output (output="sparse", simplex.py:296-300 / 328-331): with the
+// captured list adopted, the nonzero x are among the captured elements; each
+// warp appends its captured elements' nonzero x as (index, value) pairs
+// through a grid counter (the host sorts them by index) -- no dense x at all.
+template <bool L1>
+DEVI void spx_sparse_output(const SpxParams<double>& p, double lam, int64_t m_cap) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t G = gridDim.x;
+  if (warp >= kConsW) return;
+  for (int64_t i = lane; i < m_cap; i += 32) {
+    const int64_t pos = ((int64_t)blockIdx.x + (i / kSegY) * G) * kTileY + kSegY * warp + (i % kSegY);
+    const int64_t idx = __ldcg(p.sidx + pos);
+    const double yv = p.y[idx];
+    const double v = add_rn(spx_wv<L1>(yv), lam);
+    if (!(v > 0.0)) continue;  // simplex.py:298: tvals > 0
+    double x = v;
+    if (L1) x = mul_rn(yv > 0.0 ? 1.0 : (yv < 0.0 ? -1.0 : 0.0), v);
+    const unsigned long long slot = atomicAdd(p.out_cnt, 1ull);
+    if ((int64_t)slot < p.out_cap) {
+      p.out_idx[slot] = idx;
+      p.out_val[slot] = x;
+    }
+  }
+}
+
 // Master CTA: sum the per-CTA bucket rows (integers, any order), suffix-scan
 // c_j and j c_j from the top, and take the largest k whose lower bound
 // (r / kHistB) sum_{j > k} c_j (j - 1 - k) reaches r.  Two buckets per
@@ -529,6 +554,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
       }
     }
     const TileWalk work{p.n, ntiles, in_scratch ? s_nslots : -1};
+    if (c.phase == PH_FINAL && c.sparse && p.out_idx && p.sidx) {  // output="sparse"
+      if (!producer) drain<kStagesY>(pp, spec);
+      spx_sparse_output<L1>(p, c.lam, m_cap);
+      break;
+    }
     const bool sparse = c.phase == PH_FINAL && c.sparse && p.x && p.sidx && p.ar.tiles;
     if (sparse) {  // the capture start's final: signed zeros + a scatter, y not re-read
       if (blockIdx.x <= 1 && threadIdx.x == 0) tl_mark(p.sync, epoch, 10 + 2 * blockIdx.x);

@@ -13,6 +13,7 @@ the device (par_simplex_init semantics, `sharpened` as given) and Algorithm 4
 on its free set.
 """
 
+import ctypes
 from dataclasses import dataclass
 
 import numpy as np
@@ -209,6 +210,50 @@ def _project(y, r, opts, lambda0, trace, l1, start="auto", xbar=None, sharpened=
     return x, res
 
 
+SPARSE_MIN_N = 4_000_000  # the capture start's size (CQK_SPX_CAPTURE_MIN_N)
+
+
+def _project_sparse(y, r, opts, l1, start):
+    """output="sparse" straight from the device (spx_project_sparse_f64): the
+    nonzero x as (index, value) in index order, no dense x.  None when the
+    route does not apply (the caller takes the dense one)."""
+    if opts is None:
+        opts = SolverOptions()
+    yv, dt, dev = _prep(y)
+    if dt != np.float64:
+        return None
+    n = int(yv.shape[0])
+    if n < SPARSE_MIN_N:
+        return None
+    cap = min(n // 64 + 1, 1 << 22)
+    h = N.handle(yv.get_device() if dev else None)
+    h.use_current_stream()
+    if dev:
+        import torch
+
+        idx = torch.empty(cap, dtype=torch.int64, device=yv.device)
+        val = torch.empty(cap, dtype=torch.float64, device=yv.device)
+        yp, ip, vp, mem = yv.data_ptr(), idx.data_ptr(), val.data_ptr(), N.MEM_DEVICE
+    else:
+        idx = np.empty(cap, dtype=np.int64)
+        val = np.empty(cap, dtype=np.float64)
+        yp, ip, vp, mem = yv.ctypes.data, idx.ctypes.data, val.ctypes.data, N.MEM_HOST
+    o = N.make_options(opts, compact_ratio=getattr(opts, "compact_ratio", None), start=start,
+                       tau=opts.tau(dt))
+    res = N.Result()
+    cnt = ctypes.c_int64()
+    rc = h.lib.spx_project_sparse_f64(h.ptr, mem, yp, n, float(r), o, 1 if l1 else 0, ip, vp, cap,
+                                      ctypes.byref(cnt), res)
+    if rc in (N.SPARSE_DENSE, N.SPARSE_OVERFLOW):
+        return None
+    if rc == N.E_DOMAIN:
+        raise DomainError("r", None, ("l1 radius" if l1 else "simplex level") + " r must be positive")
+    if rc != N.SOLVED:
+        raise N.NativeError(f"sparse projection failed ({rc}): {N.last_error()}")
+    k = int(cnt.value)
+    return (idx[:k], val[:k]), res
+
+
 def _sparse(x, dev):
     if dev:
         import torch
@@ -233,6 +278,14 @@ def newton_project_simplex(y, r, opts=None, xbar=None, output="dense", sharpened
     free set.  All routes return the same projection."""
     if not r > 0:
         raise DomainError("r", None, "simplex level r must be positive")
+    if output == "sparse" and xbar is None and not sharpened and lambda0 is None and trace is None \
+            and start != "alg2":
+        got = _project_sparse(y, r, opts, False, start)
+        if got is not None:
+            sparse, res = got
+            return SolveOutcome(status=Status.SOLVED, lam=float(res.lam), x=None,
+                                iterations=int(res.iterations), phi_evals=int(res.phi_evals),
+                                fixed_count=int(res.fixed_count), sparse=sparse, stats=res.stats())
     x, res = _project(y, r, opts, lambda0, trace, l1=False, start=start, xbar=xbar,
                       sharpened=sharpened)
     dev = _is_torch(x)
@@ -249,6 +302,10 @@ def project_l1(y, r, opts=None, output="dense", xbar=None, start="auto"):
     """Project y onto the l1 ball of radius r (simplex.py:311-333)."""
     if not r > 0:
         raise DomainError("r", None, "l1 radius r must be positive")
+    if output == "sparse" and xbar is None and start != "alg2":
+        got = _project_sparse(y, r, opts, True, start)
+        if got is not None:
+            return got[0]
     try:
         x, res = _project(y, r, opts, None, None, l1=True, start=start, xbar=xbar, sharpened=True)
     except DomainError as e:

@@ -174,3 +174,41 @@ def test_capture_edge_inputs(name, l1, r):
         sg = (y > 0).double() - (y < 0).double()
         xr = sg * xr
     assert torch.equal(cap.x.view(torch.int64), xr.view(torch.int64))
+
+
+@pytest.mark.parametrize("l1", [False, True])
+@pytest.mark.parametrize("dev", [False, True])
+def test_sparse_output_straight_from_the_capture(l1, dev):
+    """output="sparse" (simplex.py:296-300, 328-331) without a dense x: the
+    same (index, value) pairs, in index order, as the dense route's nonzeros."""
+    import torch
+
+    p = P()
+    n = 6_000_007
+    y = p.gen_simplex_y("simplex-n01", n, 12)
+    yin = torch.from_numpy(y).cuda() if dev else y
+    if l1:
+        idx, val = p.project_l1(yin, 1.0, output="sparse")
+        xd = p.project_l1(yin, 1.0)
+    else:
+        out = p.newton_project_simplex(yin, 1.0, output="sparse")
+        assert out.x is None
+        idx, val = out.sparse
+        xd = p.newton_project_simplex(yin, 1.0).x
+    if dev:
+        idx, val, xd = idx.cpu().numpy(), val.cpu().numpy(), xd.cpu().numpy()
+    ref_idx = np.flatnonzero(xd != 0)
+    assert np.array_equal(idx, ref_idx)
+    assert np.array_equal(val, xd[ref_idx])
+    assert abs(np.abs(val).sum() - 1.0) <= 1e-12
+
+
+def test_sparse_output_falls_back_when_dense():
+    """u01: half of y is captured -- the dense route answers, same contract."""
+    p = P()
+    n = 4_100_000
+    y = p.gen_simplex_y("simplex-u01", n, 3)
+    out = p.newton_project_simplex(y, 1.0, output="sparse")
+    idx, val = out.sparse
+    x = p.newton_project_simplex(y, 1.0).x
+    assert np.array_equal(idx, np.flatnonzero(x > 0)) and np.array_equal(val, x[idx])
