@@ -30,3 +30,21 @@ P.project_l1(y, 1.0)
 Y = y[: 64 * 1024].reshape(64, 1024)
 P.project_simplex_rows(Y, 1.0)
 print("probe ok")
+
+# the large-n routes at probe sizes: run with CQK_FUSED_MIN_N=0
+# CQK_SPX_CAPTURE_MIN_N=0 CQK_FUSED_GUESS=2 (forced guess) to sanitize the fused
+# start, the direction guess, the capture start, the sparse final and the sparse output
+if os.environ.get("PROBE_LARGE_ROUTES"):
+    import torch
+
+    P.simplex.SPARSE_MIN_N = 0
+    out = P.solve_cqk(inst)
+    ref = P.solve_cqk(inst, P.SolverOptions(compact_ratio=2.0))
+    assert out.status is P.Status.SOLVED and abs(out.lam - ref.lam) <= 1e-12 * max(1.0, abs(ref.lam))
+    yd = torch.from_numpy(y).cuda()
+    for l1 in (False, True):
+        x = P.project_l1(yd, 1.0) if l1 else P.newton_project_simplex(yd, 1.0).x
+        idx, val = P.project_l1(yd, 1.0, output="sparse") if l1 else \
+            P.newton_project_simplex(yd, 1.0, output="sparse").sparse
+        assert torch.equal(idx, torch.nonzero(x != 0).flatten())
+    print("large routes ok")
