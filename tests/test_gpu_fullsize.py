@@ -117,3 +117,45 @@ def test_fused_start_random_stress():
         json.dump({"instances": 40, "iteration_mismatches": mism, "lam_worst_rel": worst,
                    "mismatches": rows}, f, indent=1)
     assert mism <= 4, rows
+
+
+def test_capture_start_random_stress():
+    """The simplex / l1 capture start (and its sparse final) serves n >= 4e6
+    per rank: 24 random projections against the oracle's same-route
+    Algorithm 4 (lambda to 1e-12, iteration counts recorded;
+    gpurun_out/stress_capture.json)."""
+    import paper_2603_15910_b200 as P
+
+    rng = np.random.default_rng(2028)
+    mism, worst, rows = 0, 0.0, []
+    for k in range(24):
+        n = int(rng.integers(4_000_000, 7_000_001))
+        fam = ("simplex-n01", "simplex-u01")[k % 2]
+        l1 = bool(k % 3 == 0)
+        start = ("tight", "formula")[(k // 2) % 2]
+        r = float(rng.choice([1.0, 0.01, 100.0]))
+        y = O.gen_simplex_y(fam, n, 7000 + k)
+        w = np.abs(y) if l1 else y
+        s_w = float(O.pairwise_sum(w))
+        lam0 = (r - s_w) / n
+        if start == "tight":
+            lam0 = min(lam0, r - float(w.max()))
+        if l1 and s_w <= r:
+            continue
+        ref = O.newton_project_simplex(w, r, lam0=lam0)
+        out = (P.simplex.project_l1_outcome(y, r, start=start) if l1
+               else P.newton_project_simplex(y, r, start=start))
+        rel = abs(out.lam - ref["lam"]) / max(1.0, abs(ref["lam"]))
+        worst = max(worst, rel)
+        assert rel <= 1e-12, (fam, n, k, l1, start, r, out.lam, ref["lam"])
+        xr = np.sign(y) * ref["x"] if l1 else ref["x"]
+        assert np.abs(out.x - xr).max() <= 1e-12 * max(1.0, r)
+        if out.iterations != ref["iterations"]:
+            mism += 1
+            rows.append({"family": fam, "n": n, "seed": 7000 + k, "l1": l1, "start": start, "r": r,
+                         "gpu": out.iterations, "oracle": ref["iterations"]})
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(ROOT, "gpurun_out", "stress_capture.json"), "w") as f:
+        json.dump({"instances": 24, "iteration_mismatches": mism, "lam_worst_rel": worst,
+                   "mismatches": rows}, f, indent=1)
+    assert mism <= 2, rows
