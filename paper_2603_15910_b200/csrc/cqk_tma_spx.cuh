@@ -486,7 +486,6 @@ __global__ void __launch_bounds__(kTmaThreads, 1) spx_tma_kernel(SpxParams<doubl
   __shared__ int s_tail;              // master: finish the iterations in this CTA
   __shared__ int s_scan[kConsW + 1];
   __shared__ int s_hist[kHistB];      // start "auto": first-scan bucket counts
-  __shared__ double s_lam_hist;
   __shared__ long long s_tix[kStagesY];  // dynamic final pass: tile index per stage
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool producer = warp == kConsW;
