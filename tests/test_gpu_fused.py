@@ -217,3 +217,21 @@ def test_fused_sharded(world, guess):
                                                           ref["fixed_count"])
     x = np.concatenate([oo.x.cpu().numpy() for oo in outs])
     assert np.abs(x - ref["x"]).max() <= 1e-12 * 25.0
+
+
+@pytest.mark.parametrize("guess", [0, 1, 2, 3])
+def test_fused_infinite_bounds(guess):
+    """l = -inf / u = +inf entries (allowed by validate, core.py:126-165): never
+    classified at a bound, never fixed there; the fused start with every
+    guess mode returns the oracle's solve."""
+    p = P()
+    n = 400_003
+    d, a, b, l, u, r = p.instances.gen_cqk_arrays("cqk-weakly-correlated", n, 21)
+    rng = np.random.default_rng(21)
+    l = l.copy()
+    u = u.copy()
+    l[rng.random(n) < 0.2] = -np.inf
+    u[rng.random(n) < 0.2] = np.inf
+    ref = O.solve_cqk(d, a, b, l, u, r)
+    out = solve(inst_of(d, a, b, l, u, r), True, guess=guess)
+    check(out, ref)
