@@ -95,3 +95,31 @@ def test_tiny_instance_on_a_group(monkeypatch):
     inst = P.CqkInstance(d=[1.0, 2.0], a=[0.0, 0.0], b=[1.0, 1.0], l=[0.0, 0.0], u=[1.0, 1.0], r=1.0)
     out = P.solve_cqk(inst)
     assert abs(out.lam - 2.0 / 3.0) <= 1e-12
+
+
+def test_group_with_warm_start(monkeypatch):
+    """xbar (core.py:245-254: lambda0 over the interior set of xbar) through
+    the group's shards: the interior sums cross the in-kernel exchange."""
+    import paper_2603_15910_b200 as P
+
+    n = 2_000_003
+    d, a, b, l, u, r = P.instances.gen_cqk_arrays("cqk-weakly-correlated", n, 13)
+    inst = P.CqkInstance(d=d, a=a, b=b, l=l, u=u, r=r)
+    xbar = np.clip((a + 5.0) / d, l, u)
+    ref = O.solve_cqk(d, a, b, l, u, r, xbar=xbar)
+    monkeypatch.setenv("CQK_DEVICES", "0,0")
+    out = P.solve_cqk(inst, xbar=xbar)
+    assert close(out.lam, ref["lam"]) and out.iterations == ref["iterations"]
+    assert np.abs(out.x - ref["x"]).max() <= 1e-12 * max(1.0, np.abs(ref["x"]).max())
+
+
+def test_group_float32_takes_the_single_device_float32_path(monkeypatch):
+    import paper_2603_15910_b200 as P
+
+    n = 300_001
+    d, a, b, l, u, r = P.instances.gen_cqk_arrays("cqk-uncorrelated", n, 14)
+    inst = P.CqkInstance(*[v.astype(np.float32) for v in (d, a, b, l, u)], r=r)
+    plain = P.solve_cqk(inst)
+    monkeypatch.setenv("CQK_DEVICES", "0,0")
+    out = P.solve_cqk(inst)
+    assert out.x.dtype == np.float32 and out.lam == plain.lam and np.array_equal(out.x, plain.x)
