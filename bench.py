@@ -441,6 +441,9 @@ def run_c3(args, cfg, world, rank, local):
                 "lam": out.lam, "iterations": out.iterations, "phi_evals": out.phi_evals,
                 "fixed_count": out.fixed_count, "inst": k % len(insts)}
 
+    # every rank's first sharded solve spins on its peers' mailboxes (4 s
+    # timeout): start the warm-up together
+    barrier(world)
     with torch.cuda.stream(stream):
         for k in range(args.warmup):
             step(k)
@@ -501,6 +504,7 @@ def e2e_cqk(args, world, rank, stream, dev, rs, host0, solvers, n, n_local):
         host = [t.cpu().pin_memory().numpy() for t in dev[0]]
         xh = torch.empty(n_local, dtype=torch.float64, pin_memory=True).numpy()
         s = solvers[0]
+        barrier(world)  # pinning takes rank-dependent time; the solves exchange in-kernel
         with torch.cuda.stream(stream):
             for _ in range(2):
                 assert s.solve_host(host, xh).status is P.Status.SOLVED
@@ -609,6 +613,7 @@ def run_c4(args, cfg, world, rank, local):
             return {"device_ms": out.stats["device_ms"], "bytes_model": out.stats["bytes_model"],
                     "lam": out.lam, "iterations": out.iterations, "phi_evals": out.phi_evals}
 
+        barrier(world)
         for k in range(args.warmup):
             step(k)
         ms, outs, clocks = Timed(world, local, stream).run(args.steps, step)
@@ -623,6 +628,7 @@ def run_c4(args, cfg, world, rank, local):
                 run = lambda: proj.solve_host(yp.numpy(), cfg["r"], l1=True)  # noqa: E731
             else:
                 run = lambda: P.project_l1(yp.numpy(), cfg["r"])  # noqa: E731
+            barrier(world)
             run()
             torch.cuda.synchronize()
             barrier(world)
