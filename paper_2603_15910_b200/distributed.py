@@ -5,9 +5,11 @@ contiguous chunks, parallel.py:82-85, and the fixed-order _tree_sum,
 parallel.py:62-72) at node scale: rank q owns the contiguous shard
 [n*q/W, n*(q+1)/W) of every array and runs the same persistent kernel as the
 single-GPU solve on it.  The cross-GPU step is fused into that kernel: once per
-Newton epoch each rank's master thread stores its partial-sum vector into every
-peer's mailbox over NVLink (CUDA IPC mapped device memory) and reduces the W
-vectors in rank order, so all ranks take the identical decision with no
+Newton epoch one warp of each rank stores its partial-sum vector into every
+peer's mailbox over NVLink (CUDA IPC mapped device memory; lane k stores value
+k to all peers, one system-scope fence, lane q raises peer q's flag), and every
+CTA reduces the W vectors in rank order, so all ranks take the identical
+decision with no
 collective library call and no host round trip.  torch.distributed is used
 once, at set-up, to exchange the 64-byte IPC handles.
 """
@@ -217,7 +219,6 @@ class ShardedProjection:
                             x=self.x, iterations=int(res.iterations),
                             phi_evals=int(res.phi_evals), fixed_count=int(res.fixed_count),
                             stats=res.stats())
-
 
     def solve_host(self, y_host, r, l1=False, opts=None, start="tight", x_out=None):
         """Collective projection of this rank's shard given in HOST memory
