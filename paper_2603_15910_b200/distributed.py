@@ -9,8 +9,7 @@ Newton epoch one warp of each rank stores its partial-sum vector into every
 peer's mailbox over NVLink (CUDA IPC mapped device memory; lane k stores value
 k to all peers, one system-scope fence, lane q raises peer q's flag), and every
 CTA reduces the W vectors in rank order, so all ranks take the identical
-decision with no
-collective library call and no host round trip.  torch.distributed is used
+decision with no collective library call and no host round trip.  torch.distributed is used
 once, at set-up, to exchange the 64-byte IPC handles.
 """
 
