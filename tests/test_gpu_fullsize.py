@@ -159,3 +159,27 @@ def test_capture_start_random_stress():
         json.dump({"instances": 24, "iteration_mismatches": mism, "lam_worst_rel": worst,
                    "mismatches": rows}, f, indent=1)
     assert mism <= 2, rows
+
+
+@pytest.mark.parametrize("fam,level", [("cqk-uncorrelated", 0.02), ("cqk-weakly-correlated", 0.5),
+                                       ("cqk-correlated", 0.98)])
+def test_cqk_config_scale_other_levels(fam, level):
+    """C2-scale solves (n = 1.2e7: fused start, direction guess, compaction)
+    at right-hand sides r = b.l + level (b.u - b.l) the generator does not
+    produce, against the oracle's solve_cqk (newton.py:209-342): lambda and
+    x to 1e-12, identical iterations, phi evaluations and fixed counts."""
+    import torch
+
+    import paper_2603_15910_b200 as P
+
+    d, a, b, l, u, _ = O.gen_cqk(fam, 12_000_000, 8100)
+    bl, bu = float(O.pairwise_sum(b * l)), float(O.pairwise_sum(b * u))
+    r = bl + level * (bu - bl)
+    ref = O.solve_cqk(d, a, b, l, u, r)
+    out = P.solve_cqk(P.CqkInstance(*[torch.from_numpy(v).cuda() for v in (d, a, b, l, u)], r=r))
+    assert out.status is P.Status.SOLVED and ref["status"] == 0
+    assert abs(out.lam - ref["lam"]) <= 1e-12 * max(1.0, abs(ref["lam"]))
+    x = out.x.cpu().numpy()
+    assert np.abs(x - ref["x"]).max() <= 1e-12 * max(1.0, np.abs(ref["x"]).max())
+    assert (out.iterations, out.phi_evals, out.fixed_count) == \
+        (ref["iterations"], ref["phi_evals"], ref["fixed_count"])
